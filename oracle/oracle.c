@@ -1,0 +1,188 @@
+/*
+ * oracle/oracle.c -- plain, slow, obviously-correct fp64 CPU reference for the
+ * FeatGraph hot path (arXiv 2008.11359).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load or call this
+ * library.  It shares no code, header, table or constant with the CUDA path
+ * (paper_2008_11359_b200/csrc); the two meet only at the seeded inputs of gen/.
+ *
+ * Every routine is a direct per-edge loop in the order the paper writes the
+ * computation, accumulating in fp64 ("direct per-edge
+ * interpretation", "accumulate in f64"); OpenMP parallelises over
+ * destination rows only (each row is an independent reduction).  No blocking,
+ * no fusion, no reordering of a row's edges.
+ *
+ * Besides the value `ref`, each routine returns `abssum` = sum of |terms| for
+ * every output element; it normalises the tolerance |gpu - ref| <= 1e-4 *
+ * abssum (BASELINE.json north_star: "relative error of 1e-4 ... normalised by
+ * the sum of absolute terms").
+ *
+ * Graph: destination-major CSR.  row v = [row_ptr[v], row_ptr[v+1]) lists the
+ * sources u = col_idx[p] of the in-edges u->v (Eq. (1) reduces over N(v),
+ * PAPER.md P:141-143; Eq. (3) H_V = A X_V).  The edge id of CSR position
+ * p is eid[p] (eid == NULL: eid(p) = p); edge tensors are indexed by edge id
+ * (SPEC.md S:23).
+ *
+ * Parity pins: tests/test_oracle_pins.py (dense A.X, masked max, complete-graph
+ * X.Y^T, closed-form MLP max, adjoint identity, softmax invariants, SPEC
+ * worked examples under tests/golden/).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <math.h>
+
+/* message ops (oracle's own numbering; the binding maps names to these) */
+#define OR_COPY_U  0   /* phi = x_u                              P:252-254 (Fig. 3a) */
+#define OR_U_MUL_E 1   /* phi = x_u[h,:] * x_uv[h]               P:375 (DGL builtin) */
+#define OR_MLP     2   /* phi = ReLU((x_u + x_v) W)              P:289-296 (Fig. 3b) */
+#define OR_SUM 0       /* aggregation: sum */
+#define OR_MAX 1       /* aggregation: max                       P:56 (Fig. 1) */
+
+static inline int64_t edge_id(const int32_t* eid, int64_t p) { return eid ? (int64_t)eid[p] : p; }
+
+/*
+ * Generalized SpMM, Eq. (1):  h_v = (+)_{u in N(v)} phi(x_u, x_v, x_uv)
+ * evaluated for the listed destination rows (rows == NULL: all rows 0..n_rows-1).
+ *
+ * Output element (r, j), r = index into the row list, j < F:
+ *   copy_u : t = X[u][j]                                   (F = H*D)
+ *   u_mul_e: t = X[u][j] * E[eid][j / D]                   (F = H*D, E is [nnz][H])
+ *   mlp    : t = max(0, sum_{k<d_in} (X[u][k] + X_dst[v][k]) * W[k][j])   (F = d2; Fig. 3b: ReLU
+ *            applied after the full d1 contraction)
+ *   sum: ref = sum over the row's edges in CSR order; abssum = sum |t| (mlp: sum_e sum_k |a_k W_kj|)
+ *   max: ref = max_t with the FIRST edge (lowest CSR position) winning ties;
+ *        u_mul_e compares the fp32-rounded product (the kernel's precision);
+ *        abssum = |terms| of the winning message; arg_u/arg_e = col_idx / eid of the winner.
+ *   empty row: ref = +0.0, abssum = 0, arg = -1.
+ */
+void or_spmm(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr, const int32_t* col_idx,
+             const int32_t* eid, int op, int red, int H, int D,
+             const float* X, const float* E, const float* W, int d_in, const float* X_dst,
+             double* ref, double* abssum, int32_t* arg_u, int32_t* arg_e) {
+    const int64_t F = (op == OR_MLP) ? (int64_t)D : (int64_t)H * D;
+    #pragma omp parallel
+    {
+        int64_t* best = (int64_t*)malloc(sizeof(int64_t) * (size_t)(F > 0 ? F : 1));
+        #pragma omp for schedule(dynamic, 16)
+        for (int64_t r = 0; r < n_rows; ++r) {
+            const int64_t v = rows ? rows[r] : r;
+            double* acc = ref + r * F;          /* h_v, accumulated in place */
+            double* ab = abssum + r * F;
+            for (int64_t j = 0; j < F; ++j) {
+                acc[j] = (red == OR_SUM) ? 0.0 : -INFINITY;
+                ab[j] = 0.0;
+                best[j] = -1;
+            }
+            /* for each in-edge u -> v (ascending CSR position p): message phi, then (+) */
+            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {
+                const int64_t u = col_idx[p];
+                const int64_t e = edge_id(eid, p);
+                for (int64_t j = 0; j < F; ++j) {
+                    double t, t_abs;
+                    if (op == OR_COPY_U) {
+                        t = (double)X[u * F + j];
+                        t_abs = fabs(t);
+                    } else if (op == OR_U_MUL_E) {
+                        t = (double)X[u * F + j] * (double)E[e * H + j / D];   /* exact in fp64 */
+                        t_abs = fabs(t);
+                    } else {
+                        double z = 0.0; t_abs = 0.0;
+                        for (int k = 0; k < d_in; ++k) {
+                            double a = (double)X[u * d_in + k] + (double)X_dst[v * d_in + k];
+                            double term = a * (double)W[(int64_t)k * F + j];
+                            z += term; t_abs += fabs(term);
+                        }
+                        t = z > 0.0 ? z : 0.0;   /* ReLU = tvm.max(., 0), canonical +0.0 */
+                    }
+                    if (red == OR_SUM) {
+                        acc[j] += t; ab[j] += t_abs;
+                    } else {
+                        double key = (op == OR_U_MUL_E) ? (double)(float)t : t;
+                        if (key > acc[j]) { acc[j] = key; best[j] = p; ab[j] = t_abs; }  /* strict >: first wins */
+                    }
+                }
+            }
+            for (int64_t j = 0; j < F; ++j) {
+                if (row_ptr[v + 1] == row_ptr[v]) { acc[j] = 0.0; ab[j] = 0.0; }
+                if (red == OR_MAX) {
+                    if (arg_u) arg_u[r * F + j] = best[j] < 0 ? -1 : col_idx[best[j]];
+                    if (arg_e) arg_e[r * F + j] = best[j] < 0 ? -1 : (int32_t)edge_id(eid, best[j]);
+                }
+            }
+        }
+        free(best);
+    }
+}
+
+/*
+ * Generalized SDDMM, Eq. (2)/(4) with the dot-product edge function of Fig. 5a
+ * and its multi-head form Fig. 5b:
+ *   h_uv[h] = sum_{d<D} X[u][h][d] * Y[v][h][d]
+ * for every edge of the listed rows, written at position o = (offset of row r in
+ * the list) + (p - row_ptr[v]) of ref/abssum ([edges of listed rows][H]).
+ * Heads are independent reductions.
+ */
+void or_sddmm(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr, const int32_t* col_idx,
+              int H, int D, const float* X, const float* Y, double* ref, double* abssum) {
+    const int64_t F = (int64_t)H * D;
+    int64_t* off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_rows + 1));
+    off[0] = 0;
+    for (int64_t r = 0; r < n_rows; ++r) {
+        int64_t v = rows ? rows[r] : r;
+        off[r + 1] = off[r] + (row_ptr[v + 1] - row_ptr[v]);
+    }
+    #pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t r = 0; r < n_rows; ++r) {
+        const int64_t v = rows ? rows[r] : r;
+        for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {
+            const int64_t u = col_idx[p];
+            const int64_t o = off[r] + (p - row_ptr[v]);
+            for (int h = 0; h < H; ++h) {
+                double s = 0.0, a = 0.0;
+                for (int d = 0; d < D; ++d) {
+                    double t = (double)X[u * F + (int64_t)h * D + d] * (double)Y[v * F + (int64_t)h * D + d];
+                    s += t; a += fabs(t);
+                }
+                ref[o * H + h] = s;
+                abssum[o * H + h] = a;
+            }
+        }
+    }
+    free(off);
+}
+
+/*
+ * Edge softmax over the in-edges of each destination, per head (not in the
+ * paper; the standard GAT / DGL definition needed by the GAT layer, P:983;
+ * SURVEY L6):  alpha[p][h] = exp(s[p][h] - mx) / sum_q exp(s[q][h] - mx),
+ * mx = max_q s[q][h], q over the row of p.  Scores are read at edge id eid(p)
+ * (S[eid][h]); alpha is written at the listed-row position like or_sddmm.
+ */
+void or_edge_softmax(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr, const int32_t* eid,
+                     int H, const float* S, double* alpha) {
+    int64_t* off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_rows + 1));
+    off[0] = 0;
+    for (int64_t r = 0; r < n_rows; ++r) {
+        int64_t v = rows ? rows[r] : r;
+        off[r + 1] = off[r] + (row_ptr[v + 1] - row_ptr[v]);
+    }
+    #pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t r = 0; r < n_rows; ++r) {
+        const int64_t v = rows ? rows[r] : r;
+        for (int h = 0; h < H; ++h) {
+            double mx = -INFINITY, sum = 0.0;
+            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {
+                double s = (double)S[edge_id(eid, p) * H + h];
+                if (s > mx) mx = s;
+            }
+            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p)
+                sum += exp((double)S[edge_id(eid, p) * H + h] - mx);
+            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {
+                const int64_t o = off[r] + (p - row_ptr[v]);
+                alpha[o * H + h] = exp((double)S[edge_id(eid, p) * H + h] - mx) / sum;
+            }
+        }
+    }
+    free(off);
+}

@@ -1,0 +1,360 @@
+"""Pins for the fp64 oracle against things other than itself (CPU only).
+
+Each check is chosen so a plausible mistake in oracle/oracle.c (dropped term,
+wrong sign/index, transposed operand, wrong tie rule, wrong edge direction)
+fails at least one of them:
+  * dense A.X (Eq. (3)) and |A|.|X| for the abs-sums;
+  * all-ones X -> in-degree exactly;
+  * numpy masked max / first-occurrence argmax; relabelling invariance;
+  * weighted dense A_w.X per head, E == 1 reduces to copy_u;
+  * MLP max closed form ReLU(max_u (XW)[u] + (XW)[v]) (distributivity +
+    monotone ReLU), brute-force MLP sum;
+  * complete graph u_dot_v == dense X.Y^T per head (Eq. (4));
+  * adjoint identity of the gradient duality;
+  * softmax: rows sum to 1, shift invariance, constant -> 1/deg, torch.softmax
+    on a dense -inf-masked matrix;
+  * SPEC.md worked examples in tests/golden/spec_examples.json.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from helpers import csr_from_edges, dense_adjacency, edge_rows
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def small_graph(n=257, m=3000, seed=5, empty_rows=True, uniform=False):
+    g = gen.random_graph(n, m, seed, sigma=1.0, n_empty=max(1, n // 20) if empty_rows else 0,
+                         uniform_sources=uniform)
+    assert (g.degrees() == 0).any() == empty_rows
+    return g
+
+
+# ------------------------------------------------------------------ copy_u
+@pytest.mark.parametrize("F", [1, 4, 12, 32])
+def test_copy_u_sum_dense(F):
+    g = small_graph()
+    X = gen.features((g.n_src, F), 11, 0)
+    ref, ab, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", "sum", X)
+    A = dense_adjacency(g.row_ptr, g.col_idx, g.n_src)
+    np.testing.assert_allclose(ref, A @ X.astype(np.float64), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(ab, A @ np.abs(X.astype(np.float64)), rtol=1e-12, atol=1e-12)
+
+
+def test_copy_u_sum_ones_is_indegree():
+    g = small_graph(n=500, m=9000)
+    X = np.ones((g.n_src, 8), np.float32)
+    ref, _, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", "sum", X)
+    assert np.array_equal(ref, np.repeat(g.degrees()[:, None].astype(np.float64), 8, 1))
+
+
+def test_spec_copy_u_example():
+    ex = GOLD["copy_u_sum"]
+    rp, ci = csr_from_edges(ex["n"], ex["edges"])
+    ref, _, _, _ = oracle.spmm(rp, ci, "copy_u", "sum", np.array(ex["X"], np.float32))
+    assert np.array_equal(ref, np.array(ex["expected"], np.float64))
+
+
+def _masked_max(row_ptr, col_idx, n_src, M):
+    """numpy masked max over messages M[v, u, j] (only edges u->v count),
+    argmax = first occurrence along ascending u (== lowest CSR position)."""
+    A = dense_adjacency(row_ptr, col_idx, n_src) > 0
+    Mm = np.where(A[:, :, None], M, -np.inf)
+    val = Mm.max(axis=1)
+    arg = Mm.argmax(axis=1)
+    empty = ~A.any(axis=1)
+    val[empty] = 0.0
+    arg[empty] = -1
+    return val, arg
+
+
+def _eid_of(row_ptr, col_idx, v, u):
+    p = np.searchsorted(col_idx[row_ptr[v]:row_ptr[v + 1]], u) + row_ptr[v]
+    assert col_idx[p] == u
+    return p
+
+
+@pytest.mark.parametrize("regime", [gen.REAL, gen.INT])
+def test_copy_u_max_masked(regime):
+    g = small_graph()
+    X = gen.features((g.n_src, 6), 13, 0, regime, lo=-3, hi=3)   # INT: many ties
+    ref, ab, au, ae = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", "max", X)
+    M = np.broadcast_to(X.astype(np.float64)[None], (g.n_dst, g.n_src, 6))
+    val, arg = _masked_max(g.row_ptr, g.col_idx, g.n_src, M)
+    assert np.array_equal(ref, val)
+    assert np.array_equal(au, arg)
+    assert np.array_equal(ab, np.abs(val))
+    for v in range(0, g.n_dst, 7):
+        for j in range(6):
+            if arg[v, j] >= 0:
+                assert ae[v, j] == _eid_of(g.row_ptr, g.col_idx, v, arg[v, j])
+            else:
+                assert ae[v, j] == -1
+
+
+def test_copy_u_max_relabel_invariance():
+    g = small_graph(n=120, m=1500, seed=9)
+    X = gen.features((g.n_src, 5), 3, 0, gen.INT, lo=-4, hi=4)
+    ref, _, au, _ = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", "max", X)
+    pi = gen.permutation(g.n_dst, 99)                 # new id of old vertex i = pi[i]
+    src, dst = g.col_idx.astype(np.int64), edge_rows(g.row_ptr)
+    rp2, ci2 = csr_from_edges(g.n_dst, np.stack([pi[src], pi[dst]], 1))
+    X2 = np.empty_like(X)
+    X2[pi] = X
+    ref2, _, au2, _ = oracle.spmm(rp2, ci2, "copy_u", "max", X2)
+    assert np.array_equal(ref2[pi], ref)
+    # the max VALUE is relabelling-invariant; the winner is the same vertex when
+    # no tie occurs (ties resolve by position, which relabelling changes)
+    Xd = X.astype(np.float64)
+    for v in range(g.n_dst):
+        for j in range(5):
+            if au[v, j] >= 0:
+                assert Xd[au[v, j], j] == ref[v, j]
+                assert X2[au2[pi[v], j], j] == ref[v, j]
+
+
+# ------------------------------------------------------------------ u_mul_e
+def test_u_mul_e_sum_weighted_dense():
+    g = small_graph()
+    H, D = 3, 4
+    X = gen.features((g.n_src, H * D), 21, 0)
+    E = gen.features((g.nnz, H), 21, 1, gen.UNIT)
+    ref, ab, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", "sum", X, H=H, E=E)
+    for h in range(H):
+        Aw = dense_adjacency(g.row_ptr, g.col_idx, g.n_src, E[:, h].astype(np.float64))
+        blk = slice(h * D, (h + 1) * D)
+        np.testing.assert_allclose(ref[:, blk], Aw @ X[:, blk].astype(np.float64), rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(ab[:, blk], np.abs(Aw) @ np.abs(X[:, blk].astype(np.float64)),
+                                   rtol=1e-12, atol=1e-12)
+
+
+def test_u_mul_e_with_eid_permutation():
+    """E is indexed by edge id, not CSR position."""
+    g = small_graph(n=90, m=800)
+    H = 2
+    X = gen.features((g.n_src, 2 * H), 4, 0)
+    E = gen.features((g.nnz, H), 4, 1, gen.UNIT)
+    eid = gen.permutation(g.nnz, 5).astype(np.int32)
+    ref, _, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", "sum", X, H=H, E=E, eid=eid)
+    Epos = E[eid]   # value seen at CSR position p
+    ref2, _, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", "sum", X, H=H, E=Epos)
+    assert np.array_equal(ref, ref2)
+
+
+@pytest.mark.parametrize("red", ["sum", "max"])
+def test_u_mul_e_ones_is_copy_u(red):
+    g = small_graph()
+    X = gen.features((g.n_src, 8), 23, 0)
+    E = np.ones((g.nnz, 2), np.float32)
+    a = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", red, X, H=2, E=E)
+    b = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", red, X)
+    for x, y in zip(a, b):
+        if x is not None:
+            assert np.array_equal(x, y)
+
+
+def test_u_mul_e_max_fp32_products():
+    """max compares the fp32-rounded product (numpy float32 multiply is RN)."""
+    g = small_graph()
+    H, D = 2, 3
+    X = gen.features((g.n_src, H * D), 31, 0)
+    E = gen.features((g.nnz, H), 31, 1, gen.UNIT)
+    ref, _, au, ae = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", "max", X, H=H, E=E)
+    rows = edge_rows(g.row_ptr)
+    M = np.full((g.n_dst, g.n_src, H * D), -np.inf)
+    for h in range(H):
+        prod = X[g.col_idx][:, h * D:(h + 1) * D] * E[:, h:h + 1]        # float32 RN products
+        M[rows, g.col_idx, h * D:(h + 1) * D] = prod.astype(np.float64)
+    A = dense_adjacency(g.row_ptr, g.col_idx, g.n_src) > 0
+    val = M.max(axis=1)
+    arg = M.argmax(axis=1)
+    empty = ~A.any(axis=1)
+    val[empty], arg[empty] = 0.0, -1
+    assert np.array_equal(ref, val)
+    assert np.array_equal(au, arg)
+
+
+# ------------------------------------------------------------------ mlp
+@pytest.mark.parametrize("regime", [gen.INT, gen.REAL])
+def test_mlp_max_closed_form(regime):
+    """max_u ReLU((x_u + x_v) W) == ReLU(max_u (XW)[u] + (XW)[v]) exactly in the
+    reals (distributivity; ReLU(. + c) monotone).  SURVEY §8(c) pin table."""
+    g = small_graph(n=150, m=2000, seed=7)
+    d1, d2 = 8, 16
+    if regime == gen.INT:
+        X = gen.features((g.n_src, d1), 41, 0, gen.INT, lo=-8, hi=8)
+        W = gen.features((d1, d2), 41, 1, gen.INT, lo=-4, hi=4)
+    else:
+        X = gen.features((g.n_src, d1), 41, 0)
+        W = gen.features((d1, d2), 41, 1, gen.SCALED, scale=1 / np.sqrt(d1))
+    ref, ab, au, ae = oracle.spmm(g.row_ptr, g.col_idx, "mlp", "max", X, W=W)
+    P = X.astype(np.float64) @ W.astype(np.float64)
+    A = dense_adjacency(g.row_ptr, g.col_idx, g.n_src) > 0
+    Pm = np.where(A[:, :, None], P[None], -np.inf)
+    best = Pm.max(axis=1)
+    closed = np.maximum(best + P, 0.0)
+    empty = ~A.any(axis=1)
+    closed[empty] = 0.0
+    if regime == gen.INT:
+        assert np.array_equal(ref, closed)
+        # argmax: first max of the pre-activation if positive, else the row's first edge
+        first = np.array([g.col_idx[g.row_ptr[v]] if g.row_ptr[v + 1] > g.row_ptr[v] else -1
+                          for v in range(g.n_dst)])
+        am = Pm.argmax(axis=1)
+        exp_arg = np.where(best + P > 0, am, first[:, None])
+        exp_arg[empty] = -1
+        assert np.array_equal(au, exp_arg)
+    else:
+        np.testing.assert_allclose(ref, closed, rtol=0, atol=1e-12)
+    # abs-sum of the winning message: sum_k |(x_u + x_v)_k W_kj|
+    v = int(np.argmax(g.degrees()))
+    for j in range(d2):
+        u = au[v, j]
+        a = X[u].astype(np.float64) + X[v].astype(np.float64)
+        assert ab[v, j] == pytest.approx(np.abs(a * W[:, j].astype(np.float64)).sum(), rel=1e-12)
+
+
+def test_mlp_sum_brute_force():
+    g = small_graph(n=40, m=300, seed=3)
+    d1, d2 = 8, 5
+    X = gen.features((g.n_src, d1), 43, 0)
+    W = gen.features((d1, d2), 43, 1)
+    ref, _, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "mlp", "sum", X, W=W)
+    for v in range(g.n_dst):
+        acc = [0.0] * d2
+        for p in range(g.row_ptr[v], g.row_ptr[v + 1]):
+            u = g.col_idx[p]
+            for i in range(d2):
+                z = sum((float(X[u, k]) + float(X[v, k])) * float(W[k, i]) for k in range(d1))
+                acc[i] += max(z, 0.0)
+        np.testing.assert_allclose(ref[v], acc, rtol=1e-12, atol=1e-13)
+
+
+def test_mlp_x_dst_separate():
+    """X_dst enters only through x_v: mlp with W = I, X_dst = 0 is ReLU(copy_u max)."""
+    g = small_graph(n=60, m=500, seed=8)
+    d = 8
+    X = gen.features((g.n_src, d), 47, 0)
+    ref, _, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "mlp", "max", X, W=np.eye(d, dtype=np.float32),
+                               X_dst=np.zeros_like(X))
+    cm, _, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", "max", X)
+    assert np.array_equal(ref, np.maximum(cm, 0.0))
+
+
+@pytest.mark.parametrize("key", ["mlp_max", "mlp_relu"])
+def test_spec_mlp_examples(key):
+    ex = GOLD[key]
+    rp, ci = csr_from_edges(ex["n"], ex["edges"])
+    ref, _, au, _ = oracle.spmm(rp, ci, "mlp", "max", np.array(ex["X"], np.float32),
+                                W=np.array(ex["W"], np.float32))
+    assert np.array_equal(ref[1], np.array(ex["expected_row1"], np.float64))
+    if "expected_arg_u_row1" in ex:
+        assert list(au[1]) == ex["expected_arg_u_row1"]
+
+
+# ------------------------------------------------------------------ sddmm
+@pytest.mark.parametrize("H,D", [(1, 7), (4, 4), (8, 2)])
+def test_u_dot_v_complete_graph_is_dense(H, D):
+    n = 37
+    rp = np.arange(n + 1, dtype=np.int64) * n
+    ci = np.tile(np.arange(n, dtype=np.int32), n)
+    X = gen.features((n, H * D), 51, 0)
+    Y = gen.features((n, H * D), 51, 1)
+    ref, ab = oracle.sddmm(rp, ci, X, Y, H=H)
+    for h in range(H):
+        blk = slice(h * D, (h + 1) * D)
+        dense = Y[:, blk].astype(np.float64) @ X[:, blk].astype(np.float64).T   # [v, u]
+        np.testing.assert_allclose(ref[:, h].reshape(n, n), dense, rtol=1e-12, atol=1e-13)
+        dabs = np.abs(Y[:, blk].astype(np.float64)) @ np.abs(X[:, blk].astype(np.float64)).T
+        np.testing.assert_allclose(ab[:, h].reshape(n, n), dabs, rtol=1e-12, atol=1e-13)
+
+
+def test_spec_dot_examples():
+    ex = GOLD["dot"]
+    rp, ci = csr_from_edges(ex["n"], ex["edges"])
+    ref, _ = oracle.sddmm(rp, ci, np.array(ex["X"], np.float32))
+    assert ref.tolist() == ex["expected"]
+    ex = GOLD["orthogonal_dot"]
+    rp, ci = csr_from_edges(ex["n"], ex["edges"])
+    ref, _ = oracle.sddmm(rp, ci, np.array(ex["X"], np.float32))
+    assert ref.tolist() == ex["expected"]
+    ex = GOLD["multi_head_dot"]
+    rp, ci = csr_from_edges(2, [[0, 1]])
+    X = np.zeros((2, 6), np.float32)
+    X[0] = np.array(ex["src"], np.float32).reshape(-1)
+    X[1] = np.array(ex["dst"], np.float32).reshape(-1)
+    ref, _ = oracle.sddmm(rp, ci, X, H=ex["H"])
+    assert ref[0].tolist() == ex["expected"]
+
+
+def test_sddmm_rows_subset_matches_full():
+    g = small_graph()
+    X = gen.features((g.n_src, 8), 53, 0)
+    full, _ = oracle.sddmm(g.row_ptr, g.col_idx, X, H=2)
+    rows = np.array([5, 0, 100, 3], np.int64)
+    sub, _ = oracle.sddmm(g.row_ptr, g.col_idx, X, H=2, rows=rows)
+    assert np.array_equal(sub, full[oracle.edge_positions(g.row_ptr, rows)])
+
+
+@pytest.mark.parametrize("regime", [gen.INT, gen.REAL])
+def test_adjoint_identity(regime):
+    """Gradient duality: <G, spmm_{u_mul_e,sum}(A, X, a)> ==
+    <a, sddmm_{u_dot_v}(X_src = X, Y_dst = G)>, per head."""
+    g = small_graph()
+    H, D = 2, 4
+    lo, hi = -5, 5
+    X = gen.features((g.n_src, H * D), 61, 0, regime, lo=lo, hi=hi)
+    G = gen.features((g.n_dst, H * D), 61, 1, regime, lo=lo, hi=hi)
+    a = gen.features((g.nnz, H), 61, 2, gen.INT if regime == gen.INT else gen.UNIT, lo=0, hi=4)
+    out, _, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", "sum", X, H=H, E=a)
+    s, _ = oracle.sddmm(g.row_ptr, g.col_idx, X, G, H=H)
+    lhs = float((G.astype(np.float64) * out).sum())
+    rhs = float((a.astype(np.float64) * s).sum())
+    if regime == gen.INT:
+        assert lhs == rhs
+    else:
+        assert lhs == pytest.approx(rhs, rel=1e-12, abs=1e-9)
+
+
+# ------------------------------------------------------------------ edge softmax
+def test_edge_softmax_invariants():
+    g = small_graph()
+    H = 4
+    S = gen.features((g.nnz, H), 71, 0)
+    al = oracle.edge_softmax(g.row_ptr, S, H=H)
+    rows = edge_rows(g.row_ptr)
+    sums = np.zeros((g.n_dst, H))
+    np.add.at(sums, rows, al)
+    nonempty = g.degrees() > 0
+    np.testing.assert_allclose(sums[nonempty], 1.0, rtol=0, atol=1e-13)
+    # shift invariance s -> s + c_v
+    c = gen.features((g.n_dst,), 71, 1, gen.INT, lo=-3, hi=3)
+    al2 = oracle.edge_softmax(g.row_ptr, S + c[rows][:, None], H=H)
+    np.testing.assert_allclose(al2, al, rtol=1e-6, atol=0)
+    # constant scores -> 1/deg; degree-1 rows -> exactly 1
+    al3 = oracle.edge_softmax(g.row_ptr, np.full((g.nnz, H), 0.25, np.float32), H=H)
+    np.testing.assert_allclose(al3, 1.0 / g.degrees()[rows][:, None] * np.ones((1, H)), rtol=1e-15)
+    d1 = g.degrees()[rows] == 1
+    assert (al[d1] == 1.0).all()
+
+
+def test_edge_softmax_matches_torch_dense():
+    import torch
+    g = small_graph(n=64, m=700, seed=12)
+    H = 2
+    S = gen.features((g.nnz, H), 73, 0) * 4
+    eid = gen.permutation(g.nnz, 3).astype(np.int32)
+    al = oracle.edge_softmax(g.row_ptr, S, H=H, eid=eid)
+    rows = edge_rows(g.row_ptr)
+    for h in range(H):
+        M = torch.full((g.n_dst, g.n_src), float("-inf"), dtype=torch.float64)
+        M[torch.from_numpy(rows), torch.from_numpy(g.col_idx.astype(np.int64))] = \
+            torch.from_numpy(S[eid, h].astype(np.float64))
+        P = torch.softmax(M, dim=1)
+        got = P[torch.from_numpy(rows), torch.from_numpy(g.col_idx.astype(np.int64))].numpy()
+        np.testing.assert_allclose(al[:, h], got, rtol=1e-12, atol=0)
