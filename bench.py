@@ -1,0 +1,494 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for the FeatGraph hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: dst-row sharded)
+
+Workload (BASELINE.json metric "gSpMM/gSDDMM ms/op & HBM GB/s vs ~8 TB/s, feat
+32-512"; north-star target graph): the reddit-shaped synthetic graph
+(232,965 vertices, 114,615,892 edges, lognormal in-degrees, Chung-Lu sources;
+DESIGN.md "Input recipe").  One STEP = one pass of every SURVEY §8(a) row over
+that graph, fp32:
+    a1  gSpMM copy_u-sum   F=512              (GCN aggregation, Table tab:gpu-kernel(a))
+    a4  gSDDMM u_dot_v     H=1, F=512         (dot-product attention, tab:gpu-kernel(c))
+    a4  gSDDMM u_dot_v     H=8, D=32          (GAT scores, BASELINE configs[2])
+    a5  edge softmax       H=8                (in place)
+    a2  gSpMM u_mul_e-sum  H=8, D=32          (GAT aggregation)
+    a1  gSpMM copy_u-max   F=128 + arg_u/arg_e
+    a3  gSpMM mlp-max      d1=8, d2=128 + args (MLP aggregation, tab:gpu-kernel(b))
+    a6  (N > 1) NCCL all-gather of every source-feature tensor (row shards)
+a0 (fg_graph_create) is per-topology preprocessing, amortised and
+outside the step.
+
+value = algorithmic bytes of the step (SURVEY §8(d) gather model, summed over
+ops, whole graph) / device time per step (CUDA events on the launching stream,
+max over ranks), in GB/s.  L2 is flushed (256 MB write) before every timed
+step, outside the timed events.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GRAPH = "reddit"
+F_GCN, F_DOT, H_GAT, D_GAT, F_MAX, D1, D2 = 512, 512, 8, 32, 128, 8, 128
+OPS = ["spmm_copy_u_sum_F512", "sddmm_u_dot_v_H1_F512", "sddmm_u_dot_v_H8_D32", "edge_softmax_H8",
+       "spmm_u_mul_e_sum_H8_D32", "spmm_copy_u_max_F128_args", "spmm_mlp_max_d8_d128_args"]
+DOMINANT = "spmm_copy_u_sum_F512"
+
+
+def metric_name() -> str:
+    try:
+        return json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+    except Exception:
+        return "gSpMM/gSDDMM ms/op & HBM GB/s vs ~8 TB/s, feat 32-512, at 1/2/4/8 B200"
+
+
+def op_bytes(n_rows: int, m: int) -> dict:
+    """Algorithmic bytes per op (SURVEY §8(d) gather model; row_ptr is int64):
+    index arrays + per-edge source-row gathers + per-row reads/writes."""
+    idx = 8 * (n_rows + 1) + 4 * m
+    return {
+        "spmm_copy_u_sum_F512": idx + 4 * m * F_GCN + 4 * n_rows * F_GCN,
+        "sddmm_u_dot_v_H1_F512": idx + 4 * m * F_DOT + 4 * n_rows * F_DOT + 4 * m,
+        "sddmm_u_dot_v_H8_D32": idx + 4 * m * H_GAT * D_GAT + 4 * n_rows * H_GAT * D_GAT + 4 * m * H_GAT,
+        "edge_softmax_H8": 8 * (n_rows + 1) + 2 * 4 * m * H_GAT,
+        "spmm_u_mul_e_sum_H8_D32": idx + 4 * m * H_GAT * D_GAT + 4 * m * H_GAT + 4 * n_rows * H_GAT * D_GAT,
+        "spmm_copy_u_max_F128_args": idx + 4 * m * F_MAX + 3 * 4 * n_rows * F_MAX,
+        "spmm_mlp_max_d8_d128_args": idx + 4 * m * D1 + 4 * n_rows * D1 + 4 * D1 * D2 + 3 * 4 * n_rows * D2,
+    }
+
+
+def mlp_flops(m: int) -> int:
+    return 2 * m * D1 * D2
+
+
+# ----------------------------------------------------------------- inputs (host, seeded)
+def make_inputs(g):
+    import gen
+    s = gen.feature_seed(GRAPH)
+    n = g.n_dst
+    return {
+        "X512": gen.features((n, F_GCN), s, 0),
+        "X256": gen.features((n, H_GAT * D_GAT), s, 1) * np.float32(0.25),
+        "X128": gen.features((n, F_MAX), s, 2),
+        "X8": gen.features((n, D1), s, 3),
+        "W": gen.features((D1, D2), s, 4, gen.SCALED, scale=1 / np.sqrt(D1)),
+    }
+
+
+# ----------------------------------------------------------------- clocks sampler
+class Clocks:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, dev_id: str):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", dev_id, "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def gpu_id_for_smi(local_rank: int) -> str:
+    import torch
+    try:
+        u = str(torch.cuda.get_device_properties(local_rank).uuid)
+        if u and u != "None":
+            return u if u.startswith("GPU-") else "GPU-" + u
+    except Exception:
+        pass
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        return vis.split(",")[local_rank]
+    return str(local_rank)
+
+
+# ----------------------------------------------------------------- the GPU step
+class Step:
+    """Device-resident state of one rank and the enqueue of one hot-path step."""
+
+    def __init__(self, g, shard, host, comm, stream):
+        import torch
+        import paper_2008_11359_b200 as fgp
+        self.fgp, self.torch = fgp, torch
+        self.shard, self.comm, self.stream = shard, comm, stream
+        self.n = g.n_dst
+        nl = shard.n_local if shard else g.n_dst
+        self.nl = nl
+        lo = shard.lo if shard else 0
+        dev = torch.device("cuda")
+        rp = shard.row_ptr if shard else g.row_ptr
+        ci = shard.col_idx if shard else g.col_idx
+        self.rp_d = torch.from_numpy(rp).to(dev)
+        self.ci_d = torch.from_numpy(ci).to(dev)
+        self.G = fgp.Graph(self.rp_d, self.ci_d, n_src=g.n_src, validate=True)
+        self.m = int(rp[-1])
+        self.lo = lo
+        # full-size source feature buffers (the all-gather target when sharded)
+        self.X = {k: torch.from_numpy(host[k]).to(dev) for k in ("X512", "X256", "X128", "X8")}
+        self.W = torch.from_numpy(host["W"]).to(dev)
+        f = lambda *s: torch.empty(*s, device=dev)  # noqa: E731
+        i = lambda *s: torch.empty(*s, dtype=torch.int32, device=dev)  # noqa: E731
+        self.out512 = f(nl, F_GCN)
+        self.s1 = f(self.m, 1)
+        self.s8 = f(self.m, H_GAT)
+        self.o256 = f(nl, H_GAT * D_GAT)
+        self.o128, self.au128, self.ae128 = f(nl, F_MAX), i(nl, F_MAX), i(nl, F_MAX)
+        self.omlp, self.aumlp, self.aemlp = f(nl, D2), i(nl, D2), i(nl, D2)
+        self.ev = None
+
+    def ydst(self, k):
+        return self.X[k][self.lo:self.lo + self.nl]
+
+    def allgather(self):
+        if self.comm is None:
+            return
+        for k in ("X512", "X256", "X128", "X8"):
+            x = self.X[k]
+            self.comm.allgather_rows(self.shard.offsets, x[self.lo:self.lo + self.nl], x, stream=self.stream)
+
+    def enqueue(self, events=None):
+        """All ops of one step on self.stream; events[i] recorded before op i (and at the end)."""
+        fgp, st = self.fgp, self.stream
+        rec = (lambda i: events[i].record(st)) if events is not None else (lambda i: None)
+        G, X = self.G, self.X
+        rec(0)
+        self.allgather()
+        rec(1)
+        fgp.spmm(G, "copy_u", "sum", X["X512"], out=self.out512, stream=st)
+        rec(2)
+        fgp.sddmm(G, X["X512"], self.ydst("X512"), H=1, out=self.s1, stream=st)
+        rec(3)
+        fgp.sddmm(G, X["X256"], self.ydst("X256"), H=H_GAT, out=self.s8, stream=st)
+        rec(4)
+        fgp.edge_softmax(G, self.s8, H=H_GAT, out=self.s8, stream=st)
+        rec(5)
+        fgp.spmm(G, "u_mul_e", "sum", X["X256"], H=H_GAT, E=self.s8, out=self.o256, stream=st)
+        rec(6)
+        fgp.spmm(G, "copy_u", "max", X["X128"], out=self.o128, arg_u=self.au128, arg_e=self.ae128, stream=st)
+        rec(7)
+        fgp.spmm(G, "mlp", "max", X["X8"], W=self.W, X_dst=self.ydst("X8"), out=self.omlp, arg_u=self.aumlp,
+                 arg_e=self.aemlp, stream=st)
+        rec(8)
+
+    LAUNCHES_PER_STEP = 7   # libfg kernels per step (one per fg_* call)
+
+    def outputs(self):
+        return [self.out512, self.s1, self.o256, self.o128, self.au128, self.ae128, self.omlp, self.aumlp,
+                self.aemlp]
+
+
+# ----------------------------------------------------------------- CPU oracle leg
+def oracle_sample_step(g, host, rows):
+    """Run every op of the step with the fp64 oracle on the sub-graph of `rows`
+    (their in-edges, global source ids).  Returns (seconds, bytes, threads)."""
+    import oracle
+    rows = np.sort(np.asarray(rows, np.int64))
+    deg = g.row_ptr[rows + 1] - g.row_ptr[rows]
+    rp = np.zeros(rows.size + 1, np.int64)
+    np.cumsum(deg, out=rp[1:])
+    pos = oracle.edge_positions(g.row_ptr, rows)
+    ci = g.col_idx[pos]
+    X512, X256, X128, X8, W = host["X512"], host["X256"], host["X128"], host["X8"], host["W"]
+    t0 = time.perf_counter()
+    oracle.spmm(rp, ci, "copy_u", "sum", X512)
+    oracle.sddmm(rp, ci, X512, X512[rows], H=1)
+    s8, _ = oracle.sddmm(rp, ci, X256, X256[rows], H=H_GAT)
+    a8 = oracle.edge_softmax(rp, s8.astype(np.float32), H=H_GAT)
+    oracle.spmm(rp, ci, "u_mul_e", "sum", X256, H=H_GAT, E=a8.astype(np.float32))
+    oracle.spmm(rp, ci, "copy_u", "max", X128)
+    oracle.spmm(rp, ci, "mlp", "max", X8, W=W, X_dst=X8[rows])
+    dt = time.perf_counter() - t0
+    b = sum(op_bytes(rows.size, int(rp[-1])).values())
+    return dt, b, int(rp[-1])
+
+
+def sample_rows(g, edge_budget: int, seed: int = 11) -> np.ndarray:
+    import gen
+    perm = gen.permutation(g.n_dst, seed, 31)
+    deg = np.diff(g.row_ptr)[perm]
+    k = int(np.searchsorted(np.cumsum(deg), edge_budget)) + 1
+    return perm[:max(1, min(k, g.n_dst))]
+
+
+def cpu_threads() -> int:
+    try:
+        return int(os.environ.get("OMP_NUM_THREADS") or len(os.sched_getaffinity(0)))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def calibrate_sample(g, host, target_s: float):
+    rows = sample_rows(g, 20000)
+    dt, _, _ = oracle_sample_step(g, host, rows)
+    budget = int(20000 * max(1.0, target_s / max(dt, 1e-3)))
+    return sample_rows(g, min(budget, g.nnz))
+
+
+def cpu_baseline(g, host, target_s: float = 12.0) -> dict:
+    rows = calibrate_sample(g, host, target_s)
+    dt, b, me = oracle_sample_step(g, host, rows)
+    return {"value": b / dt / 1e9, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle",
+            "sample": f"all 7 ops of the step on {rows.size} seeded-random destination rows "
+                      f"({me} in-edges, {me / g.nnz:.2%} of the graph), fp64 C oracle, OpenMP over rows; "
+                      f"{dt:.1f} s", "seconds": dt}
+
+
+# ----------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--uniform-sources", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    import gen
+    import paper_2008_11359_b200 as fgp
+    from paper_2008_11359_b200.shard import make_shard
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    g = gen.make_graph(GRAPH, uniform_sources=args.uniform_sources)
+    host = make_inputs(g)
+    comm, shard = None, None
+    if world > 1:
+        shard = make_shard(g.row_ptr, g.col_idx, rank, world)
+        uid = [fgp.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = fgp.Comm(uid[0], world, rank)
+    stream = torch.cuda.Stream()
+    S = Step(g, shard, host, comm, stream)
+    S.total_bytes = sum(op_bytes(g.n_dst, g.nnz).values())
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.fill_(1.0)
+            S.enqueue()
+    sync_all()
+    nev = 9
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
+    clocks = Clocks(gpu_id_for_smi(local_rank)) if rank == 0 else None
+    time.sleep(0.3 if rank == 0 else 0)
+    sync_all()
+    with torch.cuda.stream(stream):
+        for k in range(args.steps):
+            flush.fill_(float(k))        # L2 flush outside the timed events
+            S.enqueue(evs[k])
+    sync_all()
+    clk = clocks.stop() if clocks else None
+    step_ms = np.array([evs[k][0].elapsed_time(evs[k][8]) for k in range(args.steps)])
+    op_ms = {OPS[i]: float(np.mean([evs[k][i + 1].elapsed_time(evs[k][i + 2]) for k in range(args.steps)]))
+             for i in range(7)}
+    ag_ms = float(np.mean([evs[k][0].elapsed_time(evs[k][1]) for k in range(args.steps)]))
+    ms = float(step_ms.mean())
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # end-to-end through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(S, host, args, world, sync_all, flush)
+
+    total_bytes = sum(op_bytes(g.n_dst, g.nnz).values())
+    local_bytes = op_bytes(S.nl, S.m)
+    ob_full = op_bytes(g.n_dst, g.nnz)
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(g, host)
+    dom_ms = op_ms[DOMINANT]
+    achieved = local_bytes[DOMINANT] / (dom_ms * 1e-3) / 1e9
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(DOMINANT, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": metric_name(),
+        "value": total_bytes / (ms * 1e-3) / 1e9,
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {
+            "workload": "reddit-shaped synthetic graph (232,965 v, 114,615,892 e; lognormal sigma=1.2, "
+                        "Chung-Lu sources" + (", UNIFORM sources" if args.uniform_sources else "") +
+                        "): copy_u-sum F512, u_dot_v H1 F512, GAT (u_dot_v H8D32 -> edge_softmax -> "
+                        "u_mul_e-sum), copy_u-max F128+argmax, mlp-max d1=8 d2=128+argmax",
+            "graph": GRAPH, "n": g.n_dst, "nnz": g.nnz,
+            "parallelism": f"dst-row shards x{world} + NCCL all-gather of X" if world > 1 else "single GPU",
+            "l2": "flushed before every timed step (256 MB write, outside the events)",
+            "bytes_per_step": total_bytes,
+        },
+        "ops_ms": {k: round(v, 4) for k, v in op_ms.items()},
+        "ops_gbs": {k: round(ob_full[k] / world / (op_ms[k] * 1e-3) / 1e9, 1) for k in OPS} if world == 1 else
+        {k: round(local_bytes[k] / (op_ms[k] * 1e-3) / 1e9, 1) for k in OPS},
+        "allgather_ms": round(ag_ms, 4) if world > 1 else 0.0,
+        "mlp_tflops": round(mlp_flops(S.m) / (op_ms["spmm_mlp_max_d8_d128_args"] * 1e-3) / 1e12, 2),
+        "roofline": {"kernel": DOMINANT, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": Step.LAUNCHES_PER_STEP * args.steps,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(S, host, args, world, sync_all, flush):
+    """Same step through the public API from pinned HOST buffers: H2D of the
+    step's inputs, the step, D2H of every op's result, all inside the events."""
+    import torch
+    st = S.stream
+    lo, nl = S.lo, S.nl
+    ins = {k: torch.from_numpy(np.ascontiguousarray(host[k][lo:lo + nl])).pin_memory() for k in
+           ("X512", "X256", "X128", "X8")}
+    w_h = torch.from_numpy(host["W"]).pin_memory()
+    outs_d = S.outputs()
+    outs_h = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs_d]
+    h2d = sum(t.numel() * t.element_size() for t in ins.values()) + w_h.numel() * 4
+    d2h = sum(t.numel() * t.element_size() for t in outs_h)
+    k_steps = max(1, min(args.steps, 5))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k_steps + 1)]
+    with torch.cuda.stream(st):
+        for k in range(k_steps + 1):
+            flush.fill_(float(k))
+            evs[k][0].record(st)
+            for key, t in ins.items():
+                S.X[key][lo:lo + nl].copy_(t, non_blocking=True)
+            S.W.copy_(w_h, non_blocking=True)
+            S.enqueue()
+            for od, oh in zip(outs_d, outs_h):
+                oh.copy_(od, non_blocking=True)
+            evs[k][1].record(st)
+    sync_all()
+    ms = float(np.mean([evs[k][0].elapsed_time(evs[k][1]) for k in range(1, k_steps + 1)]))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_bytes = S.total_bytes
+    return {"value": total_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s",
+            "ms_per_step": ms, "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+            "steps": k_steps}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the fp64 CPU oracle (this tier's reference arm), on
+    bounded row samples of the same workload, on the host cores."""
+    if world > 1 and rank != 0:
+        return
+    import gen
+    g = gen.make_graph(GRAPH, uniform_sources=args.uniform_sources)
+    host = make_inputs(g)
+    rows = calibrate_sample(g, host, target_s=4.0)
+    for _ in range(args.warmup):
+        oracle_sample_step(g, host, rows)
+    dts, b, me = [], 0, 0
+    for _ in range(args.steps):
+        dt, b, me = oracle_sample_step(g, host, rows)
+        dts.append(dt)
+    dt = float(np.mean(dts))
+    value = b / dt / 1e9
+    sample = (f"each step: all 7 ops on {rows.size} seeded-random destination rows ({me} in-edges, "
+              f"{me / g.nnz:.2%} of the graph); fp64 C oracle, OpenMP over rows")
+    line = {
+        "metric": metric_name(), "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "reddit-shaped synthetic graph, same 7-op step as the GPU arm, bounded row sample",
+                   "graph": GRAPH, "n": g.n_dst, "nnz": g.nnz, "sample_rows": int(rows.size),
+                   "sample_edges": int(me)},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

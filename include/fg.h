@@ -1,0 +1,204 @@
+/*
+ * fg.h -- C ABI of libfg.so, the B200-native (sm_100a) hot path of FeatGraph
+ * (Hu et al., "FeatGraph: A Flexible and Efficient Backend for Graph Neural
+ * Network Systems", SC20, arXiv 2008.11359).
+ *
+ * The paper's interface (§3.2):
+ *   featgraph.spmat(shape=(n,n), nnz=m)
+ *   featgraph.spmm(A, msgfunc, aggregation, target, fds)
+ *   featgraph.sddmm(A, edgefunc, target, fds)
+ * maps to fg_graph_create / fg_spmm / fg_sddmm below.  `target` is always
+ * sm_100a and the feature-dimension schedule (FDS) is internal to the library
+ * (launch configuration chosen per (F, degree bin)); the UDFs are the fixed
+ * enums fg_msg_op / fg_edge_op, which cover every UDF the paper evaluates
+ * (Fig. 3a copy-src, Fig. 3b MLP, Fig. 5 (multi-head) dot product, and the DGL
+ * vertex-x-edge builtin of P:375).  Edge softmax (fg_edge_softmax) is not in
+ * the paper; it is the standard GAT normalisation the paper's GAT layer needs
+ * (P:983).
+ *
+ * CONVENTIONS (all functions)
+ *  - No C++ or CUDA types cross this boundary: tensors are plain pointers, sizes
+ *    are int64_t, a stream is an opaque `fg_stream` (a cudaStream_t / CUstream;
+ *    NULL = the legacy default stream).
+ *  - Graph: destination-major CSR (Eq. (3) P:158 H_V = A X_V
+ *    "rows in the adjacency matrix"): row v = [row_ptr[v], row_ptr[v+1]) lists
+ *    the sources u = col_idx[p] of the in-edges u -> v, strictly ascending
+ *    (no duplicate edges; self-loops allowed).  Edge id of CSR position p is
+ *    eid[p] (eid == NULL: identity).  Edge tensors (E, SDDMM output, scores)
+ *    are indexed by edge id.
+ *  - Every tensor pointer passed to fg_spmm / fg_sddmm / fg_edge_softmax /
+ *    fg_graph_create is a DEVICE pointer owned by the caller; the library never
+ *    frees caller memory.  Float tensors are fp32, row-major, and must be
+ *    16-byte aligned (128-bit lane accesses); F % 4 == 0 (F = H*D, or d2).
+ *  - fg_graph borrows row_ptr / col_idx / eid: they must stay alive and
+ *    unmodified until fg_graph_destroy.  The handle owns only derived tables.
+ *  - Calls are asynchronous on `stream` except fg_graph_create (which
+ *    synchronises once: it reads row_ptr back to build the degree bins).
+ *    Argument errors are detected on the host BEFORE any launch: a non-OK
+ *    status means nothing was launched and outputs are untouched.  Device
+ *    faults surface at the caller's next synchronisation.
+ *  - Outputs are fully overwritten, never accumulated into.
+ *  - Results are deterministic: no floating-point atomics; reruns are bitwise
+ *    identical.
+ *  - A handle is immutable after creation: concurrent calls on different
+ *    streams are safe.  fg_last_error() is thread-local.
+ */
+#ifndef FG_H_
+#define FG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FG_ABI_VERSION 1
+
+typedef enum {
+    FG_OK = 0,
+    FG_EINVAL = 1,        /* null pointer, bad enum, misaligned pointer */
+    FG_ESHAPE = 2,        /* inconsistent or unsupported dimensions */
+    FG_EUNSUPPORTED = 3,  /* valid request, combination not implemented */
+    FG_EGRAPH = 4,        /* CSR invariant violated (validate = 1) */
+    FG_ECUDA = 5,         /* CUDA runtime / launch error */
+    FG_ENOMEM = 6,        /* device or host allocation failed */
+    FG_ENCCL = 7          /* NCCL error (multi-GPU calls) */
+} fg_status;
+
+/* Message functions phi of Eq. (1). */
+typedef enum {
+    FG_MSG_COPY_U = 0,   /* phi = x_u                       Fig. 3a */
+    FG_MSG_U_MUL_E = 1,  /* phi[h,d] = x_u[h,d] * x_uv[h]   DGL builtin P:375; GAT P:983 */
+    FG_MSG_MLP = 2       /* phi = ReLU((x_u + x_v) W)       Fig. 3b */
+} fg_msg_op;
+
+/* Aggregations (+) of Eq. (1): sum (Fig. 3a), max (Fig. 1). */
+typedef enum { FG_REDUCE_SUM = 0, FG_REDUCE_MAX = 1 } fg_reduce_op;
+
+/* Edge functions psi of Eq. (2). */
+typedef enum {
+    FG_EDGE_U_DOT_V = 0  /* psi[h] = sum_d x_u[h,d] y_v[h,d]   Eq. (4); Fig. 5 */
+} fg_edge_op;
+
+typedef struct fg_graph fg_graph;          /* opaque, immutable after create */
+typedef struct CUstream_st* fg_stream;      /* == cudaStream_t */
+
+/* ---------------------------------------------------------------- graph */
+/*
+ * fg_graph_create -- featgraph.spmat.  Builds the per-topology tables
+ * (degree-sorted row order, degree bins, SDDMM edge-chunk table), amortised
+ * over calls as the paper amortises per-topology code generation.
+ *   n_dst, n_src : rows / columns of A (n_dst >= 0, n_src >= 0)
+ *   nnz          : number of edges, 0 <= nnz < 2^31
+ *   row_ptr      : device int64[n_dst+1]
+ *   col_idx      : device int32[nnz]   (may be NULL iff nnz == 0)
+ *   eid          : device int32[nnz] or NULL (identity)
+ *   validate     : nonzero -> check row_ptr[0] == 0, row_ptr non-decreasing,
+ *                  row_ptr[n_dst] == nnz, 0 <= col_idx < n_src strictly
+ *                  ascending per row, eid a permutation of [0,nnz); violations
+ *                  return FG_EGRAPH (detail in fg_last_error()).
+ *   stream       : stream used for the (synchronous) preprocessing.
+ *   out          : receives the handle (set only on FG_OK).
+ */
+fg_status fg_graph_create(int64_t n_dst, int64_t n_src, int64_t nnz, const int64_t* row_ptr,
+                          const int32_t* col_idx, const int32_t* eid, int validate,
+                          fg_stream stream, fg_graph** out);
+fg_status fg_graph_destroy(fg_graph* g);
+
+/* Host-side description of a handle (tests / tooling). */
+typedef struct {
+    int64_t n_dst, n_src, nnz;
+    int64_t max_degree;
+    int64_t n_empty_rows;     /* rows of degree 0 */
+    int64_t n_sddmm_units;    /* (row, edge chunk) work units of fg_sddmm */
+    int64_t device_bytes;     /* bytes of derived tables owned by the handle */
+} fg_graph_info_t;
+fg_status fg_graph_info(const fg_graph* g, fg_graph_info_t* info);
+
+/* ---------------------------------------------------------------- gSpMM */
+/*
+ * fg_spmm -- featgraph.spmm(A, msgfunc, aggregation), Eq. (1):
+ *     out[v] = (+)_{u -> v} phi(x_u, x_v, x_uv)
+ *
+ *   msg = FG_MSG_COPY_U   : X [n_src][H*D]; E, W, X_dst NULL; d_in = 0.
+ *   msg = FG_MSG_U_MUL_E  : X [n_src][H*D]; E [nnz][H] indexed by edge id.
+ *   msg = FG_MSG_MLP      : H == 1, D == d2 (output width); X [n_src][d_in],
+ *                           W [d_in][d2], X_dst [n_dst][d_in] (NULL -> X, which
+ *                           requires n_src == n_dst); 1 <= d_in <= 32 (d_in = 8
+ *                           in the paper).  ReLU after the full
+ *                           contraction (Fig. 3b).  Runs on the
+ *                           tcgen05 tensor cores (split-TF32).
+ *   out   : [n_dst][H*D] fp32, fully overwritten.
+ *   red   : FG_REDUCE_SUM or FG_REDUCE_MAX (elementwise per feature column).
+ *   arg_u, arg_e : max only, each optional (NULL); int32 [n_dst][H*D]:
+ *           source id / edge id of the winning edge.  Ties -> lowest CSR
+ *           position.  Must be NULL for sum.
+ *   Empty rows: out = +0.0 and arg = -1.
+ *   workspace / workspace_bytes: scratch from fg_spmm_workspace_size (may be
+ *           NULL when that size is 0).
+ *   Errors: FG_EINVAL (null/misaligned pointer, bad enum, arg_* with sum),
+ *           FG_ESHAPE (H < 1, D < 1, (H*D) % 4 != 0, mlp with H != 1 or d_in
+ *           out of range, u_mul_e/copy_u with d_in != 0), FG_ECUDA.
+ */
+fg_status fg_spmm_workspace_size(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D,
+                                 int d_in, size_t* bytes);
+fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D,
+                  const float* X, const float* E, const float* W, int d_in, const float* X_dst,
+                  float* out, int32_t* arg_u, int32_t* arg_e, void* workspace,
+                  size_t workspace_bytes, fg_stream stream);
+
+/* ---------------------------------------------------------------- gSDDMM */
+/*
+ * fg_sddmm -- featgraph.sddmm(A, edgefunc), Eq. (2)/(4):
+ *     out[eid(p)][h] = sum_{d<D} X[u][h][d] * Y[v][h][d]   for every edge p = (u -> v)
+ *   X : [n_src][H][D];  Y : [n_dst][H][D] (may equal X: Eq. (4) uses X_V on
+ *       both sides);  out : [nnz][H], fully overwritten.
+ *   Heads are independent reductions (Fig. 5b).  Requires (H*D) % 4 == 0 and,
+ *   for H > 1, D % 4 == 0 with D/4 a power of two (else FG_ESHAPE).
+ */
+fg_status fg_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, const float* X, const float* Y,
+                   float* out, fg_stream stream);
+
+/* ---------------------------------------------------------------- edge softmax */
+/*
+ * fg_edge_softmax -- per destination v and head h, over the in-edges of v:
+ *     alpha[e][h] = exp(s[e][h] - max_row) / sum_row exp(s[.][h] - max_row)
+ *   scores, out : [nnz][H] indexed by edge id; out may alias scores (in place).
+ *   Not in the paper (GAT normalisation).
+ */
+fg_status fg_edge_softmax(const fg_graph* g, int H, const float* scores, float* out,
+                          fg_stream stream);
+
+/* ---------------------------------------------------------------- multi-GPU */
+/*
+ * Destination-row sharding (one process per GPU).  Each rank
+ * owns rows [lo, hi) of A and of X (shard_offsets[r] .. shard_offsets[r+1]);
+ * its local graph keeps GLOBAL source ids.  Before a local fg_spmm / fg_sddmm
+ * the source features are all-gathered over NVLink with NCCL.
+ *
+ * fg_comm_init: communicator from an ncclUniqueId (128 bytes) the caller
+ *   exchanged out of band (torch.distributed broadcast).  NCCL is loaded at
+ *   run time (libnccl.so.2); FG_ENCCL if it is unavailable.
+ * fg_comm_unique_id: fills 128 bytes with a fresh ncclUniqueId (rank 0).
+ * fg_allgather_rows: X_full[shard_offsets[r] + i][:] = rank r's X_local[i][:]
+ *   for every rank r (an all-gather-v of row blocks of `row_elems` fp32 each),
+ *   enqueued on `stream`.  X_local may point inside X_full at this rank's block
+ *   (in-place).  shard_offsets is a HOST int64[nranks+1].
+ */
+typedef struct fg_comm fg_comm;
+fg_status fg_comm_unique_id(void* unique_id_128);
+fg_status fg_comm_init(const void* unique_id_128, int nranks, int rank, fg_comm** out);
+fg_status fg_comm_destroy(fg_comm* c);
+fg_status fg_allgather_rows(fg_comm* c, const int64_t* shard_offsets, int64_t row_elems,
+                            const float* X_local, float* X_full, fg_stream stream);
+
+/* ---------------------------------------------------------------- errors */
+const char* fg_status_string(fg_status s);
+const char* fg_last_error(void);   /* thread-local detail of the last non-OK status */
+int fg_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FG_H_ */

@@ -1,0 +1,8 @@
+"""paper_2008_11359_b200 -- B200-native (sm_100a) gSpMM / gSDDMM / edge softmax,
+the data-parallel hot path of FeatGraph (SC20, arXiv 2008.11359).
+
+The product is libfg.so (C ABI, include/fg.h); this package is its thin
+binding (fg.py) plus the in-tree build (build.py) and the dst-row sharding
+helpers (shard.py).
+"""
+from .fg import (FGError, Graph, Comm, comm_unique_id, edge_softmax, lib, sddmm, spmm)  # noqa: F401

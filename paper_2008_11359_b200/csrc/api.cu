@@ -1,0 +1,118 @@
+// api.cu -- the C ABI of include/fg.h: argument validation (host, before any
+// launch) and dispatch to the sm_100a kernels.
+#include <cstdarg>
+#include <cstdio>
+
+#include "fg_internal.h"
+
+namespace {
+thread_local char g_err[512] = "";
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+}  // namespace
+
+namespace fgk {
+fg_status set_error(fg_status s, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+fg_status check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(FG_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return FG_OK;
+}
+}  // namespace fgk
+
+using fgk::set_error;
+
+extern "C" const char* fg_status_string(fg_status s) {
+    switch (s) {
+        case FG_OK: return "FG_OK";
+        case FG_EINVAL: return "FG_EINVAL: invalid argument (null/misaligned pointer or bad enum)";
+        case FG_ESHAPE: return "FG_ESHAPE: inconsistent or unsupported dimensions";
+        case FG_EUNSUPPORTED: return "FG_EUNSUPPORTED: combination not implemented";
+        case FG_EGRAPH: return "FG_EGRAPH: CSR invariant violated";
+        case FG_ECUDA: return "FG_ECUDA: CUDA error";
+        case FG_ENOMEM: return "FG_ENOMEM: out of memory";
+        case FG_ENCCL: return "FG_ENCCL: NCCL error";
+    }
+    return "unknown fg_status";
+}
+
+extern "C" const char* fg_last_error(void) { return g_err; }
+extern "C" int fg_abi_version(void) { return FG_ABI_VERSION; }
+
+extern "C" fg_status fg_spmm_workspace_size(const fg_graph* g, fg_msg_op, fg_reduce_op, int, int, int,
+                                            size_t* bytes) {
+    if (!g || !bytes) return set_error(FG_EINVAL, "fg_spmm_workspace_size: NULL argument");
+    *bytes = 0;   // heavy rows combine on chip (CTA per row); no scratch needed
+    return FG_OK;
+}
+
+extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D,
+                             const float* X, const float* E, const float* W, int d_in, const float* X_dst,
+                             float* out, int32_t* arg_u, int32_t* arg_e, void* workspace,
+                             size_t workspace_bytes, fg_stream stream) {
+    (void)workspace; (void)workspace_bytes;
+    if (!g) return set_error(FG_EINVAL, "fg_spmm: NULL graph");
+    if (msg != FG_MSG_COPY_U && msg != FG_MSG_U_MUL_E && msg != FG_MSG_MLP)
+        return set_error(FG_EINVAL, "fg_spmm: bad msg op %d", int(msg));
+    if (red != FG_REDUCE_SUM && red != FG_REDUCE_MAX) return set_error(FG_EINVAL, "fg_spmm: bad reduce op %d", int(red));
+    if (red == FG_REDUCE_SUM && (arg_u || arg_e)) return set_error(FG_EINVAL, "fg_spmm: arg_u/arg_e must be NULL for sum");
+    if (H < 1 || D < 1) return set_error(FG_ESHAPE, "fg_spmm: H=%d D=%d must be >= 1", H, D);
+    const int64_t F = int64_t(H) * D;
+    if (F % 4 != 0) return set_error(FG_ESHAPE, "fg_spmm: H*D=%lld must be a multiple of 4", (long long)F);
+    if (F > (int64_t(1) << 20)) return set_error(FG_ESHAPE, "fg_spmm: H*D=%lld too large", (long long)F);
+    if (!out && g->n_dst > 0) return set_error(FG_EINVAL, "fg_spmm: out is NULL");
+    if (!aligned16(out) || !aligned16(X) || !aligned16(arg_u) || !aligned16(arg_e))
+        return set_error(FG_EINVAL, "fg_spmm: X/out/arg pointers must be 16-byte aligned");
+    if (msg == FG_MSG_MLP) {
+        if (H != 1) return set_error(FG_ESHAPE, "fg_spmm(mlp): H must be 1 (got %d)", H);
+        if (d_in < 1 || d_in > 32) return set_error(FG_ESHAPE, "fg_spmm(mlp): d_in=%d must be in [1,32]", d_in);
+        if (!W) return set_error(FG_EINVAL, "fg_spmm(mlp): W is NULL");
+        if (!X_dst && g->n_src != g->n_dst)
+            return set_error(FG_ESHAPE, "fg_spmm(mlp): X_dst = NULL needs n_src == n_dst");
+        if (E) return set_error(FG_EINVAL, "fg_spmm(mlp): E must be NULL");
+    } else {
+        if (d_in != 0 || W || X_dst) return set_error(FG_EINVAL, "fg_spmm: W/X_dst/d_in are for mlp only");
+        if (msg == FG_MSG_U_MUL_E && !E && g->nnz > 0) return set_error(FG_EINVAL, "fg_spmm(u_mul_e): E is NULL");
+        if (msg == FG_MSG_COPY_U && E) return set_error(FG_EINVAL, "fg_spmm(copy_u): E must be NULL");
+    }
+    if (!X && g->nnz > 0) return set_error(FG_EINVAL, "fg_spmm: X is NULL");
+    if (g->n_dst == 0) return FG_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (msg == FG_MSG_MLP)
+        return fgk::launch_spmm_mlp(g, red, D, X, W, d_in, X_dst ? X_dst : X, out, arg_u, arg_e, st);
+    return fgk::launch_spmm_gather(g, msg, red, H, D, X, E, out, arg_u, arg_e, st);
+}
+
+extern "C" fg_status fg_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, const float* X, const float* Y,
+                              float* out, fg_stream stream) {
+    if (!g) return set_error(FG_EINVAL, "fg_sddmm: NULL graph");
+    if (op != FG_EDGE_U_DOT_V) return set_error(FG_EINVAL, "fg_sddmm: bad edge op %d", int(op));
+    if (H < 1 || D < 1) return set_error(FG_ESHAPE, "fg_sddmm: H=%d D=%d must be >= 1", H, D);
+    const int64_t F = int64_t(H) * D;
+    if (F % 4 != 0) return set_error(FG_ESHAPE, "fg_sddmm: H*D must be a multiple of 4");
+    if (H > 1 && (D % 4 != 0 || ((D / 4) & (D / 4 - 1)) != 0))
+        return set_error(FG_ESHAPE, "fg_sddmm: with H > 1, D must be 4 * 2^k (got D=%d)", D);
+    if (F > (int64_t(1) << 20)) return set_error(FG_ESHAPE, "fg_sddmm: H*D too large");
+    if (g->nnz == 0) return FG_OK;
+    if (!X || !Y || !out) return set_error(FG_EINVAL, "fg_sddmm: NULL tensor");
+    if (!aligned16(X) || !aligned16(Y) || !aligned16(out))
+        return set_error(FG_EINVAL, "fg_sddmm: X/Y/out must be 16-byte aligned");
+    return fgk::launch_sddmm(g, H, D, X, Y, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" fg_status fg_edge_softmax(const fg_graph* g, int H, const float* scores, float* out, fg_stream stream) {
+    if (!g) return set_error(FG_EINVAL, "fg_edge_softmax: NULL graph");
+    if (H < 1 || H > 4096) return set_error(FG_ESHAPE, "fg_edge_softmax: H=%d out of range", H);
+    if (g->nnz == 0) return FG_OK;
+    if (!scores || !out) return set_error(FG_EINVAL, "fg_edge_softmax: NULL tensor");
+    if (!aligned16(scores) || !aligned16(out))
+        return set_error(FG_EINVAL, "fg_edge_softmax: scores/out must be 16-byte aligned");
+    return fgk::launch_edge_softmax(g, H, scores, out, reinterpret_cast<cudaStream_t>(stream));
+}

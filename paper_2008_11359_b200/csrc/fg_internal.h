@@ -1,0 +1,63 @@
+// fg_internal.h -- shared internals of libfg.so (NOT part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/fg.h"
+
+struct fg_graph {
+    int64_t n_dst = 0, n_src = 0, nnz = 0;
+    const int64_t* row_ptr = nullptr;   // borrowed, device
+    const int32_t* col_idx = nullptr;   // borrowed, device
+    const int32_t* eid = nullptr;       // borrowed, device (nullptr = identity)
+    int device = 0;
+
+    // derived (owned, device)
+    int32_t* rows_by_deg = nullptr;     // [n_dst] rows sorted by degree, descending (stable)
+    int32_t* unit_row = nullptr;        // [n_units] SDDMM work units: (row, first edge)
+    int64_t* unit_p0 = nullptr;
+    int64_t n_units = 0;
+    int unit_chunk = 0;                 // edges per SDDMM unit
+
+    // derived (owned, host)
+    std::vector<int64_t> deg_sorted;    // degrees in rows_by_deg order (descending)
+    int64_t n_nonempty = 0;
+    int64_t max_deg = 0;
+    int64_t device_bytes = 0;
+};
+
+namespace fgk {
+
+// thread-local error detail
+fg_status set_error(fg_status s, const char* fmt, ...);
+
+// number of rows in the degree-sorted list with degree >= t
+int64_t rows_with_degree_at_least(const fg_graph* g, int64_t t);
+
+// kernels launchers (return FG_OK or FG_ECUDA); arguments already validated
+fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D,
+                             const float* X, const float* E, float* out, int32_t* arg_u,
+                             int32_t* arg_e, cudaStream_t st);
+fg_status launch_spmm_mlp(const fg_graph* g, fg_reduce_op red, int d2, const float* X,
+                          const float* W, int d_in, const float* X_dst, float* out,
+                          int32_t* arg_u, int32_t* arg_e, cudaStream_t st);
+fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const float* Y, float* out,
+                       cudaStream_t st);
+fg_status launch_edge_softmax(const fg_graph* g, int H, const float* S, float* out, cudaStream_t st);
+
+fg_status check_launch(const char* what);
+
+inline int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+}  // namespace fgk

@@ -1,0 +1,111 @@
+// mlp_simt.cu -- gSpMM with the MLP message on CUDA cores (FFMA): the
+// ablation baseline for the tcgen05 kernel (mlp_tcgen05.cu), and the path for
+// shapes the tensor-core kernel does not take.
+//
+// Fig. 3b: phi(u, v) = ReLU((x_u + x_v) W), W in R^{d1 x d2},
+// aggregated by max (Fig. 1 "picking the maximum") or sum.
+// Using (x_u + x_v) W = x_u W + x_v W, the per-destination term q_v = x_v W is
+// computed once per row and the per-edge work is a_e = x_u W (d1*d2 FMAs).
+//   max: out = ReLU(max_e a_e + q_v); arg = first argmax of a_e if that is > 0,
+//        else the row's first edge (all messages are +0 then; first wins)
+//        -- exact in real arithmetic because ReLU(. + q) is monotone.
+//   sum: out = sum_e ReLU(a_e + q_v).
+// One warp per destination row (degree-descending order), lane owns NC columns.
+#include "fg_internal.h"
+
+namespace {
+constexpr int THREADS = 256;
+
+template <int NC, bool MAX>
+__global__ void __launch_bounds__(THREADS) mlp_simt_kernel(const int32_t* __restrict__ rows, int64_t n_rows,
+                                                           const int64_t* __restrict__ rp,
+                                                           const int32_t* __restrict__ ci,
+                                                           const int32_t* __restrict__ eid,
+                                                           const float* __restrict__ X,
+                                                           const float* __restrict__ Xd,
+                                                           const float* __restrict__ W, int d_in, int d2,
+                                                           float* __restrict__ out, int32_t* __restrict__ arg_u,
+                                                           int32_t* __restrict__ arg_e) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t(blockIdx.x) * THREADS + threadIdx.x) >> 5;
+    if (r >= n_rows) return;
+    const int64_t v = rows[r];
+    const int cbase = blockIdx.y * 32 * NC;
+    const int64_t s = rp[v], e = rp[v + 1];
+    float q[NC], best[NC];
+    int pos[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        const int c = cbase + lane + 32 * j;
+        float a = 0.f;
+        if (c < d2)
+            for (int k = 0; k < d_in; ++k) a = fmaf(__ldg(Xd + v * d_in + k), __ldg(W + int64_t(k) * d2 + c), a);
+        q[j] = a;
+        best[j] = MAX ? -INFINITY : 0.f;
+        pos[j] = -1;
+    }
+    for (int64_t p = s; p < e; ++p) {
+        const int64_t u = __ldg(ci + p);
+        const float* xu = X + u * d_in;
+        float a[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) a[j] = 0.f;
+        for (int k = 0; k < d_in; ++k) {
+            const float xk = __ldg(xu + k);
+#pragma unroll
+            for (int j = 0; j < NC; ++j) {
+                const int c = cbase + lane + 32 * j;
+                a[j] = fmaf(xk, (c < d2) ? __ldg(W + int64_t(k) * d2 + c) : 0.f, a[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+            if (MAX) {
+                if (a[j] > best[j]) { best[j] = a[j]; pos[j] = int(p); }
+            } else {
+                best[j] += fmaxf(a[j] + q[j], 0.f);
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        const int c = cbase + lane + 32 * j;
+        if (c >= d2) continue;
+        const int64_t o = v * d2 + c;
+        if (!MAX) { out[o] = best[j]; continue; }
+        if (e == s) {
+            out[o] = 0.f;
+            if (arg_u) arg_u[o] = -1;
+            if (arg_e) arg_e[o] = -1;
+            continue;
+        }
+        const float z = best[j] + q[j];
+        const int pw = (z > 0.f) ? pos[j] : int(s);
+        out[o] = z > 0.f ? z : 0.f;
+        if (arg_u) arg_u[o] = __ldg(ci + pw);
+        if (arg_e) arg_e[o] = eid ? __ldg(eid + pw) : pw;
+    }
+}
+}  // namespace
+
+namespace fgk {
+fg_status launch_spmm_mlp_simt(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W,
+                               int d_in, const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e,
+                               cudaStream_t st) {
+    const int64_t n_rows = g->n_dst;
+    constexpr int NC = 4;
+    dim3 grid(unsigned((n_rows * 32 + THREADS - 1) / THREADS), unsigned((d2 + 32 * NC - 1) / (32 * NC)));
+    if (red == FG_REDUCE_MAX)
+        mlp_simt_kernel<NC, true><<<grid, THREADS, 0, st>>>(g->rows_by_deg, n_rows, g->row_ptr, g->col_idx, g->eid,
+                                                            X, X_dst, W, d_in, d2, out, arg_u, arg_e);
+    else
+        mlp_simt_kernel<NC, false><<<grid, THREADS, 0, st>>>(g->rows_by_deg, n_rows, g->row_ptr, g->col_idx, g->eid,
+                                                             X, X_dst, W, d_in, d2, out, arg_u, arg_e);
+    return check_launch("mlp_simt_kernel");
+}
+
+fg_status launch_spmm_mlp(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W, int d_in,
+                          const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e, cudaStream_t st) {
+    return launch_spmm_mlp_simt(g, red, d2, X, W, d_in, X_dst, out, arg_u, arg_e, st);
+}
+}  // namespace fgk

@@ -1,0 +1,221 @@
+"""Thin ctypes binding of libfg.so (include/fg.h): argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; this module
+only turns torch CUDA tensors into device pointers + sizes + the current CUDA
+stream, and raises on a non-OK status.  There is no fallback: if libfg.so is
+missing or CUDA is unavailable, calls fail loudly.
+
+Names follow include/fg.h and the paper (§3.2): graph_create
+(featgraph.spmat), spmm (featgraph.spmm), sddmm
+(featgraph.sddmm), edge_softmax (GAT normalisation).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libfg.so")
+
+FG_OK, FG_EINVAL, FG_ESHAPE, FG_EUNSUPPORTED, FG_EGRAPH, FG_ECUDA, FG_ENOMEM, FG_ENCCL = range(8)
+MSG = {"copy_u": 0, "u_mul_e": 1, "mlp": 2}
+REDUCE = {"sum": 0, "max": 1}
+EDGE = {"u_dot_v": 0}
+
+# exported symbols declared in include/fg.h (checked by tests/test_abi.py)
+SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
+           "fg_sddmm", "fg_edge_softmax", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
+           "fg_allgather_rows", "fg_status_string", "fg_last_error", "fg_abi_version"]
+
+
+class FGError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+class GraphInfo(ctypes.Structure):
+    _fields_ = [("n_dst", ctypes.c_int64), ("n_src", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("max_degree", ctypes.c_int64), ("n_empty_rows", ctypes.c_int64),
+                ("n_sddmm_units", ctypes.c_int64), ("device_bytes", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libfg.so (raises if it was not built -- no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise FGError(FG_ECUDA, f"libfg.so not built at {LIB_PATH}: run `python -m paper_2008_11359_b200.build`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+    L.fg_graph_create.argtypes = [i64, i64, i64, vp, vp, vp, i32, vp, ctypes.POINTER(vp)]
+    L.fg_graph_destroy.argtypes = [vp]
+    L.fg_graph_info.argtypes = [vp, ctypes.POINTER(GraphInfo)]
+    L.fg_spmm_workspace_size.argtypes = [vp, i32, i32, i32, i32, i32, ctypes.POINTER(sz)]
+    L.fg_spmm.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]
+    L.fg_sddmm.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
+    L.fg_edge_softmax.argtypes = [vp, i32, vp, vp, vp]
+    L.fg_comm_unique_id.argtypes = [vp]
+    L.fg_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
+    L.fg_comm_destroy.argtypes = [vp]
+    L.fg_allgather_rows.argtypes = [vp, vp, i64, vp, vp, vp]
+    for f in ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
+              "fg_sddmm", "fg_edge_softmax", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
+              "fg_allgather_rows"]:
+        getattr(L, f).restype = i32
+    L.fg_status_string.argtypes = [i32]
+    L.fg_status_string.restype = ctypes.c_char_p
+    L.fg_last_error.restype = ctypes.c_char_p
+    L.fg_abi_version.restype = i32
+    _lib = L
+    return L
+
+
+def _check(status: int, what: str):
+    if status != FG_OK:
+        L = lib()
+        raise FGError(status, f"{what}: {L.fg_status_string(status).decode()} -- {L.fg_last_error().decode()}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev(t, dtype, name):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise FGError(FG_EINVAL, f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise FGError(FG_EINVAL, f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise FGError(FG_EINVAL, f"{name} must be contiguous")
+    return t
+
+
+class Graph:
+    """fg_graph handle (featgraph.spmat).  Borrows row_ptr/col_idx/eid: the
+    tensors are kept referenced by this object."""
+
+    def __init__(self, row_ptr: torch.Tensor, col_idx: torch.Tensor, n_src: int | None = None,
+                 eid: torch.Tensor | None = None, validate: bool = True, stream=None):
+        self.row_ptr = _dev(row_ptr, torch.int64, "row_ptr")
+        self.col_idx = _dev(col_idx, torch.int32, "col_idx")
+        self.eid = _dev(eid, torch.int32, "eid")
+        self.n_dst = row_ptr.numel() - 1
+        self.n_src = self.n_dst if n_src is None else int(n_src)
+        self.nnz = col_idx.numel()
+        h = ctypes.c_void_p()
+        _check(lib().fg_graph_create(self.n_dst, self.n_src, self.nnz, _ptr(self.row_ptr),
+                                     _ptr(self.col_idx) if self.nnz else None, _ptr(self.eid),
+                                     int(bool(validate)), _stream(stream), ctypes.byref(h)),
+               "fg_graph_create")
+        self.handle = h
+
+    def info(self) -> GraphInfo:
+        inf = GraphInfo()
+        _check(lib().fg_graph_info(self.handle, ctypes.byref(inf)), "fg_graph_info")
+        return inf
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().fg_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def spmm(g: Graph, msg: str, reduce: str, X: torch.Tensor, *, H: int = 1, E: torch.Tensor | None = None,
+         W: torch.Tensor | None = None, X_dst: torch.Tensor | None = None, out: torch.Tensor | None = None,
+         arg_u: torch.Tensor | bool | None = None, arg_e: torch.Tensor | bool | None = None, stream=None):
+    """featgraph.spmm (Eq. (1)).  Returns out, or (out, arg_u, arg_e) when args requested."""
+    X = _dev(X, torch.float32, "X")
+    E, W, X_dst = _dev(E, torch.float32, "E"), _dev(W, torch.float32, "W"), _dev(X_dst, torch.float32, "X_dst")
+    if msg == "mlp":
+        d_in, F = W.shape
+        H_, D = 1, F
+    else:
+        d_in = 0
+        F = X.numel() // max(X.shape[0], 1) if X.dim() > 1 else 1
+        H_, D = H, F // H
+    if out is None:
+        out = torch.empty((g.n_dst, F), dtype=torch.float32, device=X.device)
+    want = reduce == "max" and (arg_u is not None or arg_e is not None)
+    if arg_u is True:
+        arg_u = torch.empty((g.n_dst, F), dtype=torch.int32, device=X.device)
+    if arg_e is True:
+        arg_e = torch.empty((g.n_dst, F), dtype=torch.int32, device=X.device)
+    arg_u = arg_u if isinstance(arg_u, torch.Tensor) else None
+    arg_e = arg_e if isinstance(arg_e, torch.Tensor) else None
+    _check(lib().fg_spmm(g.handle, MSG[msg], REDUCE[reduce], H_, D, _ptr(X), _ptr(E), _ptr(W), d_in, _ptr(X_dst),
+                         _ptr(out), _ptr(arg_u), _ptr(arg_e), None, 0, _stream(stream)), f"fg_spmm({msg},{reduce})")
+    if want:
+        return out, arg_u, arg_e
+    return out
+
+
+def sddmm(g: Graph, X: torch.Tensor, Y: torch.Tensor | None = None, *, H: int = 1, op: str = "u_dot_v",
+          out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """featgraph.sddmm (Eq. (4), Fig. 5): out[eid][h] = <X[u,h,:], Y[v,h,:]>."""
+    X = _dev(X, torch.float32, "X")
+    Y = X if Y is None else _dev(Y, torch.float32, "Y")
+    F = X.numel() // max(X.shape[0], 1)
+    if out is None:
+        out = torch.empty((g.nnz, H), dtype=torch.float32, device=X.device)
+    _check(lib().fg_sddmm(g.handle, EDGE[op], H, F // H, _ptr(X), _ptr(Y), _ptr(out), _stream(stream)), "fg_sddmm")
+    return out
+
+
+def edge_softmax(g: Graph, scores: torch.Tensor, *, H: int = 1, out: torch.Tensor | None = None,
+                 stream=None) -> torch.Tensor:
+    """Per-destination softmax over in-edges, per head (GAT)."""
+    scores = _dev(scores, torch.float32, "scores")
+    if out is None:
+        out = torch.empty_like(scores)
+    _check(lib().fg_edge_softmax(g.handle, H, _ptr(scores), _ptr(out), _stream(stream)), "fg_edge_softmax")
+    return out
+
+
+# ------------------------------------------------------------------ multi-GPU
+def comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().fg_comm_unique_id(buf), "fg_comm_unique_id")
+    return buf.raw
+
+
+class Comm:
+    def __init__(self, unique_id: bytes, nranks: int, rank: int):
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(unique_id, 128)
+        _check(lib().fg_comm_init(buf, nranks, rank, ctypes.byref(h)), "fg_comm_init")
+        self.handle, self.nranks, self.rank = h, nranks, rank
+
+    def allgather_rows(self, shard_offsets, X_local: torch.Tensor | None, X_full: torch.Tensor, stream=None):
+        import numpy as np
+        off = np.ascontiguousarray(np.asarray(shard_offsets, dtype=np.int64))
+        row_elems = X_full.numel() // max(X_full.shape[0], 1)
+        _check(lib().fg_allgather_rows(self.handle, ctypes.c_void_p(off.ctypes.data), row_elems, _ptr(X_local),
+                                       _ptr(X_full), _stream(stream)), "fg_allgather_rows")
+        return X_full
+
+    def close(self):
+        if self.handle:
+            lib().fg_comm_destroy(self.handle)
+            self.handle = None

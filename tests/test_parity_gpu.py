@@ -1,0 +1,356 @@
+"""GPU-vs-oracle parity through the C ABI (libfg.so), on seeded inputs from gen/.
+
+Bar (BASELINE.json north_star):
+  * integer / index outputs (argmax) bit-exact;
+  * fp32 outputs |gpu - ref| <= 1e-4 * sum|terms| against the fp64 oracle;
+  * integer-regime inputs: every output bit-exact (except softmax);
+  * copy_u / u_mul_e max values bit-exact in every regime;
+  * mlp argmax in the real regime checked as VALID.
+Sizes span several CTAs / tiles, heavy (CTA-per-row) rows and ragged tails.
+"""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+from helpers import check_close, csr_from_edges
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib(cuda_ok):
+    import paper_2008_11359_b200 as fgp
+    fgp.lib()
+    return fgp
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+class G:
+    """A graph on both sides: numpy arrays for the oracle, an fg handle for the GPU."""
+
+    def __init__(self, row_ptr, col_idx, n_src=None, eid=None):
+        import paper_2008_11359_b200 as fgp
+        self.row_ptr = np.asarray(row_ptr, np.int64)
+        self.col_idx = np.asarray(col_idx, np.int32)
+        self.n_dst = self.row_ptr.size - 1
+        self.n_src = self.n_dst if n_src is None else n_src
+        self.nnz = int(self.row_ptr[-1])
+        self.eid = None if eid is None else np.asarray(eid, np.int32)
+        self.h = fgp.Graph(dev(self.row_ptr), dev(self.col_idx), n_src=self.n_src,
+                           eid=None if eid is None else dev(self.eid))
+
+
+def graph_of(g, eid=None):
+    return G(g.row_ptr, g.col_idx, g.n_src, eid)
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return graph_of(gen.make_graph("tiny"))
+
+
+@pytest.fixture(scope="module")
+def skewed():
+    # 3000 rows, 120K edges, heavy rows up to 3000 (CTA-per-row path for every F), empty rows
+    g = gen.random_graph(3000, 120000, 77, sigma=1.6, n_empty=50)
+    return graph_of(g)
+
+
+@pytest.fixture(scope="module")
+def skewed_eid(skewed):
+    return G(skewed.row_ptr, skewed.col_idx, skewed.n_src, eid=gen.permutation(skewed.nnz, 13).astype(np.int32))
+
+
+def feats(shape, seed, regime, lo=-8, hi=8):
+    return gen.features(shape, seed, 0, regime, lo=lo, hi=hi)
+
+
+# ------------------------------------------------------------------ copy_u
+@pytest.mark.parametrize("F", [4, 8, 16, 32, 48, 128, 200, 256, 512, 640])
+@pytest.mark.parametrize("regime", [gen.REAL, gen.INT])
+def test_copy_u_sum(skewed, F, regime):
+    import paper_2008_11359_b200 as fgp
+    X = feats((skewed.n_src, F), 100 + F, regime)
+    out = fgp.spmm(skewed.h, "copy_u", "sum", dev(X)).cpu().numpy()
+    ref, ab, _, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", "sum", X)
+    if regime == gen.INT:
+        assert np.array_equal(out.astype(np.float64), ref)
+    else:
+        check_close(out, ref, ab, TOL, f"copy_u-sum F={F}")
+
+
+@pytest.mark.parametrize("F", [4, 16, 32, 64, 128, 384, 512, 1024])
+@pytest.mark.parametrize("regime", [gen.REAL, gen.INT])
+def test_copy_u_max(skewed, F, regime):
+    import paper_2008_11359_b200 as fgp
+    X = feats((skewed.n_src, F), 200 + F, regime, lo=-3, hi=3)   # INT: heavy ties
+    out, au, ae = fgp.spmm(skewed.h, "copy_u", "max", dev(X), arg_u=True, arg_e=True)
+    ref, _, rau, rae = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", "max", X)
+    assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+    assert np.array_equal(au.cpu().numpy(), rau)
+    assert np.array_equal(ae.cpu().numpy(), rae)
+
+
+def test_tiny_config_all_ops(tiny):
+    """BASELINE.json configs[0]: tiny graph, F=16, copy_u sum/max + u_dot_v."""
+    import paper_2008_11359_b200 as fgp
+    F = 16
+    X = feats((tiny.n_src, F), 1, gen.REAL)
+    out = fgp.spmm(tiny.h, "copy_u", "sum", dev(X)).cpu().numpy()
+    ref, ab, _, _ = oracle.spmm(tiny.row_ptr, tiny.col_idx, "copy_u", "sum", X)
+    check_close(out, ref, ab, TOL, "tiny copy_u-sum")
+    out, au, ae = fgp.spmm(tiny.h, "copy_u", "max", dev(X), arg_u=True, arg_e=True)
+    ref, _, rau, rae = oracle.spmm(tiny.row_ptr, tiny.col_idx, "copy_u", "max", X)
+    assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+    assert np.array_equal(au.cpu().numpy(), rau) and np.array_equal(ae.cpu().numpy(), rae)
+    s = fgp.sddmm(tiny.h, dev(X)).cpu().numpy()
+    ref, ab = oracle.sddmm(tiny.row_ptr, tiny.col_idx, X)
+    check_close(s, ref, ab, TOL, "tiny u_dot_v")
+
+
+# ------------------------------------------------------------------ u_mul_e
+@pytest.mark.parametrize("H,D", [(1, 4), (1, 128), (2, 2), (8, 2), (4, 4), (8, 32), (8, 64), (3, 12)])
+@pytest.mark.parametrize("red", ["sum", "max"])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_u_mul_e(skewed, skewed_eid, H, D, red, use_eid):
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    F = H * D
+    X = feats((g.n_src, F), 300 + F, gen.REAL)
+    E = gen.features((g.nnz, H), 301, 1, gen.UNIT)
+    ref, ab, rau, rae = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", red, X, H=H, E=E, eid=g.eid)
+    if red == "sum":
+        out = fgp.spmm(g.h, "u_mul_e", "sum", dev(X), H=H, E=dev(E)).cpu().numpy()
+        check_close(out, ref, ab, TOL, f"u_mul_e-sum H={H} D={D}")
+    else:
+        out, au, ae = fgp.spmm(g.h, "u_mul_e", "max", dev(X), H=H, E=dev(E), arg_u=True, arg_e=True)
+        assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+        assert np.array_equal(au.cpu().numpy(), rau)
+        assert np.array_equal(ae.cpu().numpy(), rae)
+
+
+def test_u_mul_e_int_regime_exact(skewed):
+    import paper_2008_11359_b200 as fgp
+    H, D = 8, 32
+    X = feats((skewed.n_src, H * D), 311, gen.INT)
+    E = gen.features((skewed.nnz, H), 312, 1, gen.INT, lo=0, hi=4)
+    out = fgp.spmm(skewed.h, "u_mul_e", "sum", dev(X), H=H, E=dev(E)).cpu().numpy()
+    ref, _, _, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "u_mul_e", "sum", X, H=H, E=E)
+    assert np.array_equal(out.astype(np.float64), ref)
+
+
+# ------------------------------------------------------------------ mlp
+@pytest.mark.parametrize("d2", [16, 128, 256])
+@pytest.mark.parametrize("red", ["max", "sum"])
+def test_mlp_int_exact(skewed, d2, red):
+    import paper_2008_11359_b200 as fgp
+    d1 = 8
+    X = feats((skewed.n_src, d1), 400, gen.INT)
+    W = gen.features((d1, d2), 401, 1, gen.INT, lo=-4, hi=4)
+    ref, _, rau, rae = oracle.spmm(skewed.row_ptr, skewed.col_idx, "mlp", red, X, W=W)
+    if red == "max":
+        out, au, ae = fgp.spmm(skewed.h, "mlp", "max", dev(X), W=dev(W), arg_u=True, arg_e=True)
+        assert np.array_equal(au.cpu().numpy(), rau)
+        assert np.array_equal(ae.cpu().numpy(), rae)
+    else:
+        out = fgp.spmm(skewed.h, "mlp", "sum", dev(X), W=dev(W))
+    assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("d2", [32, 128])
+@pytest.mark.parametrize("red", ["max", "sum"])
+def test_mlp_real(skewed, d2, red):
+    import paper_2008_11359_b200 as fgp
+    d1 = 8
+    X = feats((skewed.n_src, d1), 410, gen.REAL)
+    W = gen.features((d1, d2), 411, 1, gen.SCALED, scale=1 / np.sqrt(d1))
+    ref, ab, _, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "mlp", red, X, W=W)
+    if red == "sum":
+        out = fgp.spmm(skewed.h, "mlp", "sum", dev(X), W=dev(W)).cpu().numpy()
+        check_close(out, ref, ab, TOL, f"mlp-sum d2={d2}")
+        return
+    out, au, ae = fgp.spmm(skewed.h, "mlp", "max", dev(X), W=dev(W), arg_u=True, arg_e=True)
+    out, au, ae = out.cpu().numpy(), au.cpu().numpy(), ae.cpu().numpy()
+    check_close(out, ref, ab, TOL, f"mlp-max d2={d2}")
+    # argmax VALID: the oracle's message at the GPU's winning edge is within tolerance of the max
+    Xd, Wd = X.astype(np.float64), W.astype(np.float64)
+    deg = np.diff(skewed.row_ptr)
+    for v in np.flatnonzero(deg)[::7]:
+        u = au[v]
+        assert (skewed.col_idx[ae[v]] == u).all()
+        msg = np.maximum(((Xd[u] + Xd[v][None, :]) * Wd.T).sum(1), 0.0)
+        assert (np.abs(msg - ref[v]) <= TOL * ab[v] + 1e-30).all()
+
+
+def test_mlp_separate_x_dst():
+    import paper_2008_11359_b200 as fgp
+    g = graph_of(gen.random_graph(500, 8000, 5, n_empty=5))
+    X = feats((g.n_src, 8), 420, gen.INT)
+    Xd = feats((g.n_dst, 8), 421, gen.INT)
+    W = gen.features((8, 64), 422, 1, gen.INT, lo=-4, hi=4)
+    out, au, _ = fgp.spmm(g.h, "mlp", "max", dev(X), W=dev(W), X_dst=dev(Xd), arg_u=True)
+    ref, _, rau, _ = oracle.spmm(g.row_ptr, g.col_idx, "mlp", "max", X, W=W, X_dst=Xd)
+    assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+    assert np.array_equal(au.cpu().numpy(), rau)
+
+
+# ------------------------------------------------------------------ sddmm
+@pytest.mark.parametrize("H,D", [(1, 4), (1, 16), (1, 48), (1, 128), (1, 512), (1, 1024), (2, 4), (8, 4),
+                                 (8, 32), (4, 64), (2, 256), (8, 8)])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_sddmm(skewed, skewed_eid, H, D, use_eid):
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    F = H * D
+    X = feats((g.n_src, F), 500 + F, gen.REAL)
+    Y = feats((g.n_dst, F), 501 + F, gen.REAL)
+    out = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+    ref, ab = oracle.sddmm(g.row_ptr, g.col_idx, X, Y, H=H)   # CSR order
+    pos = np.arange(g.nnz) if g.eid is None else g.eid
+    check_close(out[pos], ref, ab, TOL, f"u_dot_v H={H} D={D}")
+
+
+def test_sddmm_int_exact(skewed):
+    import paper_2008_11359_b200 as fgp
+    H, D = 8, 32
+    X = feats((skewed.n_src, H * D), 510, gen.INT)
+    out = fgp.sddmm(skewed.h, dev(X), H=H).cpu().numpy()
+    ref, _ = oracle.sddmm(skewed.row_ptr, skewed.col_idx, X, H=H)
+    assert np.array_equal(out.astype(np.float64), ref)
+
+
+# ------------------------------------------------------------------ edge softmax
+@pytest.mark.parametrize("H", [1, 2, 8, 3])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_edge_softmax(skewed, skewed_eid, H, use_eid):
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    S = gen.features((g.nnz, H), 600 + H, 0, gen.REAL) * 8
+    out = fgp.edge_softmax(g.h, dev(S), H=H).cpu().numpy()
+    ref = oracle.edge_softmax(g.row_ptr, S, H=H, eid=g.eid)   # CSR order
+    pos = np.arange(g.nnz) if g.eid is None else g.eid
+    got = out[pos].astype(np.float64)
+    assert (np.abs(got - ref) <= TOL * ref).all()
+    rows = np.repeat(np.arange(g.n_dst), np.diff(g.row_ptr))
+    sums = np.zeros((g.n_dst, H))
+    np.add.at(sums, rows, got)
+    nz = np.diff(g.row_ptr) > 0
+    assert np.abs(sums[nz] - 1).max() <= TOL
+    # in place
+    St = dev(S)
+    fgp.edge_softmax(g.h, St, H=H, out=St)
+    assert np.array_equal(St.cpu().numpy(), out)
+
+
+def test_edge_softmax_special_values(skewed):
+    import paper_2008_11359_b200 as fgp
+    H = 4
+    S = np.full((skewed.nnz, H), 0.75, np.float32)
+    out = fgp.edge_softmax(skewed.h, dev(S), H=H).cpu().numpy()
+    deg = np.diff(skewed.row_ptr)
+    rows = np.repeat(np.arange(skewed.n_dst), deg)
+    expect = (np.float32(1.0) / deg[rows].astype(np.float32))[:, None]
+    assert np.array_equal(out, np.broadcast_to(expect, out.shape))   # constant -> 1/deg (correctly rounded)
+
+
+# ------------------------------------------------------------------ chain (GAT layer, config 3 shape at small size)
+def test_gat_layer_chain(skewed):
+    """sddmm -> edge_softmax -> u_mul_e, each op checked in isolation on the
+    GPU's own fp32 inputs (no compounding through exp)."""
+    import paper_2008_11359_b200 as fgp
+    H, D = 8, 32
+    X = feats((skewed.n_src, H * D), 700, gen.REAL) * 0.25
+    Xt = dev(X)
+    s = fgp.sddmm(skewed.h, Xt, H=H)
+    a = fgp.edge_softmax(skewed.h, s, H=H)
+    out = fgp.spmm(skewed.h, "u_mul_e", "sum", Xt, H=H, E=a).cpu().numpy()
+    s_np, a_np = s.cpu().numpy(), a.cpu().numpy()
+    ref, ab = oracle.sddmm(skewed.row_ptr, skewed.col_idx, X, H=H)
+    check_close(s_np, ref, ab, TOL, "gat sddmm")
+    ref_a = oracle.edge_softmax(skewed.row_ptr, s_np, H=H)
+    assert (np.abs(a_np - ref_a) <= TOL * ref_a).all()
+    ref_o, ab_o, _, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "u_mul_e", "sum", X, H=H, E=a_np)
+    check_close(out, ref_o, ab_o, TOL, "gat aggregation")
+
+
+# ------------------------------------------------------------------ degenerate graphs and ABI behaviour
+@pytest.mark.parametrize("case", ["n1_m0", "all_empty", "one_row_all_edges", "self_loop", "n_src_ne_n_dst"])
+def test_degenerate(case):
+    import paper_2008_11359_b200 as fgp
+    if case == "n1_m0":
+        g = G(np.array([0, 0]), np.zeros(0, np.int32))
+    elif case == "all_empty":
+        g = G(np.zeros(65, np.int64), np.zeros(0, np.int32))
+    elif case == "one_row_all_edges":
+        n = 5000
+        rp = np.zeros(n + 1, np.int64)
+        rp[1:] = n
+        g = G(rp, np.arange(n, dtype=np.int32))
+    elif case == "self_loop":
+        rp, ci = csr_from_edges(3, [[0, 0], [1, 1], [2, 2], [0, 2]])
+        g = G(rp, ci)
+    else:
+        rp, ci = csr_from_edges(4, [[0, 1], [5, 1], [6, 3], [2, 0]], n_src=7)
+        g = G(rp, ci, n_src=7)
+    for F in (4, 32, 512):
+        X = feats((g.n_src, F), 800 + F, gen.REAL)
+        out = torch.full((g.n_dst, F), float("nan"), device="cuda")
+        fgp.spmm(g.h, "copy_u", "sum", dev(X), out=out)
+        ref, ab, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", "sum", X)
+        check_close(out.cpu().numpy(), ref, ab, TOL, f"{case} sum F={F}")
+        out = torch.full((g.n_dst, F), float("nan"), device="cuda")
+        au = torch.full((g.n_dst, F), 7, dtype=torch.int32, device="cuda")
+        fgp.spmm(g.h, "copy_u", "max", dev(X), out=out, arg_u=au)
+        ref, _, rau, _ = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", "max", X)
+        assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+        assert np.array_equal(au.cpu().numpy(), rau)
+        if g.nnz:
+            Y = feats((g.n_dst, F), 900 + F, gen.REAL)
+            s = fgp.sddmm(g.h, dev(X), dev(Y)).cpu().numpy()
+            ref, ab = oracle.sddmm(g.row_ptr, g.col_idx, X, Y)
+            check_close(s, ref, ab, TOL, f"{case} sddmm F={F}")
+
+
+def test_determinism(skewed):
+    import paper_2008_11359_b200 as fgp
+    X = dev(feats((skewed.n_src, 256), 950, gen.REAL))
+    a = fgp.spmm(skewed.h, "copy_u", "sum", X)
+    b = fgp.spmm(skewed.h, "copy_u", "sum", X)
+    assert torch.equal(a, b)
+    s1, s2 = fgp.sddmm(skewed.h, X, H=8), fgp.sddmm(skewed.h, X, H=8)
+    assert torch.equal(s1, s2)
+
+
+def test_abi_errors_on_device(skewed):
+    import paper_2008_11359_b200 as fgp
+    from paper_2008_11359_b200.fg import FGError, FG_EINVAL, FG_ESHAPE, FG_EGRAPH
+    X = torch.zeros((skewed.n_src * 8 + 1,), device="cuda")
+    with pytest.raises(FGError) as ei:   # misaligned X
+        fgp.spmm(skewed.h, "copy_u", "sum", X[1:].view(skewed.n_src, 8))
+    assert ei.value.status == FG_EINVAL
+    with pytest.raises(FGError) as ei:   # F % 4 != 0
+        fgp.spmm(skewed.h, "copy_u", "sum", torch.zeros((skewed.n_src, 6), device="cuda"))
+    assert ei.value.status == FG_ESHAPE
+    with pytest.raises(FGError) as ei:   # arg with sum
+        fgp.spmm(skewed.h, "copy_u", "sum", torch.zeros((skewed.n_src, 8), device="cuda"), arg_u=True)
+    assert ei.value.status == FG_EINVAL
+    out = torch.full((skewed.n_dst, 8), 3.0, device="cuda")
+    with pytest.raises(FGError):
+        fgp.spmm(skewed.h, "copy_u", "sum", torch.zeros((skewed.n_src, 6), device="cuda"), out=out)
+    assert (out == 3.0).all()   # untouched on error
+    # CSR validation
+    rp = np.array([0, 2, 3], np.int64)
+    for ci, why in [(np.array([1, 0, 0], np.int32), "unsorted"), (np.array([0, 5, 1], np.int32), "range")]:
+        with pytest.raises(FGError) as ei:
+            fgp.Graph(dev(rp), dev(ci), n_src=2)
+        assert ei.value.status == FG_EGRAPH, why
+    with pytest.raises(FGError) as ei:
+        fgp.Graph(dev(np.array([0, 1, 2], np.int64)), dev(np.array([0, 1], np.int32)),
+                  eid=dev(np.array([1, 1], np.int32)))
+    assert ei.value.status == FG_EGRAPH
