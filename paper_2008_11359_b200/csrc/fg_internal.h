@@ -43,6 +43,12 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
 fg_status launch_spmm_mlp(const fg_graph* g, fg_reduce_op red, int d2, const float* X,
                           const float* W, int d_in, const float* X_dst, float* out,
                           int32_t* arg_u, int32_t* arg_e, cudaStream_t st);
+fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W,
+                                  int d_in, const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e,
+                                  cudaStream_t st);
+fg_status launch_spmm_mlp_simt(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W,
+                               int d_in, const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e,
+                               cudaStream_t st);
 fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const float* Y, float* out,
                        cudaStream_t st);
 fg_status launch_edge_softmax(const fg_graph* g, int H, const float* S, float* out, cudaStream_t st);

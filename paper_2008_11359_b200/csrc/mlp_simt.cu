@@ -11,6 +11,8 @@
 //        -- exact in real arithmetic because ReLU(. + q) is monotone.
 //   sum: out = sum_e ReLU(a_e + q_v).
 // One warp per destination row (degree-descending order), lane owns NC columns.
+#include <cstdlib>
+
 #include "fg_internal.h"
 
 namespace {
@@ -27,10 +29,16 @@ __global__ void __launch_bounds__(THREADS) mlp_simt_kernel(const int32_t* __rest
                                                            float* __restrict__ out, int32_t* __restrict__ arg_u,
                                                            int32_t* __restrict__ arg_e) {
     const int lane = threadIdx.x & 31;
+    const int cbase = blockIdx.y * 32 * NC;
+    __shared__ float sW[32][32 * NC];            // W[:, cbase : cbase + 32*NC] (d_in <= 32)
+    for (int i = threadIdx.x; i < 32 * 32 * NC; i += THREADS) {
+        const int k = i / (32 * NC), c = cbase + i % (32 * NC);
+        sW[k][i % (32 * NC)] = (k < d_in && c < d2) ? W[int64_t(k) * d2 + c] : 0.f;
+    }
+    __syncthreads();
     const int64_t r = (int64_t(blockIdx.x) * THREADS + threadIdx.x) >> 5;
     if (r >= n_rows) return;
     const int64_t v = rows[r];
-    const int cbase = blockIdx.y * 32 * NC;
     const int64_t s = rp[v], e = rp[v + 1];
     float q[NC], best[NC];
     int pos[NC];
@@ -38,8 +46,7 @@ __global__ void __launch_bounds__(THREADS) mlp_simt_kernel(const int32_t* __rest
     for (int j = 0; j < NC; ++j) {
         const int c = cbase + lane + 32 * j;
         float a = 0.f;
-        if (c < d2)
-            for (int k = 0; k < d_in; ++k) a = fmaf(__ldg(Xd + v * d_in + k), __ldg(W + int64_t(k) * d2 + c), a);
+        for (int k = 0; k < d_in; ++k) a = fmaf(__ldg(Xd + v * d_in + k), sW[k][lane + 32 * j], a);
         q[j] = a;
         best[j] = MAX ? -INFINITY : 0.f;
         pos[j] = -1;
@@ -53,10 +60,7 @@ __global__ void __launch_bounds__(THREADS) mlp_simt_kernel(const int32_t* __rest
         for (int k = 0; k < d_in; ++k) {
             const float xk = __ldg(xu + k);
 #pragma unroll
-            for (int j = 0; j < NC; ++j) {
-                const int c = cbase + lane + 32 * j;
-                a[j] = fmaf(xk, (c < d2) ? __ldg(W + int64_t(k) * d2 + c) : 0.f, a[j]);
-            }
+            for (int j = 0; j < NC; ++j) a[j] = fmaf(xk, sW[k][lane + 32 * j], a[j]);
         }
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
@@ -104,8 +108,15 @@ fg_status launch_spmm_mlp_simt(const fg_graph* g, fg_reduce_op red, int d2, cons
     return check_launch("mlp_simt_kernel");
 }
 
+// The product path is the tcgen05 kernel; FG_MLP_SIMT=1 selects the FFMA kernel
+// (ablation only: same semantics, CUDA cores instead of tensor cores).
 fg_status launch_spmm_mlp(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W, int d_in,
                           const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e, cudaStream_t st) {
-    return launch_spmm_mlp_simt(g, red, d2, X, W, d_in, X_dst, out, arg_u, arg_e, st);
+    static const bool simt = [] {
+        const char* e = getenv("FG_MLP_SIMT");
+        return e && e[0] == '1';
+    }();
+    if (simt) return launch_spmm_mlp_simt(g, red, d2, X, W, d_in, X_dst, out, arg_u, arg_e, st);
+    return launch_spmm_mlp_tcgen05(g, red, d2, X, W, d_in, X_dst, out, arg_u, arg_e, st);
 }
 }  // namespace fgk

@@ -1,0 +1,453 @@
+// mlp_tcgen05.cu -- gSpMM with the MLP message on the 5th-generation tensor
+// cores.
+//
+// Fig. 3b: phi(u, v) = ReLU(sum_k (x_u[k] + x_v[k]) W[k, i]),
+// aggregated by max (Fig. 1 "picking the maximum"; MLP aggregation of
+// Table tab:gpu-kernel(b), d1 = 8) or sum.
+// Using (x_u + x_v) W = x_u W + x_v W:
+//     a_e[i] = x_u W[:, i]    -- a real dense contraction: a gathered tile of NT
+//                                edges x d1 against the shared W (tensor cores)
+//     q_v[i] = x_v W[:, i]    -- once per destination row (epilogue, FFMA)
+//     max: out[v][i] = ReLU(max_e a_e[i] + q_v[i]); argmax = first e attaining the
+//          max if that is > 0, else the row's first edge (all messages are +0);
+//     sum: out[v][i] = sum_e ReLU(a_e[i] + q_v[i]).
+// (exact in real arithmetic: ReLU(. + q) is monotone -- SURVEY §8(c) pin table).
+//
+// The paper's V100 schedule bound d2 to blocks and tree-reduced d1 over threads
+// (listing fig:schedule-mlp-conv-gpu).  Here, per CTA (persistent,
+// 2 per SM, each owning a contiguous range of destination rows and therefore a
+// contiguous range of CSR edges):
+//   * producer warps gather x_u for NT = 128 edges (L2-resident: n x d1 x 4 B),
+//     split each fp32 into tf32 hi + lo and store the B operand (K-major,
+//     no-swizzle canonical layout) into a 4-stage shared-memory ring;
+//   * one thread issues tcgen05.mma.kind::tf32, M = 128 features (W^T, staged
+//     once), N = 128 edges, K = 8, three times per tile
+//     (hi*hi + hi*lo + lo*hi = "3xTF32", error ~2^-21 relative: fp32-grade,
+//     the 1e-4 bound needs more than one tf32 pass), accumulating in
+//     TMEM (2 x 128 columns, double-buffered), and commits to mbarriers;
+//   * 4 epilogue warps read the accumulator with tcgen05.ld (thread = feature,
+//     walking edge columns, so the per-row segmented max needs no cross-lane
+//     reduction) and write each finished row with coalesced stores.
+#include <cstdint>
+
+#include "fg_internal.h"
+
+namespace {
+
+constexpr int NT = 128;                   // edges per tile (MMA N)
+constexpr int MT = 128;                   // features per CTA (MMA M)
+constexpr int STAGES = 4;
+constexpr int NEPI = 4;                   // epilogue warps 0..3 (TMEM lane quarters)
+constexpr int MMA_WARP = 4;
+constexpr int NPROD = 2;                  // producer warps 5..6
+constexpr int THREADS = (NEPI + 1 + NPROD) * 32;
+constexpr int TMEM_COLS = 2 * NT;
+constexpr int TILE_BYTES = 8 * 4 * 128;   // one K-step operand tile: 128 rows x 8 tf32 = 4 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// Shared-memory matrix descriptor: K-major, SWIZZLE_NONE canonical layout,
+// core matrix = 8 rows x 16 B; LBO = 128 B (next 16-byte K chunk), SBO = 256 B
+// (next 8-row group); version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+    return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) |
+           (uint64_t(1) << 46);
+}
+// byte offset of element (row r, k in [0,8)) inside a 128 x 8 tf32 operand tile
+__device__ __forceinline__ uint32_t tile_off(int r, int k) {
+    return uint32_t((r >> 3) * 256 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
+}
+// instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, N = NT, M = MT
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NT >> 3) << 17) | (uint32_t(MT >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+// wait for this thread's outstanding tcgen05.ld; v is threaded through the asm so no use of
+// the loaded registers can be scheduled before the wait
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.wait::ld.sync.aligned;"
+        : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+          "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]),
+          "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+          "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+        :
+        : "memory");
+}
+
+__device__ __forceinline__ int64_t lower_bound_rp(const int64_t* rp, int64_t n1, int64_t target) {
+    int64_t lo = 0, hi = n1;   // first i in [0, n1) with rp[i] >= target
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(rp + mid) < target) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+struct Args {
+    const int64_t* row_ptr;
+    const int32_t* col_idx;
+    const int32_t* eid;
+    const float* X;       // [n_src][d_in]
+    const float* Xd;      // [n_dst][d_in]
+    const float* W;       // [d_in][d2]
+    float* out;           // [n_dst][d2]
+    int32_t* arg_u;
+    int32_t* arg_e;
+    int64_t n_dst, nnz;
+    int d_in, d2;
+};
+
+template <int KS>
+struct Smem {
+    float a_hi[KS][MT * 8];
+    float a_lo[KS][MT * 8];
+    float b_hi[STAGES][KS][NT * 8];
+    float b_lo[STAGES][KS][NT * 8];
+    uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+    uint32_t tmem_base;
+    int64_t r_lo, r_hi;
+};
+
+// Epilogue state of one thread (= one feature column i of the CTA's M tile).
+template <int KS, bool MAX>
+struct Epi {
+    const Args* A;
+    int64_t r, r_hi, rs, re;
+    float best, q;
+    int bpos;
+    float w[KS * 8];
+    int i;            // global feature index
+    bool active;      // i < d2
+
+    __device__ __forceinline__ void start_row() {
+        best = MAX ? -INFINITY : 0.f;
+        bpos = -1;
+        float a = 0.f;
+        const float* xv = A->Xd + r * A->d_in;
+#pragma unroll
+        for (int k = 0; k < KS * 8; ++k)
+            if (k < A->d_in) a = fmaf(__ldg(xv + k), w[k], a);
+        q = a;
+    }
+    __device__ __forceinline__ void finish_row() {
+        if (!active) return;
+        const int64_t o = r * A->d2 + i;
+        if (!MAX) {
+            A->out[o] = best;
+            return;
+        }
+        if (re == rs) {
+            A->out[o] = 0.f;
+            if (A->arg_u) A->arg_u[o] = -1;
+            if (A->arg_e) A->arg_e[o] = -1;
+            return;
+        }
+        const float z = best + q;
+        const int pw = (z > 0.f) ? bpos : int(rs);
+        A->out[o] = (z > 0.f) ? z : 0.f;
+        if (A->arg_u) A->arg_u[o] = __ldg(A->col_idx + pw);
+        if (A->arg_e) A->arg_e[o] = A->eid ? __ldg(A->eid + pw) : pw;
+    }
+    // finish row r and move to r+1 (uniform across the epilogue threads)
+    __device__ __forceinline__ void advance() {
+        finish_row();
+        ++r;
+        if (r < r_hi) {
+            rs = re;
+            re = __ldg(A->row_ptr + r + 1);
+            start_row();
+        }
+    }
+    // consume 32 accumulator columns for CSR positions [pc0, pc0 + nvalid)
+    __device__ __forceinline__ void consume(const uint32_t (&v)[32], int64_t pc0, int nvalid) {
+        int c0 = 0;
+        while (c0 < nvalid) {
+            while (pc0 + c0 >= re) advance();
+            const int c1 = int(min(int64_t(nvalid), re - pc0));
+            if (MAX) {
+                // two interleaved partial maxima for ILP; ties -> lowest column
+                float b0 = -INFINITY, b1 = -INFINITY;
+                int k0 = 0, k1 = 0;
+                if (c0 == 0 && c1 == 32) {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        const float x0 = __uint_as_float(v[c]), x1 = __uint_as_float(v[c + 1]);
+                        if (x0 > b0) { b0 = x0; k0 = c; }
+                        if (x1 > b1) { b1 = x1; k1 = c + 1; }
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        const float x0 = __uint_as_float(v[c]), x1 = __uint_as_float(v[c + 1]);
+                        if (c >= c0 && c < c1 && x0 > b0) { b0 = x0; k0 = c; }
+                        if (c + 1 >= c0 && c + 1 < c1 && x1 > b1) { b1 = x1; k1 = c + 1; }
+                    }
+                }
+                if (b1 > b0 || (b1 == b0 && k1 < k0)) { b0 = b1; k0 = k1; }
+                if (b0 > best) { best = b0; bpos = int(pc0) + k0; }
+            } else {
+                float s0 = 0.f, s1 = 0.f;
+                if (c0 == 0 && c1 == 32) {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        s0 += fmaxf(__uint_as_float(v[c]) + q, 0.f);
+                        s1 += fmaxf(__uint_as_float(v[c + 1]) + q, 0.f);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        if (c >= c0 && c < c1) s0 += fmaxf(__uint_as_float(v[c]) + q, 0.f);
+                        if (c + 1 >= c0 && c + 1 < c1) s1 += fmaxf(__uint_as_float(v[c + 1]) + q, 0.f);
+                    }
+                }
+                best += s0 + s1;
+            }
+            c0 = c1;
+        }
+    }
+};
+
+template <int KS, bool MAX>
+__global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_constant__ Args A) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    Smem<KS>& S = *reinterpret_cast<Smem<KS>*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int mbase = blockIdx.y * MT;
+
+    if (tid == 0) {
+        const int64_t nb = gridDim.x, b = blockIdx.x;
+        const int64_t t_lo = (A.nnz * b) / nb, t_hi = (A.nnz * (b + 1)) / nb;
+        S.r_lo = (b == 0) ? 0 : lower_bound_rp(A.row_ptr, A.n_dst + 1, t_lo);
+        S.r_hi = (b == nb - 1) ? A.n_dst : lower_bound_rp(A.row_ptr, A.n_dst + 1, t_hi);
+        if (S.r_hi < S.r_lo) S.r_hi = S.r_lo;
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&S.full[s], NPROD * 32); mbar_init(&S.empty[s], 1); }
+        for (int b2 = 0; b2 < 2; ++b2) { mbar_init(&S.tfull[b2], 1); mbar_init(&S.tempty[b2], NEPI * 32); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // stage W^T (A operand) as tf32 hi / lo: row = feature, k = input dim
+    for (int idx = tid; idx < KS * MT * 8; idx += THREADS) {
+        const int ks = idx / (MT * 8), rem = idx % (MT * 8), r = rem / 8, k = rem % 8;
+        const int kk = ks * 8 + k, col = mbase + r;
+        const float w = (kk < A.d_in && col < A.d2) ? A.W[int64_t(kk) * A.d2 + col] : 0.f;
+        const float hi = tf32_rna(w);
+        const float lo = tf32_rna(w - hi);
+        *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(S.a_hi[ks]) + tile_off(r, k)) = hi;
+        *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(S.a_lo[ks]) + tile_off(r, k)) = lo;
+    }
+    fence_async_smem();
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = S.tmem_base;
+    const int64_t r_lo = S.r_lo, r_hi = S.r_hi;
+    const int64_t E0 = __ldg(A.row_ptr + r_lo), E1 = __ldg(A.row_ptr + r_hi);
+    const int ntiles = int((E1 - E0 + NT - 1) / NT);
+
+    if (warp >= MMA_WARP + 1) {
+        // ------------------------------------------------ producers: gather x_u, split, stage B
+        const int pt = tid - (MMA_WARP + 1) * 32;          // 0 .. NPROD*32-1
+        for (int t = 0; t < ntiles; ++t) {
+            const int s = t % STAGES;
+            mbar_wait(&S.empty[s], ((t / STAGES) & 1) ^ 1);
+            const int64_t tb = E0 + int64_t(t) * NT;
+            for (int e = pt; e < NT; e += NPROD * 32) {
+                const int64_t p = tb + e;
+                const bool ok = p < E1;
+                const int64_t u = ok ? __ldg(A.col_idx + p) : 0;
+                const float* xr = A.X + u * A.d_in;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int k0 = ks * 8 + c * 4;
+                        float4 x;
+                        if (ok && (A.d_in & 3) == 0 && k0 + 4 <= A.d_in) {
+                            x = __ldg(reinterpret_cast<const float4*>(xr + k0));
+                        } else {
+                            x.x = (ok && k0 + 0 < A.d_in) ? __ldg(xr + k0 + 0) : 0.f;
+                            x.y = (ok && k0 + 1 < A.d_in) ? __ldg(xr + k0 + 1) : 0.f;
+                            x.z = (ok && k0 + 2 < A.d_in) ? __ldg(xr + k0 + 2) : 0.f;
+                            x.w = (ok && k0 + 3 < A.d_in) ? __ldg(xr + k0 + 3) : 0.f;
+                        }
+                        float4 h, l;
+                        h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
+                        h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
+                        h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
+                        h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+                        const uint32_t off = tile_off(e, c * 4);
+                        *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(S.b_hi[s][ks]) + off) = h;
+                        *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(S.b_lo[s][ks]) + off) = l;
+                    }
+                }
+            }
+            fence_async_smem();
+            mbar_arrive(&S.full[s]);
+        }
+    } else if (warp == MMA_WARP) {
+        // ------------------------------------------------ MMA issuer (one thread)
+        if (lane == 0) {
+            for (int t = 0; t < ntiles; ++t) {
+                const int s = t % STAGES, b = t & 1;
+                mbar_wait(&S.full[s], (t / STAGES) & 1);
+                mbar_wait(&S.tempty[b], ((t >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + uint32_t(b * NT);
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    const uint64_t ah = smem_desc(smem_u32(S.a_hi[ks])), al = smem_desc(smem_u32(S.a_lo[ks]));
+                    const uint64_t bh = smem_desc(smem_u32(S.b_hi[s][ks])), bl = smem_desc(smem_u32(S.b_lo[s][ks]));
+                    mma_tf32(d, ah, bh, ks > 0 ? 1u : 0u);
+                    mma_tf32(d, ah, bl, 1u);
+                    mma_tf32(d, al, bh, 1u);
+                }
+                mma_commit(&S.empty[s]);
+                mma_commit(&S.tfull[b]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ epilogue: thread = feature
+        Epi<KS, MAX> ep;
+        ep.A = &A;
+        ep.i = mbase + tid;
+        ep.active = ep.i < A.d2;
+#pragma unroll
+        for (int k = 0; k < KS * 8; ++k)
+            ep.w[k] = (k < A.d_in && ep.active) ? __ldg(A.W + int64_t(k) * A.d2 + ep.i) : 0.f;
+        ep.r = r_lo;
+        ep.r_hi = r_hi;
+        if (r_lo < r_hi) {
+            ep.rs = __ldg(A.row_ptr + r_lo);
+            ep.re = __ldg(A.row_ptr + r_lo + 1);
+            ep.start_row();
+        }
+        const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+        for (int t = 0; t < ntiles; ++t) {
+            const int b = t & 1;
+            mbar_wait(&S.tfull[b], (t >> 1) & 1);
+            tc_fence_after();
+            const int64_t tb = E0 + int64_t(t) * NT;
+            const int nv_tile = int(min(int64_t(NT), E1 - tb));
+            uint32_t v0[32], v1[32];
+            tmem_ld32(lane_base + uint32_t(b * NT), v0);
+            tmem_wait_ld(v0);
+#pragma unroll
+            for (int ch = 0; ch < NT / 32; ch += 2) {   // chunk ch+1 loads while chunk ch is consumed
+                tmem_ld32(lane_base + uint32_t(b * NT + (ch + 1) * 32), v1);
+                ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)));
+                tmem_wait_ld(v1);
+                if (ch + 2 < NT / 32) tmem_ld32(lane_base + uint32_t(b * NT + (ch + 2) * 32), v0);
+                ep.consume(v1, tb + (ch + 1) * 32, max(0, min(32, nv_tile - (ch + 1) * 32)));
+                if (ch + 2 < NT / 32) tmem_wait_ld(v0);
+            }
+            tc_fence_before();
+            mbar_arrive(&S.tempty[b]);
+        }
+        while (ep.r < r_hi) ep.advance();   // trailing rows (empty rows after the last edge)
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == MMA_WARP) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
+template <int KS, bool MAX>
+fg_status launch_ks(const Args& A, cudaStream_t st) {
+    const int smem = int(sizeof(Smem<KS>)) + 1024;
+    // >= 100 KB per CTA keeps residency at <= 2 CTAs / SM (TMEM: 2 x 256 columns)
+    const int smem_req = smem < 100 * 1024 ? 100 * 1024 : smem;
+    auto kfn = mlp_tcgen05_kernel<KS, MAX>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_req);
+    if (e != cudaSuccess) return fgk::set_error(FG_ECUDA, "mlp_tcgen05: smem attribute: %s", cudaGetErrorString(e));
+    int nb = 2 * fgk::num_sms();
+    const int64_t want = (A.nnz + 4 * NT - 1) / (4 * NT);   // >= 4 tiles per CTA
+    if (want < nb) nb = int(want < 1 ? 1 : want);
+    const dim3 grid{unsigned(nb), unsigned((A.d2 + MT - 1) / MT), 1u};
+    kfn<<<grid, THREADS, smem_req, st>>>(A);
+    return fgk::check_launch("mlp_tcgen05_kernel");
+}
+
+}  // namespace
+
+namespace fgk {
+
+fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W,
+                                  int d_in, const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e,
+                                  cudaStream_t st) {
+    Args A;
+    A.row_ptr = g->row_ptr;
+    A.col_idx = g->col_idx;
+    A.eid = g->eid;
+    A.X = X;
+    A.Xd = X_dst;
+    A.W = W;
+    A.out = out;
+    A.arg_u = arg_u;
+    A.arg_e = arg_e;
+    A.n_dst = g->n_dst;
+    A.nnz = g->nnz;
+    A.d_in = d_in;
+    A.d2 = d2;
+    const bool mx = red == FG_REDUCE_MAX;
+    const int ks = (d_in + 7) / 8;
+    switch (ks) {
+        case 1: return mx ? launch_ks<1, true>(A, st) : launch_ks<1, false>(A, st);
+        case 2: return mx ? launch_ks<2, true>(A, st) : launch_ks<2, false>(A, st);
+        case 3: return mx ? launch_ks<3, true>(A, st) : launch_ks<3, false>(A, st);
+        default: return mx ? launch_ks<4, true>(A, st) : launch_ks<4, false>(A, st);
+    }
+}
+
+}  // namespace fgk

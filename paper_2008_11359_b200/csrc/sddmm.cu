@@ -9,15 +9,23 @@
 // sm_100a the reduction is a register butterfly (__shfl_xor_sync) inside a
 // group of G lanes, and the traversal is ROW-major in work units of <= 256
 // edges of one destination row (fg_graph unit table): the group loads Y[v]
-// into registers once per unit and then only gathers X[u] (coalesced
-// LDG.128 per lane), so the kernel is bound by the gather bytes m*F*4.
-// Heads are independent reductions: lanes that share a head
-// (D/4 consecutive lanes) reduce together.
+// into registers once per unit and then only gathers X[u] (coalesced LDG.128
+// per lane), so the kernel is bound by the gather bytes m*F*4.  Heads are
+// independent reductions: lanes that share a head (D/4
+// consecutive lanes) reduce together.
+//
+// Per batch of 32 edges the group stages the neighbour indices in shared
+// memory (one coalesced load) and the results in shared memory (one coalesced
+// store), so the loop body holds no global store and no unrolled-per-edge
+// index bookkeeping: the compact body keeps the instruction stream in cache
+// (the first version, fully unrolled, was instruction-fetch bound).
 #include "fg_internal.h"
 
 namespace {
 
 constexpr int THREADS = 256;
+
+enum { MODE_H1 = 0, MODE_HEADS = 1, MODE_GENERAL = 2 };
 
 template <int G>
 __device__ __forceinline__ unsigned group_mask(int lane) {
@@ -33,9 +41,6 @@ struct Args {
     const int64_t* row_ptr;
     const int32_t* col_idx;
     const int32_t* eid;
-    const float4* X;
-    const float4* Y;
-    float* out;
     int H, D4, F4;
 };
 
@@ -52,17 +57,24 @@ __device__ __forceinline__ float group_sum(float x, int W, unsigned mask) {
     return x;
 }
 
-// One group per work unit.  Mode A (H > 1, D4 <= G): every float4 chunk j of a
-// lane belongs to head (c / D4); reduce over D4 lanes per chunk.  Mode B (H == 1
-// or D4 > G): accumulate chunks in-lane, flush (reduce over all G lanes) at each
-// head boundary.
-template <int G, int NV>
-__global__ void __launch_bounds__(THREADS) sddmm_kernel(Args A) {
+// MODE_H1      : H == 1 and F <= 4*G*NV: one dot per edge, reduce over all G lanes.
+// MODE_HEADS   : H > 1, D4 = D/4 <= G (power of two), F <= 4*G*NV: chunk j of a
+//                lane belongs to head c / D4; reduce over D4 lanes per chunk.
+// MODE_GENERAL : H == 1 with F > 4*G*NV (column tiles; Y re-read through L1), or
+//                H > 1 with D4 > G (a head spans several chunks of a lane).
+template <int G, int NV, int MODE>
+__global__ void __launch_bounds__(THREADS, 2) sddmm_kernel(const Args A, const float4* __restrict__ X,
+                                                           const float4* __restrict__ Y, float* __restrict__ out) {
     constexpr int TW = G * NV;
-    constexpr int U = NV >= 4 ? 2 : (NV >= 2 ? 4 : 8);
-    constexpr int B = 32, R = B / G;
+    constexpr int B = G >= 4 ? 32 : 8;              // edges per batch
+    constexpr int U = NV >= 3 ? 2 : (NV == 2 ? 4 : 8);   // edges in flight per lane
+    constexpr int NGRP = THREADS / G;
+    constexpr int CAP = 32 * G;                           // staged results per group
+    __shared__ int s_idx[NGRP][B];
+    __shared__ float s_res[NGRP][CAP];
     const int lane = threadIdx.x & 31;
     const int gl = threadIdx.x & (G - 1);
+    const int gi = threadIdx.x / G;
     const unsigned mask = group_mask<G>(lane);
     const int64_t unit = (int64_t(blockIdx.x) * THREADS + threadIdx.x) / G;
     if (unit >= A.n_units) return;
@@ -70,12 +82,12 @@ __global__ void __launch_bounds__(THREADS) sddmm_kernel(Args A) {
     const int64_t s = A.unit_p0[unit];
     const int64_t e = min(s + A.unit_chunk, A.row_ptr[v + 1]);
     const int F4 = A.F4, H = A.H, D4 = A.D4;
-    const bool modeA = (H > 1) && (D4 <= G);
-    const int ntiles = (F4 + TW - 1) / TW;
+    const bool stage = (H * B <= CAP);
+    int* idx = s_idx[gi];
+    float* res = s_res[gi];
 
-    // Y[v] tile 0 stays in registers (single-tile case covers F <= 4*G*NV)
     float4 y0[NV];
-    const float4* yr = A.Y + v * F4;
+    const float4* yr = Y + v * F4;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const int c = gl + G * j;
@@ -84,22 +96,17 @@ __global__ void __launch_bounds__(THREADS) sddmm_kernel(Args A) {
 
     for (int64_t p0 = s; p0 < e; p0 += B) {
         const int cnt = int(min((int64_t)B, e - p0));
-        int uix[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int64_t p = p0 + gl + r * G;
-            uix[r] = (p < e) ? __ldg(A.col_idx + p) : 0;
-        }
-#pragma unroll
-        for (int t0 = 0; t0 < B; t0 += U) {
-            if (t0 >= cnt) break;
+        __syncwarp(mask);
+        for (int t = gl; t < cnt; t += G) idx[t] = __ldg(A.col_idx + p0 + t);
+        __syncwarp(mask);
+        for (int t0 = 0; t0 < cnt; t0 += U) {
             float4 x[U][NV];
             int us[U];
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
                 const int t = t0 + uu;
-                us[uu] = __shfl_sync(mask, uix[t / G], t % G, G);
-                const float4* xr = A.X + int64_t(us[uu]) * F4;
+                us[uu] = (t < cnt) ? idx[t] : 0;
+                const float4* xr = X + int64_t(us[uu]) * F4;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     const int c = gl + G * j;
@@ -110,45 +117,59 @@ __global__ void __launch_bounds__(THREADS) sddmm_kernel(Args A) {
             for (int uu = 0; uu < U; ++uu) {
                 const int t = t0 + uu;
                 if (t >= cnt) break;
-                const int64_t p = p0 + t;
-                const int64_t ed = A.eid ? int64_t(__ldg(A.eid + p)) : p;
-                float* o = A.out + ed * H;
-                if (modeA) {
+                float* rr = stage ? res + t * H
+                                  : out + (A.eid ? int64_t(__ldg(A.eid + p0 + t)) : (p0 + t)) * H;
+                if constexpr (MODE == MODE_H1) {
+                    float hs = 0.f;
+#pragma unroll
+                    for (int j = 0; j < NV; ++j) hs += dot4(x[uu][j], y0[j]);
+                    hs = group_sum<G>(hs, G, mask);
+                    if (gl == 0) rr[0] = hs;
+                } else if constexpr (MODE == MODE_HEADS) {
 #pragma unroll
                     for (int j = 0; j < NV; ++j) {
-                        const int c = gl + G * j;   // single tile: F4 <= TW when modeA (D4 <= G, checked at launch)
-                        float part = dot4(x[uu][j], y0[j]);
-                        part = group_sum<G>(part, D4, mask);
-                        if (c < F4 && (gl & (D4 - 1)) == 0) o[c / D4] = part;
+                        const int c = gl + G * j;
+                        const float part = group_sum<G>(dot4(x[uu][j], y0[j]), D4, mask);
+                        if (c < F4 && (gl & (D4 - 1)) == 0) rr[c / D4] = part;
                     }
                 } else {
+                    const int ntiles = (F4 + TW - 1) / TW;
                     float hs = 0.f;
                     int head = 0;
 #pragma unroll
                     for (int j = 0; j < NV; ++j) {
                         hs += dot4(x[uu][j], y0[j]);
-                        const int cend = G * (j + 1);          // first chunk index after this j
-                        if (j == NV - 1 || (H > 1 && cend % D4 == 0)) {
-                            if (ntiles == 1 || H > 1) {
-                                const float tot = group_sum<G>(hs, G, mask);
-                                if (gl == 0 && head < H && G * j < F4) o[head] = tot;
-                                hs = 0.f;
-                                ++head;
-                            }
+                        const int cend = G * (j + 1);
+                        if (H > 1 && (j == NV - 1 || cend % D4 == 0)) {
+                            const float tot = group_sum<G>(hs, G, mask);
+                            if (gl == 0 && head < H) rr[head] = tot;
+                            hs = 0.f;
+                            ++head;
                         }
                     }
-                    if (ntiles > 1 && H == 1) {
-                        // H == 1 with F > 4*G*NV: remaining tiles, Y re-read through L1
-                        const float4* xr = A.X + int64_t(us[uu]) * F4;
-                        for (int tile = 1; tile < ntiles; ++tile) {
+                    if (H == 1) {
+                        const float4* xr = X + int64_t(us[uu]) * F4;
+                        for (int tile = 1; tile < ntiles; ++tile)
                             for (int j = 0; j < NV; ++j) {
                                 const int c = tile * TW + gl + G * j;
                                 if (c < F4) hs += dot4(__ldg(xr + c), __ldg(yr + c));
                             }
-                        }
                         const float tot = group_sum<G>(hs, G, mask);
-                        if (gl == 0) o[0] = tot;
+                        if (gl == 0) rr[0] = tot;
                     }
+                }
+            }
+        }
+        if (stage) {   // coalesced write-back of the batch's results
+            __syncwarp(mask);
+            const int tot = cnt * H;
+            if (A.eid == nullptr) {
+                float* o = out + p0 * H;
+                for (int q = gl; q < tot; q += G) o[q] = res[q];
+            } else {
+                for (int q = gl; q < tot; q += G) {
+                    const int t = q / H, h = q - t * H;
+                    out[int64_t(__ldg(A.eid + p0 + t)) * H + h] = res[q];
                 }
             }
         }
@@ -156,11 +177,17 @@ __global__ void __launch_bounds__(THREADS) sddmm_kernel(Args A) {
 }
 
 template <int G, int NV>
-fg_status launch_t(const Args& A, cudaStream_t st) {
+fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, cudaStream_t st) {
     const int64_t per_block = THREADS / G;
     const int64_t blocks = (A.n_units + per_block - 1) / per_block;
     if (blocks == 0) return FG_OK;
-    sddmm_kernel<G, NV><<<unsigned(blocks), THREADS, 0, st>>>(A);
+    const int TW = G * NV;
+    if (A.H == 1 && A.F4 <= TW)
+        sddmm_kernel<G, NV, MODE_H1><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
+    else if (A.H > 1 && A.D4 <= G && A.F4 <= TW)
+        sddmm_kernel<G, NV, MODE_HEADS><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
+    else
+        sddmm_kernel<G, NV, MODE_GENERAL><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
     return fgk::check_launch("sddmm_kernel");
 }
 
@@ -178,9 +205,6 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     A.row_ptr = g->row_ptr;
     A.col_idx = g->col_idx;
     A.eid = g->eid;
-    A.X = reinterpret_cast<const float4*>(X);
-    A.Y = reinterpret_cast<const float4*>(Y);
-    A.out = out;
     A.H = H;
     A.F4 = H * D / 4;
     A.D4 = (H > 1) ? D / 4 : A.F4;
@@ -195,21 +219,21 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     } else if (F4 <= 96) {
         NV = 3;
     }
-    // multi-head with F > 4*G*NV: heads larger than a tile are handled by mode B
-    // only when a head boundary falls on a tile boundary of a single tile.
     if (H > 1 && F4 > G * NV)
         return set_error(FG_EUNSUPPORTED, "fg_sddmm: multi-head with H*D > 512 not implemented");
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    const float4* Y4 = reinterpret_cast<const float4*>(Y);
     switch (G) {
-        case 1: return launch_t<1, 1>(A, st);
-        case 2: return launch_t<2, 1>(A, st);
-        case 4: return launch_t<4, 1>(A, st);
-        case 8: return launch_t<8, 1>(A, st);
-        case 16: return launch_t<16, 1>(A, st);
+        case 1: return launch_t<1, 1>(A, X4, Y4, out, st);
+        case 2: return launch_t<2, 1>(A, X4, Y4, out, st);
+        case 4: return launch_t<4, 1>(A, X4, Y4, out, st);
+        case 8: return launch_t<8, 1>(A, X4, Y4, out, st);
+        case 16: return launch_t<16, 1>(A, X4, Y4, out, st);
         default:
-            if (NV == 1) return launch_t<32, 1>(A, st);
-            if (NV == 2) return launch_t<32, 2>(A, st);
-            if (NV == 3) return launch_t<32, 3>(A, st);
-            return launch_t<32, 4>(A, st);
+            if (NV == 1) return launch_t<32, 1>(A, X4, Y4, out, st);
+            if (NV == 2) return launch_t<32, 2>(A, X4, Y4, out, st);
+            if (NV == 3) return launch_t<32, 3>(A, X4, Y4, out, st);
+            return launch_t<32, 4>(A, X4, Y4, out, st);
     }
 }
 
