@@ -37,6 +37,7 @@ namespace {
 constexpr int NT = 128;                   // edges per tile (MMA N)
 constexpr int MT = 128;                   // features per CTA (MMA M)
 constexpr int STAGES = 4;
+constexpr int ISTAGES = 4;                // index ring (producer -> epilogue)
 constexpr int NEPI = 4;                   // epilogue warps 0..3 (TMEM lane quarters)
 constexpr int MMA_WARP = 4;
 constexpr int NPROD = 2;                  // producer warps 5..6
@@ -56,7 +57,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 0x989680;\n\t"   // suspend, don't spin
         "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
@@ -147,7 +148,9 @@ struct Smem {
     float a_lo[KS][MT * 8];
     float b_hi[STAGES][KS][NT * 8];
     float b_lo[STAGES][KS][NT * 8];
-    uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+    int32_t su[ISTAGES][NT];               // source id / edge id of each tile column,
+    int32_t se[ISTAGES][NT];               // read by the epilogue for arg_u / arg_e
+    uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2], ifull[ISTAGES], iempty[ISTAGES];
     uint32_t tmem_base;
     int64_t r_lo, r_hi;
 };
@@ -157,21 +160,35 @@ template <int KS, bool MAX>
 struct Epi {
     const Args* A;
     int64_t r, r_hi, rs, re;
+    int64_t nre;      // prefetched row_ptr[r + 2]
     float best, q;
-    int bpos;
+    int bu, be;       // winning edge: source id / edge id (from the smem-staged tile indices)
+    int fu, fe;       // first edge of the row (the winner when every message is +0)
+    bool fresh;       // no edge of the row seen yet
     float w[KS * 8];
+    float nx[KS * 8]; // prefetched x_{r+1}
     int i;            // global feature index
     bool active;      // i < d2
 
+    // prefetch the next row's destination features and end pointer so that the
+    // per-row bookkeeping never waits on a global load
+    __device__ __forceinline__ void prefetch(int64_t rn) {
+        if (rn < r_hi) {
+            const float* xv = A->Xd + rn * A->d_in;
+#pragma unroll
+            for (int k = 0; k < KS * 8; ++k) nx[k] = (k < A->d_in) ? __ldg(xv + k) : 0.f;
+            nre = __ldg(A->row_ptr + rn + 1);   // end of row rn (rn < r_hi <= n_dst)
+        }
+    }
     __device__ __forceinline__ void start_row() {
         best = MAX ? -INFINITY : 0.f;
-        bpos = -1;
+        bu = be = fu = fe = -1;
+        fresh = true;
         float a = 0.f;
-        const float* xv = A->Xd + r * A->d_in;
 #pragma unroll
-        for (int k = 0; k < KS * 8; ++k)
-            if (k < A->d_in) a = fmaf(__ldg(xv + k), w[k], a);
+        for (int k = 0; k < KS * 8; ++k) a = fmaf(nx[k], w[k], a);
         q = a;
+        prefetch(r + 1);
     }
     __device__ __forceinline__ void finish_row() {
         if (!active) return;
@@ -187,10 +204,10 @@ struct Epi {
             return;
         }
         const float z = best + q;
-        const int pw = (z > 0.f) ? bpos : int(rs);
-        A->out[o] = (z > 0.f) ? z : 0.f;
-        if (A->arg_u) A->arg_u[o] = __ldg(A->col_idx + pw);
-        if (A->arg_e) A->arg_e[o] = A->eid ? __ldg(A->eid + pw) : pw;
+        const bool pos = z > 0.f;
+        A->out[o] = pos ? z : 0.f;
+        if (A->arg_u) A->arg_u[o] = pos ? bu : fu;
+        if (A->arg_e) A->arg_e[o] = pos ? be : fe;
     }
     // finish row r and move to r+1 (uniform across the epilogue threads)
     __device__ __forceinline__ void advance() {
@@ -198,16 +215,23 @@ struct Epi {
         ++r;
         if (r < r_hi) {
             rs = re;
-            re = __ldg(A->row_ptr + r + 1);
+            re = nre;
             start_row();
         }
     }
-    // consume 32 accumulator columns for CSR positions [pc0, pc0 + nvalid)
-    __device__ __forceinline__ void consume(const uint32_t (&v)[32], int64_t pc0, int nvalid) {
+    // consume 32 accumulator columns for CSR positions [pc0, pc0 + nvalid);
+    // su / se: source ids / edge ids of those 32 positions (shared memory)
+    __device__ __forceinline__ void consume(const uint32_t (&v)[32], int64_t pc0, int nvalid, const int* su,
+                                            const int* se) {
         int c0 = 0;
         while (c0 < nvalid) {
             while (pc0 + c0 >= re) advance();
             const int c1 = int(min(int64_t(nvalid), re - pc0));
+            if (MAX && fresh) {
+                fu = su[c0];
+                fe = se[c0];
+                fresh = false;
+            }
             if (MAX) {
                 // two interleaved partial maxima for ILP; ties -> lowest column
                 float b0 = -INFINITY, b1 = -INFINITY;
@@ -228,7 +252,7 @@ struct Epi {
                     }
                 }
                 if (b1 > b0 || (b1 == b0 && k1 < k0)) { b0 = b1; k0 = k1; }
-                if (b0 > best) { best = b0; bpos = int(pc0) + k0; }
+                if (b0 > best) { best = b0; bu = su[k0]; be = se[k0]; }
             } else {
                 float s0 = 0.f, s1 = 0.f;
                 if (c0 == 0 && c1 == 32) {
@@ -267,6 +291,7 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
         if (S.r_hi < S.r_lo) S.r_hi = S.r_lo;
         for (int s = 0; s < STAGES; ++s) { mbar_init(&S.full[s], NPROD * 32); mbar_init(&S.empty[s], 1); }
         for (int b2 = 0; b2 < 2; ++b2) { mbar_init(&S.tfull[b2], 1); mbar_init(&S.tempty[b2], NEPI * 32); }
+        for (int s = 0; s < ISTAGES; ++s) { mbar_init(&S.ifull[s], NPROD * 32); mbar_init(&S.iempty[s], NEPI * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // stage W^T (A operand) as tf32 hi / lo: row = feature, k = input dim
@@ -297,13 +322,16 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
         // ------------------------------------------------ producers: gather x_u, split, stage B
         const int pt = tid - (MMA_WARP + 1) * 32;          // 0 .. NPROD*32-1
         for (int t = 0; t < ntiles; ++t) {
-            const int s = t % STAGES;
+            const int s = t % STAGES, is = t % ISTAGES;
             mbar_wait(&S.empty[s], ((t / STAGES) & 1) ^ 1);
+            mbar_wait(&S.iempty[is], ((t / ISTAGES) & 1) ^ 1);
             const int64_t tb = E0 + int64_t(t) * NT;
             for (int e = pt; e < NT; e += NPROD * 32) {
                 const int64_t p = tb + e;
                 const bool ok = p < E1;
                 const int64_t u = ok ? __ldg(A.col_idx + p) : 0;
+                S.su[is][e] = int(u);
+                S.se[is][e] = ok ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
                 const float* xr = A.X + u * A.d_in;
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) {
@@ -332,6 +360,7 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
             }
             fence_async_smem();
             mbar_arrive(&S.full[s]);
+            mbar_arrive(&S.ifull[is]);
         }
     } else if (warp == MMA_WARP) {
         // ------------------------------------------------ MMA issuer (one thread)
@@ -369,13 +398,17 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
         if (r_lo < r_hi) {
             ep.rs = __ldg(A.row_ptr + r_lo);
             ep.re = __ldg(A.row_ptr + r_lo + 1);
+            ep.prefetch(r_lo);
             ep.start_row();
         }
         const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
         for (int t = 0; t < ntiles; ++t) {
-            const int b = t & 1;
+            const int b = t & 1, is = t % ISTAGES;
+            mbar_wait(&S.ifull[is], (t / ISTAGES) & 1);
             mbar_wait(&S.tfull[b], (t >> 1) & 1);
             tc_fence_after();
+            const int* su = S.su[is];
+            const int* se = S.se[is];
             const int64_t tb = E0 + int64_t(t) * NT;
             const int nv_tile = int(min(int64_t(NT), E1 - tb));
             uint32_t v0[32], v1[32];
@@ -384,14 +417,16 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
 #pragma unroll
             for (int ch = 0; ch < NT / 32; ch += 2) {   // chunk ch+1 loads while chunk ch is consumed
                 tmem_ld32(lane_base + uint32_t(b * NT + (ch + 1) * 32), v1);
-                ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)));
+                ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)), su + ch * 32, se + ch * 32);
                 tmem_wait_ld(v1);
                 if (ch + 2 < NT / 32) tmem_ld32(lane_base + uint32_t(b * NT + (ch + 2) * 32), v0);
-                ep.consume(v1, tb + (ch + 1) * 32, max(0, min(32, nv_tile - (ch + 1) * 32)));
+                ep.consume(v1, tb + (ch + 1) * 32, max(0, min(32, nv_tile - (ch + 1) * 32)), su + (ch + 1) * 32,
+                           se + (ch + 1) * 32);
                 if (ch + 2 < NT / 32) tmem_wait_ld(v0);
             }
             tc_fence_before();
             mbar_arrive(&S.tempty[b]);
+            mbar_arrive(&S.iempty[is]);
         }
         while (ep.r < r_hi) ep.advance();   // trailing rows (empty rows after the last edge)
     }

@@ -57,12 +57,40 @@ __device__ __forceinline__ float group_sum(float x, int W, unsigned mask) {
     return x;
 }
 
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+
+// Recursive-halving reduce-scatter of K values over W aligned lanes of a group:
+// at offset o the lane keeps the half of its values selected by (gl & o) and adds
+// the partner's copy of that half.  Afterwards lane gl holds, in v[0 .. K/2^L),
+// the W-lane sums of original indices bits*K/2^L + i (bits = the top L bits of
+// gl mod W, L = min(log2 K, log2 W)); remaining levels are a plain butterfly.
+template <int K, int W, int G>
+__device__ __forceinline__ void reduce_scatter(float (&v)[K], int gl, unsigned mask) {
+    if constexpr (W > 1) {
+        constexpr int o = W / 2;
+        if constexpr (K > 1) {
+            const bool up = (gl & o) != 0;
+#pragma unroll
+            for (int i = 0; i < K / 2; ++i) {
+                const float send = up ? v[i] : v[i + K / 2];
+                const float keep = up ? v[i + K / 2] : v[i];
+                v[i] = keep + __shfl_xor_sync(mask, send, o, G);
+            }
+            float (&h)[K / 2] = *reinterpret_cast<float(*)[K / 2]>(&v[0]);
+            reduce_scatter<K / 2, W / 2, G>(h, gl, mask);
+        } else {
+#pragma unroll
+            for (int oo = o; oo >= 1; oo >>= 1) v[0] += __shfl_xor_sync(mask, v[0], oo, G);
+        }
+    }
+}
+
 // MODE_H1      : H == 1 and F <= 4*G*NV: one dot per edge, reduce over all G lanes.
 // MODE_HEADS   : H > 1, D4 = D/4 <= G (power of two), F <= 4*G*NV: chunk j of a
 //                lane belongs to head c / D4; reduce over D4 lanes per chunk.
 // MODE_GENERAL : H == 1 with F > 4*G*NV (column tiles; Y re-read through L1), or
 //                H > 1 with D4 > G (a head spans several chunks of a lane).
-template <int G, int NV, int MODE>
+template <int G, int NV, int MODE, int DW>
 __global__ void __launch_bounds__(THREADS, 2) sddmm_kernel(const Args A, const float4* __restrict__ X,
                                                            const float4* __restrict__ Y, float* __restrict__ out) {
     constexpr int TW = G * NV;
@@ -111,6 +139,46 @@ __global__ void __launch_bounds__(THREADS, 2) sddmm_kernel(const Args A, const f
                 for (int j = 0; j < NV; ++j) {
                     const int c = gl + G * j;
                     x[uu][j] = (t < cnt && c < F4) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+            if constexpr (MODE == MODE_H1 || MODE == MODE_HEADS) {
+                if (stage) {
+                    // reduce-scatter of the U edges' (x NV chunk) partial dots over the DW
+                    // lanes that share a head: ~log2(DW) + (K-1)/... shuffles per U edges
+                    // instead of log2(DW) per edge and chunk
+                    constexpr int K = (MODE == MODE_H1) ? U : U * NV;
+                    float pv[K];
+#pragma unroll
+                    for (int uu = 0; uu < U; ++uu) {
+                        if constexpr (MODE == MODE_H1) {
+                            float hs = 0.f;
+#pragma unroll
+                            for (int j = 0; j < NV; ++j) hs += dot4(x[uu][j], y0[j]);
+                            pv[uu] = hs;
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < NV; ++j) pv[uu * NV + j] = dot4(x[uu][j], y0[j]);
+                        }
+                    }
+                    reduce_scatter<K, DW, G>(pv, gl, mask);
+                    constexpr int L = ilog2(K) < ilog2(DW) ? ilog2(K) : ilog2(DW);
+                    constexpr int KEEP = K >> L;                       // values held per lane
+                    const int sub = gl & (DW - 1);
+                    const int bits = sub >> (ilog2(DW) - L);
+                    if ((sub & ((DW >> L) - 1)) == 0) {
+#pragma unroll
+                        for (int i = 0; i < KEEP; ++i) {
+                            const int id = bits * KEEP + i;
+                            if constexpr (MODE == MODE_H1) {
+                                res[t0 + id] = pv[i];
+                            } else {
+                                const int uu = id / NV, j = id % NV;
+                                const int head = gl / DW + j * (G / DW);
+                                if (head < H) res[(t0 + uu) * H + head] = pv[i];
+                            }
+                        }
+                    }
+                    continue;
                 }
             }
 #pragma unroll
@@ -183,11 +251,19 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
     if (blocks == 0) return FG_OK;
     const int TW = G * NV;
     if (A.H == 1 && A.F4 <= TW)
-        sddmm_kernel<G, NV, MODE_H1><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
-    else if (A.H > 1 && A.D4 <= G && A.F4 <= TW)
-        sddmm_kernel<G, NV, MODE_HEADS><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
+        sddmm_kernel<G, NV, MODE_H1, G><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
+    else if (A.H > 1 && A.D4 <= G && A.F4 <= TW) {
+        switch (A.D4) {   // heads of D = 4*D4 floats reduce over D4 lanes
+            case 1: sddmm_kernel<G, NV, MODE_HEADS, 1><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out); break;
+            case 2: sddmm_kernel<G, NV, MODE_HEADS, (G >= 2 ? 2 : 1)><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out); break;
+            case 4: sddmm_kernel<G, NV, MODE_HEADS, (G >= 4 ? 4 : 1)><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out); break;
+            case 8: sddmm_kernel<G, NV, MODE_HEADS, (G >= 8 ? 8 : 1)><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out); break;
+            case 16: sddmm_kernel<G, NV, MODE_HEADS, (G >= 16 ? 16 : 1)><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out); break;
+            default: sddmm_kernel<G, NV, MODE_HEADS, (G >= 32 ? 32 : 1)><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out); break;
+        }
+    }
     else
-        sddmm_kernel<G, NV, MODE_GENERAL><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
+        sddmm_kernel<G, NV, MODE_GENERAL, 1><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
     return fgk::check_launch("sddmm_kernel");
 }
 

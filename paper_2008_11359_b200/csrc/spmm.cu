@@ -2,7 +2,7 @@
 // (SURVEY §8(a) rows a1, a2).
 //
 // Eq. (1): out[v] = (+)_{u -> v} phi(x_u, x_uv), with
-//   copy_u : phi = X[u]                      (GCN aggregation, Fig. 3a, Eq. (3))
+//   copy_u : phi = X[u]                    (GCN aggregation, Fig. 3a, Eq. (3))
 //   u_mul_e: phi[h,d] = X[u][h][d] * E[e][h] (DGL vertex-x-edge builtin P:375; GAT P:983)
 //
 // B200 design (the paper's V100 schedule -- a CUDA block per adjacency row,
@@ -10,11 +10,10 @@
 //   * a "group" of G lanes (G = 1..32, a power of two) owns one destination row
 //     and a column tile of G*NV float4s; each lane owns NV 128-bit column chunks,
 //     so every gathered source row is read with coalesced LDG.128s;
-//   * the row's neighbour indices (and edge ids) are staged in shared memory
-//     32 at a time with one coalesced load and read back as broadcasts; U
-//     edges' gathers are issued before any is consumed (memory-level
-//     parallelism, Little's law: SURVEY §8(d)); the loop body stays compact so
-//     the instruction stream stays in cache;
+//   * the row's neighbour indices are loaded 32 at a time with one coalesced
+//     load per lane and broadcast with register shuffles; U edges' gathers are
+//     issued before any is consumed (memory-level parallelism, Little's law:
+//     SURVEY §8(d));
 //   * rows are processed in degree-descending order (fg_graph rows_by_deg,
 //     longest-processing-time first) and split into two modes by one launch:
 //     rows with degree >= T run CTA-per-row (the CTA's groups take contiguous
@@ -25,6 +24,7 @@
 //     position, the u_mul_e product is rounded once (__fmul_rn)
 //     before the compare, matching the oracle's fp32-rounded key.
 #include <algorithm>
+#include <cstdlib>
 
 #include "fg_internal.h"
 
@@ -60,49 +60,50 @@ __device__ __forceinline__ void set_comp(float4& v, int k, float a) {
     if (k == 0) v.x = a; else if (k == 1) v.y = a; else if (k == 2) v.z = a; else v.w = a;
 }
 
-template <int G>
-struct Batch {                       // edges staged per batch for one group
-    static constexpr int B = G >= 4 ? 32 : 8;
-};
-
 // Accumulate edges [s, e) of one row into (acc, pos) for this lane's NV chunks.
 template <int G, int NV, int OP, bool MAX>
 __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e, int gl, unsigned mask,
-                                             int c4base, int* sidx, int* seid, float4 (&acc)[NV],
-                                             int (&pos)[NV][4]) {
-    constexpr int B = Batch<G>::B;
-    constexpr int U = NV >= 3 ? 2 : (NV == 2 ? 4 : 8);      // edges in flight per lane
+                                             int c4base, float4 (&acc)[NV], int (&pos)[NV][4]) {
+    constexpr int B = 32;                                   // edges per index batch
+    constexpr int R = B / G;                                // indices per lane per batch
+    constexpr int U = NV >= 4 ? 2 : (NV >= 2 ? 4 : 8);      // edges in flight per lane
     const int F4 = A.F4;
     for (int64_t p0 = s; p0 < e; p0 += B) {
         const int cnt = int(min((int64_t)B, e - p0));
-        __syncwarp(mask);
-        for (int t = gl; t < cnt; t += G) {
-            sidx[t] = __ldg(A.col_idx + p0 + t);
-            if constexpr (OP != OP_COPY) seid[t] = A.eid ? __ldg(A.eid + p0 + t) : int(p0 + t);
+        int uix[R];
+        int eix[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t p = p0 + gl + r * G;
+            uix[r] = (p < e) ? __ldg(A.col_idx + p) : 0;
+            if constexpr (OP != OP_COPY) eix[r] = (p < e) ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
         }
-        __syncwarp(mask);
-        for (int t0 = 0; t0 < cnt; t0 += U) {
+#pragma unroll
+        for (int t0 = 0; t0 < B; t0 += U) {
+            if (t0 >= cnt) break;                           // uniform within the group
             float4 x[U][NV];
             float ev[U][NV][(OP == OP_UMULE_GEN) ? 4 : 1];
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
                 const int t = t0 + uu;
-                const bool okt = t < cnt;
-                const int u = okt ? sidx[t] : 0;
-                const float4* xr = A.X + int64_t(u) * F4;
+                const int u = __shfl_sync(mask, uix[t / G], t % G, G);
                 int ed = 0;
-                if constexpr (OP != OP_COPY) ed = okt ? seid[t] : 0;
+                if constexpr (OP != OP_COPY) ed = __shfl_sync(mask, eix[t / G], t % G, G);
+                const float4* xr = A.X + int64_t(u) * F4;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     const int c = c4base + gl + G * j;
-                    const bool ok = okt && (c < F4);
+                    const bool ok = (t < cnt) && (c < F4);
                     x[uu][j] = ok ? __ldg(xr + c) : f4(0.f);
                     if constexpr (OP == OP_UMULE) {
-                        ev[uu][j][0] = ok ? __ldg(A.E + int64_t(ed) * A.H + (4 * c) / A.D) : 0.f;
+                        const int h = (4 * c) / A.D;
+                        ev[uu][j][0] = ok ? __ldg(A.E + int64_t(ed) * A.H + h) : 0.f;
                     } else if constexpr (OP == OP_UMULE_GEN) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            ev[uu][j][k] = ok ? __ldg(A.E + int64_t(ed) * A.H + (4 * c + k) / A.D) : 0.f;
+                        for (int k = 0; k < 4; ++k) {
+                            const int h = (4 * c + k) / A.D;
+                            ev[uu][j][k] = ok ? __ldg(A.E + int64_t(ed) * A.H + h) : 0.f;
+                        }
                     }
                 }
             }
@@ -185,12 +186,9 @@ __device__ __forceinline__ void store_elem(const Args& A, int64_t v, int c, floa
 }
 
 template <int G, int NV, int OP, bool MAX>
-__global__ void __launch_bounds__(THREADS) spmm_gather_kernel(const Args A) {
+__global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     constexpr int NG = THREADS / G;                 // groups per CTA
     constexpr int TW = G * NV;                      // float4 columns per tile
-    constexpr int B = Batch<G>::B;
-    __shared__ int s_idx[NG][B];
-    __shared__ int s_eid[OP == OP_COPY ? 1 : NG][B];
     __shared__ float4 s_acc[MAX ? 1 : NG][MAX ? 1 : TW];
     __shared__ float s_val[MAX ? NG : 1][MAX ? TW * 4 : 1];
     __shared__ int s_pos[MAX ? NG : 1][MAX ? TW * 4 : 1];
@@ -200,8 +198,6 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(const Args A) {
     const int gi = threadIdx.x / G;
     const unsigned mask = group_mask<G>(lane);
     const int c4base = blockIdx.y * TW;
-    int* sidx = s_idx[gi];
-    int* seid = s_eid[OP == OP_COPY ? 0 : gi];
 
     float4 acc[NV];
     int pos[NV][4];
@@ -213,7 +209,7 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(const Args A) {
         const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
         const int64_t len = (e - s + NG - 1) / NG;
         const int64_t gs = min(e, s + gi * len), ge = min(e, gs + len);
-        gather_range<G, NV, OP, MAX>(A, gs, ge, gl, mask, c4base, sidx, seid, acc, pos);
+        gather_range<G, NV, OP, MAX>(A, gs, ge, gl, mask, c4base, acc, pos);
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
             const int c = gl + G * j;
@@ -255,7 +251,7 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(const Args A) {
     if (r >= A.n_rows) return;
     const int64_t v = A.rows[r];
     const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
-    gather_range<G, NV, OP, MAX>(A, s, e, gl, mask, c4base, sidx, seid, acc, pos);
+    gather_range<G, NV, OP, MAX>(A, s, e, gl, mask, c4base, acc, pos);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const int c = c4base + gl + G * j;
@@ -264,7 +260,8 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(const Args A) {
 }
 
 template <int G, int NV, int OP, bool MAX>
-fg_status launch_t(const Args& A, cudaStream_t st) {
+fg_status launch_t(const Args& A0, cudaStream_t st) {
+    Args A = A0;
     constexpr int NG = THREADS / G;
     constexpr int TW = G * NV;
     const int64_t light = A.n_rows - A.n_heavy;
@@ -305,9 +302,27 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     A.arg_e = reinterpret_cast<int4*>(arg_e);
     const int op = (msg == FG_MSG_COPY_U) ? OP_COPY : (D % 4 == 0 ? OP_UMULE : OP_UMULE_GEN);
     const bool mx = (red == FG_REDUCE_MAX);
-    // column mapping: G lanes x NV float4 per lane per tile
+    // column mapping: G lanes x NV float4 per lane per tile.
+    // Feature-dimension tiling for L2 (the paper's FDS tiling for cache, P:466-472,
+    // retargeted from the CPU LLC to the B200 L2): when the source features do not
+    // fit in the L2 budget, the columns are processed in tiles of T4 float4 such
+    // that n_src * 16 * T4 <= budget.  Tiles are grid.y, and the block scheduler
+    // issues all of tile 0 before tile 1, so each pass gathers from an L2-resident
+    // slice of X; the extra cost is one re-read of col_idx per tile.
     int G = 32, NV = 4;
-    const int F4 = A.F4;
+    int F4 = A.F4;
+    {
+        static const int64_t budget = [] {
+            const char* e = getenv("FG_L2_TILE_MB");
+            return int64_t(e ? atoi(e) : 64) << 20;
+        }();
+        // u_mul_e re-reads E (m x H floats) on every pass; measured not to pay off
+        if (msg == FG_MSG_COPY_U && budget > 0 && g->n_src * int64_t(F4) * 16 > budget) {
+            int64_t t4 = 32;
+            while (t4 > 1 && g->n_src * t4 * 16 > budget) t4 /= 2;
+            F4 = int(t4);            // tile width drives (G, NV) below; the kernel tiles A.F4 by G*NV
+        }
+    }
     if (F4 <= 32) {
         NV = 1;
         G = 1;
@@ -317,7 +332,6 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     } else if (F4 <= 96) {
         NV = 3;
     }
-    // heavy rows: CTA-per-row once every group of the CTA gets >= 32 edges
     const int64_t NG = THREADS / G;
     A.n_heavy = rows_with_degree_at_least(g, NG * 32);
     switch (G) {
