@@ -406,7 +406,11 @@ def main():
         "mlp_tflops": round(mlp_flops(S.m) / (op_ms["spmm_mlp_max_d8_d128_args"] * 1e-3) / 1e12, 2),
         "roofline": {"kernel": DOMINANT, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
+                     "bytes_model": "gather model (SURVEY 8(d)): every per-edge source-row read counted at "
+                                    "full width; L2 serves most of them (feature-dimension tiling), so "
+                                    "achieved/peak > 1; 'traffic' is the ncu DRAM bytes of one launch",
+                     "dram_frac": (round(traffic / (dom_ms * 1e-3) / 1e9 / peak, 4) if traffic else None)},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": Step.LAUNCHES_PER_STEP * args.steps,

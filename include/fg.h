@@ -170,6 +170,43 @@ fg_status fg_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, const float* 
 fg_status fg_edge_softmax(const fg_graph* g, int H, const float* scores, float* out,
                           fg_stream stream);
 
+/* ---------------------------------------------------------------- backward */
+/*
+ * Gradients by the paper's gradient duality (the gradient
+ * of SpMM follows the SDDMM pattern and vice versa).  Deterministic pulls, no
+ * atomics.
+ *
+ * fg_graph_transpose -- the transposed handle gT (rows = sources, CSC of g),
+ *   each row ascending, with eid mapping every transposed position to g's edge
+ *   id, so edge tensors are shared between g and gT.  gT OWNS its arrays (built
+ *   on the host from a copy of g's CSR; synchronous, per topology, like
+ *   fg_graph_create).  Destroy with fg_graph_destroy.
+ *
+ * fg_spmm_backward -- for out = fg_spmm(g, msg, red, H, D, X, E, ...):
+ *   msg in {FG_MSG_COPY_U, FG_MSG_U_MUL_E} (mlp: FG_EUNSUPPORTED -- SPEC.md
+ *   S:380 non-goal);
+ *   dOut [n_dst][H*D];  dX [n_src][H*D] (optional, needs gT);  dE [nnz][H]
+ *   (optional, u_mul_e only, needs X);  max needs arg_u from the forward (only
+ *   the winning edge of each (v, j) receives dOut[v][j]).  Outputs overwritten.
+ *
+ * fg_sddmm_backward -- for s = fg_sddmm(g, u_dot_v, H, D, X, Y):
+ *   dX [n_src][H*D] = sum_{e=u->v} dS[e] Y[v] (needs gT, Y);
+ *   dY [n_dst][H*D] = sum_{e=u->v} dS[e] X[u] (needs X).  Either may be NULL.
+ *   When Y is X (square graph) the caller adds dX + dY.
+ *
+ * fg_edge_softmax_backward -- for alpha = fg_edge_softmax(g, H, s):
+ *   dscores[e][h] = alpha[e][h] (dalpha[e][h] - sum_{e' in row(e)} alpha[e'][h] dalpha[e'][h]).
+ *   dscores must not alias alpha or dalpha.
+ */
+fg_status fg_graph_transpose(const fg_graph* g, fg_stream stream, fg_graph** out);
+fg_status fg_spmm_backward(const fg_graph* g, const fg_graph* gT, fg_msg_op msg, fg_reduce_op red, int H, int D,
+                           const float* X, const float* E, const float* dOut, const int32_t* arg_u, float* dX,
+                           float* dE, fg_stream stream);
+fg_status fg_sddmm_backward(const fg_graph* g, const fg_graph* gT, fg_edge_op op, int H, int D, const float* X,
+                            const float* Y, const float* dS, float* dX, float* dY, fg_stream stream);
+fg_status fg_edge_softmax_backward(const fg_graph* g, int H, const float* alpha, const float* dalpha,
+                                   float* dscores, fg_stream stream);
+
 /* ---------------------------------------------------------------- multi-GPU */
 /*
  * Destination-row sharding (one process per GPU).  Each rank

@@ -137,3 +137,58 @@ def edge_positions(row_ptr, rows) -> np.ndarray:
     lens = ends - starts
     idx = np.repeat(starts - np.concatenate([[0], np.cumsum(lens)[:-1]]), lens)
     return idx + np.arange(lens.sum())
+
+
+# ------------------------------------------------------------------ backward (gradient duality)
+def _bind_backward():
+    lib = _L()
+    if getattr(lib, "_bw_bound", False):
+        return lib
+    i64, i32, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+    lib.or_spmm_backward.argtypes = [i64, i64, i64, vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]
+    lib.or_spmm_backward.restype = None
+    lib.or_sddmm_backward.argtypes = [i64, i64, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]
+    lib.or_sddmm_backward.restype = None
+    lib.or_edge_softmax_backward.argtypes = [i64, vp, vp, i32, vp, vp, vp]
+    lib.or_edge_softmax_backward.restype = None
+    lib._bw_bound = True
+    return lib
+
+
+def spmm_backward(row_ptr, col_idx, op: str, red: str, X, dOut, *, n_src: int, H: int = 1, E=None, eid=None,
+                  arg_u=None, want_dE: bool = False):
+    """Gradients of Eq. (1) (copy_u / u_mul_e, sum / max).  Returns (dX, dE) fp64."""
+    row_ptr, col_idx, eid = _c(row_ptr, np.int64), _c(col_idx, np.int32), _c(eid, np.int32)
+    X, dOut, E = _c(X, np.float32), _c(dOut, np.float32), _c(E, np.float32)
+    arg_u = _c(arg_u, np.int32)
+    n_dst = row_ptr.size - 1
+    nnz = int(row_ptr[-1])
+    F = dOut.reshape(n_dst, -1).shape[1] if n_dst else X.reshape(n_src, -1).shape[1]
+    D = F // H
+    dX = np.empty((n_src, F), np.float64)
+    dE = np.empty((nnz, H), np.float64) if want_dE else None
+    _bind_backward().or_spmm_backward(n_dst, n_src, nnz, _p(row_ptr), _p(col_idx), _p(eid), OPS[op], REDS[red], H,
+                                      D, _p(X), _p(E), _p(dOut), _p(arg_u), _p(dX), _p(dE))
+    return dX, dE
+
+
+def sddmm_backward(row_ptr, col_idx, X, Y, dS, *, H: int = 1, eid=None):
+    """Gradients of Eq. (4) u_dot_v w.r.t. X (sources) and Y (destinations), fp64."""
+    row_ptr, col_idx, eid = _c(row_ptr, np.int64), _c(col_idx, np.int32), _c(eid, np.int32)
+    X, Y, dS = _c(X, np.float32), _c(Y, np.float32), _c(dS, np.float32)
+    n_dst, n_src = row_ptr.size - 1, X.shape[0]
+    F = X.reshape(n_src, -1).shape[1]
+    dX = np.empty((n_src, F), np.float64)
+    dY = np.empty((n_dst, F), np.float64)
+    _bind_backward().or_sddmm_backward(n_dst, n_src, _p(row_ptr), _p(col_idx), _p(eid), H, F // H, _p(X), _p(Y),
+                                       _p(dS), _p(dX), _p(dY))
+    return dX, dY
+
+
+def edge_softmax_backward(row_ptr, alpha, dalpha, *, H: int = 1, eid=None):
+    row_ptr, eid = _c(row_ptr, np.int64), _c(eid, np.int32)
+    alpha, dalpha = _c(alpha, np.float32), _c(dalpha, np.float32)
+    ds = np.empty(alpha.shape, np.float64)
+    _bind_backward().or_edge_softmax_backward(row_ptr.size - 1, _p(row_ptr), _p(eid), H, _p(alpha), _p(dalpha),
+                                              _p(ds))
+    return ds

@@ -186,3 +186,78 @@ void or_edge_softmax(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr
     }
     free(off);
 }
+
+/* ======================================================================
+ * Backward (gradients) -- the gradient duality of PAPER.md P:171-173 ("the
+ * gradient computation of SpMM with respect to A requires a dot product ...
+ * thus following the SDDMM pattern; likewise the gradient computation of
+ * SDDMM follows the SpMM pattern"), written as the chain rule per edge.
+ * All over the ORIGINAL graph (edge p = u -> v of row v); accumulations in
+ * fp64; dX / dY / dE are zeroed here.  Pinned by torch autograd on dense
+ * formulations (tests/test_oracle_backward.py).
+ * ====================================================================== */
+
+/* d/dX and d/dE of Eq. (1) for copy_u / u_mul_e with sum or max.
+ * sum : dX[u][j] += dOut[v][j] * (u_mul_e ? E[e][j/D] : 1)
+ *       dE[e][h] += sum_{d<D} dOut[v][h*D+d] * X[u][h*D+d]           (u_mul_e)
+ * max : only the winning edge of (v, j) (arg_u[v][j] = its source, the
+ *       forward's first-wins argmax; -1 for empty rows) gets the gradient. */
+void or_spmm_backward(int64_t n_dst, int64_t n_src, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                      const int32_t* eid, int op, int red, int H, int D, const float* X, const float* E,
+                      const float* dOut, const int32_t* arg_u, double* dX, double* dE) {
+    const int64_t F = (int64_t)H * D;
+    if (dX) for (int64_t i = 0; i < n_src * F; ++i) dX[i] = 0.0;
+    if (dE) for (int64_t i = 0; i < nnz * H; ++i) dE[i] = 0.0;
+    for (int64_t v = 0; v < n_dst; ++v) {
+        for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {
+            const int64_t u = col_idx[p];
+            const int64_t e = edge_id(eid, p);
+            for (int64_t j = 0; j < F; ++j) {
+                if (red == OR_MAX && arg_u[v * F + j] != u) continue;   /* not the winner */
+                const double g = (double)dOut[v * F + j];
+                const double w = (op == OR_U_MUL_E) ? (double)E[e * H + j / D] : 1.0;
+                if (dX) dX[u * F + j] += g * w;
+                if (dE && op == OR_U_MUL_E) dE[e * H + j / D] += g * (double)X[u * F + j];
+            }
+        }
+    }
+}
+
+/* d/dX and d/dY of Eq. (4) u_dot_v: s[e][h] = sum_d X[u][h,d] Y[v][h,d]. */
+void or_sddmm_backward(int64_t n_dst, int64_t n_src, const int64_t* row_ptr, const int32_t* col_idx,
+                       const int32_t* eid, int H, int D, const float* X, const float* Y, const float* dS,
+                       double* dX, double* dY) {
+    const int64_t F = (int64_t)H * D;
+    if (dX) for (int64_t i = 0; i < n_src * F; ++i) dX[i] = 0.0;
+    if (dY) for (int64_t i = 0; i < n_dst * F; ++i) dY[i] = 0.0;
+    for (int64_t v = 0; v < n_dst; ++v)
+        for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {
+            const int64_t u = col_idx[p];
+            const int64_t e = edge_id(eid, p);
+            for (int h = 0; h < H; ++h) {
+                const double g = (double)dS[e * H + h];
+                for (int d = 0; d < D; ++d) {
+                    const int64_t j = (int64_t)h * D + d;
+                    if (dX) dX[u * F + j] += g * (double)Y[v * F + j];
+                    if (dY) dY[v * F + j] += g * (double)X[u * F + j];
+                }
+            }
+        }
+}
+
+/* d/ds of the edge softmax: ds[e][h] = alpha[e][h] * (dalpha[e][h] - sum_{e' in row} alpha[e'][h] dalpha[e'][h]). */
+void or_edge_softmax_backward(int64_t n_dst, const int64_t* row_ptr, const int32_t* eid, int H, const float* alpha,
+                              const float* dalpha, double* ds) {
+    for (int64_t v = 0; v < n_dst; ++v)
+        for (int h = 0; h < H; ++h) {
+            double dot = 0.0;
+            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {
+                const int64_t e = edge_id(eid, p);
+                dot += (double)alpha[e * H + h] * (double)dalpha[e * H + h];
+            }
+            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {
+                const int64_t e = edge_id(eid, p);
+                ds[e * H + h] = (double)alpha[e * H + h] * ((double)dalpha[e * H + h] - dot);
+            }
+        }
+}

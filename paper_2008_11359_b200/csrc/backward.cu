@@ -1,0 +1,276 @@
+// backward.cu -- gradients of the hot-path ops.
+//
+// The gradient duality of PAPER.md P:171-173: "the gradient computation of
+// SpMM with respect to A requires a dot product between the gradients of
+// source and destination vertex features, thus following the SDDMM pattern.
+// Likewise, the gradient computation of SDDMM follows the SpMM pattern."
+// Concretely (edge p = u -> v with edge id e, rows of g are destinations,
+// rows of the transposed handle gT are sources):
+//   spmm sum   dX = spmm(gT, dOut)            (u_mul_e: weighted by E via gT's eid)
+//              dE = sddmm(g, X, dOut)         (u_mul_e)
+//   spmm max   only the forward's winning edge of (v, j) gets dOut[v][j]:
+//              dX[u][j] = sum_{v: arg_u[v][j] == u} dOut[v][j] (* E[e][j/D])   -- masked gather over gT
+//              dE[e][h] = sum_{j in h: arg_u[v][j] == u} dOut[v][j] * X[u][j]  -- masked SDDMM over g
+//   sddmm      dX = spmm_{u_mul_e}(gT, Y, dS),  dY = spmm_{u_mul_e}(g, X, dS)
+//   softmax    ds[e][h] = alpha[e][h] * (dalpha[e][h] - sum_row alpha * dalpha)
+// Every kernel is a pull over rows (no atomics): deterministic.
+#include <algorithm>
+#include <vector>
+
+#include "fg_internal.h"
+
+namespace {
+constexpr int THREADS = 256;
+
+// dX[u][:] for max aggregation: one warp per row u of gT, lanes over float4 columns.
+template <bool UMULE>
+__global__ void __launch_bounds__(THREADS) max_backward_dx_kernel(
+    const int32_t* __restrict__ rows, int64_t n_rows, const int64_t* __restrict__ rpT,
+    const int32_t* __restrict__ ciT, const int32_t* __restrict__ eidT, const float4* __restrict__ dOut,
+    const int4* __restrict__ arg_u, const float* __restrict__ E, int H, int D, int F4, float4* __restrict__ dX) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t(blockIdx.x) * THREADS + threadIdx.x) >> 5;
+    if (r >= n_rows) return;
+    const int64_t u = rows[r];
+    const int64_t s = rpT[u], e = rpT[u + 1];
+    for (int c0 = 0; c0 < F4; c0 += 32) {
+        const int c = c0 + lane;
+        if (c >= F4) break;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t p = s; p < e; ++p) {
+            const int64_t v = __ldg(ciT + p);
+            const int4 a = __ldg(arg_u + v * F4 + c);
+            if (a.x != u && a.y != u && a.z != u && a.w != u) continue;
+            const float4 g = __ldg(dOut + v * F4 + c);
+            float w0 = 1.f, w1 = 1.f, w2 = 1.f, w3 = 1.f;
+            if (UMULE) {
+                const int64_t ed = eidT ? int64_t(__ldg(eidT + p)) : p;
+                w0 = __ldg(E + ed * H + (4 * c + 0) / D);
+                w1 = __ldg(E + ed * H + (4 * c + 1) / D);
+                w2 = __ldg(E + ed * H + (4 * c + 2) / D);
+                w3 = __ldg(E + ed * H + (4 * c + 3) / D);
+            }
+            if (a.x == u) acc.x = fmaf(g.x, w0, acc.x);
+            if (a.y == u) acc.y = fmaf(g.y, w1, acc.y);
+            if (a.z == u) acc.z = fmaf(g.z, w2, acc.z);
+            if (a.w == u) acc.w = fmaf(g.w, w3, acc.w);
+        }
+        dX[u * F4 + c] = acc;
+    }
+}
+
+// dE[e][h] for u_mul_e max: one thread per (edge, head) of g.
+__global__ void __launch_bounds__(THREADS) max_backward_de_kernel(
+    int64_t n_dst, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const int32_t* __restrict__ eid,
+    const float* __restrict__ X, const float* __restrict__ dOut, const int32_t* __restrict__ arg_u, int H, int D,
+    int64_t nnz, float* __restrict__ dE) {
+    const int64_t t = int64_t(blockIdx.x) * THREADS + threadIdx.x;
+    if (t >= nnz * H) return;
+    const int64_t p = t / H;
+    const int h = int(t % H);
+    // destination row of CSR position p: binary search on row_ptr
+    int64_t lo = 0, hi = n_dst;   // largest v with rp[v] <= p
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(rp + mid) <= p) lo = mid; else hi = mid;
+    }
+    const int64_t v = lo, u = __ldg(ci + p);
+    const int64_t F = int64_t(H) * D;
+    float acc = 0.f;
+    for (int d = 0; d < D; ++d) {
+        const int64_t j = int64_t(h) * D + d;
+        if (__ldg(arg_u + v * F + j) == u) acc = fmaf(__ldg(dOut + v * F + j), __ldg(X + u * F + j), acc);
+    }
+    dE[(eid ? int64_t(__ldg(eid + p)) : p) * H + h] = acc;
+}
+
+// softmax backward, H divides 32: warp per row, lane-strided over (edge, head).
+__global__ void __launch_bounds__(THREADS) softmax_backward_warp_kernel(
+    const int32_t* __restrict__ rows, int64_t n_rows, const int64_t* __restrict__ rp, const int32_t* __restrict__ eid,
+    int H, const float* __restrict__ alpha, const float* __restrict__ dalpha, float* __restrict__ ds) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t(blockIdx.x) * THREADS + threadIdx.x) >> 5;
+    if (r >= n_rows) return;
+    const int64_t v = rows[r];
+    const int64_t s0 = rp[v], n = (rp[v + 1] - s0) * H;
+    const int h = lane % H;
+    float dot = 0.f;
+    for (int64_t q = lane; q < n; q += 32) {
+        const int64_t idx = eid ? int64_t(__ldg(eid + s0 + q / H)) * H + h : s0 * H + q;
+        dot = fmaf(__ldg(alpha + idx), __ldg(dalpha + idx), dot);
+    }
+    for (int o = 16; o >= H; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    for (int64_t q = lane; q < n; q += 32) {
+        const int64_t idx = eid ? int64_t(__ldg(eid + s0 + q / H)) * H + h : s0 * H + q;
+        ds[idx] = __ldg(alpha + idx) * (__ldg(dalpha + idx) - dot);
+    }
+}
+
+// softmax backward, generic H: thread per (row, head).
+__global__ void __launch_bounds__(THREADS) softmax_backward_thread_kernel(
+    const int32_t* __restrict__ rows, int64_t n_rows, const int64_t* __restrict__ rp, const int32_t* __restrict__ eid,
+    int H, const float* __restrict__ alpha, const float* __restrict__ dalpha, float* __restrict__ ds) {
+    const int64_t t = int64_t(blockIdx.x) * THREADS + threadIdx.x;
+    if (t >= n_rows * H) return;
+    const int64_t v = rows[t / H];
+    const int h = int(t % H);
+    float dot = 0.f;
+    for (int64_t p = rp[v]; p < rp[v + 1]; ++p) {
+        const int64_t idx = (eid ? int64_t(eid[p]) : p) * H + h;
+        dot = fmaf(alpha[idx], dalpha[idx], dot);
+    }
+    for (int64_t p = rp[v]; p < rp[v + 1]; ++p) {
+        const int64_t idx = (eid ? int64_t(eid[p]) : p) * H + h;
+        ds[idx] = alpha[idx] * (dalpha[idx] - dot);
+    }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool is_transpose_of(const fg_graph* g, const fg_graph* gT) {
+    return gT && gT->n_dst == g->n_src && gT->n_src == g->n_dst && gT->nnz == g->nnz;
+}
+}  // namespace
+
+using fgk::set_error;
+
+extern "C" fg_status fg_graph_transpose(const fg_graph* g, fg_stream stream, fg_graph** out) {
+    if (!g || !out) return set_error(FG_EINVAL, "fg_graph_transpose: NULL argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t nd = g->n_dst, ns = g->n_src, m = g->nnz;
+    std::vector<int64_t> rp(static_cast<size_t>(nd + 1)), rpT(static_cast<size_t>(ns + 1), 0);
+    std::vector<int32_t> ci(static_cast<size_t>(m)), eid(g->eid ? static_cast<size_t>(m) : 0),
+        ciT(static_cast<size_t>(m)), eidT(static_cast<size_t>(m));
+    cudaError_t e = cudaMemcpyAsync(rp.data(), g->row_ptr, sizeof(int64_t) * size_t(nd + 1), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && m) e = cudaMemcpyAsync(ci.data(), g->col_idx, sizeof(int32_t) * size_t(m), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && m && g->eid) e = cudaMemcpyAsync(eid.data(), g->eid, sizeof(int32_t) * size_t(m), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_error(FG_ECUDA, "fg_graph_transpose: %s", cudaGetErrorString(e));
+    // counting sort by source; iterating destinations in order keeps every
+    // transposed row ascending (deterministic CSC)
+    for (int64_t p = 0; p < m; ++p) rpT[size_t(ci[size_t(p)]) + 1]++;
+    for (int64_t u = 0; u < ns; ++u) rpT[size_t(u + 1)] += rpT[size_t(u)];
+    std::vector<int64_t> cur(rpT.begin(), rpT.end() - 1);
+    for (int64_t v = 0; v < nd; ++v)
+        for (int64_t p = rp[size_t(v)]; p < rp[size_t(v + 1)]; ++p) {
+            const int64_t q = cur[size_t(ci[size_t(p)])]++;
+            ciT[size_t(q)] = int32_t(v);
+            eidT[size_t(q)] = g->eid ? eid[size_t(p)] : int32_t(p);   // original edge id
+        }
+    int64_t* d_rp = nullptr;
+    int32_t *d_ci = nullptr, *d_eid = nullptr;
+    e = cudaMalloc(&d_rp, sizeof(int64_t) * size_t(ns + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&d_ci, sizeof(int32_t) * size_t(std::max<int64_t>(m, 1)));
+    if (e == cudaSuccess) e = cudaMalloc(&d_eid, sizeof(int32_t) * size_t(std::max<int64_t>(m, 1)));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_rp, rpT.data(), sizeof(int64_t) * size_t(ns + 1), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && m) e = cudaMemcpyAsync(d_ci, ciT.data(), sizeof(int32_t) * size_t(m), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && m) e = cudaMemcpyAsync(d_eid, eidT.data(), sizeof(int32_t) * size_t(m), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_eid);
+        return set_error(e == cudaErrorMemoryAllocation ? FG_ENOMEM : FG_ECUDA, "fg_graph_transpose: %s",
+                         cudaGetErrorString(e));
+    }
+    fg_graph* gT = nullptr;
+    fg_status s = fg_graph_create(ns, nd, m, d_rp, d_ci, d_eid, 0, stream, &gT);
+    if (s != FG_OK) {
+        cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_eid);
+        return s;
+    }
+    gT->owned_row_ptr = d_rp;
+    gT->owned_col_idx = d_ci;
+    gT->owned_eid = d_eid;
+    gT->device_bytes += sizeof(int64_t) * (ns + 1) + 8 * m;
+    *out = gT;
+    return FG_OK;
+}
+
+extern "C" fg_status fg_spmm_backward(const fg_graph* g, const fg_graph* gT, fg_msg_op msg, fg_reduce_op red, int H,
+                                      int D, const float* X, const float* E, const float* dOut,
+                                      const int32_t* arg_u, float* dX, float* dE, fg_stream stream) {
+    if (!g) return set_error(FG_EINVAL, "fg_spmm_backward: NULL graph");
+    if (msg != FG_MSG_COPY_U && msg != FG_MSG_U_MUL_E)
+        return set_error(FG_EUNSUPPORTED, "fg_spmm_backward: only copy_u / u_mul_e (SPEC non-goal: mlp through W)");
+    if (red != FG_REDUCE_SUM && red != FG_REDUCE_MAX) return set_error(FG_EINVAL, "fg_spmm_backward: bad reduce op");
+    if (H < 1 || D < 1 || (int64_t(H) * D) % 4) return set_error(FG_ESHAPE, "fg_spmm_backward: H*D must be a multiple of 4");
+    if (!dOut) return set_error(FG_EINVAL, "fg_spmm_backward: dOut is NULL");
+    if (dX && !is_transpose_of(g, gT)) return set_error(FG_EINVAL, "fg_spmm_backward: dX needs gT = fg_graph_transpose(g)");
+    if (msg == FG_MSG_U_MUL_E && !E) return set_error(FG_EINVAL, "fg_spmm_backward: u_mul_e needs E");
+    if (dE && (msg != FG_MSG_U_MUL_E || !X)) return set_error(FG_EINVAL, "fg_spmm_backward: dE needs u_mul_e and X");
+    if (red == FG_REDUCE_MAX && !arg_u) return set_error(FG_EINVAL, "fg_spmm_backward: max needs the forward's arg_u");
+    if (!aligned16(dOut) || !aligned16(dX) || !aligned16(X) || !aligned16(arg_u))
+        return set_error(FG_EINVAL, "fg_spmm_backward: tensors must be 16-byte aligned");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int F4 = H * D / 4;
+    if (red == FG_REDUCE_SUM) {
+        if (dX) {
+            fg_status s = fgk::launch_spmm_gather(gT, msg, FG_REDUCE_SUM, H, D, dOut, msg == FG_MSG_U_MUL_E ? E : nullptr,
+                                                  dX, nullptr, nullptr, st);
+            if (s != FG_OK) return s;
+        }
+        if (dE) return fg_sddmm(g, FG_EDGE_U_DOT_V, H, D, X, dOut, dE, stream);
+        return FG_OK;
+    }
+    if (dX && gT->n_dst > 0) {
+        const int64_t blocks = (gT->n_dst * 32 + THREADS - 1) / THREADS;
+        if (msg == FG_MSG_U_MUL_E)
+            max_backward_dx_kernel<true><<<unsigned(blocks), THREADS, 0, st>>>(
+                gT->rows_by_deg, gT->n_dst, gT->row_ptr, gT->col_idx, gT->eid, reinterpret_cast<const float4*>(dOut),
+                reinterpret_cast<const int4*>(arg_u), E, H, D, F4, reinterpret_cast<float4*>(dX));
+        else
+            max_backward_dx_kernel<false><<<unsigned(blocks), THREADS, 0, st>>>(
+                gT->rows_by_deg, gT->n_dst, gT->row_ptr, gT->col_idx, gT->eid, reinterpret_cast<const float4*>(dOut),
+                reinterpret_cast<const int4*>(arg_u), E, H, D, F4, reinterpret_cast<float4*>(dX));
+        fg_status s = fgk::check_launch("max_backward_dx_kernel");
+        if (s != FG_OK) return s;
+    }
+    if (dE && g->nnz > 0) {
+        const int64_t blocks = (g->nnz * H + THREADS - 1) / THREADS;
+        max_backward_de_kernel<<<unsigned(blocks), THREADS, 0, st>>>(g->n_dst, g->row_ptr, g->col_idx, g->eid, X, dOut,
+                                                                    arg_u, H, D, g->nnz, dE);
+        return fgk::check_launch("max_backward_de_kernel");
+    }
+    return FG_OK;
+}
+
+extern "C" fg_status fg_sddmm_backward(const fg_graph* g, const fg_graph* gT, fg_edge_op op, int H, int D,
+                                       const float* X, const float* Y, const float* dS, float* dX, float* dY,
+                                       fg_stream stream) {
+    if (!g) return set_error(FG_EINVAL, "fg_sddmm_backward: NULL graph");
+    if (op != FG_EDGE_U_DOT_V) return set_error(FG_EINVAL, "fg_sddmm_backward: bad edge op");
+    if (!dS) return set_error(FG_EINVAL, "fg_sddmm_backward: dS is NULL");
+    if (dX && (!Y || !is_transpose_of(g, gT)))
+        return set_error(FG_EINVAL, "fg_sddmm_backward: dX needs Y and gT = fg_graph_transpose(g)");
+    if (dY && !X) return set_error(FG_EINVAL, "fg_sddmm_backward: dY needs X");
+    // dX[u] = sum_{e = u->v} dS[e] * Y[v]  : u_mul_e-sum over gT with features Y
+    if (dX) {
+        fg_status s = fg_spmm(gT, FG_MSG_U_MUL_E, FG_REDUCE_SUM, H, D, Y, dS, nullptr, 0, nullptr, dX, nullptr, nullptr,
+                              nullptr, 0, stream);
+        if (s != FG_OK) return s;
+    }
+    // dY[v] = sum_{e = u->v} dS[e] * X[u]  : u_mul_e-sum over g with features X
+    if (dY)
+        return fg_spmm(g, FG_MSG_U_MUL_E, FG_REDUCE_SUM, H, D, X, dS, nullptr, 0, nullptr, dY, nullptr, nullptr,
+                       nullptr, 0, stream);
+    return FG_OK;
+}
+
+extern "C" fg_status fg_edge_softmax_backward(const fg_graph* g, int H, const float* alpha, const float* dalpha,
+                                              float* dscores, fg_stream stream) {
+    if (!g) return set_error(FG_EINVAL, "fg_edge_softmax_backward: NULL graph");
+    if (H < 1 || H > 4096) return set_error(FG_ESHAPE, "fg_edge_softmax_backward: bad H");
+    if (g->nnz == 0) return FG_OK;
+    if (!alpha || !dalpha || !dscores) return set_error(FG_EINVAL, "fg_edge_softmax_backward: NULL tensor");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t n_rows = g->n_nonempty;
+    if (32 % H == 0) {
+        const int64_t blocks = (n_rows * 32 + THREADS - 1) / THREADS;
+        softmax_backward_warp_kernel<<<unsigned(blocks), THREADS, 0, st>>>(g->rows_by_deg, n_rows, g->row_ptr, g->eid,
+                                                                           H, alpha, dalpha, dscores);
+    } else {
+        const int64_t blocks = (n_rows * H + THREADS - 1) / THREADS;
+        softmax_backward_thread_kernel<<<unsigned(blocks), THREADS, 0, st>>>(g->rows_by_deg, n_rows, g->row_ptr,
+                                                                             g->eid, H, alpha, dalpha, dscores);
+    }
+    return fgk::check_launch("edge_softmax_backward");
+}

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -13,6 +14,10 @@ struct fg_graph {
     const int32_t* col_idx = nullptr;   // borrowed, device
     const int32_t* eid = nullptr;       // borrowed, device (nullptr = identity)
     int device = 0;
+    // set only for handles made by fg_graph_transpose (the library owns their CSR)
+    int64_t* owned_row_ptr = nullptr;
+    int32_t* owned_col_idx = nullptr;
+    int32_t* owned_eid = nullptr;
 
     // derived (owned, device)
     int32_t* rows_by_deg = nullptr;     // [n_dst] rows sorted by degree, descending (stable)
@@ -54,6 +59,13 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
 fg_status launch_edge_softmax(const fg_graph* g, int H, const float* S, float* out, cudaStream_t st);
 
 fg_status check_launch(const char* what);
+
+// L2 budget (bytes) for feature-dimension tiling of the gathered operand;
+// FG_L2_TILE_MB overrides the default (64 MiB, half the 126 MB L2), 0 disables.
+inline int64_t l2_tile_budget() {
+    const char* e = getenv("FG_L2_TILE_MB");
+    return int64_t(e ? atoi(e) : 64) << 20;
+}
 
 inline int num_sms() {
     static int n = 0;

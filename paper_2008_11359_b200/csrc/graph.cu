@@ -199,6 +199,9 @@ extern "C" fg_status fg_graph_destroy(fg_graph* g) {
     if (g->rows_by_deg) cudaFree(g->rows_by_deg);
     if (g->unit_row) cudaFree(g->unit_row);
     if (g->unit_p0) cudaFree(g->unit_p0);
+    if (g->owned_row_ptr) cudaFree(g->owned_row_ptr);
+    if (g->owned_col_idx) cudaFree(g->owned_col_idx);
+    if (g->owned_eid) cudaFree(g->owned_eid);
     delete g;
     return FG_OK;
 }

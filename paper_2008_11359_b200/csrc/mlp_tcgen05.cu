@@ -320,42 +320,69 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
 
     if (warp >= MMA_WARP + 1) {
         // ------------------------------------------------ producers: gather x_u, split, stage B
+        // Each thread owns EPT edges of every tile.  The indices of tile t+1 are
+        // loaded while tile t's feature rows are in flight, and all EPT rows of a
+        // tile are requested before any is converted: one L2 round trip per tile
+        // instead of two dependent ones per edge.
+        constexpr int EPT = NT / (NPROD * 32);
         const int pt = tid - (MMA_WARP + 1) * 32;          // 0 .. NPROD*32-1
+        int u_nx[EPT], e_nx[EPT];
+        auto load_idx = [&](int t, int (&u)[EPT], int (&ed)[EPT]) {
+            const int64_t tb = E0 + int64_t(t) * NT;
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                const int64_t p = tb + pt + i * NPROD * 32;
+                const bool ok = p < E1;
+                u[i] = ok ? __ldg(A.col_idx + p) : -1;
+                ed[i] = ok ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
+            }
+        };
+        if (ntiles > 0) load_idx(0, u_nx, e_nx);
         for (int t = 0; t < ntiles; ++t) {
             const int s = t % STAGES, is = t % ISTAGES;
+            int u_cur[EPT], e_cur[EPT];
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) { u_cur[i] = u_nx[i]; e_cur[i] = e_nx[i]; }
+            float4 xa[EPT][2 * KS];
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                const bool ok = u_cur[i] >= 0;
+                const float* xr = A.X + int64_t(ok ? u_cur[i] : 0) * A.d_in;
+#pragma unroll
+                for (int c = 0; c < 2 * KS; ++c) {
+                    const int k0 = c * 4;
+                    float4 x;
+                    if (ok && (A.d_in & 3) == 0 && k0 + 4 <= A.d_in) {
+                        x = __ldg(reinterpret_cast<const float4*>(xr + k0));
+                    } else {
+                        x.x = (ok && k0 + 0 < A.d_in) ? __ldg(xr + k0 + 0) : 0.f;
+                        x.y = (ok && k0 + 1 < A.d_in) ? __ldg(xr + k0 + 1) : 0.f;
+                        x.z = (ok && k0 + 2 < A.d_in) ? __ldg(xr + k0 + 2) : 0.f;
+                        x.w = (ok && k0 + 3 < A.d_in) ? __ldg(xr + k0 + 3) : 0.f;
+                    }
+                    xa[i][c] = x;
+                }
+            }
+            if (t + 1 < ntiles) load_idx(t + 1, u_nx, e_nx);
             mbar_wait(&S.empty[s], ((t / STAGES) & 1) ^ 1);
             mbar_wait(&S.iempty[is], ((t / ISTAGES) & 1) ^ 1);
-            const int64_t tb = E0 + int64_t(t) * NT;
-            for (int e = pt; e < NT; e += NPROD * 32) {
-                const int64_t p = tb + e;
-                const bool ok = p < E1;
-                const int64_t u = ok ? __ldg(A.col_idx + p) : 0;
-                S.su[is][e] = int(u);
-                S.se[is][e] = ok ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
-                const float* xr = A.X + u * A.d_in;
 #pragma unroll
-                for (int ks = 0; ks < KS; ++ks) {
+            for (int i = 0; i < EPT; ++i) {
+                const int e = pt + i * NPROD * 32;
+                S.su[is][e] = u_cur[i];
+                S.se[is][e] = e_cur[i];
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        const int k0 = ks * 8 + c * 4;
-                        float4 x;
-                        if (ok && (A.d_in & 3) == 0 && k0 + 4 <= A.d_in) {
-                            x = __ldg(reinterpret_cast<const float4*>(xr + k0));
-                        } else {
-                            x.x = (ok && k0 + 0 < A.d_in) ? __ldg(xr + k0 + 0) : 0.f;
-                            x.y = (ok && k0 + 1 < A.d_in) ? __ldg(xr + k0 + 1) : 0.f;
-                            x.z = (ok && k0 + 2 < A.d_in) ? __ldg(xr + k0 + 2) : 0.f;
-                            x.w = (ok && k0 + 3 < A.d_in) ? __ldg(xr + k0 + 3) : 0.f;
-                        }
-                        float4 h, l;
-                        h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
-                        h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
-                        h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
-                        h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
-                        const uint32_t off = tile_off(e, c * 4);
-                        *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(S.b_hi[s][ks]) + off) = h;
-                        *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(S.b_lo[s][ks]) + off) = l;
-                    }
+                for (int c = 0; c < 2 * KS; ++c) {
+                    const int ks = c / 2;
+                    const float4 x = xa[i][c];
+                    float4 h, l;
+                    h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
+                    h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
+                    h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
+                    h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+                    const uint32_t off = tile_off(e, (c % 2) * 4);
+                    *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(S.b_hi[s][ks]) + off) = h;
+                    *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(S.b_lo[s][ks]) + off) = l;
                 }
             }
             fence_async_smem();

@@ -19,6 +19,8 @@
 // store), so the loop body holds no global store and no unrolled-per-edge
 // index bookkeeping: the compact body keeps the instruction stream in cache
 // (the first version, fully unrolled, was instruction-fetch bound).
+#include <cstdlib>
+
 #include "fg_internal.h"
 
 namespace {
@@ -42,6 +44,9 @@ struct Args {
     const int32_t* col_idx;
     const int32_t* eid;
     int H, D4, F4;
+    int c4base;       // first float4 column of this pass (feature-dimension tiling, H == 1)
+    int accumulate;   // pass > 0: out += partial
+    int tile4;        // float4 columns per pass (0: one pass over all F4)
 };
 
 __device__ __forceinline__ float dot4(const float4& a, const float4& b) {
@@ -118,7 +123,7 @@ __global__ void __launch_bounds__(THREADS, 2) sddmm_kernel(const Args A, const f
     const float4* yr = Y + v * F4;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-        const int c = gl + G * j;
+        const int c = A.c4base + gl + G * j;
         y0[j] = (c < F4) ? __ldg(yr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(THREADS, 2) sddmm_kernel(const Args A, const f
                 const float4* xr = X + int64_t(us[uu]) * F4;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
-                    const int c = gl + G * j;
+                    const int c = A.c4base + gl + G * j;
                     x[uu][j] = (t < cnt && c < F4) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
@@ -233,11 +238,15 @@ __global__ void __launch_bounds__(THREADS, 2) sddmm_kernel(const Args A, const f
             const int tot = cnt * H;
             if (A.eid == nullptr) {
                 float* o = out + p0 * H;
-                for (int q = gl; q < tot; q += G) o[q] = res[q];
+                if (A.accumulate)
+                    for (int q = gl; q < tot; q += G) o[q] += res[q];
+                else
+                    for (int q = gl; q < tot; q += G) o[q] = res[q];
             } else {
                 for (int q = gl; q < tot; q += G) {
                     const int t = q / H, h = q - t * H;
-                    out[int64_t(__ldg(A.eid + p0 + t)) * H + h] = res[q];
+                    float* o = out + int64_t(__ldg(A.eid + p0 + t)) * H + h;
+                    *o = A.accumulate ? *o + res[q] : res[q];
                 }
             }
         }
@@ -250,7 +259,7 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
     const int64_t blocks = (A.n_units + per_block - 1) / per_block;
     if (blocks == 0) return FG_OK;
     const int TW = G * NV;
-    if (A.H == 1 && A.F4 <= TW)
+    if (A.H == 1 && (A.tile4 ? A.tile4 : A.F4) <= TW)
         sddmm_kernel<G, NV, MODE_H1, G><<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
     else if (A.H > 1 && A.D4 <= G && A.F4 <= TW) {
         switch (A.D4) {   // heads of D = 4*D4 floats reduce over D4 lanes
@@ -284,7 +293,42 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     A.H = H;
     A.F4 = H * D / 4;
     A.D4 = (H > 1) ? D / 4 : A.F4;
-    const int F4 = A.F4;
+    A.c4base = 0;
+    A.accumulate = 0;
+    A.tile4 = 0;
+    int F4 = A.F4;
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    const float4* Y4 = reinterpret_cast<const float4*>(Y);
+    // Feature-dimension tiling for L2 (as in spmm.cu): for H == 1 and
+    // X larger than the L2 budget, pass k computes the partial dot over float4
+    // columns [k*T4, (k+1)*T4) and accumulates into out (fixed pass order:
+    // deterministic).  Each pass gathers from an L2-resident slice of X.
+    {
+        const int64_t budget = fgk::l2_tile_budget();
+        // opt-in (FG_SDDMM_L2_TILE=1): measured slower than one pass on reddit F=512
+        // (8 passes re-read col_idx and read-modify-write the output each time)
+        const char* on = getenv("FG_SDDMM_L2_TILE");
+        if (on && on[0] == '1' && H == 1 && budget > 0 && g->n_src * int64_t(F4) * 16 > budget) {
+            int t4 = 32;
+            while (t4 > 1 && g->n_src * int64_t(t4) * 16 > budget) t4 /= 2;
+            A.tile4 = t4;
+            for (int c4 = 0; c4 < F4; c4 += t4) {
+                A.c4base = c4;
+                A.accumulate = c4 > 0;
+                fg_status r;
+                switch (t4) {
+                    case 1: r = launch_t<1, 1>(A, X4, Y4, out, st); break;
+                    case 2: r = launch_t<2, 1>(A, X4, Y4, out, st); break;
+                    case 4: r = launch_t<4, 1>(A, X4, Y4, out, st); break;
+                    case 8: r = launch_t<8, 1>(A, X4, Y4, out, st); break;
+                    case 16: r = launch_t<16, 1>(A, X4, Y4, out, st); break;
+                    default: r = launch_t<32, 1>(A, X4, Y4, out, st); break;
+                }
+                if (r != FG_OK) return r;
+            }
+            return FG_OK;
+        }
+    }
     int G = 32, NV = 4;
     if (F4 <= 32) {
         NV = 1;
@@ -297,8 +341,6 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     }
     if (H > 1 && F4 > G * NV)
         return set_error(FG_EUNSUPPORTED, "fg_sddmm: multi-head with H*D > 512 not implemented");
-    const float4* X4 = reinterpret_cast<const float4*>(X);
-    const float4* Y4 = reinterpret_cast<const float4*>(Y);
     switch (G) {
         case 1: return launch_t<1, 1>(A, X4, Y4, out, st);
         case 2: return launch_t<2, 1>(A, X4, Y4, out, st);

@@ -312,10 +312,7 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     int G = 32, NV = 4;
     int F4 = A.F4;
     {
-        static const int64_t budget = [] {
-            const char* e = getenv("FG_L2_TILE_MB");
-            return int64_t(e ? atoi(e) : 64) << 20;
-        }();
+        const int64_t budget = fgk::l2_tile_budget();
         // u_mul_e re-reads E (m x H floats) on every pass; measured not to pay off
         if (msg == FG_MSG_COPY_U && budget > 0 && g->n_src * int64_t(F4) * 16 > budget) {
             int64_t t4 = 32;

@@ -26,7 +26,8 @@ EDGE = {"u_dot_v": 0}
 
 # exported symbols declared in include/fg.h (checked by tests/test_abi.py)
 SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
-           "fg_sddmm", "fg_edge_softmax", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
+           "fg_sddmm", "fg_edge_softmax", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
+           "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
            "fg_allgather_rows", "fg_status_string", "fg_last_error", "fg_abi_version"]
 
 
@@ -61,12 +62,17 @@ def lib() -> ctypes.CDLL:
     L.fg_spmm.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]
     L.fg_sddmm.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
     L.fg_edge_softmax.argtypes = [vp, i32, vp, vp, vp]
+    L.fg_graph_transpose.argtypes = [vp, vp, ctypes.POINTER(vp)]
+    L.fg_spmm_backward.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
+    L.fg_sddmm_backward.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]
+    L.fg_edge_softmax_backward.argtypes = [vp, i32, vp, vp, vp, vp]
     L.fg_comm_unique_id.argtypes = [vp]
     L.fg_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.fg_comm_destroy.argtypes = [vp]
     L.fg_allgather_rows.argtypes = [vp, vp, i64, vp, vp, vp]
     for f in ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
-              "fg_sddmm", "fg_edge_softmax", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
+              "fg_sddmm", "fg_edge_softmax", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
+              "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
               "fg_allgather_rows"]:
         getattr(L, f).restype = i32
     L.fg_status_string.argtypes = [i32]
@@ -124,6 +130,19 @@ class Graph:
                                      int(bool(validate)), _stream(stream), ctypes.byref(h)),
                "fg_graph_create")
         self.handle = h
+
+    @classmethod
+    def _from_handle(cls, h, n_dst, n_src, nnz):
+        obj = cls.__new__(cls)
+        obj.row_ptr = obj.col_idx = obj.eid = None   # owned by the library
+        obj.n_dst, obj.n_src, obj.nnz, obj.handle = n_dst, n_src, nnz, h
+        return obj
+
+    def transpose(self, stream=None) -> "Graph":
+        """fg_graph_transpose: the CSC handle (rows = sources) sharing edge ids."""
+        h = ctypes.c_void_p()
+        _check(lib().fg_graph_transpose(self.handle, _stream(stream), ctypes.byref(h)), "fg_graph_transpose")
+        return Graph._from_handle(h, self.n_src, self.n_dst, self.nnz)
 
     def info(self) -> GraphInfo:
         inf = GraphInfo()
@@ -191,6 +210,43 @@ def edge_softmax(g: Graph, scores: torch.Tensor, *, H: int = 1, out: torch.Tenso
         out = torch.empty_like(scores)
     _check(lib().fg_edge_softmax(g.handle, H, _ptr(scores), _ptr(out), _stream(stream)), "fg_edge_softmax")
     return out
+
+
+# ------------------------------------------------------------------ backward
+def spmm_backward(g: Graph, gT: Graph | None, msg: str, reduce: str, dOut: torch.Tensor, *, H: int = 1,
+                  X: torch.Tensor | None = None, E: torch.Tensor | None = None, arg_u: torch.Tensor | None = None,
+                  want_dX: bool = True, want_dE: bool = False, stream=None):
+    """Gradients of fg_spmm (copy_u / u_mul_e).  Returns (dX, dE)."""
+    dOut = _dev(dOut, torch.float32, "dOut")
+    F = dOut.shape[1]
+    dX = torch.empty((g.n_src, F), dtype=torch.float32, device=dOut.device) if want_dX else None
+    dE = torch.empty((g.nnz, H), dtype=torch.float32, device=dOut.device) if want_dE else None
+    _check(lib().fg_spmm_backward(g.handle, gT.handle if gT is not None else None, MSG[msg], REDUCE[reduce], H,
+                                  F // H, _ptr(_dev(X, torch.float32, "X")), _ptr(_dev(E, torch.float32, "E")),
+                                  _ptr(dOut), _ptr(_dev(arg_u, torch.int32, "arg_u")), _ptr(dX), _ptr(dE),
+                                  _stream(stream)), "fg_spmm_backward")
+    return dX, dE
+
+
+def sddmm_backward(g: Graph, gT: Graph | None, X: torch.Tensor, Y: torch.Tensor, dS: torch.Tensor, *, H: int = 1,
+                   want_dX: bool = True, want_dY: bool = True, stream=None):
+    """Gradients of fg_sddmm(u_dot_v) w.r.t. X (sources) and Y (destinations)."""
+    X, Y, dS = _dev(X, torch.float32, "X"), _dev(Y, torch.float32, "Y"), _dev(dS, torch.float32, "dS")
+    F = X.shape[1]
+    dX = torch.empty((g.n_src, F), dtype=torch.float32, device=X.device) if want_dX else None
+    dY = torch.empty((g.n_dst, F), dtype=torch.float32, device=X.device) if want_dY else None
+    _check(lib().fg_sddmm_backward(g.handle, gT.handle if gT is not None else None, EDGE["u_dot_v"], H, F // H,
+                                   _ptr(X), _ptr(Y), _ptr(dS), _ptr(dX), _ptr(dY), _stream(stream)),
+           "fg_sddmm_backward")
+    return dX, dY
+
+
+def edge_softmax_backward(g: Graph, alpha: torch.Tensor, dalpha: torch.Tensor, *, H: int = 1, stream=None):
+    alpha, dalpha = _dev(alpha, torch.float32, "alpha"), _dev(dalpha, torch.float32, "dalpha")
+    ds = torch.empty_like(alpha)
+    _check(lib().fg_edge_softmax_backward(g.handle, H, _ptr(alpha), _ptr(dalpha), _ptr(ds), _stream(stream)),
+           "fg_edge_softmax_backward")
+    return ds
 
 
 # ------------------------------------------------------------------ multi-GPU

@@ -354,3 +354,28 @@ def test_abi_errors_on_device(skewed):
         fgp.Graph(dev(np.array([0, 1, 2], np.int64)), dev(np.array([0, 1], np.int32)),
                   eid=dev(np.array([1, 1], np.int32)))
     assert ei.value.status == FG_EGRAPH
+
+
+# ------------------------------------------------------------------ L2 feature-dimension tiling paths
+@pytest.mark.parametrize("F", [128, 512, 1024])
+def test_l2_column_tiling(skewed, F, monkeypatch):
+    """Force the column-tiled (multi-pass) paths with a tiny L2 budget: copy_u
+    sum/max and H=1 u_dot_v must still match the oracle (max bit-exact)."""
+    import paper_2008_11359_b200 as fgp
+    monkeypatch.setenv("FG_L2_TILE_MB", "1")
+    monkeypatch.setenv("FG_SDDMM_L2_TILE", "1")
+    X = feats((skewed.n_src, F), 960 + F, gen.REAL)
+    Y = feats((skewed.n_dst, F), 961 + F, gen.REAL)
+    out = fgp.spmm(skewed.h, "copy_u", "sum", dev(X)).cpu().numpy()
+    ref, ab, _, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", "sum", X)
+    check_close(out, ref, ab, TOL, f"tiled copy_u-sum F={F}")
+    mx, au, ae = fgp.spmm(skewed.h, "copy_u", "max", dev(X), arg_u=True, arg_e=True)
+    ref, _, rau, rae = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", "max", X)
+    assert np.array_equal(mx.cpu().numpy().astype(np.float64), ref)
+    assert np.array_equal(au.cpu().numpy(), rau) and np.array_equal(ae.cpu().numpy(), rae)
+    s = fgp.sddmm(skewed.h, dev(X), dev(Y)).cpu().numpy()
+    ref, ab = oracle.sddmm(skewed.row_ptr, skewed.col_idx, X, Y)
+    check_close(s, ref, ab, TOL, f"tiled u_dot_v F={F}")
+    monkeypatch.setenv("FG_L2_TILE_MB", "0")
+    s0 = fgp.sddmm(skewed.h, dev(X), dev(Y)).cpu().numpy()
+    check_close(s0, ref, ab, TOL, f"untiled u_dot_v F={F}")

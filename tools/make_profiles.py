@@ -1,0 +1,89 @@
+"""Turn the ncu captures of one round into the committed summaries under profiles/.
+
+    python tools/make_profiles.py r01c
+
+Reads gpurun_out/prof_{mlp,sddmm,spmm,softmax}_<tag>.ncu-rep and
+gpurun_out/launches_<tag>.csv; writes
+  profiles/ncu_summary_<tag>.md    per-kernel metrics (time, DRAM bytes, L2 hit,
+                                   occupancy, issue, tensor pipe, top stalls)
+  profiles/ncu_traffic.json        DRAM bytes per launch per bench op (bench.py
+                                   reads this for roofline.traffic)
+  profiles/launches_<tag>.md       per-launch device times of one bench step
+"""
+import csv
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from ncu_summary import summarise  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+OPS_BY_FILE = {
+    "spmm": ["spmm_copy_u_sum_F512", "spmm_u_mul_e_sum_H8_D32", "spmm_copy_u_max_F128_args"],
+    "sddmm": ["sddmm_u_dot_v_H1_F512", "sddmm_u_dot_v_H8_D32"],
+    "softmax": ["edge_softmax_H8"],
+    "mlp": ["spmm_mlp_max_d8_d128_args"],
+}
+
+
+def num(s):
+    try:
+        v, u = s.split(" ", 1)
+        v = float(v.replace(",", ""))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ms": 1e-3, "us": 1e-6,
+                 "ns": 1e-9, "s": 1.0}.get(u.strip(), 1.0)
+        return v * scale
+    except Exception:
+        return None
+
+
+lines = [f"# ncu --set full summaries ({tag})", "",
+         "Captured with `ncu --set full --clock-control none --import-source on` on one B200 (gpurun), "
+         "kernels of one timed `bench.py` step (reddit-shaped graph, 232,965 v / 114,615,892 e). "
+         "Times are ncu replay times (cold-cache, serialised), not bench values.", ""]
+traffic = {}
+for key, ops in OPS_BY_FILE.items():
+    path = os.path.join(ROOT, "gpurun_out", f"prof_{key}_{tag}.ncu-rep")
+    if not os.path.exists(path):
+        continue
+    for op, d in zip(ops, summarise(path)):
+        t = num(d.get("gpu__time_duration.sum", ""))
+        rd = num(d.get("dram__bytes_read.sum", "")) or 0.0
+        wr = num(d.get("dram__bytes_write.sum", "")) or 0.0
+        traffic[op] = {"kernel": d["kernel"], "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                       "ncu_time_s": t, "dram_gbs": (rd + wr) / t / 1e9 if t else None,
+                       "l2_hit_pct": d.get("lts__t_sector_hit_rate.pct")}
+        lines += [f"## {op}", "", f"`{d['kernel']}`", "", "| metric | value |", "|---|---|"]
+        for k, v in d.items():
+            if k in ("kernel", "top_stalls"):
+                continue
+            lines.append(f"| {k} | {v} |")
+        if t:
+            lines.append(f"| DRAM GB/s (read+write / time) | {(rd + wr) / t / 1e9:.1f} |")
+        lines.append(f"| top stall samples | {', '.join(f'{k}={v}' for k, v in d['top_stalls'].items())} |")
+        lines.append("")
+os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+open(os.path.join(ROOT, "profiles", f"ncu_summary_{tag}.md"), "w").write("\n".join(lines) + "\n")
+json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+
+lp = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
+if os.path.exists(lp):
+    rows = [r for r in csv.reader(open(lp)) if len(r) > 10]
+    hdr = rows[0]
+    ik, iv = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    data = [(r[ik], float(r[iv].replace(",", ""))) for r in rows[1:]]
+    # keep the last step: the last 7 launches of our kernels + the fill before them
+    ours = [(k, v) for k, v in data if any(s in k for s in ("spmm_gather", "sddmm", "softmax", "mlp_"))]
+    step = ours[-7:]
+    tot = sum(v for _, v in step)
+    out = [f"# Launch list of one bench step ({tag})", "",
+           "`ncu --metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 2 --warmup 3`; "
+           "the last step's 7 libfg launches.  Per-launch times are cold-cache and serialised: compare shares.", "",
+           "| # | kernel | ns | share |", "|---|---|---|---|"]
+    for i, (k, v) in enumerate(step):
+        out.append(f"| {i} | `{k[:90]}` | {v:.0f} | {v / tot:.1%} |")
+    out.append(f"| | total | {tot:.0f} | |")
+    open(os.path.join(ROOT, "profiles", f"launches_{tag}.md"), "w").write("\n".join(out) + "\n")
+print(json.dumps(traffic, indent=1)[:3000])
