@@ -348,6 +348,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
+    # f2 (next row): the fused GAT layer on the same inputs, timed separately (not part of the step)
+    extras = run_extras(S, args, sync_all, flush)
+
     # end-to-end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -415,11 +418,34 @@ def main():
         "e2e": e2e,
         "gpu_launches": Step.LAUNCHES_PER_STEP * args.steps,
         "clocks": clk,
+        "extras": extras,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_extras(S, args, sync_all, flush):
+    """Next-row kernels measured beside the step (not part of it): f2 fused GAT
+    (u_dot_v -> softmax -> u_mul_e-sum in one pass) vs the 3-kernel chain."""
+    import torch
+    st = S.stream
+    out = torch.empty_like(S.o256)
+    k_steps = max(1, min(args.steps, 5))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k_steps + 1)]
+    with torch.cuda.stream(st):
+        for k in range(k_steps + 1):
+            flush.fill_(float(k))
+            evs[k][0].record(st)
+            S.fgp.gat_attention(S.G, S.X["X256"], S.ydst("X256"), H=H_GAT, out=out, stream=st)
+            evs[k][1].record(st)
+    sync_all()
+    ms = float(np.mean([evs[k][0].elapsed_time(evs[k][1]) for k in range(1, k_steps + 1)]))
+    n, m, F = S.nl, S.m, H_GAT * D_GAT
+    b = 8 * (n + 1) + 4 * m + 4 * m * F + 2 * 4 * n * F
+    return {"gat_fused_ms": round(ms, 4), "gat_fused_gbs": round(b / (ms * 1e-3) / 1e9, 1),
+            "gat_fused_bytes_model": "8(n+1) + 4m + 4mF + 8nF (X[u] gathered once; Y read, out written)"}
 
 
 def run_e2e(S, host, args, world, sync_all, flush):

@@ -135,8 +135,11 @@ fg_status fg_graph_info(const fg_graph* g, fg_graph_info_t* info);
  *           source id / edge id of the winning edge.  Ties -> lowest CSR
  *           position.  Must be NULL for sum.
  *   Empty rows: out = +0.0 and arg = -1.
- *   workspace / workspace_bytes: scratch from fg_spmm_workspace_size (may be
- *           NULL when that size is 0).
+ *   workspace / workspace_bytes: device scratch of >= fg_spmm_workspace_size
+ *           bytes, owned by the caller, not used across calls (may be NULL
+ *           when that size is 0: copy_u / u_mul_e need none; mlp needs
+ *           2 * n_src * ceil(d_in/8) * 8 * 4 + 256 bytes for the tf32 hi/lo
+ *           split of X).  Too small -> FG_EINVAL.
  *   Errors: FG_EINVAL (null/misaligned pointer, bad enum, arg_* with sum),
  *           FG_ESHAPE (H < 1, D < 1, (H*D) % 4 != 0, mlp with H != 1 or d_in
  *           out of range, u_mul_e/copy_u with d_in != 0), FG_ECUDA.
@@ -169,6 +172,21 @@ fg_status fg_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, const float* 
  */
 fg_status fg_edge_softmax(const fg_graph* g, int H, const float* scores, float* out,
                           fg_stream stream);
+
+/* ---------------------------------------------------------------- fused GAT attention */
+/*
+ * fg_gat_attention -- gSDDMM u_dot_v -> edge softmax -> gSpMM u_mul_e-sum in ONE
+ * pass (the paper's kernel fusion, P:378-379 / P:554, applied across the three
+ * templates of the GAT layer):
+ *     out[v][h,:] = sum_{e=u->v} softmax_e(<X[u][h,:], Y[v][h,:]>) * X[u][h,:]
+ *   X [n_src][H][D], Y [n_dst][H][D] (may equal X), out [n_dst][H][D] (empty
+ *   rows -> 0); scores: optional [nnz][H] (edge id) receives the pre-softmax
+ *   scores s.  Equal in real arithmetic to fg_sddmm + fg_edge_softmax + fg_spmm
+ *   (u_mul_e, sum); here s and alpha never leave the SM and X[u] is read once.
+ *   Requires D = 4*2^k <= 128 and H*D <= 512.
+ */
+fg_status fg_gat_attention(const fg_graph* g, int H, int D, const float* X, const float* Y, float* out,
+                           float* scores, fg_stream stream);
 
 /* ---------------------------------------------------------------- backward */
 /*

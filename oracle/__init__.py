@@ -192,3 +192,23 @@ def edge_softmax_backward(row_ptr, alpha, dalpha, *, H: int = 1, eid=None):
     _bind_backward().or_edge_softmax_backward(row_ptr.size - 1, _p(row_ptr), _p(eid), H, _p(alpha), _p(dalpha),
                                               _p(ds))
     return ds
+
+
+def gat(row_ptr, col_idx, X, Y=None, *, H: int = 1):
+    """Fused GAT layer definition (sddmm -> edge softmax -> u_mul_e-sum), fp64.
+    Returns (ref, abssum) [n_dst][H*D]."""
+    row_ptr, col_idx = _c(row_ptr, np.int64), _c(col_idx, np.int32)
+    X = _c(X, np.float32)
+    Y = X if Y is None else _c(Y, np.float32)
+    n_dst = row_ptr.size - 1
+    F = X.reshape(X.shape[0], -1).shape[1]
+    lib = _L()
+    if not getattr(lib, "_gat_bound", False):
+        i64, i32, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+        lib.or_gat.argtypes = [i64, vp, vp, i32, i32, vp, vp, vp, vp]
+        lib.or_gat.restype = None
+        lib._gat_bound = True
+    ref = np.empty((n_dst, F), np.float64)
+    ab = np.empty((n_dst, F), np.float64)
+    lib.or_gat(n_dst, _p(row_ptr), _p(col_idx), H, F // H, _p(X), _p(Y), _p(ref), _p(ab))
+    return ref, ab

@@ -261,3 +261,50 @@ void or_edge_softmax_backward(int64_t n_dst, const int64_t* row_ptr, const int32
             }
         }
 }
+
+/* ======================================================================
+ * GAT attention layer as one definition (fused path f2): for each
+ * destination v and head h, the composition of Eq. (4) (u_dot_v score),
+ * the edge softmax over v's in-edges and Eq. (1) with the u_mul_e message
+ * (P:983), all in fp64:
+ *   s_e = sum_d X[u][h,d] Y[v][h,d];  a_e = exp(s_e - max s) / sum exp(. - max s);
+ *   ref[v][h,d] = sum_e a_e X[u][h,d];  abssum = sum_e a_e |X[u][h,d]|.
+ * ====================================================================== */
+void or_gat(int64_t n_dst, const int64_t* row_ptr, const int32_t* col_idx, int H, int D, const float* X,
+            const float* Y, double* ref, double* abssum) {
+    const int64_t F = (int64_t)H * D;
+    #pragma omp parallel
+    {
+        double* s = NULL;
+        int64_t cap = 0;
+        #pragma omp for schedule(dynamic, 16)
+        for (int64_t v = 0; v < n_dst; ++v) {
+            const int64_t deg = row_ptr[v + 1] - row_ptr[v];
+            if (deg > cap) { cap = deg; s = (double*)realloc(s, sizeof(double) * (size_t)cap); }
+            for (int64_t j = 0; j < F; ++j) { ref[v * F + j] = 0.0; abssum[v * F + j] = 0.0; }
+            if (deg == 0) continue;
+            for (int h = 0; h < H; ++h) {
+                double mx = -INFINITY, sum = 0.0;
+                for (int64_t k = 0; k < deg; ++k) {
+                    const int64_t u = col_idx[row_ptr[v] + k];
+                    double t = 0.0;
+                    for (int d = 0; d < D; ++d)
+                        t += (double)X[u * F + (int64_t)h * D + d] * (double)Y[v * F + (int64_t)h * D + d];
+                    s[k] = t;
+                    if (t > mx) mx = t;
+                }
+                for (int64_t k = 0; k < deg; ++k) sum += exp(s[k] - mx);
+                for (int64_t k = 0; k < deg; ++k) {
+                    const int64_t u = col_idx[row_ptr[v] + k];
+                    const double a = exp(s[k] - mx) / sum;
+                    for (int d = 0; d < D; ++d) {
+                        const int64_t j = (int64_t)h * D + d;
+                        ref[v * F + j] += a * (double)X[u * F + j];
+                        abssum[v * F + j] += a * fabs((double)X[u * F + j]);
+                    }
+                }
+            }
+        }
+        free(s);
+    }
+}

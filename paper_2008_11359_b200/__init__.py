@@ -5,5 +5,5 @@ The product is libfg.so (C ABI, include/fg.h); this package is its thin
 binding (fg.py) plus the in-tree build (build.py) and the dst-row sharding
 helpers (shard.py).
 """
-from .fg import (FGError, Graph, Comm, comm_unique_id, edge_softmax, edge_softmax_backward, lib,  # noqa: F401
+from .fg import (FGError, Graph, Comm, comm_unique_id, edge_softmax, edge_softmax_backward, gat_attention, lib,  # noqa: F401
                  sddmm, sddmm_backward, spmm, spmm_backward)

@@ -46,10 +46,11 @@ extern "C" const char* fg_status_string(fg_status s) {
 extern "C" const char* fg_last_error(void) { return g_err; }
 extern "C" int fg_abi_version(void) { return FG_ABI_VERSION; }
 
-extern "C" fg_status fg_spmm_workspace_size(const fg_graph* g, fg_msg_op, fg_reduce_op, int, int, int,
+extern "C" fg_status fg_spmm_workspace_size(const fg_graph* g, fg_msg_op msg, fg_reduce_op, int, int, int d_in,
                                             size_t* bytes) {
     if (!g || !bytes) return set_error(FG_EINVAL, "fg_spmm_workspace_size: NULL argument");
-    *bytes = 0;   // heavy rows combine on chip (CTA per row); no scratch needed
+    // gather messages: none (heavy rows combine on chip); mlp: tf32 hi/lo split of X
+    *bytes = (msg == FG_MSG_MLP && d_in > 0) ? fgk::mlp_workspace_bytes(g->n_src, d_in) : 0;
     return FG_OK;
 }
 
@@ -57,7 +58,6 @@ extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
                              const float* X, const float* E, const float* W, int d_in, const float* X_dst,
                              float* out, int32_t* arg_u, int32_t* arg_e, void* workspace,
                              size_t workspace_bytes, fg_stream stream) {
-    (void)workspace; (void)workspace_bytes;
     if (!g) return set_error(FG_EINVAL, "fg_spmm: NULL graph");
     if (msg != FG_MSG_COPY_U && msg != FG_MSG_U_MUL_E && msg != FG_MSG_MLP)
         return set_error(FG_EINVAL, "fg_spmm: bad msg op %d", int(msg));
@@ -77,6 +77,9 @@ extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
         if (!X_dst && g->n_src != g->n_dst)
             return set_error(FG_ESHAPE, "fg_spmm(mlp): X_dst = NULL needs n_src == n_dst");
         if (E) return set_error(FG_EINVAL, "fg_spmm(mlp): E must be NULL");
+        if (!workspace || workspace_bytes < fgk::mlp_workspace_bytes(g->n_src, d_in))
+            return set_error(FG_EINVAL, "fg_spmm(mlp): workspace of >= %zu bytes required (fg_spmm_workspace_size)",
+                             fgk::mlp_workspace_bytes(g->n_src, d_in));
     } else {
         if (d_in != 0 || W || X_dst) return set_error(FG_EINVAL, "fg_spmm: W/X_dst/d_in are for mlp only");
         if (msg == FG_MSG_U_MUL_E && !E && g->nnz > 0) return set_error(FG_EINVAL, "fg_spmm(u_mul_e): E is NULL");
@@ -86,7 +89,7 @@ extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     if (g->n_dst == 0) return FG_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (msg == FG_MSG_MLP)
-        return fgk::launch_spmm_mlp(g, red, D, X, W, d_in, X_dst ? X_dst : X, out, arg_u, arg_e, st);
+        return fgk::launch_spmm_mlp(g, red, D, X, W, d_in, X_dst ? X_dst : X, out, arg_u, arg_e, workspace, st);
     return fgk::launch_spmm_gather(g, msg, red, H, D, X, E, out, arg_u, arg_e, st);
 }
 

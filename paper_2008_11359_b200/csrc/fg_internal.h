@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <string>
+#include <deque>
+#include <mutex>
 #include <vector>
 
 #include "../../include/fg.h"
@@ -26,6 +28,17 @@ struct fg_graph {
     int64_t n_units = 0;
     int unit_chunk = 0;                 // edges per SDDMM unit
 
+    // source-segmented SDDMM unit tables (1D source partitioning retargeted to the
+    // L2): built lazily per segment width, cached for the handle's life
+    struct SegUnits {
+        int64_t seg_rows = 0, n_units = 0;
+        int32_t* row = nullptr;
+        int64_t* p0 = nullptr;
+        int64_t* p1 = nullptr;
+    };
+    std::deque<SegUnits> seg_units;      // deque: references stay valid as it grows
+    std::mutex seg_mu;                   // lazily built under this lock (handle shared across streams)
+
     // derived (owned, host)
     std::vector<int64_t> deg_sorted;    // degrees in rows_by_deg order (descending)
     int64_t n_nonempty = 0;
@@ -47,10 +60,11 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
                              int32_t* arg_e, cudaStream_t st);
 fg_status launch_spmm_mlp(const fg_graph* g, fg_reduce_op red, int d2, const float* X,
                           const float* W, int d_in, const float* X_dst, float* out,
-                          int32_t* arg_u, int32_t* arg_e, cudaStream_t st);
+                          int32_t* arg_u, int32_t* arg_e, void* workspace, cudaStream_t st);
 fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W,
                                   int d_in, const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e,
-                                  cudaStream_t st);
+                                  void* workspace, cudaStream_t st);
+size_t mlp_workspace_bytes(int64_t n_src, int d_in);
 fg_status launch_spmm_mlp_simt(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W,
                                int d_in, const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e,
                                cudaStream_t st);
@@ -59,6 +73,10 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
 fg_status launch_edge_softmax(const fg_graph* g, int H, const float* S, float* out, cudaStream_t st);
 
 fg_status check_launch(const char* what);
+
+// source-segmented unit table for segments of seg_rows source vertices (built on
+// first use; the handle owns it)
+fg_status get_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t st, const fg_graph::SegUnits** out);
 
 // L2 budget (bytes) for feature-dimension tiling of the gathered operand;
 // FG_L2_TILE_MB overrides the default (64 MiB, half the 126 MB L2), 0 disables.

@@ -58,7 +58,98 @@ __global__ void validate_eid(int64_t nnz, const int32_t* __restrict__ eid, unsig
 
 }  // namespace
 
+__device__ __forceinline__ int64_t lb_row(const int32_t* __restrict__ ci, int64_t lo, int64_t hi, int64_t key) {
+    while (lo < hi) {   // first position in [lo, hi) with ci >= key
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(ci + mid) < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// units per (segment, row): segment-major layout cnt[s * n + v]
+__global__ void seg_count_kernel(int64_t n, int nseg, int64_t seg_rows, int chunk, const int64_t* __restrict__ rp,
+                                 const int32_t* __restrict__ ci, int64_t* __restrict__ cnt) {
+    const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int64_t s0 = rp[v], s1 = rp[v + 1];
+    int64_t lo = s0;
+    for (int s = 0; s < nseg; ++s) {
+        const int64_t hi = (s == nseg - 1) ? s1 : lb_row(ci, lo, s1, (s + 1) * seg_rows);
+        cnt[int64_t(s) * n + v] = (hi - lo + chunk - 1) / chunk;
+        lo = hi;
+    }
+}
+
+__global__ void seg_write_kernel(int64_t n, int nseg, int64_t seg_rows, int chunk, const int64_t* __restrict__ rp,
+                                 const int32_t* __restrict__ ci, const int64_t* __restrict__ off,
+                                 int32_t* __restrict__ urow, int64_t* __restrict__ up0, int64_t* __restrict__ up1) {
+    const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int64_t s0 = rp[v], s1 = rp[v + 1];
+    int64_t lo = s0;
+    for (int s = 0; s < nseg; ++s) {
+        const int64_t hi = (s == nseg - 1) ? s1 : lb_row(ci, lo, s1, (s + 1) * seg_rows);
+        int64_t o = off[int64_t(s) * n + v];
+        for (int64_t p = lo; p < hi; p += chunk, ++o) {
+            urow[o] = int32_t(v);
+            up0[o] = p;
+            up1[o] = min(p + chunk, hi);
+        }
+        lo = hi;
+    }
+}
+
 namespace fgk {
+fg_status get_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t st, const fg_graph::SegUnits** out) {
+    std::lock_guard<std::mutex> lock(g->seg_mu);
+    for (auto& su : g->seg_units)
+        if (su.seg_rows == seg_rows) {
+            *out = &su;
+            return FG_OK;
+        }
+    const int64_t n = g->n_dst;
+    const int nseg = int((g->n_src + seg_rows - 1) / seg_rows);
+    fg_graph::SegUnits su;
+    su.seg_rows = seg_rows;
+    int64_t* cnt = nullptr;
+    std::vector<int64_t> h(size_t(n) * nseg + 1, 0);
+    fg_status stt = FG_OK;
+    cudaError_t e = cudaMalloc(&cnt, sizeof(int64_t) * (size_t(n) * nseg + 1));
+    if (e == cudaSuccess && n > 0) {
+        seg_count_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(n, nseg, seg_rows, chunk, g->row_ptr, g->col_idx, cnt);
+        e = cudaMemcpyAsync(h.data(), cnt, sizeof(int64_t) * size_t(n) * nseg, cudaMemcpyDeviceToHost, st);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) {
+        int64_t acc = 0;   // exclusive scan, segment-major: all units of segment 0 first
+        for (size_t i = 0; i < size_t(n) * nseg; ++i) {
+            const int64_t c = h[i];
+            h[i] = acc;
+            acc += c;
+        }
+        su.n_units = acc;
+        e = cudaMemcpyAsync(cnt, h.data(), sizeof(int64_t) * size_t(n) * nseg, cudaMemcpyHostToDevice, st);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&su.row, sizeof(int32_t) * size_t(std::max<int64_t>(su.n_units, 1)));
+    if (e == cudaSuccess) e = cudaMalloc(&su.p0, sizeof(int64_t) * size_t(std::max<int64_t>(su.n_units, 1)));
+    if (e == cudaSuccess) e = cudaMalloc(&su.p1, sizeof(int64_t) * size_t(std::max<int64_t>(su.n_units, 1)));
+    if (e == cudaSuccess && n > 0) {
+        seg_write_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(n, nseg, seg_rows, chunk, g->row_ptr, g->col_idx,
+                                                                    cnt, su.row, su.p0, su.p1);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(cnt);
+    if (e != cudaSuccess) {
+        cudaFree(su.row); cudaFree(su.p0); cudaFree(su.p1);
+        return set_error(FG_ECUDA, "segmented SDDMM units: %s", cudaGetErrorString(e));
+    }
+    g->device_bytes += 20 * su.n_units;
+    g->seg_units.push_back(su);
+    *out = &g->seg_units.back();
+    return stt;
+}
+
 int64_t rows_with_degree_at_least(const fg_graph* g, int64_t t) {
     // deg_sorted is descending: first index with deg < t
     auto it = std::lower_bound(g->deg_sorted.begin(), g->deg_sorted.end(), t,
@@ -199,6 +290,11 @@ extern "C" fg_status fg_graph_destroy(fg_graph* g) {
     if (g->rows_by_deg) cudaFree(g->rows_by_deg);
     if (g->unit_row) cudaFree(g->unit_row);
     if (g->unit_p0) cudaFree(g->unit_p0);
+    for (auto& su : g->seg_units) {
+        cudaFree(su.row);
+        cudaFree(su.p0);
+        cudaFree(su.p1);
+    }
     if (g->owned_row_ptr) cudaFree(g->owned_row_ptr);
     if (g->owned_col_idx) cudaFree(g->owned_col_idx);
     if (g->owned_eid) cudaFree(g->owned_eid);

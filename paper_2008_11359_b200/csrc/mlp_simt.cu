@@ -111,12 +111,13 @@ fg_status launch_spmm_mlp_simt(const fg_graph* g, fg_reduce_op red, int d2, cons
 // The product path is the tcgen05 kernel; FG_MLP_SIMT=1 selects the FFMA kernel
 // (ablation only: same semantics, CUDA cores instead of tensor cores).
 fg_status launch_spmm_mlp(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W, int d_in,
-                          const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e, cudaStream_t st) {
+                          const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e, void* workspace,
+                          cudaStream_t st) {
     static const bool simt = [] {
         const char* e = getenv("FG_MLP_SIMT");
         return e && e[0] == '1';
     }();
     if (simt) return launch_spmm_mlp_simt(g, red, d2, X, W, d_in, X_dst, out, arg_u, arg_e, st);
-    return launch_spmm_mlp_tcgen05(g, red, d2, X, W, d_in, X_dst, out, arg_u, arg_e, st);
+    return launch_spmm_mlp_tcgen05(g, red, d2, X, W, d_in, X_dst, out, arg_u, arg_e, workspace, st);
 }
 }  // namespace fgk

@@ -29,12 +29,14 @@
 //     walking edge columns, so the per-row segmented max needs no cross-lane
 //     reduction) and write each finished row with coalesced stores.
 #include <cstdint>
+#include <cstdlib>
 
 #include "fg_internal.h"
 
 namespace {
 
 constexpr int NT = 128;                   // edges per tile (MMA N)
+constexpr int NBUF = 2;                   // TMEM accumulator buffers (double buffer)
 constexpr int MT = 128;                   // features per CTA (MMA M)
 constexpr int STAGES = 4;
 constexpr int ISTAGES = 4;                // index ring (producer -> epilogue)
@@ -42,7 +44,7 @@ constexpr int NEPI = 4;                   // epilogue warps 0..3 (TMEM lane quar
 constexpr int MMA_WARP = 4;
 constexpr int NPROD = 2;                  // producer warps 5..6
 constexpr int THREADS = (NEPI + 1 + NPROD) * 32;
-constexpr int TMEM_COLS = 2 * NT;
+constexpr int TMEM_COLS = NBUF * NT;      // 256: two CTAs per SM share the 512 columns
 constexpr int TILE_BYTES = 8 * 4 * 128;   // one K-step operand tile: 128 rows x 8 tf32 = 4 KB
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -57,7 +59,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 0x989680;\n\t"   // suspend, don't spin
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
@@ -119,6 +121,28 @@ __device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[32]) {
         : "memory");
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+// arrive on the mbarrier once all of this thread's prior cp.async copies have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Split X into tf32 hi / lo rows of KS*8 floats (zero-padded beyond d_in), once per call.
+template <int KS>
+__global__ void __launch_bounds__(256) mlp_split_kernel(const float* __restrict__ X, int64_t n, int d_in,
+                                                      float* __restrict__ Xhi, float* __restrict__ Xlo) {
+    const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+    if (i >= n * KS * 8) return;
+    const int64_t r = i / (KS * 8);
+    const int k = int(i % (KS * 8));
+    const float x = (k < d_in) ? __ldg(X + r * d_in + k) : 0.f;
+    const float hi = tf32_rna(x);
+    Xhi[i] = hi;
+    Xlo[i] = tf32_rna(x - hi);
+}
+
 __device__ __forceinline__ int64_t lower_bound_rp(const int64_t* rp, int64_t n1, int64_t target) {
     int64_t lo = 0, hi = n1;   // first i in [0, n1) with rp[i] >= target
     while (lo < hi) {
@@ -138,8 +162,11 @@ struct Args {
     float* out;           // [n_dst][d2]
     int32_t* arg_u;
     int32_t* arg_e;
-    int64_t n_dst, nnz;
+    int64_t n_dst, nnz, n_src;
     int d_in, d2;
+    const float* Xhi;     // [n_src][KS*8] tf32 hi part of X (workspace)
+    const float* Xlo;     // [n_src][KS*8] tf32 lo part
+    int dbg;              // FG_MLP_DBG (pipeline experiments): 1 = skip epilogue math, 2 = skip gathers
 };
 
 template <int KS>
@@ -150,7 +177,7 @@ struct Smem {
     float b_lo[STAGES][KS][NT * 8];
     int32_t su[ISTAGES][NT];               // source id / edge id of each tile column,
     int32_t se[ISTAGES][NT];               // read by the epilogue for arg_u / arg_e
-    uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2], ifull[ISTAGES], iempty[ISTAGES];
+    uint64_t full[STAGES], empty[STAGES], tfull[NBUF], tempty[NBUF], ifull[ISTAGES], iempty[ISTAGES];
     uint32_t tmem_base;
     int64_t r_lo, r_hi;
 };
@@ -254,21 +281,20 @@ struct Epi {
                 if (b1 > b0 || (b1 == b0 && k1 < k0)) { b0 = b1; k0 = k1; }
                 if (b0 > best) { best = b0; bu = su[k0]; be = se[k0]; }
             } else {
-                float s0 = 0.f, s1 = 0.f;
+                float sm[4] = {0.f, 0.f, 0.f, 0.f};
                 if (c0 == 0 && c1 == 32) {
 #pragma unroll
-                    for (int c = 0; c < 32; c += 2) {
-                        s0 += fmaxf(__uint_as_float(v[c]) + q, 0.f);
-                        s1 += fmaxf(__uint_as_float(v[c + 1]) + q, 0.f);
-                    }
+                    for (int c = 0; c < 32; c += 4)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) sm[i] += fmaxf(__uint_as_float(v[c + i]) + q, 0.f);
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 32; c += 2) {
-                        if (c >= c0 && c < c1) s0 += fmaxf(__uint_as_float(v[c]) + q, 0.f);
-                        if (c + 1 >= c0 && c + 1 < c1) s1 += fmaxf(__uint_as_float(v[c + 1]) + q, 0.f);
-                    }
+                    for (int c = 0; c < 32; c += 4)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            if (c + i >= c0 && c + i < c1) sm[i] += fmaxf(__uint_as_float(v[c + i]) + q, 0.f);
                 }
-                best += s0 + s1;
+                best += (sm[0] + sm[1]) + (sm[2] + sm[3]);
             }
             c0 = c1;
         }
@@ -290,7 +316,7 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
         S.r_hi = (b == nb - 1) ? A.n_dst : lower_bound_rp(A.row_ptr, A.n_dst + 1, t_hi);
         if (S.r_hi < S.r_lo) S.r_hi = S.r_lo;
         for (int s = 0; s < STAGES; ++s) { mbar_init(&S.full[s], NPROD * 32); mbar_init(&S.empty[s], 1); }
-        for (int b2 = 0; b2 < 2; ++b2) { mbar_init(&S.tfull[b2], 1); mbar_init(&S.tempty[b2], NEPI * 32); }
+        for (int b2 = 0; b2 < NBUF; ++b2) { mbar_init(&S.tfull[b2], 1); mbar_init(&S.tempty[b2], NEPI * 32); }
         for (int s = 0; s < ISTAGES; ++s) { mbar_init(&S.ifull[s], NPROD * 32); mbar_init(&S.iempty[s], NEPI * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -319,51 +345,33 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
     const int ntiles = int((E1 - E0 + NT - 1) / NT);
 
     if (warp >= MMA_WARP + 1) {
-        // ------------------------------------------------ producers: gather x_u, split, stage B
-        // Each thread owns EPT edges of every tile.  The indices of tile t+1 are
-        // loaded while tile t's feature rows are in flight, and all EPT rows of a
-        // tile are requested before any is converted: one L2 round trip per tile
-        // instead of two dependent ones per edge.
+        // ------------------------------------------------ producers: gather pre-split x_u rows into B
+        // x_u was split once into tf32 hi / lo rows of KS*8 floats (mlp_split_kernel,
+        // workspace).  Per edge the producer issues 2*KS*2 cp.async 16-byte copies
+        // straight into the K-major canonical tile positions (no register staging,
+        // no per-edge dependent waits); cp.async.mbarrier.arrive signals full[s]
+        // when this thread's copies land.  Indices of tile t+1 are prefetched.
         constexpr int EPT = NT / (NPROD * 32);
         const int pt = tid - (MMA_WARP + 1) * 32;          // 0 .. NPROD*32-1
+        const int rowf = KS * 8;                            // floats per pre-split row
         int u_nx[EPT], e_nx[EPT];
-        auto load_idx = [&](int t, int (&u)[EPT], int (&ed)[EPT]) {
+        auto load_idx = [&](int t) {
             const int64_t tb = E0 + int64_t(t) * NT;
 #pragma unroll
             for (int i = 0; i < EPT; ++i) {
                 const int64_t p = tb + pt + i * NPROD * 32;
                 const bool ok = p < E1;
-                u[i] = ok ? __ldg(A.col_idx + p) : -1;
-                ed[i] = ok ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
+                u_nx[i] = ok ? __ldg(A.col_idx + p) : -1;
+                e_nx[i] = ok ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
             }
         };
-        if (ntiles > 0) load_idx(0, u_nx, e_nx);
+        if (ntiles > 0) load_idx(0);
         for (int t = 0; t < ntiles; ++t) {
             const int s = t % STAGES, is = t % ISTAGES;
             int u_cur[EPT], e_cur[EPT];
 #pragma unroll
             for (int i = 0; i < EPT; ++i) { u_cur[i] = u_nx[i]; e_cur[i] = e_nx[i]; }
-            float4 xa[EPT][2 * KS];
-#pragma unroll
-            for (int i = 0; i < EPT; ++i) {
-                const bool ok = u_cur[i] >= 0;
-                const float* xr = A.X + int64_t(ok ? u_cur[i] : 0) * A.d_in;
-#pragma unroll
-                for (int c = 0; c < 2 * KS; ++c) {
-                    const int k0 = c * 4;
-                    float4 x;
-                    if (ok && (A.d_in & 3) == 0 && k0 + 4 <= A.d_in) {
-                        x = __ldg(reinterpret_cast<const float4*>(xr + k0));
-                    } else {
-                        x.x = (ok && k0 + 0 < A.d_in) ? __ldg(xr + k0 + 0) : 0.f;
-                        x.y = (ok && k0 + 1 < A.d_in) ? __ldg(xr + k0 + 1) : 0.f;
-                        x.z = (ok && k0 + 2 < A.d_in) ? __ldg(xr + k0 + 2) : 0.f;
-                        x.w = (ok && k0 + 3 < A.d_in) ? __ldg(xr + k0 + 3) : 0.f;
-                    }
-                    xa[i][c] = x;
-                }
-            }
-            if (t + 1 < ntiles) load_idx(t + 1, u_nx, e_nx);
+            if (t + 1 < ntiles) load_idx(t + 1);
             mbar_wait(&S.empty[s], ((t / STAGES) & 1) ^ 1);
             mbar_wait(&S.iempty[is], ((t / ISTAGES) & 1) ^ 1);
 #pragma unroll
@@ -371,31 +379,33 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
                 const int e = pt + i * NPROD * 32;
                 S.su[is][e] = u_cur[i];
                 S.se[is][e] = e_cur[i];
+                const int64_t u = u_cur[i] >= 0 ? u_cur[i] : 0;     // padded columns read row 0 (ignored)
+                const float* xh = A.Xhi + u * rowf;
+                const float* xl = A.Xlo + u * rowf;
 #pragma unroll
-                for (int c = 0; c < 2 * KS; ++c) {
-                    const int ks = c / 2;
-                    const float4 x = xa[i][c];
-                    float4 h, l;
-                    h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
-                    h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
-                    h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
-                    h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
-                    const uint32_t off = tile_off(e, (c % 2) * 4);
-                    *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(S.b_hi[s][ks]) + off) = h;
-                    *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(S.b_lo[s][ks]) + off) = l;
+                for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const uint32_t off = tile_off(e, c * 4);
+                        if (!(A.dbg & 2)) {
+                            cp_async16(smem_u32(S.b_hi[s][ks]) + off, xh + ks * 8 + c * 4);
+                            cp_async16(smem_u32(S.b_lo[s][ks]) + off, xl + ks * 8 + c * 4);
+                        }
+                    }
                 }
             }
-            fence_async_smem();
-            mbar_arrive(&S.full[s]);
+            cp_async_arrive(&S.full[s]);
             mbar_arrive(&S.ifull[is]);
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp == MMA_WARP) {
         // ------------------------------------------------ MMA issuer (one thread)
         if (lane == 0) {
             for (int t = 0; t < ntiles; ++t) {
-                const int s = t % STAGES, b = t & 1;
+                const int s = t % STAGES, b = t % NBUF;
                 mbar_wait(&S.full[s], (t / STAGES) & 1);
-                mbar_wait(&S.tempty[b], ((t >> 1) & 1) ^ 1);
+                fence_async_smem();   // cp.async (generic proxy) writes -> tensor-core (async proxy) reads
+                mbar_wait(&S.tempty[b], ((t / NBUF) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + uint32_t(b * NT);
 #pragma unroll
@@ -430,9 +440,9 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
         }
         const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
         for (int t = 0; t < ntiles; ++t) {
-            const int b = t & 1, is = t % ISTAGES;
+            const int b = t % NBUF, is = t % ISTAGES;
             mbar_wait(&S.ifull[is], (t / ISTAGES) & 1);
-            mbar_wait(&S.tfull[b], (t >> 1) & 1);
+            mbar_wait(&S.tfull[b], (t / NBUF) & 1);
             tc_fence_after();
             const int* su = S.su[is];
             const int* se = S.se[is];
@@ -444,10 +454,10 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
 #pragma unroll
             for (int ch = 0; ch < NT / 32; ch += 2) {   // chunk ch+1 loads while chunk ch is consumed
                 tmem_ld32(lane_base + uint32_t(b * NT + (ch + 1) * 32), v1);
-                ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)), su + ch * 32, se + ch * 32);
+                if (!(A.dbg & 1)) ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)), su + ch * 32, se + ch * 32);
                 tmem_wait_ld(v1);
                 if (ch + 2 < NT / 32) tmem_ld32(lane_base + uint32_t(b * NT + (ch + 2) * 32), v0);
-                ep.consume(v1, tb + (ch + 1) * 32, max(0, min(32, nv_tile - (ch + 1) * 32)), su + (ch + 1) * 32,
+                if (!(A.dbg & 1)) ep.consume(v1, tb + (ch + 1) * 32, max(0, min(32, nv_tile - (ch + 1) * 32)), su + (ch + 1) * 32,
                            se + (ch + 1) * 32);
                 if (ch + 2 < NT / 32) tmem_wait_ld(v0);
             }
@@ -470,8 +480,19 @@ fg_status launch_ks(const Args& A, cudaStream_t st) {
     const int smem = int(sizeof(Smem<KS>)) + 1024;
     // >= 100 KB per CTA keeps residency at <= 2 CTAs / SM (TMEM: 2 x 256 columns)
     const int smem_req = smem < 100 * 1024 ? 100 * 1024 : smem;
+    {   // pre-split X into tf32 hi / lo rows (the producers' cp.async source)
+        const int64_t tot = A.n_src * KS * 8;
+        if (tot > 0)
+            mlp_split_kernel<KS><<<unsigned((tot + 255) / 256), 256, 0, st>>>(
+                A.X, A.n_src, A.d_in, const_cast<float*>(A.Xhi), const_cast<float*>(A.Xlo));
+        fg_status s = fgk::check_launch("mlp_split_kernel");
+        if (s != FG_OK) return s;
+    }
     auto kfn = mlp_tcgen05_kernel<KS, MAX>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_req);
+    // the whole unified L1/smem for shared memory: without it the driver picks a
+    // carveout that fits ONE 100 KB CTA per SM and the persistent grid runs as two waves
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return fgk::set_error(FG_ECUDA, "mlp_tcgen05: smem attribute: %s", cudaGetErrorString(e));
     int nb = 2 * fgk::num_sms();
     const int64_t want = (A.nnz + 4 * NT - 1) / (4 * NT);   // >= 4 tiles per CTA
@@ -485,10 +506,24 @@ fg_status launch_ks(const Args& A, cudaStream_t st) {
 
 namespace fgk {
 
+size_t mlp_workspace_bytes(int64_t n_src, int d_in) {
+    const int64_t ks = (d_in + 7) / 8;
+    return size_t(2 * n_src * ks * 8 * 4 + 256);
+}
+
 fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W,
                                   int d_in, const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e,
-                                  cudaStream_t st) {
+                                  void* workspace, cudaStream_t st) {
     Args A;
+    const int64_t ksz = (d_in + 7) / 8;
+    float* ws = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    A.Xhi = ws;
+    A.Xlo = ws + g->n_src * ksz * 8;
+    A.n_src = g->n_src;
+    {
+        const char* d = getenv("FG_MLP_DBG");
+        A.dbg = d ? atoi(d) : 0;
+    }
     A.row_ptr = g->row_ptr;
     A.col_idx = g->col_idx;
     A.eid = g->eid;

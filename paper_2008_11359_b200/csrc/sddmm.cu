@@ -38,6 +38,7 @@ __device__ __forceinline__ unsigned group_mask(int lane) {
 struct Args {
     const int32_t* unit_row;
     const int64_t* unit_p0;
+    const int64_t* unit_p1;   // explicit unit ends (source-segmented tables); NULL: min(p0 + chunk, row end)
     int64_t n_units;
     int unit_chunk;
     const int64_t* row_ptr;
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(THREADS, 2) sddmm_kernel(const Args A, const f
     if (unit >= A.n_units) return;
     const int64_t v = A.unit_row[unit];
     const int64_t s = A.unit_p0[unit];
-    const int64_t e = min(s + A.unit_chunk, A.row_ptr[v + 1]);
+    const int64_t e = A.unit_p1 ? A.unit_p1[unit] : min(s + A.unit_chunk, A.row_ptr[v + 1]);
     const int F4 = A.F4, H = A.H, D4 = A.D4;
     const bool stage = (H * B <= CAP);
     int* idx = s_idx[gi];
@@ -287,6 +288,7 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     A.unit_p0 = g->unit_p0;
     A.n_units = g->n_units;
     A.unit_chunk = g->unit_chunk;
+    A.unit_p1 = nullptr;
     A.row_ptr = g->row_ptr;
     A.col_idx = g->col_idx;
     A.eid = g->eid;
@@ -327,6 +329,30 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
                 if (r != FG_OK) return r;
             }
             return FG_OK;
+        }
+    }
+    // Source-segmented traversal (the paper's 1D graph partitioning by source
+    // segments, retargeted from the CPU LLC to the B200 L2): when X does
+    // not fit the L2 budget, the work units are ordered segment by segment of
+    // seg_rows source vertices (each unit = a contiguous run of one row's edges
+    // inside one segment, since rows are sorted by source).  SDDMM has no
+    // cross-edge reduction, so no merge is needed; each pass gathers from an
+    // L2-resident slice of X.  Opt-in: FG_SDDMM_SEGMENT=1.
+    {
+        const int64_t budget = fgk::l2_tile_budget();
+        const char* on = getenv("FG_SDDMM_SEGMENT");   // opt-in: measured slower on reddit (23.6 vs 20.5 ms)
+        const bool enabled = on && on[0] == '1';
+        const int64_t row_bytes = int64_t(F4) * 16;
+        if (enabled && budget > 0 && g->n_src * row_bytes > budget) {
+            int64_t seg_rows = budget / row_bytes;
+            seg_rows = seg_rows < 32 ? 32 : seg_rows;
+            const fg_graph::SegUnits* su = nullptr;
+            fg_status r = fgk::get_seg_units(const_cast<fg_graph*>(g), seg_rows, g->unit_chunk, st, &su);
+            if (r != FG_OK) return r;
+            A.unit_row = su->row;
+            A.unit_p0 = su->p0;
+            A.unit_p1 = su->p1;
+            A.n_units = su->n_units;
         }
     }
     int G = 32, NV = 4;

@@ -26,7 +26,7 @@ EDGE = {"u_dot_v": 0}
 
 # exported symbols declared in include/fg.h (checked by tests/test_abi.py)
 SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
-           "fg_sddmm", "fg_edge_softmax", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
+           "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
            "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
            "fg_allgather_rows", "fg_status_string", "fg_last_error", "fg_abi_version"]
 
@@ -62,6 +62,7 @@ def lib() -> ctypes.CDLL:
     L.fg_spmm.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]
     L.fg_sddmm.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
     L.fg_edge_softmax.argtypes = [vp, i32, vp, vp, vp]
+    L.fg_gat_attention.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp]
     L.fg_graph_transpose.argtypes = [vp, vp, ctypes.POINTER(vp)]
     L.fg_spmm_backward.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
     L.fg_sddmm_backward.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]
@@ -71,7 +72,7 @@ def lib() -> ctypes.CDLL:
     L.fg_comm_destroy.argtypes = [vp]
     L.fg_allgather_rows.argtypes = [vp, vp, i64, vp, vp, vp]
     for f in ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
-              "fg_sddmm", "fg_edge_softmax", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
+              "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
               "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
               "fg_allgather_rows"]:
         getattr(L, f).restype = i32
@@ -161,6 +162,20 @@ class Graph:
             pass
 
 
+def _workspace(g: Graph, msg: int, red: int, H: int, D: int, d_in: int, device):
+    """Scratch of fg_spmm_workspace_size bytes, cached on the graph object
+    (stream-ordered reuse: calls on one stream never overlap)."""
+    n = ctypes.c_size_t(0)
+    _check(lib().fg_spmm_workspace_size(g.handle, msg, red, H, D, d_in, ctypes.byref(n)), "fg_spmm_workspace_size")
+    if n.value == 0:
+        return None, 0
+    buf = getattr(g, "_ws", None)
+    if buf is None or buf.numel() < n.value:
+        buf = torch.empty(n.value, dtype=torch.uint8, device=device)
+        g._ws = buf
+    return buf, buf.numel()
+
+
 def spmm(g: Graph, msg: str, reduce: str, X: torch.Tensor, *, H: int = 1, E: torch.Tensor | None = None,
          W: torch.Tensor | None = None, X_dst: torch.Tensor | None = None, out: torch.Tensor | None = None,
          arg_u: torch.Tensor | bool | None = None, arg_e: torch.Tensor | bool | None = None, stream=None):
@@ -183,8 +198,10 @@ def spmm(g: Graph, msg: str, reduce: str, X: torch.Tensor, *, H: int = 1, E: tor
         arg_e = torch.empty((g.n_dst, F), dtype=torch.int32, device=X.device)
     arg_u = arg_u if isinstance(arg_u, torch.Tensor) else None
     arg_e = arg_e if isinstance(arg_e, torch.Tensor) else None
+    ws, ws_bytes = _workspace(g, MSG[msg], REDUCE[reduce], H_, D, d_in, X.device)
     _check(lib().fg_spmm(g.handle, MSG[msg], REDUCE[reduce], H_, D, _ptr(X), _ptr(E), _ptr(W), d_in, _ptr(X_dst),
-                         _ptr(out), _ptr(arg_u), _ptr(arg_e), None, 0, _stream(stream)), f"fg_spmm({msg},{reduce})")
+                         _ptr(out), _ptr(arg_u), _ptr(arg_e), _ptr(ws), ws_bytes, _stream(stream)),
+           f"fg_spmm({msg},{reduce})")
     if want:
         return out, arg_u, arg_e
     return out
@@ -210,6 +227,24 @@ def edge_softmax(g: Graph, scores: torch.Tensor, *, H: int = 1, out: torch.Tenso
         out = torch.empty_like(scores)
     _check(lib().fg_edge_softmax(g.handle, H, _ptr(scores), _ptr(out), _stream(stream)), "fg_edge_softmax")
     return out
+
+
+def gat_attention(g: Graph, X: torch.Tensor, Y: torch.Tensor | None = None, *, H: int = 1,
+                  out: torch.Tensor | None = None, scores: torch.Tensor | bool | None = None, stream=None):
+    """Fused GAT layer: u_dot_v -> edge softmax -> u_mul_e-sum in one pass.
+    Returns out (and the pre-softmax scores when scores=True or a tensor)."""
+    X = _dev(X, torch.float32, "X")
+    Y = X if Y is None else _dev(Y, torch.float32, "Y")
+    F = X.shape[1]
+    if out is None:
+        out = torch.empty((g.n_dst, F), dtype=torch.float32, device=X.device)
+    want = scores is not None and scores is not False
+    if scores is True:
+        scores = torch.empty((g.nnz, H), dtype=torch.float32, device=X.device)
+    sc = scores if isinstance(scores, torch.Tensor) else None
+    _check(lib().fg_gat_attention(g.handle, H, F // H, _ptr(X), _ptr(Y), _ptr(out), _ptr(sc), _stream(stream)),
+           "fg_gat_attention")
+    return (out, sc) if want else out
 
 
 # ------------------------------------------------------------------ backward (P:171-173)

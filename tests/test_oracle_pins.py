@@ -358,3 +358,32 @@ def test_edge_softmax_matches_torch_dense():
         P = torch.softmax(M, dim=1)
         got = P[torch.from_numpy(rows), torch.from_numpy(g.col_idx.astype(np.int64))].numpy()
         np.testing.assert_allclose(al[:, h], got, rtol=1e-12, atol=0)
+
+
+# ------------------------------------------------------------------ fused GAT definition
+def test_gat_oracle_vs_torch_dense_attention():
+    """or_gat == dense masked softmax attention per head (torch, fp64)."""
+    import torch
+    g = small_graph(n=80, m=900, seed=14)
+    H, D = 2, 4
+    X = gen.features((g.n_src, H * D), 81, 0)
+    Y = gen.features((g.n_dst, H * D), 81, 1)
+    ref, ab = oracle.gat(g.row_ptr, g.col_idx, X, Y, H=H)
+    A = torch.from_numpy(dense_adjacency(g.row_ptr, g.col_idx, g.n_src) > 0)
+    for h in range(H):
+        xs = torch.from_numpy(X[:, h * D:(h + 1) * D].astype(np.float64))
+        ys = torch.from_numpy(Y[:, h * D:(h + 1) * D].astype(np.float64))
+        S = (ys @ xs.T).masked_fill(~A, float("-inf"))
+        P = torch.softmax(S, dim=1).nan_to_num(0.0)      # empty rows -> 0
+        np.testing.assert_allclose(ref[:, h * D:(h + 1) * D], (P @ xs).numpy(), rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(ab[:, h * D:(h + 1) * D], (P @ xs.abs()).numpy(), rtol=1e-12, atol=1e-13)
+
+
+def test_gat_oracle_zero_query_is_mean():
+    """Y = 0 -> every score 0 -> alpha = 1/deg -> out = mean of in-neighbour features."""
+    g = small_graph(n=70, m=600, seed=15)
+    X = gen.features((g.n_src, 8), 82, 0)
+    ref, _ = oracle.gat(g.row_ptr, g.col_idx, X, np.zeros((g.n_dst, 8), np.float32), H=2)
+    A = dense_adjacency(g.row_ptr, g.col_idx, g.n_src)
+    deg = np.maximum(A.sum(1, keepdims=True), 1)
+    np.testing.assert_allclose(ref, (A @ X.astype(np.float64)) / deg, rtol=1e-12, atol=1e-14)

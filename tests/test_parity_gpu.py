@@ -379,3 +379,24 @@ def test_l2_column_tiling(skewed, F, monkeypatch):
     monkeypatch.setenv("FG_L2_TILE_MB", "0")
     s0 = fgp.sddmm(skewed.h, dev(X), dev(Y)).cpu().numpy()
     check_close(s0, ref, ab, TOL, f"untiled u_dot_v F={F}")
+
+
+# ------------------------------------------------------------------ fused GAT (f2)
+@pytest.mark.parametrize("H,D", [(8, 32), (4, 16), (2, 4), (1, 128), (8, 64), (1, 16)])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_gat_fused(skewed, skewed_eid, H, D, use_eid):
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    X = feats((g.n_src, H * D), 970 + D, gen.REAL) * 0.5
+    Y = feats((g.n_dst, H * D), 971 + D, gen.REAL) * 0.5
+    out, sc = fgp.gat_attention(g.h, dev(X), dev(Y), H=H, scores=True)
+    ref, ab = oracle.gat(g.row_ptr, g.col_idx, X, Y, H=H)
+    check_close(out.cpu().numpy(), ref, ab, TOL, f"gat fused H={H} D={D}")
+    rs, rab = oracle.sddmm(g.row_ptr, g.col_idx, X, Y, H=H)
+    pos = np.arange(g.nnz) if g.eid is None else g.eid
+    check_close(sc.cpu().numpy()[pos], rs, rab, TOL, "gat fused scores")
+    # the unfused chain agrees with the fused op
+    s = fgp.sddmm(g.h, dev(X), dev(Y), H=H)
+    a = fgp.edge_softmax(g.h, s, H=H)
+    o2 = fgp.spmm(g.h, "u_mul_e", "sum", dev(X), H=H, E=a).cpu().numpy()
+    check_close(o2, ref, ab, TOL, "unfused chain")

@@ -50,3 +50,7 @@ o = torch.empty(n, 128, device="cuda")
 res["mlp_max_d128"] = (timeit(lambda: fgp.spmm(G, "mlp", "max", X8, W=W, out=o, arg_u=au, arg_e=ae)), None)
 for k, (ms, gbs) in res.items():
     print(f"{k:24s} {ms:8.3f} ms  " + (f"{gbs:8.1f} GB/s" if gbs else ""))
+Xg = torch.rand(n, 256, device="cuda") * 0.25
+og = torch.empty(n, 256, device="cuda")
+ms = timeit(lambda: fgp.gat_attention(G, Xg, H=8, out=og))
+print(f"{'gat_fused':24s} {ms:8.3f} ms")
