@@ -213,7 +213,7 @@ class Step:
                  arg_e=self.aemlp, stream=st)
         rec(8)
 
-    LAUNCHES_PER_STEP = 7   # libfg kernels per step (one per fg_* call)
+    LAUNCHES_PER_STEP = 8   # libfg kernels per step: one per fg_* call, plus mlp's tf32 pre-split
 
     def outputs(self):
         return [self.out512, self.s1, self.o256, self.o128, self.au128, self.ae128, self.omlp, self.aumlp,
@@ -261,10 +261,14 @@ def cpu_threads() -> int:
 
 
 def calibrate_sample(g, host, target_s: float):
-    rows = sample_rows(g, 20000)
-    dt, _, _ = oracle_sample_step(g, host, rows)
-    budget = int(20000 * max(1.0, target_s / max(dt, 1e-3)))
-    return sample_rows(g, min(budget, g.nnz))
+    """Grow a seeded row sample until one oracle step takes ~target_s."""
+    budget = 20000
+    while True:
+        rows = sample_rows(g, budget)
+        dt, _, _ = oracle_sample_step(g, host, rows)
+        if dt >= 0.5 * target_s or budget >= g.nnz:
+            return rows
+        budget = min(g.nnz, int(budget * min(8.0, max(1.5, 0.9 * target_s / max(dt, 1e-3)))))
 
 
 def cpu_baseline(g, host, target_s: float = 12.0) -> dict:

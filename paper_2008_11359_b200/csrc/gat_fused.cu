@@ -71,18 +71,27 @@ __device__ __forceinline__ void attend_range(const Args& A, const float4* __rest
         __syncwarp(mask);
         for (int t = gl; t < cnt; t += G) sidx[t] = __ldg(A.col_idx + p0 + t);
         __syncwarp(mask);
-        for (int t0 = 0; t0 < cnt; t0 += U) {
-            float4 x[U][NV];
+        float4 xn[U][NV];   // software pipeline: next U edges' gathers in flight
+        auto gather = [&](int tb, float4 (&dst)[U][NV]) {
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
-                const int t = t0 + uu;
+                const int t = tb + uu;
                 const float4* xr = X + int64_t(t < cnt ? sidx[t] : 0) * F4;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     const int c = gl + G * j;
-                    x[uu][j] = (t < cnt && c < F4) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    dst[uu][j] = (t < cnt && c < F4) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
+        };
+        gather(0, xn);
+        for (int t0 = 0; t0 < cnt; t0 += U) {
+            float4 x[U][NV];
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu)
+#pragma unroll
+                for (int j = 0; j < NV; ++j) x[uu][j] = xn[uu][j];
+            if (t0 + U < cnt) gather(t0 + U, xn);
             float sc[U][NV];
 #pragma unroll
             for (int uu = 0; uu < U; ++uu)

@@ -63,7 +63,8 @@ __device__ __forceinline__ void set_comp(float4& v, int k, float a) {
 // Accumulate edges [s, e) of one row into (acc, pos) for this lane's NV chunks.
 template <int G, int NV, int OP, bool MAX>
 __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e, int gl, unsigned mask,
-                                             int c4base, float4 (&acc)[NV], int (&pos)[NV][4]) {
+                                             int c4base, float4 (&acc)[NV], int (&pos)[NV][4],
+                                             float* __restrict__ etile) {
     constexpr int B = 32;                                   // edges per index batch
     constexpr int R = B / G;                                // indices per lane per batch
     constexpr int U = NV >= 4 ? 2 : (NV >= 2 ? 4 : 8);      // edges in flight per lane
@@ -77,6 +78,19 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
             const int64_t p = p0 + gl + r * G;
             uix[r] = (p < e) ? __ldg(A.col_idx + p) : 0;
             if constexpr (OP != OP_COPY) eix[r] = (p < e) ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
+        }
+        // u_mul_e with identity edge ids: the batch's E rows are one contiguous span;
+        // stage it in shared memory with coalesced loads instead of one dependent
+        // scalar load per edge and chunk
+        bool staged = false;
+        if constexpr (OP == OP_UMULE && G == 32) {
+            if (A.eid == nullptr && A.H <= 16) {
+                staged = true;
+                __syncwarp(mask);
+                const float* Eb = A.E + p0 * A.H;
+                for (int q = gl; q < cnt * A.H; q += G) etile[q] = __ldg(Eb + q);
+                __syncwarp(mask);
+            }
         }
 #pragma unroll
         for (int t0 = 0; t0 < B; t0 += U) {
@@ -97,7 +111,7 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                     x[uu][j] = ok ? __ldg(xr + c) : f4(0.f);
                     if constexpr (OP == OP_UMULE) {
                         const int h = (4 * c) / A.D;
-                        ev[uu][j][0] = ok ? __ldg(A.E + int64_t(ed) * A.H + h) : 0.f;
+                        ev[uu][j][0] = !ok ? 0.f : (staged ? etile[t * A.H + h] : __ldg(A.E + int64_t(ed) * A.H + h));
                     } else if constexpr (OP == OP_UMULE_GEN) {
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
@@ -190,6 +204,7 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     constexpr int NG = THREADS / G;                 // groups per CTA
     constexpr int TW = G * NV;                      // float4 columns per tile
     __shared__ float4 s_acc[MAX ? 1 : NG][MAX ? 1 : TW];
+    __shared__ float s_etile[(OP == OP_UMULE && G == 32) ? NG : 1][(OP == OP_UMULE && G == 32) ? 32 * 16 : 1];
     __shared__ float s_val[MAX ? NG : 1][MAX ? TW * 4 : 1];
     __shared__ int s_pos[MAX ? NG : 1][MAX ? TW * 4 : 1];
 
@@ -209,7 +224,7 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
         const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
         const int64_t len = (e - s + NG - 1) / NG;
         const int64_t gs = min(e, s + gi * len), ge = min(e, gs + len);
-        gather_range<G, NV, OP, MAX>(A, gs, ge, gl, mask, c4base, acc, pos);
+        gather_range<G, NV, OP, MAX>(A, gs, ge, gl, mask, c4base, acc, pos, s_etile[gi]);
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
             const int c = gl + G * j;
@@ -251,7 +266,7 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     if (r >= A.n_rows) return;
     const int64_t v = A.rows[r];
     const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
-    gather_range<G, NV, OP, MAX>(A, s, e, gl, mask, c4base, acc, pos);
+    gather_range<G, NV, OP, MAX>(A, s, e, gl, mask, c4base, acc, pos, s_etile[gi]);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const int c = c4base + gl + G * j;

@@ -74,13 +74,21 @@ if os.path.exists(lp):
     hdr = rows[0]
     ik, iv = hdr.index("Kernel Name"), hdr.index("Metric Value")
     data = [(r[ik], float(r[iv].replace(",", ""))) for r in rows[1:]]
-    # keep the last step: the last 7 launches of our kernels + the fill before them
-    ours = [(k, v) for k, v in data if any(s in k for s in ("spmm_gather", "sddmm", "softmax", "mlp_"))]
-    step = ours[-7:]
+    # the last step = every launch after the last L2-flush fill kernel (bench.py writes
+    # a 256 MB buffer before each step)
+    segs, cur = [], []
+    for k, v in data:
+        if "FillFunctor" in k:
+            segs.append(cur)
+            cur = []
+        else:
+            cur.append((k, v))
+    segs.append(cur)
+    step = [sg for sg in segs if len(sg) >= 7][-1]   # last full step (extras follow it)
     tot = sum(v for _, v in step)
     out = [f"# Launch list of one bench step ({tag})", "",
            "`ncu --metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 2 --warmup 3`; "
-           "the last step's 7 libfg launches.  Per-launch times are cold-cache and serialised: compare shares.", "",
+           "every launch of the last step (all libfg kernels).  Per-launch times are cold-cache and serialised: compare shares.", "",
            "| # | kernel | ns | share |", "|---|---|---|---|"]
     for i, (k, v) in enumerate(step):
         out.append(f"| {i} | `{k[:90]}` | {v:.0f} | {v / tot:.1%} |")
