@@ -97,7 +97,7 @@ __device__ __forceinline__ void reduce_scatter(float (&v)[K], int gl, unsigned m
 // MODE_GENERAL : H == 1 with F > 4*G*NV (column tiles; Y re-read through L1), or
 //                H > 1 with D4 > G (a head spans several chunks of a lane).
 template <int G, int NV, int MODE, int DW>
-__global__ void __launch_bounds__(THREADS, 2) sddmm_kernel(const Args A, const float4* __restrict__ X,
+__global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const float4* __restrict__ X,
                                                            const float4* __restrict__ Y, float* __restrict__ out) {
     constexpr int TW = G * NV;
     constexpr int B = G >= 4 ? 32 : 8;              // edges per batch
@@ -133,22 +133,6 @@ __global__ void __launch_bounds__(THREADS, 2) sddmm_kernel(const Args A, const f
         __syncwarp(mask);
         for (int t = gl; t < cnt; t += G) idx[t] = __ldg(A.col_idx + p0 + t);
         __syncwarp(mask);
-        // software pipeline: the gathers of edges [t0+U, t0+2U) are in flight while
-        // edges [t0, t0+U) are reduced
-        float4 xn[U][NV];
-        auto gather = [&](int tb, float4 (&dst)[U][NV]) {
-#pragma unroll
-            for (int uu = 0; uu < U; ++uu) {
-                const int t = tb + uu;
-                const float4* xr = X + int64_t((t < cnt) ? idx[t] : 0) * F4;
-#pragma unroll
-                for (int j = 0; j < NV; ++j) {
-                    const int c = A.c4base + gl + G * j;
-                    dst[uu][j] = (t < cnt && c < F4) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            }
-        };
-        gather(0, xn);
         for (int t0 = 0; t0 < cnt; t0 += U) {
             float4 x[U][NV];
             int us[U];
@@ -156,10 +140,13 @@ __global__ void __launch_bounds__(THREADS, 2) sddmm_kernel(const Args A, const f
             for (int uu = 0; uu < U; ++uu) {
                 const int t = t0 + uu;
                 us[uu] = (t < cnt) ? idx[t] : 0;
+                const float4* xr = X + int64_t(us[uu]) * F4;
 #pragma unroll
-                for (int j = 0; j < NV; ++j) x[uu][j] = xn[uu][j];
+                for (int j = 0; j < NV; ++j) {
+                    const int c = A.c4base + gl + G * j;
+                    x[uu][j] = (t < cnt && c < F4) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
             }
-            if (t0 + U < cnt) gather(t0 + U, xn);
             if constexpr (MODE == MODE_H1 || MODE == MODE_HEADS) {
                 if (stage) {
                     // reduce-scatter of the U edges' (x NV chunk) partial dots over the DW

@@ -1,3 +1,2 @@
 timeout 300 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-timeout 300 python tools/mlp_exp.py reddit
 timeout 300 python tools/quickbench.py reddit 2>&1 | tail -12
