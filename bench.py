@@ -43,7 +43,6 @@ GRAPH = "reddit"
 F_GCN, F_DOT, H_GAT, D_GAT, F_MAX, D1, D2 = 512, 512, 8, 32, 128, 8, 128
 OPS = ["spmm_copy_u_sum_F512", "sddmm_u_dot_v_H1_F512", "sddmm_u_dot_v_H8_D32", "edge_softmax_H8",
        "spmm_u_mul_e_sum_H8_D32", "spmm_copy_u_max_F128_args", "spmm_mlp_max_d8_d128_args"]
-DOMINANT = "spmm_copy_u_sum_F512"
 
 
 def metric_name() -> str:
@@ -261,19 +260,19 @@ def cpu_threads() -> int:
 
 
 def calibrate_sample(g, host, target_s: float):
-    """Grow a seeded row sample until one oracle step takes ~target_s."""
+    """Grow a seeded row sample until one oracle step takes ~target_s.  Returns
+    (rows, seconds, bytes, edges) of the LAST (reported) measurement."""
     budget = 20000
     while True:
         rows = sample_rows(g, budget)
-        dt, _, _ = oracle_sample_step(g, host, rows)
+        dt, b, me = oracle_sample_step(g, host, rows)
         if dt >= 0.5 * target_s or budget >= g.nnz:
-            return rows
+            return rows, dt, b, me
         budget = min(g.nnz, int(budget * min(8.0, max(1.5, 0.9 * target_s / max(dt, 1e-3)))))
 
 
 def cpu_baseline(g, host, target_s: float = 12.0) -> dict:
-    rows = calibrate_sample(g, host, target_s)
-    dt, b, me = oracle_sample_step(g, host, rows)
+    rows, dt, b, me = calibrate_sample(g, host, target_s)
     return {"value": b / dt / 1e9, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle",
             "sample": f"all 7 ops of the step on {rows.size} seeded-random destination rows "
                       f"({me} in-edges, {me / g.nnz:.2%} of the graph), fp64 C oracle, OpenMP over rows; "
@@ -371,8 +370,10 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(g, host)
-    dom_ms = op_ms[DOMINANT]
-    achieved = local_bytes[DOMINANT] / (dom_ms * 1e-3) / 1e9
+    # dominant kernel = the HBM-bound op with the largest share of the step
+    dom = max((k for k in op_ms if k != "spmm_mlp_max_d8_d128_args"), key=lambda k: op_ms[k])
+    dom_ms = op_ms[dom]
+    achieved = local_bytes[dom] / (dom_ms * 1e-3) / 1e9
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -380,7 +381,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(DOMINANT, {}).get("dram_bytes_per_launch")
+            traffic = json.load(open(tp)).get(dom, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     line = {
@@ -411,12 +412,13 @@ def main():
         {k: round(local_bytes[k] / (op_ms[k] * 1e-3) / 1e9, 1) for k in OPS},
         "allgather_ms": round(ag_ms, 4) if world > 1 else 0.0,
         "mlp_tflops": round(mlp_flops(S.m) / (op_ms["spmm_mlp_max_d8_d128_args"] * 1e-3) / 1e12, 2),
-        "roofline": {"kernel": DOMINANT, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+        "roofline": {"kernel": dom, "share": round(dom_ms / sum(op_ms.values()), 4), "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
                      "bytes_model": "gather model (SURVEY 8(d)): every per-edge source-row read counted at "
-                                    "full width; L2 serves most of them (feature-dimension tiling), so "
-                                    "achieved/peak > 1; 'traffic' is the ncu DRAM bytes of one launch",
+                                    "full width; L2 serves part of them, so achieved/peak can exceed 1; "
+                                    "'traffic' is the ncu DRAM bytes of one launch and dram_frac its "
+                                    "rate against the same peak",
                      "dram_frac": (round(traffic / (dom_ms * 1e-3) / 1e9 / peak, 4) if traffic else None)},
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -499,7 +501,7 @@ def run_reference(args, world, rank):
     import gen
     g = gen.make_graph(GRAPH, uniform_sources=args.uniform_sources)
     host = make_inputs(g)
-    rows = calibrate_sample(g, host, target_s=4.0)
+    rows = calibrate_sample(g, host, target_s=4.0)[0]
     for _ in range(args.warmup):
         oracle_sample_step(g, host, rows)
     dts, b, me = [], 0, 0

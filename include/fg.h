@@ -70,15 +70,23 @@ typedef enum {
 typedef enum {
     FG_MSG_COPY_U = 0,   /* phi = x_u                       Fig. 3a */
     FG_MSG_U_MUL_E = 1,  /* phi[h,d] = x_u[h,d] * x_uv[h]   DGL builtin P:375; GAT P:983 */
-    FG_MSG_MLP = 2       /* phi = ReLU((x_u + x_v) W)       Fig. 3b */
+    FG_MSG_MLP = 2,      /* phi = ReLU((x_u + x_v) W)       Fig. 3b */
+    FG_MSG_U_ADD_E = 3,  /* phi[h,d] = x_u[h,d] + x_uv[h]   DGL builtin family P:372-375 (row f4) */
+    FG_MSG_COPY_E = 4    /* phi = x_uv (edge feature row)   same family (row f4) */
 } fg_msg_op;
 
-/* Aggregations (+) of Eq. (1): sum (Fig. 3a), max (Fig. 1). */
-typedef enum { FG_REDUCE_SUM = 0, FG_REDUCE_MAX = 1 } fg_reduce_op;
+/* Aggregations (+) of Eq. (1): sum (Fig. 3a), max (Fig. 1).
+ * min and mean are the other two reducers of the DGL builtin family the paper
+ * plugs into: min is max with the comparison
+ * flipped, mean is sum divided by the in-degree |N(v)| (IEEE fp32 division). */
+typedef enum { FG_REDUCE_SUM = 0, FG_REDUCE_MAX = 1, FG_REDUCE_MIN = 2, FG_REDUCE_MEAN = 3 } fg_reduce_op;
 
 /* Edge functions psi of Eq. (2). */
 typedef enum {
-    FG_EDGE_U_DOT_V = 0  /* psi[h] = sum_d x_u[h,d] y_v[h,d]   Eq. (4); Fig. 5 */
+    FG_EDGE_U_DOT_V = 0, /* psi[h] = sum_d x_u[h,d] y_v[h,d]   Eq. (4); Fig. 5 */
+    FG_EDGE_U_ADD_V = 1, /* psi[j] = x_u[j] + y_v[j]           DGL builtin family P:372-375 (row f4) */
+    FG_EDGE_U_SUB_V = 2, /* psi[j] = x_u[j] - y_v[j]           same */
+    FG_EDGE_U_MUL_V = 3  /* psi[j] = x_u[j] * y_v[j]           same */
 } fg_edge_op;
 
 typedef struct fg_graph fg_graph;          /* opaque, immutable after create */
@@ -123,6 +131,10 @@ fg_status fg_graph_info(const fg_graph* g, fg_graph_info_t* info);
  *
  *   msg = FG_MSG_COPY_U   : X [n_src][H*D]; E, W, X_dst NULL; d_in = 0.
  *   msg = FG_MSG_U_MUL_E  : X [n_src][H*D]; E [nnz][H] indexed by edge id.
+ *   msg = FG_MSG_U_ADD_E  : as u_mul_e with phi = x_u + e (fp32 add, rounded
+ *                           once before a max/min compare).
+ *   msg = FG_MSG_COPY_E   : X NULL; E [nnz][H*D] indexed by edge id, 16-byte
+ *                           aligned (the message is the edge's own row).
  *   msg = FG_MSG_MLP      : H == 1, D == d2 (output width); X [n_src][d_in],
  *                           W [d_in][d2], X_dst [n_dst][d_in] (NULL -> X, which
  *                           requires n_src == n_dst); 1 <= d_in <= 32 (d_in = 8
@@ -130,10 +142,11 @@ fg_status fg_graph_info(const fg_graph* g, fg_graph_info_t* info);
  *                           contraction (Fig. 3b).  Runs on the
  *                           tcgen05 tensor cores (split-TF32).
  *   out   : [n_dst][H*D] fp32, fully overwritten.
- *   red   : FG_REDUCE_SUM or FG_REDUCE_MAX (elementwise per feature column).
- *   arg_u, arg_e : max only, each optional (NULL); int32 [n_dst][H*D]:
+ *   red   : FG_REDUCE_SUM / _MAX / _MIN / _MEAN (elementwise per feature
+ *           column).  mlp supports sum and max only (else FG_EUNSUPPORTED).
+ *   arg_u, arg_e : max/min only, each optional (NULL); int32 [n_dst][H*D]:
  *           source id / edge id of the winning edge.  Ties -> lowest CSR
- *           position.  Must be NULL for sum.
+ *           position.  Must be NULL for sum and mean.
  *   Empty rows: out = +0.0 and arg = -1.
  *   workspace / workspace_bytes: device scratch of >= fg_spmm_workspace_size
  *           bytes, owned by the caller, not used across calls (may be NULL
@@ -159,6 +172,10 @@ fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int
  *       both sides);  out : [nnz][H], fully overwritten.
  *   Heads are independent reductions (Fig. 5b).  Requires (H*D) % 4 == 0 and,
  *   for H > 1, D % 4 == 0 with D/4 a power of two (else FG_ESHAPE).
+ * Elementwise ops (FG_EDGE_U_ADD_V / _SUB_V / _MUL_V, row f4):
+ *     out[eid(p)][j] = X[u][j] OP Y[v][j],  j < H*D;  out : [nnz][H*D] (H is
+ *   only a shape factor here); one IEEE fp32 operation per element, so the
+ *   result is exact to the rounding of that operation.
  */
 fg_status fg_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, const float* X, const float* Y,
                    float* out, fg_stream stream);
@@ -204,8 +221,9 @@ fg_status fg_gat_attention(const fg_graph* g, int H, int D, const float* X, cons
  *   msg in {FG_MSG_COPY_U, FG_MSG_U_MUL_E} (mlp: FG_EUNSUPPORTED -- SPEC.md
  *   S:380 non-goal);
  *   dOut [n_dst][H*D];  dX [n_src][H*D] (optional, needs gT);  dE [nnz][H]
- *   (optional, u_mul_e only, needs X);  max needs arg_u from the forward (only
- *   the winning edge of each (v, j) receives dOut[v][j]).  Outputs overwritten.
+ *   (optional, u_mul_e only, needs X);  max/min need arg_u from the forward
+ *   (only the winning edge of each (v, j) receives dOut[v][j]); mean passes
+ *   dOut[v] / |N(v)| to every in-edge of v.  Outputs overwritten.
  *
  * fg_sddmm_backward -- for s = fg_sddmm(g, u_dot_v, H, D, X, Y):
  *   dX [n_src][H*D] = sum_{e=u->v} dS[e] Y[v] (needs gT, Y);

@@ -21,8 +21,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-OPS = {"copy_u": 0, "u_mul_e": 1, "mlp": 2}
-REDS = {"sum": 0, "max": 1}
+OPS = {"copy_u": 0, "u_mul_e": 1, "mlp": 2, "u_add_e": 3, "copy_e": 4}
+REDS = {"sum": 0, "max": 1, "min": 2, "mean": 3}
 
 
 def build(force: bool = False) -> str:
@@ -46,6 +46,8 @@ def _L():
         lib.or_sddmm.restype = None
         lib.or_edge_softmax.argtypes = [i64, vp, vp, vp, i32, vp, vp]
         lib.or_edge_softmax.restype = None
+        lib.or_sddmm_binary.argtypes = [i64, vp, vp, vp, i32, i64, vp, vp, vp, vp]
+        lib.or_sddmm_binary.restype = None
         _lib = lib
     return _lib
 
@@ -68,12 +70,17 @@ def _rows(rows, n_dst):
 def spmm(row_ptr, col_idx, op: str, red: str, X, *, H: int = 1, D: int | None = None, E=None,
          W=None, X_dst=None, eid=None, rows=None, want_arg: bool = True):
     """Eq. (1) for the listed destination rows.  Returns (ref, abssum, arg_u, arg_e)
-    with ref/abssum fp64 [n_rows][F] and args int32 (max only, else None)."""
+    with ref/abssum fp64 [n_rows][F] and args int32 (max/min only, else None)."""
     row_ptr, col_idx, eid = _c(row_ptr, np.int64), _c(col_idx, np.int32), _c(eid, np.int32)
     X = _c(X, np.float32)
     n_dst = row_ptr.size - 1
     d_in = 0
-    if op == "mlp":
+    if op == "copy_e":                      # message = the edge's own feature row
+        E = _c(E, np.float32)
+        F = E.reshape(E.shape[0], -1).shape[1]
+        D = F // H if D is None else D
+        assert H * D == F
+    elif op == "mlp":
         W = _c(W, np.float32)
         d_in, F = W.shape
         H, D = 1, F
@@ -88,7 +95,7 @@ def spmm(row_ptr, col_idx, op: str, red: str, X, *, H: int = 1, D: int | None = 
     ref = np.empty((n_rows, F), np.float64)
     ab = np.empty((n_rows, F), np.float64)
     au = ae = None
-    if red == "max" and want_arg:
+    if red in ("max", "min") and want_arg:
         au = np.empty((n_rows, F), np.int32)
         ae = np.empty((n_rows, F), np.int32)
     _L().or_spmm(n_rows, _p(rows_a), _p(row_ptr), _p(col_idx), _p(eid), OPS[op], REDS[red], H, D,
@@ -110,6 +117,26 @@ def sddmm(row_ptr, col_idx, X, Y=None, *, H: int = 1, rows=None):
     ref = np.empty((ne, H), np.float64)
     ab = np.empty((ne, H), np.float64)
     _L().or_sddmm(n_rows, _p(rows_a), _p(row_ptr), _p(col_idx), H, D, _p(X), _p(Y), _p(ref), _p(ab))
+    return ref, ab
+
+
+BINOPS = {"u_add_v": 0, "u_sub_v": 1, "u_mul_v": 2}
+
+
+def sddmm_binary(row_ptr, col_idx, op: str, X, Y=None, *, rows=None):
+    """Elementwise SDDMM X[u] OP Y[v] (OP in add/sub/mul) for the edges of the
+    listed rows in CSR order.  Returns (ref, abssum) fp64 [edges][F]."""
+    row_ptr, col_idx = _c(row_ptr, np.int64), _c(col_idx, np.int32)
+    X = _c(X, np.float32)
+    Y = X if Y is None else _c(Y, np.float32)
+    F = X.reshape(X.shape[0], -1).shape[1]
+    n_rows, rows_a = _rows(rows, row_ptr.size - 1)
+    ne = int(row_ptr[-1] - row_ptr[0]) if rows_a is None else \
+        int((row_ptr[rows_a + 1] - row_ptr[rows_a]).sum())
+    ref = np.empty((ne, F), np.float64)
+    ab = np.empty((ne, F), np.float64)
+    _L().or_sddmm_binary(n_rows, _p(rows_a), _p(row_ptr), _p(col_idx), BINOPS[op], F, _p(X), _p(Y), _p(ref),
+                         _p(ab))
     return ref, ab
 
 
@@ -157,7 +184,7 @@ def _bind_backward():
 
 def spmm_backward(row_ptr, col_idx, op: str, red: str, X, dOut, *, n_src: int, H: int = 1, E=None, eid=None,
                   arg_u=None, want_dE: bool = False):
-    """Gradients of Eq. (1) (copy_u / u_mul_e, sum / max).  Returns (dX, dE) fp64."""
+    """Gradients of Eq. (1) (copy_u / u_mul_e; sum / max / min / mean).  Returns (dX, dE) fp64."""
     row_ptr, col_idx, eid = _c(row_ptr, np.int64), _c(col_idx, np.int32), _c(eid, np.int32)
     X, dOut, E = _c(X, np.float32), _c(dOut, np.float32), _c(E, np.float32)
     arg_u = _c(arg_u, np.int32)

@@ -36,8 +36,12 @@
 #define OR_COPY_U  0   /* phi = x_u                              P:252-254 (Fig. 3a) */
 #define OR_U_MUL_E 1   /* phi = x_u[h,:] * x_uv[h]               P:375 (DGL builtin) */
 #define OR_MLP     2   /* phi = ReLU((x_u + x_v) W)              P:289-296 (Fig. 3b) */
+#define OR_U_ADD_E 3   /* phi = x_u[h,:] + x_uv[h]               DGL builtin family P:372-375 */
+#define OR_COPY_E  4   /* phi = x_uv (edge feature row [F])      same family */
 #define OR_SUM 0       /* aggregation: sum */
 #define OR_MAX 1       /* aggregation: max                       P:56 (Fig. 1) */
+#define OR_MIN 2       /* aggregation: min  (DGL builtin family) */
+#define OR_MEAN 3      /* aggregation: mean = sum / |N(v)|  (same family)  */
 
 static inline int64_t edge_id(const int32_t* eid, int64_t p) { return eid ? (int64_t)eid[p] : p; }
 
@@ -50,10 +54,14 @@ static inline int64_t edge_id(const int32_t* eid, int64_t p) { return eid ? (int
  *   u_mul_e: t = X[u][j] * E[eid][j / D]                   (F = H*D, E is [nnz][H])
  *   mlp    : t = max(0, sum_{k<d_in} (X[u][k] + X_dst[v][k]) * W[k][j])   (F = d2; Fig. 3b: ReLU
  *            applied after the full d1 contraction)
+ *   u_add_e: t = X[u][j] + E[eid][j / D]                   (F = H*D, E is [nnz][H]); |t| := |x| + |e|
+ *   copy_e : t = E[eid][j]                                 (F = H*D, E is [nnz][F]; X unused)
  *   sum: ref = sum over the row's edges in CSR order; abssum = sum |t| (mlp: sum_e sum_k |a_k W_kj|)
  *   max: ref = max_t with the FIRST edge (lowest CSR position) winning ties;
  *        u_mul_e compares the fp32-rounded product (the kernel's precision);
  *        abssum = |terms| of the winning message; arg_u/arg_e = col_idx / eid of the winner.
+ *   min: as max with the comparison reversed (strict <: first wins).
+ *   mean: ref = (sum over the row) / |N(v)|, abssum = (sum |t|) / |N(v)|.
  *   empty row: ref = +0.0, abssum = 0, arg = -1.
  */
 void or_spmm(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr, const int32_t* col_idx,
@@ -70,7 +78,7 @@ void or_spmm(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr, const 
             double* acc = ref + r * F;          /* h_v, accumulated in place */
             double* ab = abssum + r * F;
             for (int64_t j = 0; j < F; ++j) {
-                acc[j] = (red == OR_SUM) ? 0.0 : -INFINITY;
+                acc[j] = (red == OR_SUM || red == OR_MEAN) ? 0.0 : (red == OR_MIN ? INFINITY : -INFINITY);
                 ab[j] = 0.0;
                 best[j] = -1;
             }
@@ -86,6 +94,12 @@ void or_spmm(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr, const 
                     } else if (op == OR_U_MUL_E) {
                         t = (double)X[u * F + j] * (double)E[e * H + j / D];   /* exact in fp64 */
                         t_abs = fabs(t);
+                    } else if (op == OR_U_ADD_E) {
+                        t = (double)X[u * F + j] + (double)E[e * H + j / D];   /* exact in fp64 */
+                        t_abs = fabs((double)X[u * F + j]) + fabs((double)E[e * H + j / D]);
+                    } else if (op == OR_COPY_E) {
+                        t = (double)E[e * F + j];
+                        t_abs = fabs(t);
                     } else {
                         double z = 0.0; t_abs = 0.0;
                         for (int k = 0; k < d_in; ++k) {
@@ -95,17 +109,21 @@ void or_spmm(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr, const 
                         }
                         t = z > 0.0 ? z : 0.0;   /* ReLU = tvm.max(., 0), canonical +0.0 */
                     }
-                    if (red == OR_SUM) {
+                    if (red == OR_SUM || red == OR_MEAN) {
                         acc[j] += t; ab[j] += t_abs;
                     } else {
-                        double key = (op == OR_U_MUL_E) ? (double)(float)t : t;
-                        if (key > acc[j]) { acc[j] = key; best[j] = p; ab[j] = t_abs; }  /* strict >: first wins */
+                        /* u_mul_e / u_add_e compare the fp32-rounded message (the kernel's precision) */
+                        double key = (op == OR_U_MUL_E || op == OR_U_ADD_E) ? (double)(float)t : t;
+                        int better = (red == OR_MIN) ? (key < acc[j]) : (key > acc[j]);
+                        if (better) { acc[j] = key; best[j] = p; ab[j] = t_abs; }  /* strict: first wins */
                     }
                 }
             }
+            const int64_t deg = row_ptr[v + 1] - row_ptr[v];
             for (int64_t j = 0; j < F; ++j) {
-                if (row_ptr[v + 1] == row_ptr[v]) { acc[j] = 0.0; ab[j] = 0.0; }
-                if (red == OR_MAX) {
+                if (deg == 0) { acc[j] = 0.0; ab[j] = 0.0; }
+                else if (red == OR_MEAN) { acc[j] /= (double)deg; ab[j] /= (double)deg; }
+                if (red == OR_MAX || red == OR_MIN) {
                     if (arg_u) arg_u[r * F + j] = best[j] < 0 ? -1 : col_idx[best[j]];
                     if (arg_e) arg_e[r * F + j] = best[j] < 0 ? -1 : (int32_t)edge_id(eid, best[j]);
                 }
@@ -146,6 +164,42 @@ void or_sddmm(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr, const
                 }
                 ref[o * H + h] = s;
                 abssum[o * H + h] = a;
+            }
+        }
+    }
+    free(off);
+}
+
+/*
+ * Elementwise SDDMM edge functions (the u_OP_v members of the DGL builtin
+ * family the paper plugs into): Eq. (2) with
+ *   psi(x_u, x_v)[j] = X[u][j] OP Y[v][j],  OP in {add (0), sub (1), mul (2)}
+ * for every edge of the listed rows, written at the listed-row position o
+ * like or_sddmm: ref/abssum [edges of listed rows][F]; abssum = |x| OP' |y|
+ * (add/sub: |x| + |y|, mul: |x y|).
+ */
+void or_sddmm_binary(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr, const int32_t* col_idx,
+                     int bop, int64_t F, const float* X, const float* Y, double* ref, double* abssum) {
+    int64_t* off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_rows + 1));
+    off[0] = 0;
+    for (int64_t r = 0; r < n_rows; ++r) {
+        int64_t v = rows ? rows[r] : r;
+        off[r + 1] = off[r] + (row_ptr[v + 1] - row_ptr[v]);
+    }
+    #pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t r = 0; r < n_rows; ++r) {
+        const int64_t v = rows ? rows[r] : r;
+        for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {
+            const int64_t u = col_idx[p];
+            const int64_t o = off[r] + (p - row_ptr[v]);
+            for (int64_t j = 0; j < F; ++j) {
+                const double x = (double)X[u * F + j], y = (double)Y[v * F + j];
+                double t;
+                if (bop == 0) t = x + y;
+                else if (bop == 1) t = x - y;
+                else t = x * y;
+                ref[o * F + j] = t;
+                abssum[o * F + j] = (bop == 2) ? fabs(t) : fabs(x) + fabs(y);
             }
         }
     }
@@ -201,7 +255,9 @@ void or_edge_softmax(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr
  * sum : dX[u][j] += dOut[v][j] * (u_mul_e ? E[e][j/D] : 1)
  *       dE[e][h] += sum_{d<D} dOut[v][h*D+d] * X[u][h*D+d]           (u_mul_e)
  * max : only the winning edge of (v, j) (arg_u[v][j] = its source, the
- *       forward's first-wins argmax; -1 for empty rows) gets the gradient. */
+ *       forward's first-wins argmax; -1 for empty rows) gets the gradient.
+ * min : as max (arg_u = the first-wins argmin).
+ * mean: as sum with dOut[v][j] / |N(v)| in place of dOut[v][j]. */
 void or_spmm_backward(int64_t n_dst, int64_t n_src, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
                       const int32_t* eid, int op, int red, int H, int D, const float* X, const float* E,
                       const float* dOut, const int32_t* arg_u, double* dX, double* dE) {
@@ -213,8 +269,9 @@ void or_spmm_backward(int64_t n_dst, int64_t n_src, int64_t nnz, const int64_t* 
             const int64_t u = col_idx[p];
             const int64_t e = edge_id(eid, p);
             for (int64_t j = 0; j < F; ++j) {
-                if (red == OR_MAX && arg_u[v * F + j] != u) continue;   /* not the winner */
-                const double g = (double)dOut[v * F + j];
+                if ((red == OR_MAX || red == OR_MIN) && arg_u[v * F + j] != u) continue;   /* not the winner */
+                double g = (double)dOut[v * F + j];
+                if (red == OR_MEAN) g /= (double)(row_ptr[v + 1] - row_ptr[v]);
                 const double w = (op == OR_U_MUL_E) ? (double)E[e * H + j / D] : 1.0;
                 if (dX) dX[u * F + j] += g * w;
                 if (dE && op == OR_U_MUL_E) dE[e * H + j / D] += g * (double)X[u * F + j];

@@ -26,7 +26,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas",
 
 
 def _deps_mtime(src: str) -> float:
-    hdrs = glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "fg.h")]
+    hdrs = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        [os.path.join(ROOT, "include", "fg.h")]
     return max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in hdrs])
 
 

@@ -59,10 +59,15 @@ extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
                              float* out, int32_t* arg_u, int32_t* arg_e, void* workspace,
                              size_t workspace_bytes, fg_stream stream) {
     if (!g) return set_error(FG_EINVAL, "fg_spmm: NULL graph");
-    if (msg != FG_MSG_COPY_U && msg != FG_MSG_U_MUL_E && msg != FG_MSG_MLP)
+    if (msg != FG_MSG_COPY_U && msg != FG_MSG_U_MUL_E && msg != FG_MSG_MLP && msg != FG_MSG_U_ADD_E &&
+        msg != FG_MSG_COPY_E)
         return set_error(FG_EINVAL, "fg_spmm: bad msg op %d", int(msg));
-    if (red != FG_REDUCE_SUM && red != FG_REDUCE_MAX) return set_error(FG_EINVAL, "fg_spmm: bad reduce op %d", int(red));
-    if (red == FG_REDUCE_SUM && (arg_u || arg_e)) return set_error(FG_EINVAL, "fg_spmm: arg_u/arg_e must be NULL for sum");
+    if (red != FG_REDUCE_SUM && red != FG_REDUCE_MAX && red != FG_REDUCE_MIN && red != FG_REDUCE_MEAN)
+        return set_error(FG_EINVAL, "fg_spmm: bad reduce op %d", int(red));
+    if ((red == FG_REDUCE_SUM || red == FG_REDUCE_MEAN) && (arg_u || arg_e))
+        return set_error(FG_EINVAL, "fg_spmm: arg_u/arg_e must be NULL for sum/mean");
+    if (msg == FG_MSG_MLP && red != FG_REDUCE_SUM && red != FG_REDUCE_MAX)
+        return set_error(FG_EUNSUPPORTED, "fg_spmm(mlp): only sum and max reducers");
     if (H < 1 || D < 1) return set_error(FG_ESHAPE, "fg_spmm: H=%d D=%d must be >= 1", H, D);
     const int64_t F = int64_t(H) * D;
     if (F % 4 != 0) return set_error(FG_ESHAPE, "fg_spmm: H*D=%lld must be a multiple of 4", (long long)F);
@@ -82,10 +87,13 @@ extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
                              fgk::mlp_workspace_bytes(g->n_src, d_in));
     } else {
         if (d_in != 0 || W || X_dst) return set_error(FG_EINVAL, "fg_spmm: W/X_dst/d_in are for mlp only");
-        if (msg == FG_MSG_U_MUL_E && !E && g->nnz > 0) return set_error(FG_EINVAL, "fg_spmm(u_mul_e): E is NULL");
+        if ((msg == FG_MSG_U_MUL_E || msg == FG_MSG_U_ADD_E || msg == FG_MSG_COPY_E) && !E && g->nnz > 0)
+            return set_error(FG_EINVAL, "fg_spmm(u_*_e / copy_e): E is NULL");
         if (msg == FG_MSG_COPY_U && E) return set_error(FG_EINVAL, "fg_spmm(copy_u): E must be NULL");
+        if (msg == FG_MSG_COPY_E && X) return set_error(FG_EINVAL, "fg_spmm(copy_e): X must be NULL");
+        if (msg == FG_MSG_COPY_E && !aligned16(E)) return set_error(FG_EINVAL, "fg_spmm(copy_e): E must be 16-byte aligned");
     }
-    if (!X && g->nnz > 0) return set_error(FG_EINVAL, "fg_spmm: X is NULL");
+    if (msg != FG_MSG_COPY_E && !X && g->nnz > 0) return set_error(FG_EINVAL, "fg_spmm: X is NULL");
     if (g->n_dst == 0) return FG_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (msg == FG_MSG_MLP)
@@ -96,17 +104,20 @@ extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
 extern "C" fg_status fg_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, const float* X, const float* Y,
                               float* out, fg_stream stream) {
     if (!g) return set_error(FG_EINVAL, "fg_sddmm: NULL graph");
-    if (op != FG_EDGE_U_DOT_V) return set_error(FG_EINVAL, "fg_sddmm: bad edge op %d", int(op));
+    if (op != FG_EDGE_U_DOT_V && op != FG_EDGE_U_ADD_V && op != FG_EDGE_U_SUB_V && op != FG_EDGE_U_MUL_V)
+        return set_error(FG_EINVAL, "fg_sddmm: bad edge op %d", int(op));
     if (H < 1 || D < 1) return set_error(FG_ESHAPE, "fg_sddmm: H=%d D=%d must be >= 1", H, D);
     const int64_t F = int64_t(H) * D;
     if (F % 4 != 0) return set_error(FG_ESHAPE, "fg_sddmm: H*D must be a multiple of 4");
-    if (H > 1 && (D % 4 != 0 || ((D / 4) & (D / 4 - 1)) != 0))
+    if (op == FG_EDGE_U_DOT_V && H > 1 && (D % 4 != 0 || ((D / 4) & (D / 4 - 1)) != 0))
         return set_error(FG_ESHAPE, "fg_sddmm: with H > 1, D must be 4 * 2^k (got D=%d)", D);
     if (F > (int64_t(1) << 20)) return set_error(FG_ESHAPE, "fg_sddmm: H*D too large");
     if (g->nnz == 0) return FG_OK;
     if (!X || !Y || !out) return set_error(FG_EINVAL, "fg_sddmm: NULL tensor");
     if (!aligned16(X) || !aligned16(Y) || !aligned16(out))
         return set_error(FG_EINVAL, "fg_sddmm: X/Y/out must be 16-byte aligned");
+    if (op != FG_EDGE_U_DOT_V)
+        return fgk::launch_sddmm_binary(g, int(op), int(F), X, Y, out, reinterpret_cast<cudaStream_t>(stream));
     return fgk::launch_sddmm(g, H, D, X, Y, out, reinterpret_cast<cudaStream_t>(stream));
 }
 

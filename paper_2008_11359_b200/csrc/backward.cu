@@ -11,6 +11,8 @@
 //   spmm max   only the forward's winning edge of (v, j) gets dOut[v][j]:
 //              dX[u][j] = sum_{v: arg_u[v][j] == u} dOut[v][j] (* E[e][j/D])   -- masked gather over gT
 //              dE[e][h] = sum_{j in h: arg_u[v][j] == u} dOut[v][j] * X[u][j]  -- masked SDDMM over g
+//   spmm min   as max (arg_u names the minimising edge)
+//   spmm mean  as sum with dOut[v] replaced by dOut[v] / |N(v)|
 //   sddmm      dX = spmm_{u_mul_e}(gT, Y, dS),  dY = spmm_{u_mul_e}(g, X, dS)
 //   softmax    ds[e][h] = alpha[e][h] * (dalpha[e][h] - sum_row alpha * dalpha)
 // Every kernel is a pull over rows (no atomics): deterministic.
@@ -22,12 +24,15 @@
 namespace {
 constexpr int THREADS = 256;
 
-// dX[u][:] for max aggregation: one warp per row u of gT, lanes over float4 columns.
-template <bool UMULE>
-__global__ void __launch_bounds__(THREADS) max_backward_dx_kernel(
+// dX[u][:] for max/min (MEAN = false: masked by the forward's arg_u) and mean
+// (MEAN = true: every edge, dOut[v] scaled by 1/|N(v)|, rp = g's row_ptr).
+// One warp per row u of gT, lanes over float4 columns.
+template <bool UMULE, bool MEAN>
+__global__ void __launch_bounds__(THREADS) sel_backward_dx_kernel(
     const int32_t* __restrict__ rows, int64_t n_rows, const int64_t* __restrict__ rpT,
     const int32_t* __restrict__ ciT, const int32_t* __restrict__ eidT, const float4* __restrict__ dOut,
-    const int4* __restrict__ arg_u, const float* __restrict__ E, int H, int D, int F4, float4* __restrict__ dX) {
+    const int4* __restrict__ arg_u, const int64_t* __restrict__ rp, const float* __restrict__ E, int H, int D, int F4,
+    float4* __restrict__ dX) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t(blockIdx.x) * THREADS + threadIdx.x) >> 5;
     if (r >= n_rows) return;
@@ -39,9 +44,16 @@ __global__ void __launch_bounds__(THREADS) max_backward_dx_kernel(
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int64_t p = s; p < e; ++p) {
             const int64_t v = __ldg(ciT + p);
-            const int4 a = __ldg(arg_u + v * F4 + c);
-            if (a.x != u && a.y != u && a.z != u && a.w != u) continue;
-            const float4 g = __ldg(dOut + v * F4 + c);
+            int4 a = make_int4(int(u), int(u), int(u), int(u));
+            if (!MEAN) {
+                a = __ldg(arg_u + v * F4 + c);
+                if (a.x != u && a.y != u && a.z != u && a.w != u) continue;
+            }
+            float4 g = __ldg(dOut + v * F4 + c);
+            if (MEAN) {
+                const float dg = float(__ldg(rp + v + 1) - __ldg(rp + v));
+                g = make_float4(g.x / dg, g.y / dg, g.z / dg, g.w / dg);
+            }
             float w0 = 1.f, w1 = 1.f, w2 = 1.f, w3 = 1.f;
             if (UMULE) {
                 const int64_t ed = eidT ? int64_t(__ldg(eidT + p)) : p;
@@ -59,8 +71,9 @@ __global__ void __launch_bounds__(THREADS) max_backward_dx_kernel(
     }
 }
 
-// dE[e][h] for u_mul_e max: one thread per (edge, head) of g.
-__global__ void __launch_bounds__(THREADS) max_backward_de_kernel(
+// dE[e][h] for u_mul_e max/min (masked) or mean (scaled): one thread per (edge, head) of g.
+template <bool MEAN>
+__global__ void __launch_bounds__(THREADS) sel_backward_de_kernel(
     int64_t n_dst, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const int32_t* __restrict__ eid,
     const float* __restrict__ X, const float* __restrict__ dOut, const int32_t* __restrict__ arg_u, int H, int D,
     int64_t nnz, float* __restrict__ dE) {
@@ -79,7 +92,12 @@ __global__ void __launch_bounds__(THREADS) max_backward_de_kernel(
     float acc = 0.f;
     for (int d = 0; d < D; ++d) {
         const int64_t j = int64_t(h) * D + d;
-        if (__ldg(arg_u + v * F + j) == u) acc = fmaf(__ldg(dOut + v * F + j), __ldg(X + u * F + j), acc);
+        if (MEAN) {
+            const float dg = float(__ldg(rp + v + 1) - __ldg(rp + v));
+            acc = fmaf(__ldg(dOut + v * F + j) / dg, __ldg(X + u * F + j), acc);
+        } else if (__ldg(arg_u + v * F + j) == u) {
+            acc = fmaf(__ldg(dOut + v * F + j), __ldg(X + u * F + j), acc);
+        }
     }
     dE[(eid ? int64_t(__ldg(eid + p)) : p) * H + h] = acc;
 }
@@ -191,13 +209,16 @@ extern "C" fg_status fg_spmm_backward(const fg_graph* g, const fg_graph* gT, fg_
     if (!g) return set_error(FG_EINVAL, "fg_spmm_backward: NULL graph");
     if (msg != FG_MSG_COPY_U && msg != FG_MSG_U_MUL_E)
         return set_error(FG_EUNSUPPORTED, "fg_spmm_backward: only copy_u / u_mul_e (SPEC non-goal: mlp through W)");
-    if (red != FG_REDUCE_SUM && red != FG_REDUCE_MAX) return set_error(FG_EINVAL, "fg_spmm_backward: bad reduce op");
+    if (red != FG_REDUCE_SUM && red != FG_REDUCE_MAX && red != FG_REDUCE_MIN && red != FG_REDUCE_MEAN)
+        return set_error(FG_EINVAL, "fg_spmm_backward: bad reduce op");
     if (H < 1 || D < 1 || (int64_t(H) * D) % 4) return set_error(FG_ESHAPE, "fg_spmm_backward: H*D must be a multiple of 4");
     if (!dOut) return set_error(FG_EINVAL, "fg_spmm_backward: dOut is NULL");
     if (dX && !is_transpose_of(g, gT)) return set_error(FG_EINVAL, "fg_spmm_backward: dX needs gT = fg_graph_transpose(g)");
     if (msg == FG_MSG_U_MUL_E && !E) return set_error(FG_EINVAL, "fg_spmm_backward: u_mul_e needs E");
     if (dE && (msg != FG_MSG_U_MUL_E || !X)) return set_error(FG_EINVAL, "fg_spmm_backward: dE needs u_mul_e and X");
-    if (red == FG_REDUCE_MAX && !arg_u) return set_error(FG_EINVAL, "fg_spmm_backward: max needs the forward's arg_u");
+    const bool mean = red == FG_REDUCE_MEAN;
+    if ((red == FG_REDUCE_MAX || red == FG_REDUCE_MIN) && !arg_u)
+        return set_error(FG_EINVAL, "fg_spmm_backward: max/min need the forward's arg_u");
     if (!aligned16(dOut) || !aligned16(dX) || !aligned16(X) || !aligned16(arg_u))
         return set_error(FG_EINVAL, "fg_spmm_backward: tensors must be 16-byte aligned");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -213,22 +234,21 @@ extern "C" fg_status fg_spmm_backward(const fg_graph* g, const fg_graph* gT, fg_
     }
     if (dX && gT->n_dst > 0) {
         const int64_t blocks = (gT->n_dst * 32 + THREADS - 1) / THREADS;
-        if (msg == FG_MSG_U_MUL_E)
-            max_backward_dx_kernel<true><<<unsigned(blocks), THREADS, 0, st>>>(
-                gT->rows_by_deg, gT->n_dst, gT->row_ptr, gT->col_idx, gT->eid, reinterpret_cast<const float4*>(dOut),
-                reinterpret_cast<const int4*>(arg_u), E, H, D, F4, reinterpret_cast<float4*>(dX));
-        else
-            max_backward_dx_kernel<false><<<unsigned(blocks), THREADS, 0, st>>>(
-                gT->rows_by_deg, gT->n_dst, gT->row_ptr, gT->col_idx, gT->eid, reinterpret_cast<const float4*>(dOut),
-                reinterpret_cast<const int4*>(arg_u), E, H, D, F4, reinterpret_cast<float4*>(dX));
-        fg_status s = fgk::check_launch("max_backward_dx_kernel");
+        auto kern = msg == FG_MSG_U_MUL_E ? (mean ? sel_backward_dx_kernel<true, true> : sel_backward_dx_kernel<true, false>)
+                                          : (mean ? sel_backward_dx_kernel<false, true> : sel_backward_dx_kernel<false, false>);
+        kern<<<unsigned(blocks), THREADS, 0, st>>>(gT->rows_by_deg, gT->n_dst, gT->row_ptr, gT->col_idx, gT->eid,
+                                                   reinterpret_cast<const float4*>(dOut),
+                                                   reinterpret_cast<const int4*>(arg_u), g->row_ptr, E, H, D, F4,
+                                                   reinterpret_cast<float4*>(dX));
+        fg_status s = fgk::check_launch("sel_backward_dx_kernel");
         if (s != FG_OK) return s;
     }
     if (dE && g->nnz > 0) {
         const int64_t blocks = (g->nnz * H + THREADS - 1) / THREADS;
-        max_backward_de_kernel<<<unsigned(blocks), THREADS, 0, st>>>(g->n_dst, g->row_ptr, g->col_idx, g->eid, X, dOut,
-                                                                    arg_u, H, D, g->nnz, dE);
-        return fgk::check_launch("max_backward_de_kernel");
+        auto kern = mean ? sel_backward_de_kernel<true> : sel_backward_de_kernel<false>;
+        kern<<<unsigned(blocks), THREADS, 0, st>>>(g->n_dst, g->row_ptr, g->col_idx, g->eid, X, dOut, arg_u, H, D,
+                                                   g->nnz, dE);
+        return fgk::check_launch("sel_backward_de_kernel");
     }
     return FG_OK;
 }
@@ -237,7 +257,7 @@ extern "C" fg_status fg_sddmm_backward(const fg_graph* g, const fg_graph* gT, fg
                                        const float* X, const float* Y, const float* dS, float* dX, float* dY,
                                        fg_stream stream) {
     if (!g) return set_error(FG_EINVAL, "fg_sddmm_backward: NULL graph");
-    if (op != FG_EDGE_U_DOT_V) return set_error(FG_EINVAL, "fg_sddmm_backward: bad edge op");
+    if (op != FG_EDGE_U_DOT_V) return set_error(FG_EUNSUPPORTED, "fg_sddmm_backward: only u_dot_v");
     if (!dS) return set_error(FG_EINVAL, "fg_sddmm_backward: dS is NULL");
     if (dX && (!Y || !is_transpose_of(g, gT)))
         return set_error(FG_EINVAL, "fg_sddmm_backward: dX needs Y and gT = fg_graph_transpose(g)");

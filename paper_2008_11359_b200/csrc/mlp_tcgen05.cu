@@ -15,8 +15,8 @@
 //
 // The paper's V100 schedule bound d2 to blocks and tree-reduced d1 over threads
 // (listing fig:schedule-mlp-conv-gpu).  Here, per CTA (persistent,
-// 2 per SM, each owning a contiguous range of destination rows and therefore a
-// contiguous range of CSR edges):
+// 4 per SM -- four independent pipelines hide the MMA/commit latency -- each
+// owning a contiguous range of destination rows and therefore of CSR edges):
 //   * producer warps gather x_u for NT = 128 edges (L2-resident: n x d1 x 4 B),
 //     split each fp32 into tf32 hi + lo and store the B operand (K-major,
 //     no-swizzle canonical layout) into a 4-stage shared-memory ring;
@@ -35,16 +35,17 @@
 
 namespace {
 
-constexpr int NT = 128;                   // edges per tile (MMA N)
+constexpr int NT = 64;                    // edges per tile (MMA N)
 constexpr int NBUF = 2;                   // TMEM accumulator buffers (double buffer)
+constexpr int CTAS_PER_SM = 4;            // 4 independent pipelines per SM hide the MMA/commit latency
 constexpr int MT = 128;                   // features per CTA (MMA M)
 constexpr int STAGES = 4;
 constexpr int ISTAGES = 4;                // index ring (producer -> epilogue)
 constexpr int NEPI = 4;                   // epilogue warps 0..3 (TMEM lane quarters)
 constexpr int MMA_WARP = 4;
-constexpr int NPROD = 2;                  // producer warps 5..6
+constexpr int NPROD = 1;                  // producer warp 5
 constexpr int THREADS = (NEPI + 1 + NPROD) * 32;
-constexpr int TMEM_COLS = NBUF * NT;      // 256: two CTAs per SM share the 512 columns
+constexpr int TMEM_COLS = NBUF * NT;      // 128: four CTAs per SM share the 512 columns
 constexpr int TILE_BYTES = 8 * 4 * 128;   // one K-step operand tile: 128 rows x 8 tf32 = 4 KB
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -166,13 +167,15 @@ struct Args {
     int d_in, d2;
     const float* Xhi;     // [n_src][KS*8] tf32 hi part of X (workspace)
     const float* Xlo;     // [n_src][KS*8] tf32 lo part
-    int dbg;              // FG_MLP_DBG (pipeline experiments): 1 = skip epilogue math, 2 = skip gathers
+    int dbg;              // FG_MLP_DBG bits (pipeline experiments): 1 skip epilogue math, 2 skip gathers,
+                          // 4 skip MMAs, 8 skip TMEM loads (results are then wrong; timing only)
 };
 
 template <int KS>
 struct Smem {
     float a_hi[KS][MT * 8];
     float a_lo[KS][MT * 8];
+    float wcol[KS * 8][MT];                // W[k][feature] in fp32 for the per-row q = x_v W (epilogue)
     float b_hi[STAGES][KS][NT * 8];
     float b_lo[STAGES][KS][NT * 8];
     int32_t su[ISTAGES][NT];               // source id / edge id of each tile column,
@@ -192,7 +195,7 @@ struct Epi {
     int bu, be;       // winning edge: source id / edge id (from the smem-staged tile indices)
     int fu, fe;       // first edge of the row (the winner when every message is +0)
     bool fresh;       // no edge of the row seen yet
-    float w[KS * 8];
+    const float* wc;  // this thread's W column in shared memory (stride MT)
     float nx[KS * 8]; // prefetched x_{r+1}
     int i;            // global feature index
     bool active;      // i < d2
@@ -213,7 +216,7 @@ struct Epi {
         fresh = true;
         float a = 0.f;
 #pragma unroll
-        for (int k = 0; k < KS * 8; ++k) a = fmaf(nx[k], w[k], a);
+        for (int k = 0; k < KS * 8; ++k) a = fmaf(nx[k], wc[k * MT], a);
         q = a;
         prefetch(r + 1);
     }
@@ -302,7 +305,7 @@ struct Epi {
 };
 
 template <int KS, bool MAX>
-__global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_constant__ Args A) {
+__global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const __grid_constant__ Args A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem<KS>& S = *reinterpret_cast<Smem<KS>*>(smem_raw);
     const int tid = threadIdx.x;
@@ -325,6 +328,7 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
         const int ks = idx / (MT * 8), rem = idx % (MT * 8), r = rem / 8, k = rem % 8;
         const int kk = ks * 8 + k, col = mbase + r;
         const float w = (kk < A.d_in && col < A.d2) ? A.W[int64_t(kk) * A.d2 + col] : 0.f;
+        S.wcol[kk][r] = w;
         const float hi = tf32_rna(w);
         const float lo = tf32_rna(w - hi);
         *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(S.a_hi[ks]) + tile_off(r, k)) = hi;
@@ -354,24 +358,25 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
         constexpr int EPT = NT / (NPROD * 32);
         const int pt = tid - (MMA_WARP + 1) * 32;          // 0 .. NPROD*32-1
         const int rowf = KS * 8;                            // floats per pre-split row
-        int u_nx[EPT], e_nx[EPT];
-        auto load_idx = [&](int t) {
+        // indices are prefetched PF tiles ahead (a register ring, static slots via
+        // the unrolled-by-PF loop): the col_idx round trip (~1 us) would otherwise
+        // bound the pipeline at one tile per load latency
+        constexpr int PF = 4;
+        int u_pf[PF][EPT], e_pf[PF][EPT];
+        auto load_idx = [&](int t, int (&u)[EPT], int (&ed)[EPT]) {
             const int64_t tb = E0 + int64_t(t) * NT;
 #pragma unroll
             for (int i = 0; i < EPT; ++i) {
                 const int64_t p = tb + pt + i * NPROD * 32;
-                const bool ok = p < E1;
-                u_nx[i] = ok ? __ldg(A.col_idx + p) : -1;
-                e_nx[i] = ok ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
+                const bool ok = t < ntiles && p < E1;
+                u[i] = ok ? __ldg(A.col_idx + p) : -1;
+                ed[i] = ok ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
             }
         };
-        if (ntiles > 0) load_idx(0);
-        for (int t = 0; t < ntiles; ++t) {
-            const int s = t % STAGES, is = t % ISTAGES;
-            int u_cur[EPT], e_cur[EPT];
 #pragma unroll
-            for (int i = 0; i < EPT; ++i) { u_cur[i] = u_nx[i]; e_cur[i] = e_nx[i]; }
-            if (t + 1 < ntiles) load_idx(t + 1);
+        for (int k = 0; k < PF; ++k) load_idx(k, u_pf[k], e_pf[k]);
+        auto tile = [&](int t, int (&u_cur)[EPT], int (&e_cur)[EPT]) {
+            const int s = t % STAGES, is = t % ISTAGES;
             mbar_wait(&S.empty[s], ((t / STAGES) & 1) ^ 1);
             mbar_wait(&S.iempty[is], ((t / ISTAGES) & 1) ^ 1);
 #pragma unroll
@@ -396,6 +401,12 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
             }
             cp_async_arrive(&S.full[s]);
             mbar_arrive(&S.ifull[is]);
+            load_idx(t + PF, u_cur, e_cur);   // refill this slot PF tiles ahead
+        };
+        for (int t0 = 0; t0 < ntiles; t0 += PF) {
+#pragma unroll
+            for (int k = 0; k < PF; ++k)
+                if (t0 + k < ntiles) tile(t0 + k, u_pf[k], e_pf[k]);
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp == MMA_WARP) {
@@ -412,9 +423,11 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
                 for (int ks = 0; ks < KS; ++ks) {
                     const uint64_t ah = smem_desc(smem_u32(S.a_hi[ks])), al = smem_desc(smem_u32(S.a_lo[ks]));
                     const uint64_t bh = smem_desc(smem_u32(S.b_hi[s][ks])), bl = smem_desc(smem_u32(S.b_lo[s][ks]));
-                    mma_tf32(d, ah, bh, ks > 0 ? 1u : 0u);
-                    mma_tf32(d, ah, bl, 1u);
-                    mma_tf32(d, al, bh, 1u);
+                    if (!(A.dbg & 4)) {
+                        mma_tf32(d, ah, bh, ks > 0 ? 1u : 0u);
+                        mma_tf32(d, ah, bl, 1u);
+                        mma_tf32(d, al, bh, 1u);
+                    }
                 }
                 mma_commit(&S.empty[s]);
                 mma_commit(&S.tfull[b]);
@@ -427,9 +440,7 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
         ep.A = &A;
         ep.i = mbase + tid;
         ep.active = ep.i < A.d2;
-#pragma unroll
-        for (int k = 0; k < KS * 8; ++k)
-            ep.w[k] = (k < A.d_in && ep.active) ? __ldg(A.W + int64_t(k) * A.d2 + ep.i) : 0.f;
+        ep.wc = &S.wcol[0][tid];
         ep.r = r_lo;
         ep.r_hi = r_hi;
         if (r_lo < r_hi) {
@@ -448,18 +459,17 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
             const int* se = S.se[is];
             const int64_t tb = E0 + int64_t(t) * NT;
             const int nv_tile = int(min(int64_t(NT), E1 - tb));
-            uint32_t v0[32], v1[32];
-            tmem_ld32(lane_base + uint32_t(b * NT), v0);
-            tmem_wait_ld(v0);
+#pragma unroll 1
+            for (int ch = 0; ch < NT / 32; ++ch) {   // single-buffered: 4 CTAs per SM supply the overlap
+                uint32_t v0[32];
+                if (!(A.dbg & 8)) {
+                    tmem_ld32(lane_base + uint32_t(b * NT + ch * 32), v0);
+                    tmem_wait_ld(v0);
+                } else {
 #pragma unroll
-            for (int ch = 0; ch < NT / 32; ch += 2) {   // chunk ch+1 loads while chunk ch is consumed
-                tmem_ld32(lane_base + uint32_t(b * NT + (ch + 1) * 32), v1);
+                    for (int q = 0; q < 32; ++q) v0[q] = 0u;
+                }
                 if (!(A.dbg & 1)) ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)), su + ch * 32, se + ch * 32);
-                tmem_wait_ld(v1);
-                if (ch + 2 < NT / 32) tmem_ld32(lane_base + uint32_t(b * NT + (ch + 2) * 32), v0);
-                if (!(A.dbg & 1)) ep.consume(v1, tb + (ch + 1) * 32, max(0, min(32, nv_tile - (ch + 1) * 32)), su + (ch + 1) * 32,
-                           se + (ch + 1) * 32);
-                if (ch + 2 < NT / 32) tmem_wait_ld(v0);
             }
             tc_fence_before();
             mbar_arrive(&S.tempty[b]);
@@ -478,8 +488,7 @@ __global__ void __launch_bounds__(THREADS, 2) mlp_tcgen05_kernel(const __grid_co
 template <int KS, bool MAX>
 fg_status launch_ks(const Args& A, cudaStream_t st) {
     const int smem = int(sizeof(Smem<KS>)) + 1024;
-    // >= 100 KB per CTA keeps residency at <= 2 CTAs / SM (TMEM: 2 x 256 columns)
-    const int smem_req = smem < 100 * 1024 ? 100 * 1024 : smem;
+    const int smem_req = smem < 56 * 1024 ? 56 * 1024 : smem;   // bounds residency at CTAS_PER_SM (TMEM)
     {   // pre-split X into tf32 hi / lo rows (the producers' cp.async source)
         const int64_t tot = A.n_src * KS * 8;
         if (tot > 0)
@@ -494,7 +503,7 @@ fg_status launch_ks(const Args& A, cudaStream_t st) {
     // carveout that fits ONE 100 KB CTA per SM and the persistent grid runs as two waves
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return fgk::set_error(FG_ECUDA, "mlp_tcgen05: smem attribute: %s", cudaGetErrorString(e));
-    int nb = 2 * fgk::num_sms();
+    int nb = CTAS_PER_SM * fgk::num_sms();
     const int64_t want = (A.nnz + 4 * NT - 1) / (4 * NT);   // >= 4 tiles per CTA
     if (want < nb) nb = int(want < 1 ? 1 : want);
     const dim3 grid{unsigned(nb), unsigned((A.d2 + MT - 1) / MT), 1u};

@@ -1,0 +1,307 @@
+// spmm_impl.cuh -- the gathered-message gSpMM kernel template shared by
+// spmm.cu (copy_u, u_mul_e) and spmm_ext.cu (u_add_e, copy_e); see spmm.cu
+// for the design notes.  Each translation unit instantiates its own ops, so
+// the two compile in parallel.
+#pragma once
+#include "fg_internal.h"
+
+namespace fgspmm {
+
+
+// OP_UMULE_GEN: u_mul_e with D % 4 != 0 (the head varies inside a float4);
+// OP_UADDE: u_add_e (per-component head lookup, any D); OP_COPYE: copy_e (the
+// message row is E[eid] itself, E is [nnz][F]).
+enum { OP_COPY = 0, OP_UMULE = 1, OP_UMULE_GEN = 2, OP_UADDE = 3, OP_COPYE = 4 };
+enum { R_SUM = 0, R_MAX = 1, R_MIN = 2, R_MEAN = 3 };
+constexpr int THREADS = 256;
+
+template <int G>
+__device__ __forceinline__ unsigned group_mask(int lane) {
+    if constexpr (G == 32) return 0xffffffffu;
+    else return ((1u << G) - 1u) << (lane & ~(G - 1));
+}
+
+struct Args {
+    const int32_t* rows;        // rows_by_deg
+    int64_t n_heavy;            // rows[0, n_heavy) -> CTA-per-row mode
+    int64_t n_rows;             // n_dst
+    const int64_t* row_ptr;
+    const int32_t* col_idx;
+    const int32_t* eid;
+    const float4* X;
+    const float* E;
+    int H, D, F4;
+    float4* out;
+    int4* arg_u;
+    int4* arg_e;
+};
+
+__device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); }
+__device__ __forceinline__ float comp(const float4& v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
+__device__ __forceinline__ void set_comp(float4& v, int k, float a) {
+    if (k == 0) v.x = a; else if (k == 1) v.y = a; else if (k == 2) v.z = a; else v.w = a;
+}
+
+// Accumulate edges [s, e) of one row into (acc, pos) for this lane's NV chunks.
+template <int G, int NV, int OP, int RED>
+__device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e, int gl, unsigned mask,
+                                             int c4base, float4 (&acc)[NV], int (&pos)[NV][4],
+                                             float* __restrict__ etile) {
+    constexpr int B = 32;                                   // edges per index batch
+    constexpr int R = B / G;                                // indices per lane per batch
+    constexpr int U = NV >= 4 ? 2 : (NV >= 2 ? 4 : 8);      // edges in flight per lane
+    constexpr bool MAX = (RED == R_MAX || RED == R_MIN);     // select-type reducers
+    const int F4 = A.F4;
+    for (int64_t p0 = s; p0 < e; p0 += B) {
+        const int cnt = int(min((int64_t)B, e - p0));
+        int uix[R];
+        int eix[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t p = p0 + gl + r * G;
+            uix[r] = (OP != OP_COPYE && p < e) ? __ldg(A.col_idx + p) : 0;   // copy_e reads no source row
+            if constexpr (OP != OP_COPY) eix[r] = (p < e) ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
+        }
+        // u_mul_e with identity edge ids: the batch's E rows are one contiguous span;
+        // stage it in shared memory with coalesced loads instead of one dependent
+        // scalar load per edge and chunk
+        bool staged = false;
+        if constexpr (OP == OP_UMULE && G == 32) {
+            if (A.eid == nullptr && A.H <= 16) {
+                staged = true;
+                __syncwarp(mask);
+                const float* Eb = A.E + p0 * A.H;
+                for (int q = gl; q < cnt * A.H; q += G) etile[q] = __ldg(Eb + q);
+                __syncwarp(mask);
+            }
+        }
+#pragma unroll
+        for (int t0 = 0; t0 < B; t0 += U) {
+            if (t0 >= cnt) break;                           // uniform within the group
+            float4 x[U][NV];
+            constexpr bool PERK = (OP == OP_UMULE_GEN || OP == OP_UADDE);   // head per component
+            float ev[U][NV][PERK ? 4 : 1];
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+                const int t = t0 + uu;
+                const int u = __shfl_sync(mask, uix[t / G], t % G, G);
+                int ed = 0;
+                if constexpr (OP != OP_COPY) ed = __shfl_sync(mask, eix[t / G], t % G, G);
+                const float4* xr = (OP == OP_COPYE) ? reinterpret_cast<const float4*>(A.E) + int64_t(ed) * F4
+                                                    : A.X + int64_t(u) * F4;
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                    const int c = c4base + gl + G * j;
+                    const bool ok = (t < cnt) && (c < F4);
+                    x[uu][j] = ok ? __ldg(xr + c) : f4(0.f);
+                    if constexpr (OP == OP_UMULE) {
+                        const int h = (4 * c) / A.D;
+                        ev[uu][j][0] = !ok ? 0.f : (staged ? etile[t * A.H + h] : __ldg(A.E + int64_t(ed) * A.H + h));
+                    } else if constexpr (PERK) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int h = (4 * c + k) / A.D;
+                            ev[uu][j][k] = ok ? __ldg(A.E + int64_t(ed) * A.H + h) : 0.f;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+                const int t = t0 + uu;
+                if (t >= cnt) break;
+                const int p = int(p0) + t;
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                    if constexpr (!MAX) {
+                        if constexpr (OP == OP_COPY) {
+                            acc[j].x += x[uu][j].x; acc[j].y += x[uu][j].y;
+                            acc[j].z += x[uu][j].z; acc[j].w += x[uu][j].w;
+                        } else if constexpr (OP == OP_UMULE) {
+                            const float w = ev[uu][j][0];
+                            acc[j].x = fmaf(x[uu][j].x, w, acc[j].x); acc[j].y = fmaf(x[uu][j].y, w, acc[j].y);
+                            acc[j].z = fmaf(x[uu][j].z, w, acc[j].z); acc[j].w = fmaf(x[uu][j].w, w, acc[j].w);
+                        } else if constexpr (OP == OP_UADDE) {
+                            acc[j].x += __fadd_rn(x[uu][j].x, ev[uu][j][0]);
+                            acc[j].y += __fadd_rn(x[uu][j].y, ev[uu][j][1]);
+                            acc[j].z += __fadd_rn(x[uu][j].z, ev[uu][j][2]);
+                            acc[j].w += __fadd_rn(x[uu][j].w, ev[uu][j][3]);
+                        } else if constexpr (OP == OP_COPYE) {
+                            acc[j].x += x[uu][j].x; acc[j].y += x[uu][j].y;
+                            acc[j].z += x[uu][j].z; acc[j].w += x[uu][j].w;
+                        } else {
+                            acc[j].x = fmaf(x[uu][j].x, ev[uu][j][0], acc[j].x);
+                            acc[j].y = fmaf(x[uu][j].y, ev[uu][j][1], acc[j].y);
+                            acc[j].z = fmaf(x[uu][j].z, ev[uu][j][2], acc[j].z);
+                            acc[j].w = fmaf(x[uu][j].w, ev[uu][j][3], acc[j].w);
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            float m = comp(x[uu][j], k);
+                            if constexpr (OP == OP_UMULE) m = __fmul_rn(m, ev[uu][j][0]);
+                            else if constexpr (OP == OP_UMULE_GEN) m = __fmul_rn(m, ev[uu][j][k]);
+                            else if constexpr (OP == OP_UADDE) m = __fadd_rn(m, ev[uu][j][k]);
+                            const bool better = (RED == R_MIN) ? (m < comp(acc[j], k)) : (m > comp(acc[j], k));
+                            if (better) { set_comp(acc[j], k, m); pos[j][k] = p; }   // strict: first wins
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int NV, int RED>
+__device__ __forceinline__ void init_acc(float4 (&acc)[NV], int (&pos)[NV][4]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        acc[j] = f4(RED == R_MAX ? -INFINITY : (RED == R_MIN ? INFINITY : 0.f));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pos[j][k] = -1;
+    }
+}
+
+template <int RED>
+__device__ __forceinline__ void store_elem(const Args& A, int64_t v, int c, float4 a, const int (&ps)[4], int64_t deg) {
+    const int64_t o = v * A.F4 + c;
+    const bool empty = deg == 0;
+    if (RED == R_SUM) {
+        A.out[o] = a;
+        return;
+    }
+    if (RED == R_MEAN) {   // sum / in-degree (IEEE division); empty rows -> 0
+        const float d = float(deg);
+        A.out[o] = empty ? f4(0.f) : make_float4(a.x / d, a.y / d, a.z / d, a.w / d);
+        return;
+    }
+    if (empty) {
+        A.out[o] = f4(0.f);
+        if (A.arg_u) A.arg_u[o] = make_int4(-1, -1, -1, -1);
+        if (A.arg_e) A.arg_e[o] = make_int4(-1, -1, -1, -1);
+        return;
+    }
+    A.out[o] = a;
+    if (A.arg_u) {
+        int4 r;
+        r.x = ps[0] < 0 ? -1 : __ldg(A.col_idx + ps[0]);
+        r.y = ps[1] < 0 ? -1 : __ldg(A.col_idx + ps[1]);
+        r.z = ps[2] < 0 ? -1 : __ldg(A.col_idx + ps[2]);
+        r.w = ps[3] < 0 ? -1 : __ldg(A.col_idx + ps[3]);
+        A.arg_u[o] = r;
+    }
+    if (A.arg_e) {
+        int4 r;
+        r.x = ps[0] < 0 ? -1 : (A.eid ? __ldg(A.eid + ps[0]) : ps[0]);
+        r.y = ps[1] < 0 ? -1 : (A.eid ? __ldg(A.eid + ps[1]) : ps[1]);
+        r.z = ps[2] < 0 ? -1 : (A.eid ? __ldg(A.eid + ps[2]) : ps[2]);
+        r.w = ps[3] < 0 ? -1 : (A.eid ? __ldg(A.eid + ps[3]) : ps[3]);
+        A.arg_e[o] = r;
+    }
+}
+
+template <int G, int NV, int OP, int RED>
+__global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
+    constexpr bool MAX = (RED == R_MAX || RED == R_MIN);
+    constexpr int NG = THREADS / G;                 // groups per CTA
+    constexpr int TW = G * NV;                      // float4 columns per tile
+    __shared__ float4 s_acc[MAX ? 1 : NG][MAX ? 1 : TW];
+    __shared__ float s_etile[(OP == OP_UMULE && G == 32) ? NG : 1][(OP == OP_UMULE && G == 32) ? 32 * 16 : 1];
+    __shared__ float s_val[MAX ? NG : 1][MAX ? TW * 4 : 1];
+    __shared__ int s_pos[MAX ? NG : 1][MAX ? TW * 4 : 1];
+
+    const int lane = threadIdx.x & 31;
+    const int gl = threadIdx.x & (G - 1);
+    const int gi = threadIdx.x / G;
+    const unsigned mask = group_mask<G>(lane);
+    const int c4base = blockIdx.y * TW;
+
+    float4 acc[NV];
+    int pos[NV][4];
+    init_acc<NV, RED>(acc, pos);
+
+    if (int64_t(blockIdx.x) < A.n_heavy) {
+        // ---- CTA-per-row: contiguous edge ranges per group, fixed-order combine
+        const int64_t v = A.rows[blockIdx.x];
+        const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
+        const int64_t len = (e - s + NG - 1) / NG;
+        const int64_t gs = min(e, s + gi * len), ge = min(e, gs + len);
+        gather_range<G, NV, OP, RED>(A, gs, ge, gl, mask, c4base, acc, pos, s_etile[gi]);
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const int c = gl + G * j;
+            if constexpr (!MAX) {
+                s_acc[gi][c] = acc[j];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) { s_val[gi][4 * c + k] = comp(acc[j], k); s_pos[gi][4 * c + k] = pos[j][k]; }
+            }
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < TW; c += THREADS) {
+            if (c4base + c >= A.F4) continue;
+            float4 a;
+            int ps[4] = {-1, -1, -1, -1};
+            if constexpr (!MAX) {
+                a = s_acc[0][c];
+                for (int g2 = 1; g2 < NG; ++g2) {
+                    const float4 b = s_acc[g2][c];
+                    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+                }
+            } else {
+                a = f4(RED == R_MIN ? INFINITY : -INFINITY);
+                for (int g2 = 0; g2 < NG; ++g2) {   // ascending ranges: strict compare keeps the lowest position
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float b = s_val[g2][4 * c + k];
+                        const bool better = (RED == R_MIN) ? (b < comp(a, k)) : (b > comp(a, k));
+                        if (better) { set_comp(a, k, b); ps[k] = s_pos[g2][4 * c + k]; }
+                    }
+                }
+            }
+            store_elem<RED>(A, v, c4base + c, a, ps, e - s);
+        }
+        return;
+    }
+
+    // ---- group-per-row
+    const int64_t r = A.n_heavy + (int64_t(blockIdx.x) - A.n_heavy) * NG + gi;
+    if (r >= A.n_rows) return;
+    const int64_t v = A.rows[r];
+    const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
+    gather_range<G, NV, OP, RED>(A, s, e, gl, mask, c4base, acc, pos, s_etile[gi]);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const int c = c4base + gl + G * j;
+        if (c < A.F4) store_elem<RED>(A, v, c, acc[j], pos[j], e - s);
+    }
+}
+
+template <int G, int NV, int OP, int RED>
+fg_status launch_t(const Args& A0, cudaStream_t st) {
+    Args A = A0;
+    constexpr int NG = THREADS / G;
+    constexpr int TW = G * NV;
+    const int64_t light = A.n_rows - A.n_heavy;
+    const int64_t blocks = A.n_heavy + (light + NG - 1) / NG;
+    const int tiles = (A.F4 + TW - 1) / TW;
+    if (blocks == 0) return FG_OK;
+    const dim3 grid{unsigned(blocks), unsigned(tiles), 1u};
+    spmm_gather_kernel<G, NV, OP, RED><<<grid, THREADS, 0, st>>>(A);
+    return fgk::check_launch("spmm_gather_kernel");
+}
+
+template <int G, int NV, int OP>
+fg_status dispatch_red(const Args& A, int red, cudaStream_t st) {
+    switch (red) {
+        case R_MAX: return launch_t<G, NV, OP, R_MAX>(A, st);
+        case R_MIN: return launch_t<G, NV, OP, R_MIN>(A, st);
+        case R_MEAN: return launch_t<G, NV, OP, R_MEAN>(A, st);
+        default: return launch_t<G, NV, OP, R_SUM>(A, st);
+    }
+}
+
+template <int G, int NV>
+fg_status dispatch_ext(const Args& A, int op, int red, cudaStream_t st);   // spmm_ext.cu
+
+}  // namespace fgspmm

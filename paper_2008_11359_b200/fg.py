@@ -20,9 +20,9 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libfg.so")
 
 FG_OK, FG_EINVAL, FG_ESHAPE, FG_EUNSUPPORTED, FG_EGRAPH, FG_ECUDA, FG_ENOMEM, FG_ENCCL = range(8)
-MSG = {"copy_u": 0, "u_mul_e": 1, "mlp": 2}
-REDUCE = {"sum": 0, "max": 1}
-EDGE = {"u_dot_v": 0}
+MSG = {"copy_u": 0, "u_mul_e": 1, "mlp": 2, "u_add_e": 3, "copy_e": 4}
+REDUCE = {"sum": 0, "max": 1, "min": 2, "mean": 3}
+EDGE = {"u_dot_v": 0, "u_add_v": 1, "u_sub_v": 2, "u_mul_v": 3}
 
 # exported symbols declared in include/fg.h (checked by tests/test_abi.py)
 SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
@@ -179,26 +179,32 @@ def _workspace(g: Graph, msg: int, red: int, H: int, D: int, d_in: int, device):
 def spmm(g: Graph, msg: str, reduce: str, X: torch.Tensor, *, H: int = 1, E: torch.Tensor | None = None,
          W: torch.Tensor | None = None, X_dst: torch.Tensor | None = None, out: torch.Tensor | None = None,
          arg_u: torch.Tensor | bool | None = None, arg_e: torch.Tensor | bool | None = None, stream=None):
-    """featgraph.spmm (Eq. (1)).  Returns out, or (out, arg_u, arg_e) when args requested."""
+    """featgraph.spmm (Eq. (1)).  Returns out, or (out, arg_u, arg_e) when args requested.
+    copy_e takes X=None and E [nnz][F]."""
     X = _dev(X, torch.float32, "X")
     E, W, X_dst = _dev(E, torch.float32, "E"), _dev(W, torch.float32, "W"), _dev(X_dst, torch.float32, "X_dst")
-    if msg == "mlp":
+    if msg == "copy_e":
+        d_in = 0
+        F = E.numel() // max(E.shape[0], 1) if E.dim() > 1 else 1
+        H_, D = H, F // H
+    elif msg == "mlp":
         d_in, F = W.shape
         H_, D = 1, F
     else:
         d_in = 0
         F = X.numel() // max(X.shape[0], 1) if X.dim() > 1 else 1
         H_, D = H, F // H
+    device = (X if X is not None else E).device
     if out is None:
-        out = torch.empty((g.n_dst, F), dtype=torch.float32, device=X.device)
-    want = reduce == "max" and (arg_u is not None or arg_e is not None)
+        out = torch.empty((g.n_dst, F), dtype=torch.float32, device=device)
+    want = reduce in ("max", "min") and (arg_u is not None or arg_e is not None)
     if arg_u is True:
-        arg_u = torch.empty((g.n_dst, F), dtype=torch.int32, device=X.device)
+        arg_u = torch.empty((g.n_dst, F), dtype=torch.int32, device=device)
     if arg_e is True:
-        arg_e = torch.empty((g.n_dst, F), dtype=torch.int32, device=X.device)
+        arg_e = torch.empty((g.n_dst, F), dtype=torch.int32, device=device)
     arg_u = arg_u if isinstance(arg_u, torch.Tensor) else None
     arg_e = arg_e if isinstance(arg_e, torch.Tensor) else None
-    ws, ws_bytes = _workspace(g, MSG[msg], REDUCE[reduce], H_, D, d_in, X.device)
+    ws, ws_bytes = _workspace(g, MSG[msg], REDUCE[reduce], H_, D, d_in, device)
     _check(lib().fg_spmm(g.handle, MSG[msg], REDUCE[reduce], H_, D, _ptr(X), _ptr(E), _ptr(W), d_in, _ptr(X_dst),
                          _ptr(out), _ptr(arg_u), _ptr(arg_e), _ptr(ws), ws_bytes, _stream(stream)),
            f"fg_spmm({msg},{reduce})")
@@ -209,12 +215,14 @@ def spmm(g: Graph, msg: str, reduce: str, X: torch.Tensor, *, H: int = 1, E: tor
 
 def sddmm(g: Graph, X: torch.Tensor, Y: torch.Tensor | None = None, *, H: int = 1, op: str = "u_dot_v",
           out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """featgraph.sddmm (Eq. (4), Fig. 5): out[eid][h] = <X[u,h,:], Y[v,h,:]>."""
+    """featgraph.sddmm (Eq. (4), Fig. 5): out[eid][h] = <X[u,h,:], Y[v,h,:]> for
+    op="u_dot_v"; the elementwise ops u_add_v / u_sub_v / u_mul_v give
+    out[eid][j] = X[u][j] OP Y[v][j] ([nnz][F])."""
     X = _dev(X, torch.float32, "X")
     Y = X if Y is None else _dev(Y, torch.float32, "Y")
     F = X.numel() // max(X.shape[0], 1)
     if out is None:
-        out = torch.empty((g.nnz, H), dtype=torch.float32, device=X.device)
+        out = torch.empty((g.nnz, H if op == "u_dot_v" else F), dtype=torch.float32, device=X.device)
     _check(lib().fg_sddmm(g.handle, EDGE[op], H, F // H, _ptr(X), _ptr(Y), _ptr(out), _stream(stream)), "fg_sddmm")
     return out
 

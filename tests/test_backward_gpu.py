@@ -40,7 +40,7 @@ def test_transpose_is_csc(G):
 
 
 @pytest.mark.parametrize("op", ["copy_u", "u_mul_e"])
-@pytest.mark.parametrize("red", ["sum", "max"])
+@pytest.mark.parametrize("red", ["sum", "max", "min", "mean"])
 def test_spmm_backward(G, op, red):
     import paper_2008_11359_b200 as fgp
     g, h, hT = G
@@ -50,20 +50,20 @@ def test_spmm_backward(G, op, red):
     E = gen.features((g.nnz, H), 21, 1, gen.UNIT)
     dOut = gen.features((g.n_dst, F), 21, 2)
     Ed = dev(E) if op == "u_mul_e" else None
-    arg_u = None
-    if red == "max":
-        _, au, _ = fgp.spmm(h, op, "max", dev(X), H=H, E=Ed, arg_u=True, arg_e=True)
+    arg_u = rau = None
+    if red in ("max", "min"):
+        _, au, _ = fgp.spmm(h, op, red, dev(X), H=H, E=Ed, arg_u=True, arg_e=True)
         arg_u = au
+        # the oracle side uses the oracle's own winners; they must match the kernel's
+        _, _, rau, _ = oracle.spmm(g.row_ptr, g.col_idx, op, red, X, H=H, E=E if op == "u_mul_e" else None)
+        assert np.array_equal(au.cpu().numpy(), rau)
     dX, dE = fgp.spmm_backward(h, hT, op, red, dev(dOut), H=H, X=dev(X), E=Ed, arg_u=arg_u,
                                want_dE=op == "u_mul_e")
     rdX, rdE = oracle.spmm_backward(g.row_ptr, g.col_idx, op, red, X, dOut, n_src=g.n_src, H=H,
-                                    E=E if op == "u_mul_e" else None,
-                                    arg_u=arg_u.cpu().numpy() if arg_u is not None else None,
-                                    want_dE=op == "u_mul_e")
+                                    E=E if op == "u_mul_e" else None, arg_u=rau, want_dE=op == "u_mul_e")
     # tolerance scale: the same gradient of |inputs|
     bdX, bdE = oracle.spmm_backward(g.row_ptr, g.col_idx, op, red, np.abs(X), np.abs(dOut), n_src=g.n_src, H=H,
-                                    E=np.abs(E) if op == "u_mul_e" else None,
-                                    arg_u=arg_u.cpu().numpy() if arg_u is not None else None,
+                                    E=np.abs(E) if op == "u_mul_e" else None, arg_u=rau,
                                     want_dE=op == "u_mul_e")
     check_close(dX.cpu().numpy(), rdX, bdX, 1e-4, f"dX {op}-{red}")
     if op == "u_mul_e":
@@ -90,11 +90,12 @@ def test_edge_softmax_backward(G, H):
     g, h, hT = G
     S = gen.features((g.nnz, H), 41, 0) * 4
     dA = gen.features((g.nnz, H), 41, 1)
-    alpha = fgp.edge_softmax(h, dev(S), H=H)
-    ds = fgp.edge_softmax_backward(h, alpha, dev(dA), H=H).cpu().numpy()
-    ref = oracle.edge_softmax_backward(g.row_ptr, alpha.cpu().numpy(), dA, H=H)
+    # alpha from the oracle's forward (rounded to fp32) feeds both sides
+    alpha32 = oracle.edge_softmax(g.row_ptr, S, H=H).astype(np.float32)
+    ds = fgp.edge_softmax_backward(h, dev(alpha32), dev(dA), H=H).cpu().numpy()
+    ref = oracle.edge_softmax_backward(g.row_ptr, alpha32, dA, H=H)
     # |terms|: alpha*|dalpha| + alpha * sum alpha*|dalpha|
-    a = alpha.cpu().numpy().astype(np.float64)
+    a = alpha32.astype(np.float64)
     bound = oracle.edge_softmax_backward(g.row_ptr, a.astype(np.float32), np.abs(dA), H=H)
     bound = np.abs(bound) + 2 * a * np.abs(dA)
     check_close(ds, ref, bound, 1e-4, f"softmax backward H={H}")

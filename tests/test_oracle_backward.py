@@ -68,6 +68,57 @@ def test_spmm_max_backward_vs_autograd(op):
         np.testing.assert_allclose(dE, Et.grad.numpy(), rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("op", ["copy_u", "u_mul_e"])
+def test_spmm_min_backward_vs_autograd(op):
+    g = graph(seed=8)
+    H, D = 2, 2
+    X = gen.features((g.n_src, H * D), 5, 0)
+    E = gen.features((g.nnz, H), 5, 1, gen.UNIT)
+    G = gen.features((g.n_dst, H * D), 5, 2)
+    Eo = E if op == "u_mul_e" else None
+    _, _, au, _ = oracle.spmm(g.row_ptr, g.col_idx, op, "min", X, H=H, E=Eo)
+    dX, dE = oracle.spmm_backward(g.row_ptr, g.col_idx, op, "min", X, G, n_src=g.n_src, H=H, E=Eo, arg_u=au,
+                                  want_dE=op == "u_mul_e")
+    Xt = t64(X).requires_grad_()
+    Et = t64(E).requires_grad_()
+    rows = edge_rows(g.row_ptr)
+    M = torch.full((g.n_dst, g.n_src, H * D), float("inf"), dtype=torch.float64)
+    msg = Xt[torch.from_numpy(g.col_idx.astype(np.int64))]
+    if op == "u_mul_e":
+        msg = msg * Et.repeat_interleave(D, dim=1)
+    M = M.index_put((torch.from_numpy(rows), torch.from_numpy(g.col_idx.astype(np.int64))), msg)
+    out = M.min(dim=1).values
+    nonempty = torch.from_numpy(np.diff(g.row_ptr) > 0)
+    (out[nonempty] * t64(G)[nonempty]).sum().backward()
+    np.testing.assert_allclose(dX, Xt.grad.numpy(), rtol=1e-12, atol=1e-12)
+    if op == "u_mul_e":
+        np.testing.assert_allclose(dE, Et.grad.numpy(), rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("op", ["copy_u", "u_mul_e"])
+def test_spmm_mean_backward_vs_autograd(op):
+    g = graph(seed=10)
+    H, D = 2, 3
+    X = gen.features((g.n_src, H * D), 7, 0)
+    E = gen.features((g.nnz, H), 7, 1, gen.UNIT)
+    G = gen.features((g.n_dst, H * D), 7, 2)
+    Eo = E if op == "u_mul_e" else None
+    dX, dE = oracle.spmm_backward(g.row_ptr, g.col_idx, op, "mean", X, G, n_src=g.n_src, H=H, E=Eo,
+                                  want_dE=op == "u_mul_e")
+    Xt = t64(X).requires_grad_()
+    Et = t64(E).requires_grad_()
+    rows = torch.from_numpy(edge_rows(g.row_ptr))
+    msg = Xt[torch.from_numpy(g.col_idx.astype(np.int64))]
+    if op == "u_mul_e":
+        msg = msg * Et.repeat_interleave(D, dim=1)
+    out = torch.zeros(g.n_dst, H * D, dtype=torch.float64).index_add(0, rows, msg)
+    deg = torch.from_numpy(np.maximum(np.diff(g.row_ptr), 1).astype(np.float64))[:, None]
+    ((out / deg) * t64(G)).sum().backward()
+    np.testing.assert_allclose(dX, Xt.grad.numpy(), rtol=1e-12, atol=1e-12)
+    if op == "u_mul_e":
+        np.testing.assert_allclose(dE, Et.grad.numpy(), rtol=1e-12, atol=1e-12)
+
+
 def test_sddmm_backward_vs_autograd():
     g = graph(seed=6)
     H, D = 2, 4

@@ -13,7 +13,11 @@ fails at least one of them:
   * adjoint identity of the gradient duality (P:171-173);
   * softmax: rows sum to 1, shift invariance, constant -> 1/deg, torch.softmax
     on a dense -inf-masked matrix;
-  * SPEC.md worked examples in tests/golden/spec_examples.json.
+  * SPEC.md worked examples in tests/golden/spec_examples.json;
+  * row f4: numpy masked min / argmin, min = -max(-.), mean = dense A_w.X / deg,
+    u_add_e = A.X + A_E.1, masked max/min of fp32 x_u + e, copy_e = row sums /
+    masked max of the E-weighted adjacency, u_OP_v on the complete graph = the
+    dense broadcast, sum_j u_mul_v = u_dot_v.
 """
 import json
 import os
@@ -116,6 +120,151 @@ def test_copy_u_max_relabel_invariance():
             if au[v, j] >= 0:
                 assert Xd[au[v, j], j] == ref[v, j]
                 assert X2[au2[pi[v], j], j] == ref[v, j]
+
+
+@pytest.mark.parametrize("regime", [gen.REAL, gen.INT])
+def test_copy_u_min_masked(regime):
+    """min (row f4): numpy masked min with first-occurrence argmin."""
+    g = small_graph()
+    X = gen.features((g.n_src, 6), 14, 0, regime, lo=-3, hi=3)
+    ref, ab, au, ae = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", "min", X)
+    A = dense_adjacency(g.row_ptr, g.col_idx, g.n_src) > 0
+    Mm = np.where(A[:, :, None], X.astype(np.float64)[None], np.inf)
+    val, arg = Mm.min(axis=1), Mm.argmin(axis=1)
+    empty = ~A.any(axis=1)
+    val[empty], arg[empty] = 0.0, -1
+    assert np.array_equal(ref, val)
+    assert np.array_equal(au, arg)
+    assert np.array_equal(ab, np.abs(val))
+    for v in range(0, g.n_dst, 5):
+        for j in range(6):
+            assert ae[v, j] == (_eid_of(g.row_ptr, g.col_idx, v, arg[v, j]) if arg[v, j] >= 0 else -1)
+
+
+def test_u_mul_e_min_is_negated_max():
+    """min_u t = -max_u (-t) with the same first-wins winner (negating E negates
+    every fp32 product exactly)."""
+    g = small_graph(n=150, m=2500, seed=12)
+    H, D = 2, 4
+    X = gen.features((g.n_src, H * D), 31, 0, gen.INT, lo=-3, hi=3)
+    E = gen.features((g.nnz, H), 31, 1, gen.INT, lo=-2, hi=2)
+    mn, _, au, ae = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", "min", X, H=H, E=E)
+    mx, _, au2, ae2 = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", "max", X, H=H, E=-E)
+    assert np.array_equal(mn, -mx + 0.0)
+    assert np.array_equal(au, au2) and np.array_equal(ae, ae2)
+
+
+@pytest.mark.parametrize("op", ["copy_u", "u_mul_e"])
+def test_mean_is_dense_over_degree(op):
+    """mean (row f4): (A_w X) / deg(v), empty rows 0."""
+    g = small_graph()
+    H, D = 2, 3
+    X = gen.features((g.n_src, H * D), 17, 0)
+    E = gen.features((g.nnz, H), 17, 1, gen.UNIT) if op == "u_mul_e" else None
+    ref, ab, au, _ = oracle.spmm(g.row_ptr, g.col_idx, op, "mean", X, H=H, E=E)
+    assert au is None
+    deg = np.maximum(g.degrees(), 1).astype(np.float64)[:, None]
+    for h in range(H):
+        w = E[:, h].astype(np.float64) if E is not None else None
+        Aw = dense_adjacency(g.row_ptr, g.col_idx, g.n_src, w)
+        blk = slice(h * D, (h + 1) * D)
+        np.testing.assert_allclose(ref[:, blk], Aw @ X[:, blk].astype(np.float64) / deg, rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(ab[:, blk], np.abs(Aw) @ np.abs(X[:, blk].astype(np.float64)) / deg,
+                                   rtol=1e-12, atol=1e-12)
+    assert np.all(ref[g.degrees() == 0] == 0.0)
+
+
+# ------------------------------------------------------------------ u_add_e, copy_e (row f4)
+def test_u_add_e_sum_dense():
+    """sum_p (x_u + e_p) = (A X)[v] + (A_E 1)[v] per head."""
+    g = small_graph()
+    H, D = 3, 4
+    X = gen.features((g.n_src, H * D), 41, 0)
+    E = gen.features((g.nnz, H), 41, 1)
+    ref, ab, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "u_add_e", "sum", X, H=H, E=E)
+    A = dense_adjacency(g.row_ptr, g.col_idx, g.n_src)
+    for h in range(H):
+        Aw = dense_adjacency(g.row_ptr, g.col_idx, g.n_src, E[:, h].astype(np.float64))
+        blk = slice(h * D, (h + 1) * D)
+        want = A @ X[:, blk].astype(np.float64) + Aw.sum(axis=1)[:, None]
+        np.testing.assert_allclose(ref[:, blk], want, rtol=1e-12, atol=1e-12)
+        wabs = A @ np.abs(X[:, blk].astype(np.float64)) + np.abs(Aw).sum(axis=1)[:, None]
+        np.testing.assert_allclose(ab[:, blk], wabs, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("red", ["max", "min"])
+def test_u_add_e_select_masked(red):
+    """max/min over fp32-rounded x_u + e_p (numpy fp32 add is IEEE RN), first wins."""
+    g = small_graph(n=180, m=2600, seed=21)
+    H, D = 2, 2
+    X = gen.features((g.n_src, H * D), 43, 0, gen.INT, lo=-3, hi=3)
+    E = gen.features((g.nnz, H), 43, 1, gen.INT, lo=-2, hi=2)
+    ref, _, au, ae = oracle.spmm(g.row_ptr, g.col_idx, "u_add_e", red, X, H=H, E=E)
+    A = dense_adjacency(g.row_ptr, g.col_idx, g.n_src) > 0
+    rows = edge_rows(g.row_ptr)
+    Ed = np.zeros((g.n_dst, g.n_src, H), np.float32)
+    Ed[rows, g.col_idx] = E
+    M = (X[None, :, :] + np.repeat(Ed, D, axis=2)).astype(np.float64)
+    fill = -np.inf if red == "max" else np.inf
+    Mm = np.where(A[:, :, None], M, fill)
+    val = Mm.max(axis=1) if red == "max" else Mm.min(axis=1)
+    arg = Mm.argmax(axis=1) if red == "max" else Mm.argmin(axis=1)
+    empty = ~A.any(axis=1)
+    val[empty], arg[empty] = 0.0, -1
+    assert np.array_equal(ref, val)
+    assert np.array_equal(au, arg)
+
+
+@pytest.mark.parametrize("red", ["sum", "max"])
+def test_copy_e_dense(red):
+    """copy_e: the message is the edge's own row; sum = row sums of the E-weighted
+    adjacency, max = masked max over it (first occurrence)."""
+    g = small_graph()
+    F = 5
+    E = gen.features((g.nnz, F), 45, 0, gen.INT if red == "max" else gen.REAL, lo=-3, hi=3)
+    eid = gen.permutation(g.nnz, 46).astype(np.int32)
+    ref, ab, au, ae = oracle.spmm(g.row_ptr, g.col_idx, "copy_e", red, None, E=E, eid=eid)
+    A = dense_adjacency(g.row_ptr, g.col_idx, g.n_src) > 0
+    for j in range(F):
+        Aw = dense_adjacency(g.row_ptr, g.col_idx, g.n_src, E[eid, j].astype(np.float64))   # value at CSR pos
+        if red == "sum":
+            np.testing.assert_allclose(ref[:, j], Aw.sum(axis=1), rtol=1e-12, atol=1e-12)
+            np.testing.assert_allclose(ab[:, j], np.abs(Aw).sum(axis=1), rtol=1e-12, atol=1e-12)
+        else:
+            Mm = np.where(A, Aw, -np.inf)
+            val, arg = Mm.max(axis=1), Mm.argmax(axis=1)
+            empty = ~A.any(axis=1)
+            val[empty], arg[empty] = 0.0, -1
+            assert np.array_equal(ref[:, j], val)
+            assert np.array_equal(au[:, j], arg)
+            for v in np.nonzero(~empty)[0][::7]:
+                assert ae[v, j] == eid[_eid_of(g.row_ptr, g.col_idx, v, arg[v])]
+
+
+@pytest.mark.parametrize("op", ["u_add_v", "u_sub_v", "u_mul_v"])
+def test_sddmm_binary_complete_graph(op):
+    """Elementwise u_OP_v on the complete graph = the dense broadcast X[u] OP Y[v]."""
+    n, F = 23, 6
+    rp = np.arange(n + 1, dtype=np.int64) * n
+    ci = np.tile(np.arange(n, dtype=np.int32), n)
+    X = gen.features((n, F), 53, 0).astype(np.float64)
+    Y = gen.features((n, F), 53, 1).astype(np.float64)
+    ref, ab = oracle.sddmm_binary(rp, ci, op, X.astype(np.float32), Y.astype(np.float32))
+    fn = {"u_add_v": np.add, "u_sub_v": np.subtract, "u_mul_v": np.multiply}[op]
+    dense = fn(X[None, :, :], Y[:, None, :])        # [v, u, j]
+    assert np.array_equal(ref.reshape(n, n, F), dense)
+    dabs = np.abs(dense) if op == "u_mul_v" else np.abs(X)[None] + np.abs(Y)[:, None]
+    assert np.array_equal(ab.reshape(n, n, F), dabs)
+
+
+def test_sddmm_binary_mul_sums_to_dot():
+    """sum_j (u_mul_v)[e][j] = u_dot_v[e] (H = 1)."""
+    g = small_graph(n=100, m=1500, seed=3)
+    X = gen.features((g.n_src, 8), 55, 0)
+    Y = gen.features((g.n_dst, 8), 55, 1)
+    m_, _ = oracle.sddmm_binary(g.row_ptr, g.col_idx, "u_mul_v", X, Y)
+    d_, _ = oracle.sddmm(g.row_ptr, g.col_idx, X, Y)
+    np.testing.assert_allclose(m_.sum(axis=1), d_[:, 0], rtol=1e-12, atol=1e-13)
 
 
 # ------------------------------------------------------------------ u_mul_e

@@ -97,6 +97,34 @@ def test_copy_u_max(skewed, F, regime):
     assert np.array_equal(ae.cpu().numpy(), rae)
 
 
+@pytest.mark.parametrize("F", [4, 32, 128, 512])
+@pytest.mark.parametrize("regime", [gen.REAL, gen.INT])
+def test_copy_u_min(skewed, F, regime):
+    """row f4: min = first-wins argmin, bit-exact with the oracle."""
+    import paper_2008_11359_b200 as fgp
+    X = feats((skewed.n_src, F), 250 + F, regime, lo=-3, hi=3)
+    out, au, ae = fgp.spmm(skewed.h, "copy_u", "min", dev(X), arg_u=True, arg_e=True)
+    ref, _, rau, rae = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", "min", X)
+    assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+    assert np.array_equal(au.cpu().numpy(), rau)
+    assert np.array_equal(ae.cpu().numpy(), rae)
+
+
+@pytest.mark.parametrize("F", [4, 32, 128, 512])
+@pytest.mark.parametrize("regime", [gen.REAL, gen.INT])
+def test_copy_u_mean(skewed, F, regime):
+    """row f4: mean = sum / |N(v)|.  INT regime: the fp32 sum is exact, so the one
+    IEEE division gives exactly fp32(oracle)."""
+    import paper_2008_11359_b200 as fgp
+    X = feats((skewed.n_src, F), 260 + F, regime)
+    out = fgp.spmm(skewed.h, "copy_u", "mean", dev(X)).cpu().numpy()
+    ref, ab, _, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", "mean", X)
+    if regime == gen.INT:
+        assert np.array_equal(out, ref.astype(np.float32))
+    else:
+        check_close(out, ref, ab, TOL, f"copy_u-mean F={F}")
+
+
 def test_tiny_config_all_ops(tiny):
     """BASELINE.json configs[0]: tiny graph, F=16, copy_u sum/max + u_dot_v."""
     import paper_2008_11359_b200 as fgp
@@ -116,7 +144,7 @@ def test_tiny_config_all_ops(tiny):
 
 # ------------------------------------------------------------------ u_mul_e
 @pytest.mark.parametrize("H,D", [(1, 4), (1, 128), (2, 2), (8, 2), (4, 4), (8, 32), (8, 64), (3, 12)])
-@pytest.mark.parametrize("red", ["sum", "max"])
+@pytest.mark.parametrize("red", ["sum", "max", "min", "mean"])
 @pytest.mark.parametrize("use_eid", [False, True])
 def test_u_mul_e(skewed, skewed_eid, H, D, red, use_eid):
     import paper_2008_11359_b200 as fgp
@@ -125,11 +153,51 @@ def test_u_mul_e(skewed, skewed_eid, H, D, red, use_eid):
     X = feats((g.n_src, F), 300 + F, gen.REAL)
     E = gen.features((g.nnz, H), 301, 1, gen.UNIT)
     ref, ab, rau, rae = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", red, X, H=H, E=E, eid=g.eid)
-    if red == "sum":
-        out = fgp.spmm(g.h, "u_mul_e", "sum", dev(X), H=H, E=dev(E)).cpu().numpy()
-        check_close(out, ref, ab, TOL, f"u_mul_e-sum H={H} D={D}")
+    if red in ("sum", "mean"):
+        out = fgp.spmm(g.h, "u_mul_e", red, dev(X), H=H, E=dev(E)).cpu().numpy()
+        check_close(out, ref, ab, TOL, f"u_mul_e-{red} H={H} D={D}")
     else:
-        out, au, ae = fgp.spmm(g.h, "u_mul_e", "max", dev(X), H=H, E=dev(E), arg_u=True, arg_e=True)
+        out, au, ae = fgp.spmm(g.h, "u_mul_e", red, dev(X), H=H, E=dev(E), arg_u=True, arg_e=True)
+        assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+        assert np.array_equal(au.cpu().numpy(), rau)
+        assert np.array_equal(ae.cpu().numpy(), rae)
+
+
+@pytest.mark.parametrize("H,D", [(1, 4), (2, 2), (8, 32), (3, 12), (4, 3), (1, 128)])
+@pytest.mark.parametrize("red", ["sum", "max", "min", "mean"])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_u_add_e(skewed, skewed_eid, H, D, red, use_eid):
+    """row f4: phi = x_u + e (E [nnz][H] broadcast over D)."""
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    F = H * D
+    X = feats((g.n_src, F), 320 + F, gen.REAL)
+    E = gen.features((g.nnz, H), 321, 1, gen.REAL)
+    ref, ab, rau, rae = oracle.spmm(g.row_ptr, g.col_idx, "u_add_e", red, X, H=H, E=E, eid=g.eid)
+    if red in ("sum", "mean"):
+        out = fgp.spmm(g.h, "u_add_e", red, dev(X), H=H, E=dev(E)).cpu().numpy()
+        check_close(out, ref, ab, TOL, f"u_add_e-{red} H={H} D={D}")
+    else:
+        out, au, ae = fgp.spmm(g.h, "u_add_e", red, dev(X), H=H, E=dev(E), arg_u=True, arg_e=True)
+        assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+        assert np.array_equal(au.cpu().numpy(), rau)
+        assert np.array_equal(ae.cpu().numpy(), rae)
+
+
+@pytest.mark.parametrize("F", [4, 32, 128, 260, 512])
+@pytest.mark.parametrize("red", ["sum", "max", "min", "mean"])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_copy_e(skewed, skewed_eid, F, red, use_eid):
+    """row f4: phi = the edge's own feature row E[eid] ([nnz][F])."""
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    E = gen.features((g.nnz, F), 330 + F, 0, gen.INT if red in ("max", "min") else gen.REAL, lo=-3, hi=3)
+    ref, ab, rau, rae = oracle.spmm(g.row_ptr, g.col_idx, "copy_e", red, None, E=E, eid=g.eid)
+    if red in ("sum", "mean"):
+        out = fgp.spmm(g.h, "copy_e", red, None, E=dev(E)).cpu().numpy()
+        check_close(out, ref, ab, TOL, f"copy_e-{red} F={F}")
+    else:
+        out, au, ae = fgp.spmm(g.h, "copy_e", red, None, E=dev(E), arg_u=True, arg_e=True)
         assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
         assert np.array_equal(au.cpu().numpy(), rau)
         assert np.array_equal(ae.cpu().numpy(), rae)
@@ -216,6 +284,22 @@ def test_sddmm(skewed, skewed_eid, H, D, use_eid):
     check_close(out[pos], ref, ab, TOL, f"u_dot_v H={H} D={D}")
 
 
+@pytest.mark.parametrize("op", ["u_add_v", "u_sub_v", "u_mul_v"])
+@pytest.mark.parametrize("F", [4, 12, 128, 516])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_sddmm_binary(skewed, skewed_eid, op, F, use_eid):
+    """row f4: elementwise u_OP_v; one IEEE op per element, so the kernel equals
+    fp32(oracle) exactly."""
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    X = feats((g.n_src, F), 400 + F, gen.REAL)
+    Y = feats((g.n_dst, F), 401 + F, gen.REAL)
+    out = fgp.sddmm(g.h, dev(X), dev(Y), op=op).cpu().numpy()
+    ref, _ = oracle.sddmm_binary(g.row_ptr, g.col_idx, op, X, Y)
+    pos = np.arange(g.nnz) if g.eid is None else g.eid
+    assert np.array_equal(out[pos], ref.astype(np.float32))
+
+
 def test_sddmm_int_exact(skewed):
     import paper_2008_11359_b200 as fgp
     H, D = 8, 32
@@ -262,21 +346,27 @@ def test_edge_softmax_special_values(skewed):
 # ------------------------------------------------------------------ chain (GAT layer, config 3 shape at small size)
 def test_gat_layer_chain(skewed):
     """sddmm -> edge_softmax -> u_mul_e, each op checked in isolation on the
-    GPU's own fp32 inputs (no compounding through exp)."""
+    ORACLE's fp32-rounded intermediates (no compounding through
+    exp; no oracle input comes from the CUDA path), then the GPU chain end to
+    end against the fused-layer definition oracle.gat."""
     import paper_2008_11359_b200 as fgp
     H, D = 8, 32
     X = feats((skewed.n_src, H * D), 700, gen.REAL) * 0.25
     Xt = dev(X)
+    ref_s, ab_s = oracle.sddmm(skewed.row_ptr, skewed.col_idx, X, H=H)
+    s32 = ref_s.astype(np.float32)
+    ref_a = oracle.edge_softmax(skewed.row_ptr, s32, H=H)
+    a32 = ref_a.astype(np.float32)
+    ref_o, ab_o, _, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "u_mul_e", "sum", X, H=H, E=a32)
     s = fgp.sddmm(skewed.h, Xt, H=H)
-    a = fgp.edge_softmax(skewed.h, s, H=H)
-    out = fgp.spmm(skewed.h, "u_mul_e", "sum", Xt, H=H, E=a).cpu().numpy()
-    s_np, a_np = s.cpu().numpy(), a.cpu().numpy()
-    ref, ab = oracle.sddmm(skewed.row_ptr, skewed.col_idx, X, H=H)
-    check_close(s_np, ref, ab, TOL, "gat sddmm")
-    ref_a = oracle.edge_softmax(skewed.row_ptr, s_np, H=H)
-    assert (np.abs(a_np - ref_a) <= TOL * ref_a).all()
-    ref_o, ab_o, _, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "u_mul_e", "sum", X, H=H, E=a_np)
+    check_close(s.cpu().numpy(), ref_s, ab_s, TOL, "gat sddmm")
+    a = fgp.edge_softmax(skewed.h, dev(s32), H=H).cpu().numpy()
+    assert (np.abs(a - ref_a) <= TOL * ref_a).all()
+    out = fgp.spmm(skewed.h, "u_mul_e", "sum", Xt, H=H, E=dev(a32)).cpu().numpy()
     check_close(out, ref_o, ab_o, TOL, "gat aggregation")
+    chain = fgp.spmm(skewed.h, "u_mul_e", "sum", Xt, H=H, E=fgp.edge_softmax(skewed.h, s, H=H)).cpu().numpy()
+    ref_g, ab_g = oracle.gat(skewed.row_ptr, skewed.col_idx, X, H=H)
+    check_close(chain, ref_g, ab_g, TOL, "gat chain end to end")
 
 
 # ------------------------------------------------------------------ degenerate graphs and ABI behaviour
@@ -340,6 +430,13 @@ def test_abi_errors_on_device(skewed):
     with pytest.raises(FGError) as ei:   # arg with sum
         fgp.spmm(skewed.h, "copy_u", "sum", torch.zeros((skewed.n_src, 8), device="cuda"), arg_u=True)
     assert ei.value.status == FG_EINVAL
+    with pytest.raises(FGError) as ei:   # arg with mean
+        fgp.spmm(skewed.h, "copy_u", "mean", torch.zeros((skewed.n_src, 8), device="cuda"), arg_u=True)
+    assert ei.value.status == FG_EINVAL
+    with pytest.raises(FGError) as ei:   # mlp supports sum / max only
+        fgp.spmm(skewed.h, "mlp", "min", torch.zeros((skewed.n_src, 8), device="cuda"),
+                 W=torch.zeros((8, 16), device="cuda"))
+    assert ei.value.status == fgp.fg.FG_EUNSUPPORTED
     out = torch.full((skewed.n_dst, 8), 3.0, device="cuda")
     with pytest.raises(FGError):
         fgp.spmm(skewed.h, "copy_u", "sum", torch.zeros((skewed.n_src, 6), device="cuda"), out=out)
@@ -373,6 +470,12 @@ def test_l2_column_tiling(skewed, F, monkeypatch):
     ref, _, rau, rae = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", "max", X)
     assert np.array_equal(mx.cpu().numpy().astype(np.float64), ref)
     assert np.array_equal(au.cpu().numpy(), rau) and np.array_equal(ae.cpu().numpy(), rae)
+    mn, au = fgp.spmm(skewed.h, "copy_u", "min", dev(X), arg_u=True)[:2]
+    ref, _, rau, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", "min", X)
+    assert np.array_equal(mn.cpu().numpy().astype(np.float64), ref) and np.array_equal(au.cpu().numpy(), rau)
+    me = fgp.spmm(skewed.h, "copy_u", "mean", dev(X)).cpu().numpy()
+    ref, ab, _, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", "mean", X)
+    check_close(me, ref, ab, TOL, f"tiled copy_u-mean F={F}")
     s = fgp.sddmm(skewed.h, dev(X), dev(Y)).cpu().numpy()
     ref, ab = oracle.sddmm(skewed.row_ptr, skewed.col_idx, X, Y)
     check_close(s, ref, ab, TOL, f"tiled u_dot_v F={F}")

@@ -14,7 +14,7 @@ def t(fn, reps=5):
         s.record(); fn(); e.record(); torch.cuda.synchronize()
         if i: ts.append(s.elapsed_time(e))
     return np.median(ts)
-for dbg in ["0", "1", "2", "3"]:
+for dbg in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "1", "2", "3"]):
     os.environ["FG_MLP_DBG"] = dbg
     print(f"{sys.argv[1] if len(sys.argv)>1 else 'reddit'} dbg={dbg} max+args {t(lambda: fgp.spmm(G, 'mlp', 'max', X8, W=W, out=o, arg_u=au, arg_e=ae)):.3f} ms"
           f"  sum {t(lambda: fgp.spmm(G, 'mlp', 'sum', X8, W=W, out=o)):.3f} ms")
