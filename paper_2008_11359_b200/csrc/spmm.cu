@@ -1,7 +1,8 @@
 // spmm.cu -- gSpMM with gathered messages: copy_u and u_mul_e x {sum, max}
-// (SURVEY §8(a) rows a1, a2), plus the min / mean reducers (row f4); the
-// u_add_e / copy_e messages (row f4) are instantiated in spmm_ext.cu.  The
-// kernel template lives in spmm_impl.cuh.
+// (SURVEY §8(a) rows a1, a2), plus the min / mean reducers and the u_add_e /
+// copy_e messages (row f4).  The kernel template lives in spmm_impl.cuh and is
+// instantiated per (reducer, op set) in spmm_inst_*.cu; this file holds the
+// host-side launch configuration.
 //
 // Eq. (1): out[v] = (+)_{u -> v} phi(x_u, x_uv), with
 //   copy_u : phi = X[u]                    (GCN aggregation, Fig. 3a, Eq. (3))
@@ -32,17 +33,6 @@
 
 #include "spmm_impl.cuh"
 
-namespace fgspmm {
-
-template <int G, int NV>
-fg_status dispatch_op(const Args& A, int op, int red, cudaStream_t st) {
-    if (op == OP_COPY) return dispatch_red<G, NV, OP_COPY>(A, red, st);
-    if (op == OP_UMULE) return dispatch_red<G, NV, OP_UMULE>(A, red, st);
-    if (op == OP_UMULE_GEN) return dispatch_red<G, NV, OP_UMULE_GEN>(A, red, st);
-    return dispatch_ext<G, NV>(A, op, red, st);
-}
-
-}  // namespace fgspmm
 
 namespace fgk {
 
@@ -97,17 +87,16 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     }
     const int64_t NG = THREADS / G;
     A.n_heavy = rows_with_degree_at_least(g, NG * 32);
-    switch (G) {
-        case 1: return dispatch_op<1, 1>(A, op, mx, st);
-        case 2: return dispatch_op<2, 1>(A, op, mx, st);
-        case 4: return dispatch_op<4, 1>(A, op, mx, st);
-        case 8: return dispatch_op<8, 1>(A, op, mx, st);
-        case 16: return dispatch_op<16, 1>(A, op, mx, st);
-        default:
-            if (NV == 1) return dispatch_op<32, 1>(A, op, mx, st);
-            if (NV == 2) return dispatch_op<32, 2>(A, op, mx, st);
-            if (NV == 3) return dispatch_op<32, 3>(A, op, mx, st);
-            return dispatch_op<32, 4>(A, op, mx, st);
+    A.src_deg = g->src_deg;
+    // hot-source L2 policy for the untiled gathers of rows wider than the budget
+    A.hot_thr = (F4 == A.F4) ? fgk::hot_threshold(g, int64_t(A.F4) * 16) : INT32_MAX;
+    A.hot_cold = fgk::hot_cold_kind();
+    const int opset = (op == OP_UADDE || op == OP_COPYE) ? 1 : 0;
+    switch (mx) {
+        case R_MAX: return opset ? dispatch_inst<R_MAX, 1>(A, G, NV, op, st) : dispatch_inst<R_MAX, 0>(A, G, NV, op, st);
+        case R_MIN: return opset ? dispatch_inst<R_MIN, 1>(A, G, NV, op, st) : dispatch_inst<R_MIN, 0>(A, G, NV, op, st);
+        case R_MEAN: return opset ? dispatch_inst<R_MEAN, 1>(A, G, NV, op, st) : dispatch_inst<R_MEAN, 0>(A, G, NV, op, st);
+        default: return opset ? dispatch_inst<R_SUM, 1>(A, G, NV, op, st) : dispatch_inst<R_SUM, 0>(A, G, NV, op, st);
     }
 }
 

@@ -1,9 +1,8 @@
-// spmm_impl.cuh -- the gathered-message gSpMM kernel template shared by
-// spmm.cu (copy_u, u_mul_e) and spmm_ext.cu (u_add_e, copy_e); see spmm.cu
-// for the design notes.  Each translation unit instantiates its own ops, so
-// the two compile in parallel.
+// spmm_impl.cuh -- the gathered-message gSpMM kernel template (design notes in
+// spmm.cu), instantiated per (reducer, op set) by spmm_inst_*.cu.
 #pragma once
 #include "fg_internal.h"
+#include "ldpol.cuh"
 
 namespace fgspmm {
 
@@ -34,6 +33,9 @@ struct Args {
     float4* out;
     int4* arg_u;
     int4* arg_e;
+    const int32_t* src_deg;     // hot-source L2 policy (ldpol.cuh): src_deg[u] >= hot_thr -> evict_last
+    int hot_thr;                // INT32_MAX: off
+    int hot_cold;               // cold-row policy kind (ldpol.cuh policy_cold)
 };
 
 __device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); }
@@ -52,6 +54,9 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
     constexpr int U = NV >= 4 ? 2 : (NV >= 2 ? 4 : 8);      // edges in flight per lane
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);     // select-type reducers
     const int F4 = A.F4;
+    // hot-source policy only where a whole warp loads one source row (G == 32)
+    const bool hotpol = (G == 32) && (OP != OP_COPYE) && A.hot_thr != INT32_MAX;
+    const uint64_t pol_hot = fgpol::policy_evict_last(), pol_cold = fgpol::policy_cold(A.hot_cold);
     for (int64_t p0 = s; p0 < e; p0 += B) {
         const int cnt = int(min((int64_t)B, e - p0));
         int uix[R];
@@ -60,6 +65,7 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
         for (int r = 0; r < R; ++r) {
             const int64_t p = p0 + gl + r * G;
             uix[r] = (OP != OP_COPYE && p < e) ? __ldg(A.col_idx + p) : 0;   // copy_e reads no source row
+            if (hotpol && p < e && __ldg(A.src_deg + uix[r]) >= A.hot_thr) uix[r] |= fgpol::HOT_BIT;
             if constexpr (OP != OP_COPY) eix[r] = (p < e) ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
         }
         // u_mul_e with identity edge ids: the batch's E rows are one contiguous span;
@@ -84,7 +90,9 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
                 const int t = t0 + uu;
-                const int u = __shfl_sync(mask, uix[t / G], t % G, G);
+                const int raw = __shfl_sync(mask, uix[t / G], t % G, G);
+                const int u = raw & fgpol::IDX_MASK;
+                const uint64_t pol = raw < 0 ? pol_hot : pol_cold;   // warp-uniform when hotpol
                 int ed = 0;
                 if constexpr (OP != OP_COPY) ed = __shfl_sync(mask, eix[t / G], t % G, G);
                 const float4* xr = (OP == OP_COPYE) ? reinterpret_cast<const float4*>(A.E) + int64_t(ed) * F4
@@ -93,7 +101,7 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                 for (int j = 0; j < NV; ++j) {
                     const int c = c4base + gl + G * j;
                     const bool ok = (t < cnt) && (c < F4);
-                    x[uu][j] = ok ? __ldg(xr + c) : f4(0.f);
+                    x[uu][j] = !ok ? f4(0.f) : (hotpol ? fgpol::ldg_policy(xr + c, pol) : __ldg(xr + c));
                     if constexpr (OP == OP_UMULE) {
                         const int h = (4 * c) / A.D;
                         ev[uu][j][0] = !ok ? 0.f : (staged ? etile[t * A.H + h] : __ldg(A.E + int64_t(ed) * A.H + h));
@@ -291,17 +299,26 @@ fg_status launch_t(const Args& A0, cudaStream_t st) {
     return fgk::check_launch("spmm_gather_kernel");
 }
 
-template <int G, int NV, int OP>
-fg_status dispatch_red(const Args& A, int red, cudaStream_t st) {
-    switch (red) {
-        case R_MAX: return launch_t<G, NV, OP, R_MAX>(A, st);
-        case R_MIN: return launch_t<G, NV, OP, R_MIN>(A, st);
-        case R_MEAN: return launch_t<G, NV, OP, R_MEAN>(A, st);
-        default: return launch_t<G, NV, OP, R_SUM>(A, st);
-    }
-}
-
-template <int G, int NV>
-fg_status dispatch_ext(const Args& A, int op, int red, cudaStream_t st);   // spmm_ext.cu
+// One explicit specialisation per (reducer, op set) -- op set 0 = copy_u /
+// u_mul_e, 1 = u_add_e / copy_e -- each compiled in its own translation unit
+// (spmm_inst_*.cu via spmm_inst.cuh) so the instantiations build in parallel.
+template <int RED, int OPSET>
+fg_status dispatch_inst(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_inst<R_SUM, 0>(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_inst<R_SUM, 1>(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_inst<R_MAX, 0>(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_inst<R_MAX, 1>(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_inst<R_MIN, 0>(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_inst<R_MIN, 1>(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_inst<R_MEAN, 0>(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_inst<R_MEAN, 1>(const Args& A, int G, int NV, int op, cudaStream_t st);
 
 }  // namespace fgspmm
