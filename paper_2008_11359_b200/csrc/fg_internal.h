@@ -39,13 +39,6 @@ struct fg_graph {
     std::deque<SegUnits> seg_units;      // deque: references stay valid as it grows
     std::mutex seg_mu;                   // lazily built under this lock (handle shared across streams)
 
-    // source out-degrees (owned, device [n_src]) and the same sorted descending
-    // (host): the hot-source set of the L2 eviction-priority policy (the B200
-    // analogue of the paper's hybrid partitioning that stages high-degree
-    // sources in fast memory)
-    int32_t* src_deg = nullptr;
-    std::vector<int32_t> src_deg_sorted;
-
     // derived (owned, host)
     std::vector<int64_t> deg_sorted;    // degrees in rows_by_deg order (descending)
     int64_t n_nonempty = 0;
@@ -60,17 +53,6 @@ fg_status set_error(fg_status s, const char* fmt, ...);
 
 // number of rows in the degree-sorted list with degree >= t
 int64_t rows_with_degree_at_least(const fg_graph* g, int64_t t);
-
-// Hot-source threshold for gathers of row_bytes-wide source rows: sources with
-// src_deg >= threshold (at most FG_HOT_MB MB of rows, default hot_budget())
-// are loaded with L2 evict_last, the rest with the FG_HOT_COLD policy.  Returns
-// INT32_MAX when the policy is off (FG_HOT_MB unset/0 -- the default, measured
-// slower -- or the rows fit the budget anyway).
-int32_t hot_threshold(const fg_graph* g, int64_t row_bytes);
-inline int hot_cold_kind() {   // FG_HOT_COLD: 0 evict_normal (default), 1 evict_first, 2 evict_unchanged
-    const char* e = getenv("FG_HOT_COLD");
-    return e ? atoi(e) : 0;
-}
 
 // kernels launchers (return FG_OK or FG_ECUDA); arguments already validated
 fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D,

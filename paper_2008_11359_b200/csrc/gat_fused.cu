@@ -19,7 +19,6 @@
 // CTA-per-row: the groups take contiguous edge ranges and their (m, l, acc)
 // partials are merged in a fixed order (deterministic, no atomics).
 #include "fg_internal.h"
-#include "ldpol.cuh"
 
 namespace {
 
@@ -38,9 +37,6 @@ struct Args {
     const int32_t* col_idx;
     const int32_t* eid;
     int H, D4, F4;
-    const int32_t* src_deg;   // hot-source L2 policy (ldpol.cuh)
-    int hot_thr;              // INT32_MAX: off
-    int hot_cold;             // cold-row policy kind (ldpol.cuh policy_cold)
 };
 
 __device__ __forceinline__ float dot4(const float4& a, const float4& b) {
@@ -70,29 +66,21 @@ __device__ __forceinline__ void attend_range(const Args& A, const float4* __rest
     constexpr int B = 32;
     constexpr int U = NV >= 3 ? 2 : 4;
     const int F4 = A.F4, D4 = A.D4, H = A.H;
-    const bool hotpol = (G == 32) && A.hot_thr != INT32_MAX;   // warp-uniform source rows only
-    const uint64_t pol_hot = fgpol::policy_evict_last(), pol_cold = fgpol::policy_cold(A.hot_cold);
     for (int64_t p0 = s; p0 < e; p0 += B) {
         const int cnt = int(min((int64_t)B, e - p0));
         __syncwarp(mask);
-        for (int t = gl; t < cnt; t += G) {
-            const int u = __ldg(A.col_idx + p0 + t);
-            sidx[t] = (hotpol && __ldg(A.src_deg + u) >= A.hot_thr) ? (u | fgpol::HOT_BIT) : u;
-        }
+        for (int t = gl; t < cnt; t += G) sidx[t] = __ldg(A.col_idx + p0 + t);
         __syncwarp(mask);
         float4 xn[U][NV];   // software pipeline: next U edges' gathers in flight
         auto gather = [&](int tb, float4 (&dst)[U][NV]) {
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
                 const int t = tb + uu;
-                const int raw = t < cnt ? sidx[t] : 0;
-                const float4* xr = X + int64_t(raw & fgpol::IDX_MASK) * F4;
-                const uint64_t pol = raw < 0 ? pol_hot : pol_cold;
+                const float4* xr = X + int64_t(t < cnt ? sidx[t] : 0) * F4;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     const int c = gl + G * j;
-                    dst[uu][j] = !(t < cnt && c < F4) ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                                      : (hotpol ? fgpol::ldg_policy(xr + c, pol) : __ldg(xr + c));
+                    dst[uu][j] = (t < cnt && c < F4) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
         };
@@ -269,9 +257,6 @@ extern "C" fg_status fg_gat_attention(const fg_graph* g, int H, int D, const flo
     A.H = H;
     A.D4 = D / 4;
     A.F4 = F4;
-    A.src_deg = g->src_deg;
-    A.hot_thr = fgk::hot_threshold(g, int64_t(F4) * 16);
-    A.hot_cold = fgk::hot_cold_kind();
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     int G = 32, NV = 4;
     if (F4 <= 32) {

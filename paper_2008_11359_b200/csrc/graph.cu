@@ -156,19 +156,6 @@ int64_t rows_with_degree_at_least(const fg_graph* g, int64_t t) {
                                [](int64_t a, int64_t b) { return a >= b; });
     return int64_t(it - g->deg_sorted.begin());
 }
-
-int32_t hot_threshold(const fg_graph* g, int64_t row_bytes) {
-    // opt-in (FG_HOT_MB=<MB>): measured slower on reddit (SDDMM H1 F512 20.6 -> 22.1-23.4 ms,
-    // H8 10.5 -> 12.8-13.2 ms for 32-96 MB and every cold-row policy), see DESIGN.md §9
-    const char* env = getenv("FG_HOT_MB");
-    const int64_t budget = int64_t(env ? atoi(env) : 0) << 20;
-    if (budget <= 0 || row_bytes <= 0 || g->src_deg_sorted.empty()) return INT32_MAX;
-    if (g->n_src * row_bytes <= budget) return INT32_MAX;    // everything fits: plain loads
-    const int64_t k = budget / row_bytes;                     // hot rows that fit
-    if (k <= 0) return INT32_MAX;
-    // sources with degree > src_deg_sorted[k] number at most k
-    return std::max<int32_t>(g->src_deg_sorted[size_t(k)] + 1, 1);
-}
 }  // namespace fgk
 
 #define CK(x)                                                                                   \
@@ -180,11 +167,6 @@ int32_t hot_threshold(const fg_graph* g, int64_t row_bytes) {
             goto fail;                                                                          \
         }                                                                                       \
     } while (0)
-
-__global__ void src_degree_kernel(int64_t nnz, const int32_t* __restrict__ ci, int32_t* deg) {
-    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < nnz; p += int64_t(gridDim.x) * blockDim.x)
-        atomicAdd(deg + ci[p], 1);   // integer histogram: order-independent, deterministic
-}
 
 extern "C" fg_status fg_graph_create(int64_t n_dst, int64_t n_src, int64_t nnz, const int64_t* row_ptr,
                                      const int32_t* col_idx, const int32_t* eid, int validate,
@@ -291,20 +273,7 @@ extern "C" fg_status fg_graph_create(int64_t n_dst, int64_t n_src, int64_t nnz, 
         CK(cudaMemcpyAsync(g->unit_p0, up0.data(), sizeof(int64_t) * size_t(g->n_units), cudaMemcpyHostToDevice, s));
         g->device_bytes += 12 * g->n_units;
     }
-    if (n_src > 0) {
-        CK(cudaMalloc(&g->src_deg, sizeof(int32_t) * size_t(n_src)));
-        CK(cudaMemsetAsync(g->src_deg, 0, sizeof(int32_t) * size_t(n_src), s));
-        if (nnz > 0) {
-            src_degree_kernel<<<148 * 8, 256, 0, s>>>(nnz, col_idx, g->src_deg);
-            CK(cudaGetLastError());
-        }
-        g->src_deg_sorted.resize(size_t(n_src));
-        CK(cudaMemcpyAsync(g->src_deg_sorted.data(), g->src_deg, sizeof(int32_t) * size_t(n_src),
-                           cudaMemcpyDeviceToHost, s));
-        g->device_bytes += sizeof(int32_t) * n_src;
-    }
     CK(cudaStreamSynchronize(s));   // host vectors die at return
-    std::sort(g->src_deg_sorted.begin(), g->src_deg_sorted.end(), std::greater<int32_t>());
     if (dflags) cudaFree(dflags);
     if (seen) cudaFree(seen);
     *out = g;
@@ -319,7 +288,6 @@ fail:
 extern "C" fg_status fg_graph_destroy(fg_graph* g) {
     if (!g) return fgk::set_error(FG_EINVAL, "fg_graph_destroy: NULL handle");
     if (g->rows_by_deg) cudaFree(g->rows_by_deg);
-    if (g->src_deg) cudaFree(g->src_deg);
     if (g->unit_row) cudaFree(g->unit_row);
     if (g->unit_p0) cudaFree(g->unit_p0);
     for (auto& su : g->seg_units) {

@@ -22,7 +22,6 @@
 #include <cstdlib>
 
 #include "fg_internal.h"
-#include "ldpol.cuh"
 
 namespace {
 
@@ -49,9 +48,6 @@ struct Args {
     int c4base;       // first float4 column of this pass (feature-dimension tiling, H == 1)
     int accumulate;   // pass > 0: out += partial
     int tile4;        // float4 columns per pass (0: one pass over all F4)
-    const int32_t* src_deg;   // hot-source L2 policy (ldpol.cuh): src_deg[u] >= hot_thr -> evict_last
-    int hot_thr;              // INT32_MAX: policy off
-    int hot_cold;             // cold-row policy kind (ldpol.cuh policy_cold)
 };
 
 __device__ __forceinline__ float dot4(const float4& a, const float4& b) {
@@ -123,9 +119,6 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
     const bool stage = (H * B <= CAP);
     int* idx = s_idx[gi];
     float* res = s_res[gi];
-    // hot-source policy: only where the whole warp gathers one source row per load
-    const bool hotpol = (G == 32) && A.hot_thr != INT32_MAX;
-    const uint64_t pol_hot = fgpol::policy_evict_last(), pol_cold = fgpol::policy_cold(A.hot_cold);
 
     float4 y0[NV];
     const float4* yr = Y + v * F4;
@@ -138,10 +131,7 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
     for (int64_t p0 = s; p0 < e; p0 += B) {
         const int cnt = int(min((int64_t)B, e - p0));
         __syncwarp(mask);
-        for (int t = gl; t < cnt; t += G) {
-            const int u = __ldg(A.col_idx + p0 + t);
-            idx[t] = (hotpol && __ldg(A.src_deg + u) >= A.hot_thr) ? (u | fgpol::HOT_BIT) : u;
-        }
+        for (int t = gl; t < cnt; t += G) idx[t] = __ldg(A.col_idx + p0 + t);
         __syncwarp(mask);
         for (int t0 = 0; t0 < cnt; t0 += U) {
             float4 x[U][NV];
@@ -149,22 +139,12 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
                 const int t = t0 + uu;
-                const int raw = (t < cnt) ? idx[t] : 0;
-                us[uu] = raw & fgpol::IDX_MASK;
+                us[uu] = (t < cnt) ? idx[t] : 0;
                 const float4* xr = X + int64_t(us[uu]) * F4;
-                if (hotpol) {   // warp-uniform: G == 32, every lane loads edge t's row
-                    const uint64_t pol = raw < 0 ? pol_hot : pol_cold;
 #pragma unroll
-                    for (int j = 0; j < NV; ++j) {
-                        const int c = A.c4base + gl + G * j;
-                        x[uu][j] = (t < cnt && c < F4) ? fgpol::ldg_policy(xr + c, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < NV; ++j) {
-                        const int c = A.c4base + gl + G * j;
-                        x[uu][j] = (t < cnt && c < F4) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
+                for (int j = 0; j < NV; ++j) {
+                    const int c = A.c4base + gl + G * j;
+                    x[uu][j] = (t < cnt && c < F4) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
             if constexpr (MODE == MODE_H1 || MODE == MODE_HEADS) {
@@ -318,9 +298,6 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     A.c4base = 0;
     A.accumulate = 0;
     A.tile4 = 0;
-    A.src_deg = g->src_deg;
-    A.hot_thr = fgk::hot_threshold(g, int64_t(H) * D * 4);
-    A.hot_cold = fgk::hot_cold_kind();
     int F4 = A.F4;
     const float4* X4 = reinterpret_cast<const float4*>(X);
     const float4* Y4 = reinterpret_cast<const float4*>(Y);
@@ -337,7 +314,6 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
             int t4 = 32;
             while (t4 > 1 && g->n_src * int64_t(t4) * 16 > budget) t4 /= 2;
             A.tile4 = t4;
-            A.hot_thr = INT32_MAX;   // each pass's slice fits the L2 budget
             for (int c4 = 0; c4 < F4; c4 += t4) {
                 A.c4base = c4;
                 A.accumulate = c4 > 0;

@@ -87,10 +87,6 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     }
     const int64_t NG = THREADS / G;
     A.n_heavy = rows_with_degree_at_least(g, NG * 32);
-    A.src_deg = g->src_deg;
-    // hot-source L2 policy for the untiled gathers of rows wider than the budget
-    A.hot_thr = (F4 == A.F4) ? fgk::hot_threshold(g, int64_t(A.F4) * 16) : INT32_MAX;
-    A.hot_cold = fgk::hot_cold_kind();
     const int opset = (op == OP_UADDE || op == OP_COPYE) ? 1 : 0;
     switch (mx) {
         case R_MAX: return opset ? dispatch_inst<R_MAX, 1>(A, G, NV, op, st) : dispatch_inst<R_MAX, 0>(A, G, NV, op, st);

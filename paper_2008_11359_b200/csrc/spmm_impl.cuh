@@ -2,7 +2,6 @@
 // spmm.cu), instantiated per (reducer, op set) by spmm_inst_*.cu.
 #pragma once
 #include "fg_internal.h"
-#include "ldpol.cuh"
 
 namespace fgspmm {
 
@@ -33,9 +32,6 @@ struct Args {
     float4* out;
     int4* arg_u;
     int4* arg_e;
-    const int32_t* src_deg;     // hot-source L2 policy (ldpol.cuh): src_deg[u] >= hot_thr -> evict_last
-    int hot_thr;                // INT32_MAX: off
-    int hot_cold;               // cold-row policy kind (ldpol.cuh policy_cold)
 };
 
 __device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); }
@@ -54,9 +50,6 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
     constexpr int U = NV >= 4 ? 2 : (NV >= 2 ? 4 : 8);      // edges in flight per lane
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);     // select-type reducers
     const int F4 = A.F4;
-    // hot-source policy only where a whole warp loads one source row (G == 32)
-    const bool hotpol = (G == 32) && (OP != OP_COPYE) && A.hot_thr != INT32_MAX;
-    const uint64_t pol_hot = fgpol::policy_evict_last(), pol_cold = fgpol::policy_cold(A.hot_cold);
     for (int64_t p0 = s; p0 < e; p0 += B) {
         const int cnt = int(min((int64_t)B, e - p0));
         int uix[R];
@@ -65,7 +58,6 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
         for (int r = 0; r < R; ++r) {
             const int64_t p = p0 + gl + r * G;
             uix[r] = (OP != OP_COPYE && p < e) ? __ldg(A.col_idx + p) : 0;   // copy_e reads no source row
-            if (hotpol && p < e && __ldg(A.src_deg + uix[r]) >= A.hot_thr) uix[r] |= fgpol::HOT_BIT;
             if constexpr (OP != OP_COPY) eix[r] = (p < e) ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
         }
         // u_mul_e with identity edge ids: the batch's E rows are one contiguous span;
@@ -90,9 +82,7 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
                 const int t = t0 + uu;
-                const int raw = __shfl_sync(mask, uix[t / G], t % G, G);
-                const int u = raw & fgpol::IDX_MASK;
-                const uint64_t pol = raw < 0 ? pol_hot : pol_cold;   // warp-uniform when hotpol
+                const int u = __shfl_sync(mask, uix[t / G], t % G, G);
                 int ed = 0;
                 if constexpr (OP != OP_COPY) ed = __shfl_sync(mask, eix[t / G], t % G, G);
                 const float4* xr = (OP == OP_COPYE) ? reinterpret_cast<const float4*>(A.E) + int64_t(ed) * F4
@@ -101,7 +91,7 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                 for (int j = 0; j < NV; ++j) {
                     const int c = c4base + gl + G * j;
                     const bool ok = (t < cnt) && (c < F4);
-                    x[uu][j] = !ok ? f4(0.f) : (hotpol ? fgpol::ldg_policy(xr + c, pol) : __ldg(xr + c));
+                    x[uu][j] = ok ? __ldg(xr + c) : f4(0.f);
                     if constexpr (OP == OP_UMULE) {
                         const int h = (4 * c) / A.D;
                         ev[uu][j][0] = !ok ? 0.f : (staged ? etile[t * A.H + h] : __ldg(A.E + int64_t(ed) * A.H + h));

@@ -11,7 +11,6 @@ import gen  # noqa: E402
 import paper_2008_11359_b200 as fgp  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "reddit"
-mode = sys.argv[2] if len(sys.argv) > 2 else "tile"
 g = gen.make_graph(name)
 G = fgp.Graph(torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col_idx).cuda())
 n, m = g.n_dst, g.nnz
@@ -30,7 +29,7 @@ def timeit(fn, reps=5):
 
 
 def setenv(**kw):
-    for k in ("FG_L2_TILE_MB", "FG_SDDMM_L2_TILE", "FG_SDDMM_SEGMENT", "FG_HOT_MB", "FG_HOT_COLD"):
+    for k in ("FG_L2_TILE_MB", "FG_SDDMM_L2_TILE", "FG_SDDMM_SEGMENT"):
         os.environ.pop(k, None)
     for k, v in kw.items():
         os.environ[k] = str(v)
@@ -39,21 +38,6 @@ def setenv(**kw):
 X = torch.rand(n, 512, device="cuda")
 out = torch.empty(n, 512, device="cuda")
 s1 = torch.empty(m, 1, device="cuda")
-if mode == "hot":
-    X256 = torch.rand(n, 256, device="cuda") * 0.25
-    s8 = torch.empty(m, 8, device="cuda")
-    o256 = torch.empty(n, 256, device="cuda")
-    for mb, cold in [(0, 0), (32, 0), (64, 0), (96, 0), (32, 2), (64, 2), (96, 2), (64, 1)]:
-        setenv(FG_HOT_MB=mb, FG_HOT_COLD=cold)
-        r = [timeit(lambda: fgp.sddmm(G, X, H=1, out=s1)),
-             timeit(lambda: fgp.sddmm(G, X256, H=8, out=s8)),
-             timeit(lambda: fgp.spmm(G, "u_mul_e", "sum", X256, H=8, E=s8, out=o256)),
-             timeit(lambda: fgp.gat_attention(G, X256, H=8, out=o256))]
-        setenv(FG_HOT_MB=mb, FG_HOT_COLD=cold, FG_L2_TILE_MB=0)
-        r.append(timeit(lambda: fgp.spmm(G, "copy_u", "sum", X, out=out)))
-        print(f"hot_mb={mb:4d} cold={cold}  sddmm_H1_F512 {r[0]:7.3f}  sddmm_H8 {r[1]:7.3f}  u_mul_e_H8 {r[2]:7.3f}  "
-              f"gat_fused {r[3]:7.3f}  copy_u_F512_untiled {r[4]:7.3f} ms", flush=True)
-    sys.exit(0)
 for mb in (0, 16, 24, 32, 48, 64, 96, 128):
     setenv(FG_L2_TILE_MB=mb)
     print(f"copy_u_sum F512 tile_mb={mb:4d}  {timeit(lambda: fgp.spmm(G, 'copy_u', 'sum', X, out=out)):7.3f} ms", flush=True)
