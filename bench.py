@@ -144,6 +144,21 @@ def gpu_id_for_smi(local_rank: int) -> str:
     return str(local_rank)
 
 
+class L2Flush:
+    """Write a 256 MB buffer (2x the 126 MB L2), then read it back: afterwards the
+    L2 holds only clean flush lines, so no write-back of the flush itself lands
+    inside the next timed region."""
+
+    def __init__(self, torch):
+        self.torch = torch
+        self.buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        self.sink = torch.empty((), dtype=torch.float32, device="cuda")
+
+    def fill_(self, v: float):
+        self.buf.fill_(v)
+        self.torch.sum(self.buf, 0, out=self.sink)
+
+
 # ----------------------------------------------------------------- the GPU step
 class Step:
     """Device-resident state of one rank and the enqueue of one hot-path step."""
@@ -216,8 +231,9 @@ class Step:
 
     def enqueue_pipelined(self, ins_h, w_h, outs_h, h2d, d2h):
         """The same step for the end-to-end leg, with the host copies overlapped:
-        H2D of each input on stream h2d (smallest first), each op on self.stream
-        as soon as its input has arrived (ops ordered by input size), and the D2H
+        H2D of each input on stream h2d (in the order the ops need them), each op
+        on self.stream as soon as its input has arrived (smallest inputs first,
+        the smallest result last), and the D2H
         of each op's results on stream d2h as soon as that op is done.  Callers
         make h2d / d2h wait on the start event and self.stream wait on d2h at
         the end."""
@@ -225,7 +241,7 @@ class Step:
         G, X, lo, nl = self.G, self.X, self.lo, self.nl
         arrived = {}
         with torch.cuda.stream(h2d):
-            for key in ("X8", "X128", "X256", "X512"):
+            for key in ("X8", "X128", "X512", "X256"):
                 X[key][lo:lo + nl].copy_(ins_h[key], non_blocking=True)
                 if key == "X8":
                     self.W.copy_(w_h, non_blocking=True)
@@ -252,16 +268,16 @@ class Step:
         ready("X128")
         fgp.spmm(G, "copy_u", "max", X["X128"], out=self.o128, arg_u=self.au128, arg_e=self.ae128, stream=st)
         ship([self.o128, self.au128, self.ae128])
-        ready("X256")
-        fgp.sddmm(G, X["X256"], self.ydst("X256"), H=H_GAT, out=self.s8, stream=st)
-        fgp.edge_softmax(G, self.s8, H=H_GAT, out=self.s8, stream=st)
-        fgp.spmm(G, "u_mul_e", "sum", X["X256"], H=H_GAT, E=self.s8, out=self.o256, stream=st)
-        ship([self.o256])
         ready("X512")
         fgp.spmm(G, "copy_u", "sum", X["X512"], out=self.out512, stream=st)
         ship([self.out512])
         fgp.sddmm(G, X["X512"], self.ydst("X512"), H=1, out=self.s1, stream=st)
         ship([self.s1])
+        ready("X256")   # the GAT chain last: the smallest result (n x 256) is the D2H tail
+        fgp.sddmm(G, X["X256"], self.ydst("X256"), H=H_GAT, out=self.s8, stream=st)
+        fgp.edge_softmax(G, self.s8, H=H_GAT, out=self.s8, stream=st)
+        fgp.spmm(G, "u_mul_e", "sum", X["X256"], H=H_GAT, E=self.s8, out=self.o256, stream=st)
+        ship([self.o256])
 
     def outputs(self):
         return [self.out512, self.s1, self.o256, self.o128, self.au128, self.ae128, self.omlp, self.aumlp,
@@ -366,7 +382,7 @@ def main():
     stream = torch.cuda.Stream()
     S = Step(g, shard, host, comm, stream)
     S.total_bytes = sum(op_bytes(g.n_dst, g.nnz).values())
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    flush = L2Flush(torch)
 
     def sync_all():
         torch.cuda.synchronize()
@@ -453,7 +469,8 @@ def main():
                         "u_mul_e-sum), copy_u-max F128+argmax, mlp-max d1=8 d2=128+argmax",
             "graph": GRAPH, "n": g.n_dst, "nnz": g.nnz,
             "parallelism": f"dst-row shards x{world} + NCCL all-gather of X" if world > 1 else "single GPU",
-            "l2": "flushed before every timed step (256 MB write, outside the events)",
+            "l2": "flushed before every timed step, outside the events: 256 MB write (2x the L2) then a "
+                  "read of it, so the flush's dirty lines are written back before the step starts",
             "bytes_per_step": total_bytes,
         },
         "ops_ms": {k: round(v, 4) for k, v in op_ms.items()},

@@ -128,10 +128,21 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
         y0[j] = (c < F4) ? __ldg(yr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
+    constexpr int PF = (B + G - 1) / G;   // running sums per lane in a tiled pass (H == 1)
     for (int64_t p0 = s; p0 < e; p0 += B) {
         const int cnt = int(min((int64_t)B, e - p0));
         __syncwarp(mask);
         for (int t = gl; t < cnt; t += G) idx[t] = __ldg(A.col_idx + p0 + t);
+        // column-tiled pass k > 0 (H == 1): fetch the batch's running sums now, so the
+        // read-modify-write at the end of the batch does not wait a DRAM round trip
+        float prev[PF];
+        if (A.accumulate) {
+#pragma unroll
+            for (int k = 0; k < PF; ++k) {
+                const int q = gl + G * k;
+                prev[k] = (q < cnt) ? out[A.eid ? int64_t(__ldg(A.eid + p0 + q)) : p0 + q] : 0.f;
+            }
+        }
         __syncwarp(mask);
         for (int t0 = 0; t0 < cnt; t0 += U) {
             float4 x[U][NV];
@@ -237,17 +248,19 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
         if (stage) {   // coalesced write-back of the batch's results
             __syncwarp(mask);
             const int tot = cnt * H;
-            if (A.eid == nullptr) {
+            if (A.accumulate) {   // H == 1: q == t
+#pragma unroll
+                for (int k = 0; k < PF; ++k) {
+                    const int q = gl + G * k;
+                    if (q < cnt) out[A.eid ? int64_t(__ldg(A.eid + p0 + q)) : p0 + q] = prev[k] + res[q];
+                }
+            } else if (A.eid == nullptr) {
                 float* o = out + p0 * H;
-                if (A.accumulate)
-                    for (int q = gl; q < tot; q += G) o[q] += res[q];
-                else
-                    for (int q = gl; q < tot; q += G) o[q] = res[q];
+                for (int q = gl; q < tot; q += G) o[q] = res[q];
             } else {
                 for (int q = gl; q < tot; q += G) {
                     const int t = q / H, h = q - t * H;
-                    float* o = out + int64_t(__ldg(A.eid + p0 + t)) * H + h;
-                    *o = A.accumulate ? *o + res[q] : res[q];
+                    out[int64_t(__ldg(A.eid + p0 + t)) * H + h] = res[q];
                 }
             }
         }

@@ -40,6 +40,13 @@ __device__ __forceinline__ void set_comp(float4& v, int k, float a) {
     if (k == 0) v.x = a; else if (k == 1) v.y = a; else if (k == 2) v.z = a; else v.w = a;
 }
 
+// u_mul_e stages each 32-edge batch's E rows in shared memory (NG x 512 floats)
+// where the static shared-memory budget allows it alongside the heavy-row combine
+template <int G, int OP, int RED>
+constexpr bool stage_e() {
+    return OP == OP_UMULE && (G == 32 || (G == 16 && RED != R_MAX && RED != R_MIN));
+}
+
 // Accumulate edges [s, e) of one row into (acc, pos) for this lane's NV chunks.
 template <int G, int NV, int OP, int RED>
 __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e, int gl, unsigned mask,
@@ -64,7 +71,7 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
         // stage it in shared memory with coalesced loads instead of one dependent
         // scalar load per edge and chunk
         bool staged = false;
-        if constexpr (OP == OP_UMULE && G == 32) {
+        if constexpr (stage_e<G, OP, RED>()) {
             if (A.eid == nullptr && A.H <= 16) {
                 staged = true;
                 __syncwarp(mask);
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     constexpr int NG = THREADS / G;                 // groups per CTA
     constexpr int TW = G * NV;                      // float4 columns per tile
     __shared__ float4 s_acc[MAX ? 1 : NG][MAX ? 1 : TW];
-    __shared__ float s_etile[(OP == OP_UMULE && G == 32) ? NG : 1][(OP == OP_UMULE && G == 32) ? 32 * 16 : 1];
+    __shared__ float s_etile[stage_e<G, OP, RED>() ? NG : 1][stage_e<G, OP, RED>() ? 32 * 16 : 1];
     __shared__ float s_val[MAX ? NG : 1][MAX ? TW * 4 : 1];
     __shared__ int s_pos[MAX ? NG : 1][MAX ? TW * 4 : 1];
 

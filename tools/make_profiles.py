@@ -81,7 +81,7 @@ if os.path.exists(lp):
         if "FillFunctor" in k:
             segs.append(cur)
             cur = []
-        else:
+        elif not k.startswith("void at::"):   # the flush's read-back reduction is not a step kernel
             cur.append((k, v))
     segs.append(cur)
     step = [sg for sg in segs if len(sg) >= 7][-1]   # last full step (extras follow it)
