@@ -76,20 +76,10 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
             F4 = int(t4);            // tile width drives (G, NV) below; the kernel tiles A.F4 by G*NV
         }
     }
-    const char* mp = getenv("FG_SPMM_MAP");
-    const int map = mp ? atoi(mp) : 1;
-    if (map == 1) {
-        // wide lanes: 4 float4 (64 B) per lane per edge wherever the width allows, so
-        // the per-edge index shuffle / address / bounds work is amortised over 4 loads
-        if (F4 <= 4) {
-            G = 1;
-            NV = F4;
-        } else {
-            NV = 4;
-            G = 2;
-            while (G * 4 < F4 && G < 32) G *= 2;
-        }
-    } else if (F4 <= 32) {   // map 0: one float4 per lane up to 32 lanes
+    // one float4 per lane up to 32 lanes, then 2-4 float4 per lane (measured: wider
+    // lanes -- G x 4 float4 at every width -- were 1.3-3x slower on reddit at
+    // F = 32..512: fewer lanes per row exposes more gather latency per row)
+    if (F4 <= 32) {
         NV = 1;
         G = 1;
         while (G < F4) G *= 2;

@@ -41,10 +41,10 @@ __device__ __forceinline__ void set_comp(float4& v, int k, float a) {
 }
 
 // u_mul_e stages each 32-edge batch's E rows in shared memory (NG x 512 floats)
-// where the static shared-memory budget allows it alongside the heavy-row combine
+// when a whole warp owns the row (G == 32)
 template <int G, int OP, int RED>
 constexpr bool stage_e() {
-    return OP == OP_UMULE && (G == 32 || (G == 16 && RED != R_MAX && RED != R_MIN));
+    return OP == OP_UMULE && G == 32;
 }
 
 // Accumulate edges [s, e) of one row into (acc, pos) for this lane's NV chunks.

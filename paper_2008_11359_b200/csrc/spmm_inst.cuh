@@ -22,19 +22,8 @@ fg_status inst_op(const Args& A, int op, cudaStream_t st) {
 
 template <>
 fg_status dispatch_inst<FG_RED, FG_OPSET>(const Args& A, int G, int NV, int op, cudaStream_t st) {
-    // (G, NV) pairs chosen by launch_spmm_gather (spmm.cu); both column maps
-    if (NV == 4) {
-        switch (G) {
-            case 1: return inst_op<1, 4>(A, op, st);
-            case 2: return inst_op<2, 4>(A, op, st);
-            case 4: return inst_op<4, 4>(A, op, st);
-            case 8: return inst_op<8, 4>(A, op, st);
-            case 16: return inst_op<16, 4>(A, op, st);
-            default: return inst_op<32, 4>(A, op, st);
-        }
-    }
-    switch (G) {
-        case 1: return NV == 1 ? inst_op<1, 1>(A, op, st) : NV == 2 ? inst_op<1, 2>(A, op, st) : inst_op<1, 3>(A, op, st);
+    switch (G) {   // the (G, NV) pairs launch_spmm_gather (spmm.cu) chooses
+        case 1: return inst_op<1, 1>(A, op, st);
         case 2: return inst_op<2, 1>(A, op, st);
         case 4: return inst_op<4, 1>(A, op, st);
         case 8: return inst_op<8, 1>(A, op, st);
@@ -42,7 +31,8 @@ fg_status dispatch_inst<FG_RED, FG_OPSET>(const Args& A, int G, int NV, int op, 
         default:
             if (NV == 1) return inst_op<32, 1>(A, op, st);
             if (NV == 2) return inst_op<32, 2>(A, op, st);
-            return inst_op<32, 3>(A, op, st);
+            if (NV == 3) return inst_op<32, 3>(A, op, st);
+            return inst_op<32, 4>(A, op, st);
     }
 }
 
