@@ -484,6 +484,25 @@ def test_l2_column_tiling(skewed, F, monkeypatch):
     check_close(s0, ref, ab, TOL, f"untiled u_dot_v F={F}")
 
 
+@pytest.mark.parametrize("H,D", [(1, 512), (1, 128), (8, 32), (2, 4)])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_sddmm_source_segmented(skewed, skewed_eid, H, D, use_eid, monkeypatch):
+    """Row f3: force the source-segmented persistent SDDMM (1 MB segments ->
+    several segments even on the small test graph) and compare with the oracle."""
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    monkeypatch.setenv("FG_SDDMM_SEG_MB", "1")
+    X = feats((g.n_src, H * D), 980 + D, gen.REAL)
+    Y = feats((g.n_dst, H * D), 981 + D, gen.REAL)
+    out = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+    ref, ab = oracle.sddmm(g.row_ptr, g.col_idx, X, Y, H=H)
+    pos = np.arange(g.nnz) if g.eid is None else g.eid
+    check_close(out[pos], ref, ab, TOL, f"segmented u_dot_v H={H} D={D}")
+    monkeypatch.setenv("FG_SDDMM_PERSIST", "1")   # one CTA per SM: every group walks many units
+    out1 = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+    assert np.array_equal(out1, out)              # same per-edge arithmetic, any schedule
+
+
 # ------------------------------------------------------------------ fused GAT (f2)
 @pytest.mark.parametrize("H,D", [(8, 32), (4, 16), (2, 4), (1, 128), (8, 64), (1, 16)])
 @pytest.mark.parametrize("use_eid", [False, True])

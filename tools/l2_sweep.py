@@ -29,7 +29,7 @@ def timeit(fn, reps=5):
 
 
 def setenv(**kw):
-    for k in ("FG_L2_TILE_MB", "FG_SDDMM_L2_TILE", "FG_SDDMM_SEGMENT"):
+    for k in ("FG_L2_TILE_MB", "FG_SDDMM_L2_TILE", "FG_SDDMM_SEGMENT", "FG_SDDMM_PERSIST", "FG_SDDMM_SEG_MB"):
         os.environ.pop(k, None)
     for k, v in kw.items():
         os.environ[k] = str(v)
@@ -38,14 +38,19 @@ def setenv(**kw):
 X = torch.rand(n, 512, device="cuda")
 out = torch.empty(n, 512, device="cuda")
 s1 = torch.empty(m, 1, device="cuda")
-for mb in (0, 16, 24, 32, 48, 64, 96, 128):
+only_sddmm = "--sddmm" in sys.argv
+for mb in (() if only_sddmm else (0, 16, 24, 32, 48, 64, 96, 128)):
     setenv(FG_L2_TILE_MB=mb)
     print(f"copy_u_sum F512 tile_mb={mb:4d}  {timeit(lambda: fgp.spmm(G, 'copy_u', 'sum', X, out=out)):7.3f} ms", flush=True)
 setenv()
 print(f"sddmm H1 F512 untiled          {timeit(lambda: fgp.sddmm(G, X, H=1, out=s1)):7.3f} ms", flush=True)
-for mb in (16, 32, 48, 64, 96, 128):
+for mb in (() if only_sddmm else (16, 32, 48, 64, 96, 128)):
     setenv(FG_L2_TILE_MB=mb, FG_SDDMM_L2_TILE=1)
     print(f"sddmm H1 F512 coltile mb={mb:4d}  {timeit(lambda: fgp.sddmm(G, X, H=1, out=s1)):7.3f} ms", flush=True)
-for mb in (16, 32, 64, 128):
-    setenv(FG_L2_TILE_MB=mb, FG_SDDMM_SEGMENT=1)
-    print(f"sddmm H1 F512 segment mb={mb:4d}  {timeit(lambda: fgp.sddmm(G, X, H=1, out=s1)):7.3f} ms", flush=True)
+X256 = torch.rand(n, 256, device="cuda")
+s8 = torch.empty(m, 8, device="cuda")
+for mb in (0, 24, 32, 48, 64, 96):
+    setenv(FG_SDDMM_SEG_MB=mb)
+    t1 = timeit(lambda: fgp.sddmm(G, X, H=1, out=s1))
+    t8 = timeit(lambda: fgp.sddmm(G, X256, H=8, out=s8))
+    print(f"sddmm segmented persistent seg_mb={mb:4d}  H1 F512 {t1:7.3f} ms   H8 D32 {t8:7.3f} ms", flush=True)

@@ -10,6 +10,9 @@ if op == "mlp":
     X8 = torch.rand(n, 8, device="cuda"); W = torch.rand(8, 128, device="cuda") - 0.5
     o = torch.empty(n, 128, device="cuda"); au = torch.empty(n, 128, dtype=torch.int32, device="cuda")
     for _ in range(3): fgp.spmm(G, "mlp", "max", X8, W=W, out=o, arg_u=au)
+elif op == "sddmm512":
+    X = torch.rand(n, 512, device="cuda"); s1 = torch.empty(g.nnz, 1, device="cuda")
+    for _ in range(2): fgp.sddmm(G, X, H=1, out=s1)
 elif op == "gat":
     X = torch.rand(n, 256, device="cuda") * 0.25; o = torch.empty(n, 256, device="cuda")
     for _ in range(3): fgp.gat_attention(G, X, H=8, out=o)
