@@ -82,9 +82,12 @@ fg_status get_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t s
 
 // L2 budget (bytes) for feature-dimension tiling of the gathered operand;
 // FG_L2_TILE_MB overrides the default (64 MiB, half the 126 MB L2), 0 disables.
+// column-tile budget of the copy_u gather (FG_L2_TILE_MB, default 32: on reddit
+// 32 MB tiles beat 64 MB for F = 128 sum / max (3.49 / 4.79 vs 3.63 / 5.46 ms) and
+// tie at F = 512; 24 MB and below drop to 4-lane groups and lose)
 inline int64_t l2_tile_budget() {
     const char* e = getenv("FG_L2_TILE_MB");
-    return int64_t(e ? atoi(e) : 64) << 20;
+    return int64_t(e ? atoi(e) : 32) << 20;
 }
 
 inline int num_sms() {
