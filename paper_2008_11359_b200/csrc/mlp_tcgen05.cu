@@ -65,6 +65,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// wait with back-off, for the producer and MMA warps: they run ahead of the
+// epilogue and would otherwise spin on try_wait, taking issue slots from the
+// epilogue warps that share their SM sub-partition (measured: 27 % of all issued
+// instructions were SYNCS / YIELD / BRA spin iterations)
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, int ns) {
+    uint32_t ok = 0;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (ok) break;
+        __nanosleep(ns);
+    }
+}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -167,8 +182,9 @@ struct Args {
     int d_in, d2;
     const float* Xhi;     // [n_src][KS*8] tf32 hi part of X (workspace)
     const float* Xlo;     // [n_src][KS*8] tf32 lo part
-    int dbg;              // FG_MLP_DBG bits (pipeline experiments): 1 skip epilogue math, 2 skip gathers,
-                          // 4 skip MMAs, 8 skip TMEM loads (results are then wrong; timing only)
+    int backoff_ns;       // producer / MMA wait back-off (FG_MLP_BACKOFF_NS)
+    int dbg;              // FG_MLP_DBG bits (pipeline experiments): 2 skip gathers, 4 skip MMAs
+                          // (results are then wrong; timing only)
 };
 
 template <int KS>
@@ -186,11 +202,15 @@ struct Smem {
 };
 
 // Epilogue state of one thread (= one feature column i of the CTA's M tile).
+// Edge positions are 32-bit offsets from the CTA's first edge E0 (a CTA owns a
+// contiguous CSR range), so the per-chunk row bookkeeping is 32-bit integer work.
 template <int KS, bool MAX>
 struct Epi {
     const Args* A;
-    int64_t r, r_hi, rs, re;
-    int64_t nre;      // prefetched row_ptr[r + 2]
+    int64_t r, r_hi;  // current row, end of the CTA's rows
+    int64_t E0;       // CSR position of the CTA's first edge
+    int rs, re;       // current row's edge range, relative to E0
+    int nre;          // prefetched end of row r + 1 (relative)
     float best, q;
     int bu, be;       // winning edge: source id / edge id (from the smem-staged tile indices)
     int fu, fe;       // first edge of the row (the winner when every message is +0)
@@ -207,7 +227,7 @@ struct Epi {
             const float* xv = A->Xd + rn * A->d_in;
 #pragma unroll
             for (int k = 0; k < KS * 8; ++k) nx[k] = (k < A->d_in) ? __ldg(xv + k) : 0.f;
-            nre = __ldg(A->row_ptr + rn + 1);   // end of row rn (rn < r_hi <= n_dst)
+            nre = int(__ldg(A->row_ptr + rn + 1) - E0);   // end of row rn (rn < r_hi <= n_dst)
         }
     }
     __device__ __forceinline__ void start_row() {
@@ -249,58 +269,81 @@ struct Epi {
             start_row();
         }
     }
-    // consume 32 accumulator columns for CSR positions [pc0, pc0 + nvalid);
-    // su / se: source ids / edge ids of those 32 positions (shared memory)
-    __device__ __forceinline__ void consume(const uint32_t (&v)[32], int64_t pc0, int nvalid, const int* su,
-                                            const int* se) {
+    // the 32 columns of a chunk that lies inside the current row (the common case)
+    __device__ __forceinline__ void consume_full(const uint32_t (&v)[32], const int* su, const int* se) {
+        if (MAX) {
+            if (fresh) {
+                fu = su[0];
+                fe = se[0];
+                fresh = false;
+            }
+            // the chunk maximum by a 3-input max tree (FMNMX3); the first column
+            // attaining it is searched only when it beats the running best (strict:
+            // ties keep the earlier winner), skipped when no feature of the warp improves
+            float t[11];
+#pragma unroll
+            for (int j = 0; j < 10; ++j)
+                t[j] = fmaxf(fmaxf(__uint_as_float(v[3 * j]), __uint_as_float(v[3 * j + 1])),
+                             __uint_as_float(v[3 * j + 2]));
+            t[10] = fmaxf(__uint_as_float(v[30]), __uint_as_float(v[31]));
+            const float m = fmaxf(fmaxf(fmaxf(fmaxf(t[0], t[1]), t[2]), fmaxf(fmaxf(t[3], t[4]), t[5])),
+                                  fmaxf(fmaxf(fmaxf(t[6], t[7]), t[8]), fmaxf(t[9], t[10])));
+            const bool imp = m > best;
+            if (__any_sync(0xffffffffu, imp)) {
+                if (imp) {
+                    int k = 31;
+#pragma unroll
+                    for (int c = 30; c >= 0; --c) k = (__uint_as_float(v[c]) == m) ? c : k;
+                    best = m;
+                    bu = su[k];
+                    be = se[k];
+                }
+            }
+        } else {
+            float sm[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int c = 0; c < 32; c += 4)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) sm[k] += fmaxf(__uint_as_float(v[c + k]) + q, 0.f);
+            best += (sm[0] + sm[1]) + (sm[2] + sm[3]);
+        }
+    }
+    // general case: chunk at relative position pc with nvalid valid columns,
+    // possibly spanning row boundaries
+    __device__ __forceinline__ void consume_split(const uint32_t (&v)[32], int pc, int nvalid, const int* su,
+                                               const int* se) {
         int c0 = 0;
         while (c0 < nvalid) {
-            while (pc0 + c0 >= re) advance();
-            const int c1 = int(min(int64_t(nvalid), re - pc0));
+            while (pc + c0 >= re) advance();
+            const int c1 = min(nvalid, re - pc);
             if (MAX && fresh) {
                 fu = su[c0];
                 fe = se[c0];
                 fresh = false;
             }
             if (MAX) {
-                // two interleaved partial maxima for ILP; ties -> lowest column
-                float b0 = -INFINITY, b1 = -INFINITY;
-                int k0 = 0, k1 = 0;
-                if (c0 == 0 && c1 == 32) {
+                float b0 = -INFINITY;   // ties -> lowest column
+                int k0 = 0;
 #pragma unroll
-                    for (int c = 0; c < 32; c += 2) {
-                        const float x0 = __uint_as_float(v[c]), x1 = __uint_as_float(v[c + 1]);
-                        if (x0 > b0) { b0 = x0; k0 = c; }
-                        if (x1 > b1) { b1 = x1; k1 = c + 1; }
-                    }
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 32; c += 2) {
-                        const float x0 = __uint_as_float(v[c]), x1 = __uint_as_float(v[c + 1]);
-                        if (c >= c0 && c < c1 && x0 > b0) { b0 = x0; k0 = c; }
-                        if (c + 1 >= c0 && c + 1 < c1 && x1 > b1) { b1 = x1; k1 = c + 1; }
-                    }
+                for (int c = 0; c < 32; ++c) {
+                    const float x = __uint_as_float(v[c]);
+                    if (c >= c0 && c < c1 && x > b0) { b0 = x; k0 = c; }
                 }
-                if (b1 > b0 || (b1 == b0 && k1 < k0)) { b0 = b1; k0 = k1; }
                 if (b0 > best) { best = b0; bu = su[k0]; be = se[k0]; }
             } else {
-                float sm[4] = {0.f, 0.f, 0.f, 0.f};
-                if (c0 == 0 && c1 == 32) {
+                float sm = 0.f;
 #pragma unroll
-                    for (int c = 0; c < 32; c += 4)
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) sm[i] += fmaxf(__uint_as_float(v[c + i]) + q, 0.f);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 32; c += 4)
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            if (c + i >= c0 && c + i < c1) sm[i] += fmaxf(__uint_as_float(v[c + i]) + q, 0.f);
-                }
-                best += (sm[0] + sm[1]) + (sm[2] + sm[3]);
+                for (int c = 0; c < 32; ++c)
+                    if (c >= c0 && c < c1) sm += fmaxf(__uint_as_float(v[c]) + q, 0.f);
+                best += sm;
             }
             c0 = c1;
         }
+    }
+    __device__ __forceinline__ void consume(const uint32_t (&v)[32], int pc, int nvalid, const int* su,
+                                            const int* se) {
+        if (nvalid == 32 && pc >= rs && pc + 32 <= re) consume_full(v, su, se);   // warp-uniform
+        else if (nvalid > 0) consume_split(v, pc, nvalid, su, se);
     }
 };
 
@@ -377,8 +420,8 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         for (int k = 0; k < PF; ++k) load_idx(k, u_pf[k], e_pf[k]);
         auto tile = [&](int t, int (&u_cur)[EPT], int (&e_cur)[EPT]) {
             const int s = t % STAGES, is = t % ISTAGES;
-            mbar_wait(&S.empty[s], ((t / STAGES) & 1) ^ 1);
-            mbar_wait(&S.iempty[is], ((t / ISTAGES) & 1) ^ 1);
+            mbar_wait_backoff(&S.empty[s], ((t / STAGES) & 1) ^ 1, A.backoff_ns);
+            mbar_wait_backoff(&S.iempty[is], ((t / ISTAGES) & 1) ^ 1, A.backoff_ns);
 #pragma unroll
             for (int i = 0; i < EPT; ++i) {
                 const int e = pt + i * NPROD * 32;
@@ -414,9 +457,9 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         if (lane == 0) {
             for (int t = 0; t < ntiles; ++t) {
                 const int s = t % STAGES, b = t % NBUF;
-                mbar_wait(&S.full[s], (t / STAGES) & 1);
+                mbar_wait_backoff(&S.full[s], (t / STAGES) & 1, A.backoff_ns);
                 fence_async_smem();   // cp.async (generic proxy) writes -> tensor-core (async proxy) reads
-                mbar_wait(&S.tempty[b], ((t / NBUF) & 1) ^ 1);
+                mbar_wait_backoff(&S.tempty[b], ((t / NBUF) & 1) ^ 1, A.backoff_ns);
                 tc_fence_after();
                 const uint32_t d = tmem + uint32_t(b * NT);
 #pragma unroll
@@ -443,9 +486,11 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         ep.wc = &S.wcol[0][tid];
         ep.r = r_lo;
         ep.r_hi = r_hi;
+        ep.E0 = E0;
+        ep.rs = ep.re = 0;
         if (r_lo < r_hi) {
-            ep.rs = __ldg(A.row_ptr + r_lo);
-            ep.re = __ldg(A.row_ptr + r_lo + 1);
+            ep.rs = 0;   // row_ptr[r_lo] == E0
+            ep.re = int(__ldg(A.row_ptr + r_lo + 1) - E0);
             ep.prefetch(r_lo);
             ep.start_row();
         }
@@ -457,19 +502,14 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
             tc_fence_after();
             const int* su = S.su[is];
             const int* se = S.se[is];
-            const int64_t tb = E0 + int64_t(t) * NT;
-            const int nv_tile = int(min(int64_t(NT), E1 - tb));
+            const int tb = t * NT;                       // relative to E0
+            const int nv_tile = min(NT, int(E1 - E0) - tb);
 #pragma unroll 1
             for (int ch = 0; ch < NT / 32; ++ch) {   // single-buffered: 4 CTAs per SM supply the overlap
                 uint32_t v0[32];
-                if (!(A.dbg & 8)) {
-                    tmem_ld32(lane_base + uint32_t(b * NT + ch * 32), v0);
-                    tmem_wait_ld(v0);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) v0[q] = 0u;
-                }
-                if (!(A.dbg & 1)) ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)), su + ch * 32, se + ch * 32);
+                tmem_ld32(lane_base + uint32_t(b * NT + ch * 32), v0);
+                tmem_wait_ld(v0);
+                ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)), su + ch * 32, se + ch * 32);
             }
             tc_fence_before();
             mbar_arrive(&S.tempty[b]);
@@ -532,6 +572,8 @@ fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, c
     {
         const char* d = getenv("FG_MLP_DBG");
         A.dbg = d ? atoi(d) : 0;
+        const char* bo = getenv("FG_MLP_BACKOFF_NS");
+        A.backoff_ns = bo ? atoi(bo) : 128;
     }
     A.row_ptr = g->row_ptr;
     A.col_idx = g->col_idx;

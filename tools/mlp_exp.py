@@ -15,6 +15,10 @@ def t(fn, reps=5):
         if i: ts.append(s.elapsed_time(e))
     return np.median(ts)
 for dbg in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "1", "2", "3"]):
-    os.environ["FG_MLP_DBG"] = dbg
+    if dbg.startswith("bo"):   # bo<ns>: back-off sweep with every stage on
+        os.environ["FG_MLP_DBG"] = "0"
+        os.environ["FG_MLP_BACKOFF_NS"] = dbg[2:]
+    else:
+        os.environ["FG_MLP_DBG"] = dbg
     print(f"{sys.argv[1] if len(sys.argv)>1 else 'reddit'} dbg={dbg} max+args {t(lambda: fgp.spmm(G, 'mlp', 'max', X8, W=W, out=o, arg_u=au, arg_e=ae)):.3f} ms"
           f"  sum {t(lambda: fgp.spmm(G, 'mlp', 'sum', X8, W=W, out=o)):.3f} ms")
