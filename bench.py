@@ -144,6 +144,26 @@ def gpu_id_for_smi(local_rank: int) -> str:
     return str(local_rank)
 
 
+def l2_gather_ceiling(torch, buf) -> dict | None:
+    """The L2 gather ceiling of this GPU, measured live (libfgprobe.so,
+    paper_2008_11359_b200/probe/l2_probe.cu): random whole-row reads of an
+    L2-resident 64 MiB X with the kernels' lane mapping, no arithmetic.  The
+    roofline denominator for the gather kernels whose source rows mostly hit L2."""
+    import ctypes
+    path = os.path.join(ROOT, "paper_2008_11359_b200", "lib", "libfgprobe.so")
+    if not os.path.exists(path):
+        return None
+    L = ctypes.CDLL(path)
+    L.fgprobe_l2.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double)]
+    out = (ctypes.c_double * 5)()
+    torch.cuda.synchronize()
+    rc = L.fgprobe_l2(ctypes.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size(), out)
+    if rc != 0:
+        return None
+    return {"gather_2k_rows": round(out[0], 1), "gather_512b_rows": round(out[1], 1),
+            "gather_128b_rows": round(out[2], 1), "stream": round(out[3], 1), "gather_best": round(out[4], 1)}
+
+
 class L2Flush:
     """Write a 256 MB buffer (2x the 126 MB L2), then read it back: afterwards the
     L2 holds only clean flush lines, so no write-back of the flush itself lands
@@ -424,6 +444,8 @@ def main():
     if not args.no_e2e:
         e2e = run_e2e(S, host, args, world, sync_all, flush)
 
+    l2peak = l2_gather_ceiling(torch, flush.buf) if rank == 0 else None
+
     total_bytes = sum(op_bytes(g.n_dst, g.nnz).values())
     local_bytes = op_bytes(S.nl, S.m)
     ob_full = op_bytes(g.n_dst, g.nnz)
@@ -442,13 +464,22 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
+    traffic = l2_bytes = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(dom, {}).get("dram_bytes_per_launch")
+            rec = json.load(open(tp)).get(dom, {})
+            traffic, l2_bytes = rec.get("dram_bytes_per_launch"), rec.get("l2_bytes_per_launch")
         except Exception:
-            traffic = None
+            traffic = l2_bytes = None
+    l2 = None
+    if l2peak and l2_bytes and world == 1:
+        ach = l2_bytes / (dom_ms * 1e-3) / 1e9
+        l2 = {"achieved": round(ach, 1), "peak": l2peak["gather_best"], "unit": "GB/s",
+              "frac": round(ach / l2peak["gather_best"], 4), "probe": l2peak,
+              "note": "achieved = ncu lts__t_sectors x 32 B of one launch (profiles/ncu_traffic.json) / "
+                      "this run's event time; peak = the L2 gather ceiling measured live in this run "
+                      "(libfgprobe: random whole-row reads of an L2-resident X, no arithmetic)"}
     line = {
         "metric": metric_name(),
         "value": total_bytes / (ms * 1e-3) / 1e9,
@@ -485,7 +516,8 @@ def main():
                                     "full width; L2 serves part of them, so achieved/peak can exceed 1; "
                                     "'traffic' is the ncu DRAM bytes of one launch and dram_frac its "
                                     "rate against the same peak",
-                     "dram_frac": (round(traffic / (dom_ms * 1e-3) / 1e9 / peak, 4) if traffic else None)},
+                     "dram_frac": (round(traffic / (dom_ms * 1e-3) / 1e9 / peak, 4) if traffic else None),
+                     "l2": l2},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": Step.LAUNCHES_PER_STEP * args.steps,

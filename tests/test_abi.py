@@ -64,3 +64,15 @@ def test_so_is_sm100a():
         pytest.skip("cuobjdump not available")
     out = subprocess.run(["cuobjdump", "--list-elf", fg.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out, out[:500]
+
+
+def test_probe_lib_loads_and_rejects_bad_args(L):
+    """libfgprobe.so (bench.py's live L2-gather-ceiling probe) is built next to
+    libfg.so, exports its entry point and rejects a too-small buffer before any
+    launch."""
+    path = os.path.join(ROOT, "paper_2008_11359_b200", "lib", "libfgprobe.so")
+    P = ctypes.CDLL(path)
+    P.fgprobe_l2.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double)]
+    out = (ctypes.c_double * 5)()
+    assert P.fgprobe_l2(None, 0, out) != 0
+    assert P.fgprobe_l2(ctypes.c_void_p(256), 1 << 20, out) != 0

@@ -52,7 +52,10 @@ for key, ops in OPS_BY_FILE.items():
         t = num(d.get("gpu__time_duration.sum", ""))
         rd = num(d.get("dram__bytes_read.sum", "")) or 0.0
         wr = num(d.get("dram__bytes_write.sum", "")) or 0.0
+        lts = num(d.get("lts__t_sectors.sum", "").replace(" sector", " byte"))
+        lts = lts * 32 if lts else None
         traffic[op] = {"kernel": d["kernel"], "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                       "l2_bytes_per_launch": lts,
                        "ncu_time_s": t, "dram_gbs": (rd + wr) / t / 1e9 if t else None,
                        "l2_hit_pct": d.get("lts__t_sector_hit_rate.pct")}
         lines += [f"## {op}", "", f"`{d['kernel']}`", "", "| metric | value |", "|---|---|"]
@@ -62,6 +65,8 @@ for key, ops in OPS_BY_FILE.items():
             lines.append(f"| {k} | {v} |")
         if t:
             lines.append(f"| DRAM GB/s (read+write / time) | {(rd + wr) / t / 1e9:.1f} |")
+            if lts:
+                lines.append(f"| L2 GB/s (lts__t_sectors x 32 B / time) | {lts / t / 1e9:.1f} |")
         lines.append(f"| top stall samples | {', '.join(f'{k}={v}' for k, v in d['top_stalls'].items())} |")
         lines.append("")
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)

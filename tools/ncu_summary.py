@@ -7,7 +7,8 @@ WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'lts__throughput.avg.pct_of_peak_sustained_elapsed', 'l1tex__throughput.avg.pct_of_peak_sustained_elapsed',
         'smsp__issue_active.avg.pct_of_peak_sustained_active', 'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active',
         'sm__pipe_tensor_op_tmem_cycles_active.avg.pct_of_peak_sustained_active',
-        'sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active', 'launch__grid_size', 'launch__block_size']
+        'sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active', 'launch__grid_size', 'launch__block_size',
+        'lts__t_sectors.sum', 'l1tex__t_sector_hit_rate.pct']
 def summarise(path):
     out = subprocess.run(['ncu', '-i', path, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
