@@ -151,8 +151,9 @@ fg_status fg_graph_info(const fg_graph* g, fg_graph_info_t* info);
  *   workspace / workspace_bytes: device scratch of >= fg_spmm_workspace_size
  *           bytes, owned by the caller, not used across calls (may be NULL
  *           when that size is 0: copy_u / u_mul_e need none; mlp needs
- *           2 * n_src * ceil(d_in/8) * 8 * 4 + 256 bytes for the tf32 hi/lo
- *           split of X).  Too small -> FG_EINVAL.
+ *           2 * n_src * ceil(d_in/8) * 8 * 4 + n_dst * D * 4 + 512 bytes for
+ *           the tf32 hi/lo split of X and the per-row q_v = x_v W).  Too
+ *           small -> FG_EINVAL.
  *   Errors: FG_EINVAL (null/misaligned pointer, bad enum, arg_* with sum),
  *           FG_ESHAPE (H < 1, D < 1, (H*D) % 4 != 0, mlp with H != 1 or d_in
  *           out of range, u_mul_e/copy_u with d_in != 0), FG_ECUDA.

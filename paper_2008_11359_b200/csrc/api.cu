@@ -46,11 +46,11 @@ extern "C" const char* fg_status_string(fg_status s) {
 extern "C" const char* fg_last_error(void) { return g_err; }
 extern "C" int fg_abi_version(void) { return FG_ABI_VERSION; }
 
-extern "C" fg_status fg_spmm_workspace_size(const fg_graph* g, fg_msg_op msg, fg_reduce_op, int, int, int d_in,
+extern "C" fg_status fg_spmm_workspace_size(const fg_graph* g, fg_msg_op msg, fg_reduce_op, int H, int D, int d_in,
                                             size_t* bytes) {
     if (!g || !bytes) return set_error(FG_EINVAL, "fg_spmm_workspace_size: NULL argument");
-    // gather messages: none (heavy rows combine on chip); mlp: tf32 hi/lo split of X
-    *bytes = (msg == FG_MSG_MLP && d_in > 0) ? fgk::mlp_workspace_bytes(g->n_src, d_in) : 0;
+    // gather messages: none (heavy rows combine on chip); mlp: tf32 hi/lo split of X + q_v = x_v W
+    *bytes = (msg == FG_MSG_MLP && d_in > 0) ? fgk::mlp_workspace_bytes(g->n_src, g->n_dst, d_in, H * D) : 0;
     return FG_OK;
 }
 
@@ -82,9 +82,9 @@ extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
         if (!X_dst && g->n_src != g->n_dst)
             return set_error(FG_ESHAPE, "fg_spmm(mlp): X_dst = NULL needs n_src == n_dst");
         if (E) return set_error(FG_EINVAL, "fg_spmm(mlp): E must be NULL");
-        if (!workspace || workspace_bytes < fgk::mlp_workspace_bytes(g->n_src, d_in))
+        if (!workspace || workspace_bytes < fgk::mlp_workspace_bytes(g->n_src, g->n_dst, d_in, D))
             return set_error(FG_EINVAL, "fg_spmm(mlp): workspace of >= %zu bytes required (fg_spmm_workspace_size)",
-                             fgk::mlp_workspace_bytes(g->n_src, d_in));
+                             fgk::mlp_workspace_bytes(g->n_src, g->n_dst, d_in, D));
     } else {
         if (d_in != 0 || W || X_dst) return set_error(FG_EINVAL, "fg_spmm: W/X_dst/d_in are for mlp only");
         if ((msg == FG_MSG_U_MUL_E || msg == FG_MSG_U_ADD_E || msg == FG_MSG_COPY_E) && !E && g->nnz > 0)

@@ -64,7 +64,7 @@ fg_status launch_spmm_mlp(const fg_graph* g, fg_reduce_op red, int d2, const flo
 fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W,
                                   int d_in, const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e,
                                   void* workspace, cudaStream_t st);
-size_t mlp_workspace_bytes(int64_t n_src, int d_in);
+size_t mlp_workspace_bytes(int64_t n_src, int64_t n_dst, int d_in, int d2);
 fg_status launch_spmm_mlp_simt(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W,
                                int d_in, const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e,
                                cudaStream_t st);

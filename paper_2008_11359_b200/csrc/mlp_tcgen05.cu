@@ -17,17 +17,22 @@
 // (listing fig:schedule-mlp-conv-gpu).  Here, per CTA (persistent,
 // 4 per SM -- four independent pipelines hide the MMA/commit latency -- each
 // owning a contiguous range of destination rows and therefore of CSR edges):
-//   * producer warps gather x_u for NT = 128 edges (L2-resident: n x d1 x 4 B),
-//     split each fp32 into tf32 hi + lo and store the B operand (K-major,
-//     no-swizzle canonical layout) into a 4-stage shared-memory ring;
+//   * producer warp gathers x_u for NT = 64 edges (L2-resident: n x d1 x 4 B),
+//     pre-split into tf32 hi + lo (mlp_split_kernel), with cp.async straight into
+//     the B operand (K-major, no-swizzle canonical layout) of an 8-stage ring;
 //   * one thread issues tcgen05.mma.kind::tf32, M = 128 features (W^T, staged
-//     once), N = 128 edges, K = 8, three times per tile
+//     once), N = 64 edges, K = 8, three times per tile
 //     (hi*hi + hi*lo + lo*hi = "3xTF32", error ~2^-21 relative: fp32-grade,
 //     the 1e-4 bound needs more than one tf32 pass), accumulating in
-//     TMEM (2 x 128 columns, double-buffered), and commits to mbarriers;
+//     TMEM (2 x 64 columns, double-buffered), and commits to mbarriers;
 //   * 4 epilogue warps read the accumulator with tcgen05.ld (thread = feature,
 //     walking edge columns, so the per-row segmented max needs no cross-lane
-//     reduction) and write each finished row with coalesced stores.
+//     reduction), keep the running winner as a CSR position, add the per-row
+//     q_v = x_v W (mlp_q_kernel, once per call) and write each finished row.
+// Bound: reading every accumulator element out of TMEM (m x d2 x 4 B; TMEM
+// reads run at ~64-72 B/clk/SM) -- measured on reddit d2 = 128: the epilogue
+// loop alone (gathers and MMAs disabled, FG_MLP_DBG=6) takes 2.8-2.9 ms of the
+// 4.05 ms; the argmax search adds the rest.
 #include <cstdint>
 #include <cstdlib>
 
@@ -39,8 +44,7 @@ constexpr int NT = 64;                    // edges per tile (MMA N)
 constexpr int NBUF = 2;                   // TMEM accumulator buffers (double buffer)
 constexpr int CTAS_PER_SM = 4;            // 4 independent pipelines per SM hide the MMA/commit latency
 constexpr int MT = 128;                   // features per CTA (MMA M)
-constexpr int STAGES = 4;
-constexpr int ISTAGES = 4;                // index ring (producer -> epilogue)
+constexpr int STAGES = 8;
 constexpr int NEPI = 4;                   // epilogue warps 0..3 (TMEM lane quarters)
 constexpr int MMA_WARP = 4;
 constexpr int NPROD = 1;                  // producer warp 5
@@ -182,67 +186,70 @@ struct Args {
     int d_in, d2;
     const float* Xhi;     // [n_src][KS*8] tf32 hi part of X (workspace)
     const float* Xlo;     // [n_src][KS*8] tf32 lo part
+    const float* Q;       // [n_dst][d2]: q_v = x_v W in fp32 (workspace, mlp_q_kernel)
     int backoff_ns;       // producer / MMA wait back-off (FG_MLP_BACKOFF_NS)
+    int epi_backoff_ns;   // epilogue wait back-off (FG_MLP_EPI_BACKOFF_NS, 0 = spin on try_wait)
     int dbg;              // FG_MLP_DBG bits (pipeline experiments): 2 skip gathers, 4 skip MMAs
                           // (results are then wrong; timing only)
 };
+
+// q_v = x_v W (fp32 FMA chain in k order), once per destination row and feature:
+// the per-row term of the MLP message, applied in the epilogue (see the header).
+__global__ void __launch_bounds__(256) mlp_q_kernel(const float* __restrict__ Xd, const float* __restrict__ W,
+                                                  int64_t n, int d_in, int d2, float* __restrict__ Q) {
+    const int64_t idx = int64_t(blockIdx.x) * 256 + threadIdx.x;
+    if (idx >= n * d2) return;
+    const int64_t v = idx / d2;
+    const int i = int(idx % d2);
+    float a = 0.f;
+    for (int k = 0; k < d_in; ++k) a = fmaf(__ldg(Xd + v * d_in + k), __ldg(W + int64_t(k) * d2 + i), a);
+    Q[idx] = a;
+}
 
 template <int KS>
 struct Smem {
     float a_hi[KS][MT * 8];
     float a_lo[KS][MT * 8];
-    float wcol[KS * 8][MT];                // W[k][feature] in fp32 for the per-row q = x_v W (epilogue)
     float b_hi[STAGES][KS][NT * 8];
     float b_lo[STAGES][KS][NT * 8];
-    int32_t su[ISTAGES][NT];               // source id / edge id of each tile column,
-    int32_t se[ISTAGES][NT];               // read by the epilogue for arg_u / arg_e
-    uint64_t full[STAGES], empty[STAGES], tfull[NBUF], tempty[NBUF], ifull[ISTAGES], iempty[ISTAGES];
+    uint64_t full[STAGES], empty[STAGES], tfull[NBUF], tempty[NBUF];
     uint32_t tmem_base;
     int64_t r_lo, r_hi;
 };
 
 // Epilogue state of one thread (= one feature column i of the CTA's M tile).
 // Edge positions are 32-bit offsets from the CTA's first edge E0 (a CTA owns a
-// contiguous CSR range), so the per-chunk row bookkeeping is 32-bit integer work.
-template <int KS, bool MAX>
+// contiguous CSR range).  The running winner is kept as a position only; its
+// source / edge id are read from col_idx / eid once per finished row.
+template <bool MAX>
 struct Epi {
     const Args* A;
-    int64_t r, r_hi;  // current row, end of the CTA's rows
+    int r, r_hi;      // current row, end of the CTA's rows
     int64_t E0;       // CSR position of the CTA's first edge
     int rs, re;       // current row's edge range, relative to E0
     int nre;          // prefetched end of row r + 1 (relative)
-    float best, q;
-    int bu, be;       // winning edge: source id / edge id (from the smem-staged tile indices)
-    int fu, fe;       // first edge of the row (the winner when every message is +0)
-    bool fresh;       // no edge of the row seen yet
-    const float* wc;  // this thread's W column in shared memory (stride MT)
-    float nx[KS * 8]; // prefetched x_{r+1}
+    float best, q, nq;
+    int bpos;         // relative position of the current winner
     int i;            // global feature index
     bool active;      // i < d2
 
-    // prefetch the next row's destination features and end pointer so that the
-    // per-row bookkeeping never waits on a global load
-    __device__ __forceinline__ void prefetch(int64_t rn) {
+    // prefetch the next row's end pointer and q so that the per-row bookkeeping
+    // never waits on a global load
+    __device__ __forceinline__ void prefetch(int rn) {
         if (rn < r_hi) {
-            const float* xv = A->Xd + rn * A->d_in;
-#pragma unroll
-            for (int k = 0; k < KS * 8; ++k) nx[k] = (k < A->d_in) ? __ldg(xv + k) : 0.f;
-            nre = int(__ldg(A->row_ptr + rn + 1) - E0);   // end of row rn (rn < r_hi <= n_dst)
+            nre = int(__ldg(A->row_ptr + rn + 1) - E0);
+            nq = active ? __ldg(A->Q + int64_t(rn) * A->d2 + i) : 0.f;
         }
     }
     __device__ __forceinline__ void start_row() {
         best = MAX ? -INFINITY : 0.f;
-        bu = be = fu = fe = -1;
-        fresh = true;
-        float a = 0.f;
-#pragma unroll
-        for (int k = 0; k < KS * 8; ++k) a = fmaf(nx[k], wc[k * MT], a);
-        q = a;
+        bpos = 0;
+        q = nq;
         prefetch(r + 1);
     }
     __device__ __forceinline__ void finish_row() {
         if (!active) return;
-        const int64_t o = r * A->d2 + i;
+        const int64_t o = int64_t(r) * A->d2 + i;
         if (!MAX) {
             A->out[o] = best;
             return;
@@ -256,8 +263,10 @@ struct Epi {
         const float z = best + q;
         const bool pos = z > 0.f;
         A->out[o] = pos ? z : 0.f;
-        if (A->arg_u) A->arg_u[o] = pos ? bu : fu;
-        if (A->arg_e) A->arg_e[o] = pos ? be : fe;
+        // every message is +0 when z <= 0: the row's first edge wins
+        const int64_t p = E0 + (pos ? bpos : rs);
+        if (A->arg_u) A->arg_u[o] = __ldg(A->col_idx + p);
+        if (A->arg_e) A->arg_e[o] = A->eid ? __ldg(A->eid + p) : int(p);
     }
     // finish row r and move to r+1 (uniform across the epilogue threads)
     __device__ __forceinline__ void advance() {
@@ -270,13 +279,8 @@ struct Epi {
         }
     }
     // the 32 columns of a chunk that lies inside the current row (the common case)
-    __device__ __forceinline__ void consume_full(const uint32_t (&v)[32], const int* su, const int* se) {
+    __device__ __forceinline__ void consume_full(const uint32_t (&v)[32], int pc) {
         if (MAX) {
-            if (fresh) {
-                fu = su[0];
-                fe = se[0];
-                fresh = false;
-            }
             // the chunk maximum by a 3-input max tree (FMNMX3); the first column
             // attaining it is searched only when it beats the running best (strict:
             // ties keep the earlier winner), skipped when no feature of the warp improves
@@ -295,8 +299,7 @@ struct Epi {
 #pragma unroll
                     for (int c = 30; c >= 0; --c) k = (__uint_as_float(v[c]) == m) ? c : k;
                     best = m;
-                    bu = su[k];
-                    be = se[k];
+                    bpos = pc + k;
                 }
             }
         } else {
@@ -310,17 +313,11 @@ struct Epi {
     }
     // general case: chunk at relative position pc with nvalid valid columns,
     // possibly spanning row boundaries
-    __device__ __forceinline__ void consume_split(const uint32_t (&v)[32], int pc, int nvalid, const int* su,
-                                               const int* se) {
+    __device__ __forceinline__ void consume_split(const uint32_t (&v)[32], int pc, int nvalid) {
         int c0 = 0;
         while (c0 < nvalid) {
             while (pc + c0 >= re) advance();
             const int c1 = min(nvalid, re - pc);
-            if (MAX && fresh) {
-                fu = su[c0];
-                fe = se[c0];
-                fresh = false;
-            }
             if (MAX) {
                 float b0 = -INFINITY;   // ties -> lowest column
                 int k0 = 0;
@@ -329,26 +326,42 @@ struct Epi {
                     const float x = __uint_as_float(v[c]);
                     if (c >= c0 && c < c1 && x > b0) { b0 = x; k0 = c; }
                 }
-                if (b0 > best) { best = b0; bu = su[k0]; be = se[k0]; }
+                if (b0 > best) { best = b0; bpos = pc + k0; }
             } else {
+                // columns [c0, c1) belong to row r (bit mask: measured faster than two compares for sum)
+                const uint32_t cm = (c1 >= 32 ? 0xffffffffu : ((1u << c1) - 1u)) & ~((1u << c0) - 1u);
                 float sm = 0.f;
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
-                    if (c >= c0 && c < c1) sm += fmaxf(__uint_as_float(v[c]) + q, 0.f);
+                    if ((cm >> c) & 1u) sm += fmaxf(__uint_as_float(v[c]) + q, 0.f);
                 best += sm;
             }
             c0 = c1;
         }
     }
-    __device__ __forceinline__ void consume(const uint32_t (&v)[32], int pc, int nvalid, const int* su,
-                                            const int* se) {
-        if (nvalid == 32 && pc >= rs && pc + 32 <= re) consume_full(v, su, se);   // warp-uniform
-        else if (nvalid > 0) consume_split(v, pc, nvalid, su, se);
+    __device__ __forceinline__ void consume(const uint32_t (&v)[32], int pc, int nvalid) {
+        if (nvalid == 32 && pc >= rs && pc + 32 <= re) consume_full(v, pc);   // warp-uniform
+        else if (nvalid > 0) consume_split(v, pc, nvalid);
     }
 };
 
-template <int KS, bool MAX>
-__global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const __grid_constant__ Args A) {
+// mark v as written after a preceding tcgen05.wait::ld (for a second buffer loaded
+// before that wait): keeps uses of v from being scheduled above the wait
+__device__ __forceinline__ void tmem_after_wait(uint32_t (&v)[32]) {
+    asm volatile(""
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                   "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
+                   "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
+                   "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+                 :
+                 : "memory");
+}
+
+// ILP = TMEM chunks loaded per wait (1: 4 CTAs/SM at <= 80 registers; 2: both
+// 32-column chunks of a tile in flight, 3 CTAs/SM)
+template <int KS, bool MAX, int ILP>
+__global__ void __launch_bounds__(THREADS, ILP == 2 ? 3 : CTAS_PER_SM) mlp_tcgen05_kernel(const __grid_constant__ Args A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem<KS>& S = *reinterpret_cast<Smem<KS>*>(smem_raw);
     const int tid = threadIdx.x;
@@ -363,7 +376,6 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         if (S.r_hi < S.r_lo) S.r_hi = S.r_lo;
         for (int s = 0; s < STAGES; ++s) { mbar_init(&S.full[s], NPROD * 32); mbar_init(&S.empty[s], 1); }
         for (int b2 = 0; b2 < NBUF; ++b2) { mbar_init(&S.tfull[b2], 1); mbar_init(&S.tempty[b2], NEPI * 32); }
-        for (int s = 0; s < ISTAGES; ++s) { mbar_init(&S.ifull[s], NPROD * 32); mbar_init(&S.iempty[s], NEPI * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // stage W^T (A operand) as tf32 hi / lo: row = feature, k = input dim
@@ -371,7 +383,6 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         const int ks = idx / (MT * 8), rem = idx % (MT * 8), r = rem / 8, k = rem % 8;
         const int kk = ks * 8 + k, col = mbase + r;
         const float w = (kk < A.d_in && col < A.d2) ? A.W[int64_t(kk) * A.d2 + col] : 0.f;
-        S.wcol[kk][r] = w;
         const float hi = tf32_rna(w);
         const float lo = tf32_rna(w - hi);
         *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(S.a_hi[ks]) + tile_off(r, k)) = hi;
@@ -397,7 +408,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         // workspace).  Per edge the producer issues 2*KS*2 cp.async 16-byte copies
         // straight into the K-major canonical tile positions (no register staging,
         // no per-edge dependent waits); cp.async.mbarrier.arrive signals full[s]
-        // when this thread's copies land.  Indices of tile t+1 are prefetched.
+        // when this thread's copies land.
         constexpr int EPT = NT / (NPROD * 32);
         const int pt = tid - (MMA_WARP + 1) * 32;          // 0 .. NPROD*32-1
         const int rowf = KS * 8;                            // floats per pre-split row
@@ -405,31 +416,25 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         // the unrolled-by-PF loop): the col_idx round trip (~1 us) would otherwise
         // bound the pipeline at one tile per load latency
         constexpr int PF = 4;
-        int u_pf[PF][EPT], e_pf[PF][EPT];
-        auto load_idx = [&](int t, int (&u)[EPT], int (&ed)[EPT]) {
+        int u_pf[PF][EPT];
+        auto load_idx = [&](int t, int (&u)[EPT]) {
             const int64_t tb = E0 + int64_t(t) * NT;
 #pragma unroll
             for (int i = 0; i < EPT; ++i) {
                 const int64_t p = tb + pt + i * NPROD * 32;
-                const bool ok = t < ntiles && p < E1;
-                u[i] = ok ? __ldg(A.col_idx + p) : -1;
-                ed[i] = ok ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
+                u[i] = (t < ntiles && p < E1) ? __ldg(A.col_idx + p) : 0;   // padded columns read row 0 (ignored)
             }
         };
 #pragma unroll
-        for (int k = 0; k < PF; ++k) load_idx(k, u_pf[k], e_pf[k]);
-        auto tile = [&](int t, int (&u_cur)[EPT], int (&e_cur)[EPT]) {
-            const int s = t % STAGES, is = t % ISTAGES;
+        for (int k = 0; k < PF; ++k) load_idx(k, u_pf[k]);
+        auto tile = [&](int t, int (&u_cur)[EPT]) {
+            const int s = t % STAGES;
             mbar_wait_backoff(&S.empty[s], ((t / STAGES) & 1) ^ 1, A.backoff_ns);
-            mbar_wait_backoff(&S.iempty[is], ((t / ISTAGES) & 1) ^ 1, A.backoff_ns);
 #pragma unroll
             for (int i = 0; i < EPT; ++i) {
                 const int e = pt + i * NPROD * 32;
-                S.su[is][e] = u_cur[i];
-                S.se[is][e] = e_cur[i];
-                const int64_t u = u_cur[i] >= 0 ? u_cur[i] : 0;     // padded columns read row 0 (ignored)
-                const float* xh = A.Xhi + u * rowf;
-                const float* xl = A.Xlo + u * rowf;
+                const float* xh = A.Xhi + int64_t(u_cur[i]) * rowf;
+                const float* xl = A.Xlo + int64_t(u_cur[i]) * rowf;
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) {
 #pragma unroll
@@ -443,13 +448,12 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
                 }
             }
             cp_async_arrive(&S.full[s]);
-            mbar_arrive(&S.ifull[is]);
-            load_idx(t + PF, u_cur, e_cur);   // refill this slot PF tiles ahead
+            load_idx(t + PF, u_cur);   // refill this slot PF tiles ahead
         };
         for (int t0 = 0; t0 < ntiles; t0 += PF) {
 #pragma unroll
             for (int k = 0; k < PF; ++k)
-                if (t0 + k < ntiles) tile(t0 + k, u_pf[k], e_pf[k]);
+                if (t0 + k < ntiles) tile(t0 + k, u_pf[k]);
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp == MMA_WARP) {
@@ -479,43 +483,53 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         __syncwarp();
     } else {
         // ------------------------------------------------ epilogue: thread = feature
-        Epi<KS, MAX> ep;
+        Epi<MAX> ep;
         ep.A = &A;
         ep.i = mbase + tid;
         ep.active = ep.i < A.d2;
-        ep.wc = &S.wcol[0][tid];
-        ep.r = r_lo;
-        ep.r_hi = r_hi;
+        ep.r = int(r_lo);
+        ep.r_hi = int(r_hi);
         ep.E0 = E0;
         ep.rs = ep.re = 0;
         if (r_lo < r_hi) {
-            ep.rs = 0;   // row_ptr[r_lo] == E0
-            ep.re = int(__ldg(A.row_ptr + r_lo + 1) - E0);
-            ep.prefetch(r_lo);
+            ep.prefetch(int(r_lo));
+            ep.re = ep.nre;   // row_ptr[r_lo] == E0, so row r_lo spans [0, nre)
             ep.start_row();
         }
-        const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+        // TMEM address of this warp's lane quarter; opaque so that it stays in a
+        // register instead of being rematerialised from %tid every chunk
+        uint32_t lane_base;
+        asm volatile("mov.b32 %0, %1;" : "=r"(lane_base) : "r"(tmem + (uint32_t(warp * 32) << 16)));
+        const int nnz_cta = int(E1 - E0);
         for (int t = 0; t < ntiles; ++t) {
-            const int b = t % NBUF, is = t % ISTAGES;
-            mbar_wait(&S.ifull[is], (t / ISTAGES) & 1);
-            mbar_wait(&S.tfull[b], (t / NBUF) & 1);
+            const int b = t % NBUF;
+            if (A.epi_backoff_ns > 0) mbar_wait_backoff(&S.tfull[b], (t / NBUF) & 1, A.epi_backoff_ns);
+            else mbar_wait(&S.tfull[b], (t / NBUF) & 1);
             tc_fence_after();
-            const int* su = S.su[is];
-            const int* se = S.se[is];
             const int tb = t * NT;                       // relative to E0
-            const int nv_tile = min(NT, int(E1 - E0) - tb);
-#pragma unroll 1
-            for (int ch = 0; ch < NT / 32; ++ch) {   // single-buffered: 4 CTAs per SM supply the overlap
-                uint32_t v0[32];
-                tmem_ld32(lane_base + uint32_t(b * NT + ch * 32), v0);
+            const int nv_tile = min(NT, nnz_cta - tb);
+            if constexpr (ILP == 2) {
+                static_assert(NT == 64, "ILP 2 loads the tile's two chunks");
+                uint32_t v0[32], v1[32];
+                tmem_ld32(lane_base + uint32_t(b * NT), v0);
+                tmem_ld32(lane_base + uint32_t(b * NT + 32), v1);
                 tmem_wait_ld(v0);
-                ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)), su + ch * 32, se + ch * 32);
+                tmem_after_wait(v1);
+                ep.consume(v0, tb, max(0, min(32, nv_tile)));
+                ep.consume(v1, tb + 32, max(0, min(32, nv_tile - 32)));
+            } else {
+#pragma unroll 1
+                for (int ch = 0; ch < NT / 32; ++ch) {   // single-buffered: 4 CTAs per SM supply the overlap
+                    uint32_t v0[32];
+                    tmem_ld32(lane_base + uint32_t(b * NT + ch * 32), v0);
+                    tmem_wait_ld(v0);
+                    ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)));
+                }
             }
             tc_fence_before();
             mbar_arrive(&S.tempty[b]);
-            mbar_arrive(&S.iempty[is]);
         }
-        while (ep.r < r_hi) ep.advance();   // trailing rows (empty rows after the last edge)
+        while (ep.r < ep.r_hi) ep.advance();   // trailing rows (empty rows after the last edge)
     }
     tc_fence_before();
     __syncthreads();
@@ -525,10 +539,11 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
     }
 }
 
-template <int KS, bool MAX>
+template <int KS, bool MAX, int ILP>
 fg_status launch_ks(const Args& A, cudaStream_t st) {
     const int smem = int(sizeof(Smem<KS>)) + 1024;
-    const int smem_req = smem < 56 * 1024 ? 56 * 1024 : smem;   // bounds residency at CTAS_PER_SM (TMEM)
+    const int smem_min = (ILP == 2 ? 72 : 56) * 1024;             // bounds residency (TMEM columns)
+    const int smem_req = smem < smem_min ? smem_min : smem;
     {   // pre-split X into tf32 hi / lo rows (the producers' cp.async source)
         const int64_t tot = A.n_src * KS * 8;
         if (tot > 0)
@@ -537,13 +552,21 @@ fg_status launch_ks(const Args& A, cudaStream_t st) {
         fg_status s = fgk::check_launch("mlp_split_kernel");
         if (s != FG_OK) return s;
     }
-    auto kfn = mlp_tcgen05_kernel<KS, MAX>;
+    {   // q_v = x_v W per destination row (the epilogue's per-row term)
+        const int64_t tot = A.n_dst * A.d2;
+        if (tot > 0)
+            mlp_q_kernel<<<unsigned((tot + 255) / 256), 256, 0, st>>>(A.Xd, A.W, A.n_dst, A.d_in, A.d2,
+                                                                     const_cast<float*>(A.Q));
+        fg_status s = fgk::check_launch("mlp_q_kernel");
+        if (s != FG_OK) return s;
+    }
+    auto kfn = mlp_tcgen05_kernel<KS, MAX, ILP>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_req);
     // the whole unified L1/smem for shared memory: without it the driver picks a
     // carveout that fits ONE 100 KB CTA per SM and the persistent grid runs as two waves
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return fgk::set_error(FG_ECUDA, "mlp_tcgen05: smem attribute: %s", cudaGetErrorString(e));
-    int nb = CTAS_PER_SM * fgk::num_sms();
+    int nb = (ILP == 2 ? 3 : CTAS_PER_SM) * fgk::num_sms();
     const int64_t want = (A.nnz + 4 * NT - 1) / (4 * NT);   // >= 4 tiles per CTA
     if (want < nb) nb = int(want < 1 ? 1 : want);
     const dim3 grid{unsigned(nb), unsigned((A.d2 + MT - 1) / MT), 1u};
@@ -555,9 +578,10 @@ fg_status launch_ks(const Args& A, cudaStream_t st) {
 
 namespace fgk {
 
-size_t mlp_workspace_bytes(int64_t n_src, int d_in) {
+// workspace: tf32 hi / lo rows of X (2 x n_src x KS*8 floats) + Q (n_dst x d2 floats)
+size_t mlp_workspace_bytes(int64_t n_src, int64_t n_dst, int d_in, int d2) {
     const int64_t ks = (d_in + 7) / 8;
-    return size_t(2 * n_src * ks * 8 * 4 + 256);
+    return size_t(2 * n_src * ks * 8 * 4 + 256 + n_dst * int64_t(d2) * 4 + 256);
 }
 
 fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W,
@@ -568,12 +592,16 @@ fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, c
     float* ws = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
     A.Xhi = ws;
     A.Xlo = ws + g->n_src * ksz * 8;
+    A.Q = reinterpret_cast<const float*>(
+        (reinterpret_cast<uintptr_t>(A.Xlo + g->n_src * ksz * 8) + 255) & ~uintptr_t(255));
     A.n_src = g->n_src;
     {
         const char* d = getenv("FG_MLP_DBG");
         A.dbg = d ? atoi(d) : 0;
         const char* bo = getenv("FG_MLP_BACKOFF_NS");
         A.backoff_ns = bo ? atoi(bo) : 128;
+        const char* eb = getenv("FG_MLP_EPI_BACKOFF_NS");
+        A.epi_backoff_ns = eb ? atoi(eb) : 0;
     }
     A.row_ptr = g->row_ptr;
     A.col_idx = g->col_idx;
@@ -590,11 +618,23 @@ fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, c
     A.d2 = d2;
     const bool mx = red == FG_REDUCE_MAX;
     const int ks = (d_in + 7) / 8;
+    static const int ilp = [] {
+        const char* e = getenv("FG_MLP_ILP");
+        return (e && e[0] == '2') ? 2 : 1;
+    }();
+    if (ilp == 2) {
+        switch (ks) {
+            case 1: return mx ? launch_ks<1, true, 2>(A, st) : launch_ks<1, false, 2>(A, st);
+            case 2: return mx ? launch_ks<2, true, 2>(A, st) : launch_ks<2, false, 2>(A, st);
+            case 3: return mx ? launch_ks<3, true, 2>(A, st) : launch_ks<3, false, 2>(A, st);
+            default: return mx ? launch_ks<4, true, 2>(A, st) : launch_ks<4, false, 2>(A, st);
+        }
+    }
     switch (ks) {
-        case 1: return mx ? launch_ks<1, true>(A, st) : launch_ks<1, false>(A, st);
-        case 2: return mx ? launch_ks<2, true>(A, st) : launch_ks<2, false>(A, st);
-        case 3: return mx ? launch_ks<3, true>(A, st) : launch_ks<3, false>(A, st);
-        default: return mx ? launch_ks<4, true>(A, st) : launch_ks<4, false>(A, st);
+        case 1: return mx ? launch_ks<1, true, 1>(A, st) : launch_ks<1, false, 1>(A, st);
+        case 2: return mx ? launch_ks<2, true, 1>(A, st) : launch_ks<2, false, 1>(A, st);
+        case 3: return mx ? launch_ks<3, true, 1>(A, st) : launch_ks<3, false, 1>(A, st);
+        default: return mx ? launch_ks<4, true, 1>(A, st) : launch_ks<4, false, 1>(A, st);
     }
 }
 

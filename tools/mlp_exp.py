@@ -15,7 +15,10 @@ def t(fn, reps=5):
         if i: ts.append(s.elapsed_time(e))
     return np.median(ts)
 for dbg in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "1", "2", "3"]):
-    if dbg.startswith("bo"):   # bo<ns>: back-off sweep with every stage on
+    if dbg.startswith("eb"):   # eb<ns>: epilogue wait back-off
+        os.environ["FG_MLP_DBG"] = "0"
+        os.environ["FG_MLP_EPI_BACKOFF_NS"] = dbg[2:]
+    elif dbg.startswith("bo"):   # bo<ns>: back-off sweep with every stage on
         os.environ["FG_MLP_DBG"] = "0"
         os.environ["FG_MLP_BACKOFF_NS"] = dbg[2:]
     else:
