@@ -1,0 +1,198 @@
+"""Parity at BASELINE.json's FULL sizes, in the
+launch configuration bench.py times, on sampled destination rows that the fp64
+oracle computes one by one.
+
+* C3/reddit step: bench.Step (same graph, inputs, calls and output buffers as
+  the timed step) runs once; every op's output is checked on a seeded row
+  sample (the heaviest rows -- CTA-per-row path --, rows of degree < 32 --
+  sub-warp groups --, and random rows) against the oracle on the sample's
+  sub-CSR (global source ids).  The GAT chain is checked op by op on the
+  ORACLE's fp32 intermediates for the sampled rows (L13): the
+  softmax input of a sampled row is the oracle's fp32 scores, the u_mul_e
+  edge weights of a sampled row are the oracle's fp32 alpha (a row's result
+  depends only on its own edges).
+* C2/proteins: copy_u-sum at F = 32, 128, 512.
+* C4/rand-100K: mlp-max d2 = 128 with arg_u / arg_e (argmax checked VALID,
+  SURVEY L5).
+* C5/reddit F = 512 dst-row shards at P = 2, 4, 8 (each shard's kernel run on
+  this GPU): concatenated outputs bit-identical to the unsharded run.
+Tolerances: |gpu - ref| <= 1e-4 * sum|terms|; max values and indices exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+from helpers import check_close
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+EDGE_BUDGET = 1_500_000
+
+
+def sample(g, seed):
+    """Heaviest rows + light rows + seeded random rows, sorted, ~EDGE_BUDGET edges."""
+    deg = np.diff(g.row_ptr)
+    order = np.argsort(-deg, kind="stable")
+    heavy = order[:3]
+    light = np.flatnonzero((deg > 0) & (deg < 32))[:200]
+    perm = gen.permutation(g.n_dst, seed, 31)
+    k = int(np.searchsorted(np.cumsum(deg[perm]), EDGE_BUDGET))
+    rows = np.unique(np.concatenate([heavy, light, perm[:max(k, 1)], [0, g.n_dst - 1]]))
+    return rows.astype(np.int64)
+
+
+def sub_csr(g, rows):
+    deg = g.row_ptr[rows + 1] - g.row_ptr[rows]
+    rp = np.zeros(rows.size + 1, np.int64)
+    np.cumsum(deg, out=rp[1:])
+    pos = oracle.edge_positions(g.row_ptr, rows)
+    return rp, g.col_idx[pos], pos
+
+
+def gpu_rows(t, rows):
+    return t[torch.from_numpy(rows).cuda()].cpu().numpy()
+
+
+def gpu_edges(t, pos):
+    return t[torch.from_numpy(pos).cuda()].cpu().numpy()
+
+
+def check_max(out, au, ae, ref, rau, rae, pos, what):
+    """copy_u-max: values and both argmax arrays exact (oracle arg_e is a
+    position in the sub-CSR -> global position through pos)."""
+    assert np.array_equal(out.astype(np.float64), ref), f"{what}: values"
+    assert np.array_equal(au, rau), f"{what}: arg_u"
+    exp_e = np.where(rae >= 0, pos[np.maximum(rae, 0)], -1)
+    assert np.array_equal(ae, exp_e), f"{what}: arg_e"
+
+
+def check_mlp_valid(out, au, ae, ref, ab, X, Xd, W, col_idx, what):
+    check_close(out, ref, ab, TOL, f"{what} values")
+    Xf, Wd = X.astype(np.float64), W.astype(np.float64)
+    for i in range(out.shape[0]):
+        if ab[i].max() == 0 and ref[i].max() == 0 and (au[i] < 0).all():
+            continue   # empty row
+        u = au[i]
+        assert (col_idx[ae[i]] == u).all(), f"{what}: arg_e / arg_u disagree at sampled row {i}"
+        msg = np.maximum(((Xf[u] + Xd[i].astype(np.float64)[None, :]) * Wd.T).sum(1), 0.0)
+        assert (np.abs(msg - ref[i]) <= TOL * ab[i] + 1e-30).all(), f"{what}: argmax not a maximiser at row {i}"
+
+
+# ------------------------------------------------------------------ C3: the bench step on reddit
+@pytest.fixture(scope="module")
+def reddit(cuda_ok):
+    import bench
+    g = gen.make_graph("reddit")
+    host = bench.make_inputs(g)
+    stream = torch.cuda.Stream()
+    S = bench.Step(g, None, host, None, stream)
+    with torch.cuda.stream(stream):
+        S.enqueue()
+    torch.cuda.synchronize()
+    rows = sample(g, 101)
+    rp, ci, pos = sub_csr(g, rows)
+    return g, host, S, rows, rp, ci, pos
+
+
+def test_reddit_copy_u_sum_F512(reddit):
+    g, host, S, rows, rp, ci, pos = reddit
+    ref, ab, _, _ = oracle.spmm(rp, ci, "copy_u", "sum", host["X512"])
+    check_close(gpu_rows(S.out512, rows), ref, ab, TOL, "reddit copy_u-sum F512")
+
+
+def test_reddit_u_dot_v_H1_F512(reddit):
+    g, host, S, rows, rp, ci, pos = reddit
+    ref, ab = oracle.sddmm(rp, ci, host["X512"], host["X512"][rows], H=1)
+    check_close(gpu_edges(S.s1, pos), ref, ab, TOL, "reddit u_dot_v H1 F512")
+
+
+def test_reddit_gat_chain_H8_D32(reddit):
+    import bench
+    import paper_2008_11359_b200 as fgp
+    g, host, S, rows, rp, ci, pos = reddit
+    H = bench.H_GAT
+    X = host["X256"]
+    # scores, same call as the step (the step then normalises them in place)
+    s8 = fgp.sddmm(S.G, S.X["X256"], S.ydst("X256"), H=H)
+    rs, rab = oracle.sddmm(rp, ci, X, X[rows], H=H)
+    check_close(gpu_edges(s8, pos), rs, rab, TOL, "reddit u_dot_v H8 D32")
+    # softmax on the oracle's fp32 scores for the sampled rows, in place as in the step
+    pos_d = torch.from_numpy(pos).cuda()
+    rs32 = rs.astype(np.float32)
+    s8[pos_d] = torch.from_numpy(rs32).cuda()
+    fgp.edge_softmax(S.G, s8, H=H, out=s8)
+    ra = oracle.edge_softmax(rp, rs32, H=H)
+    got = gpu_edges(s8, pos).astype(np.float64)
+    assert (np.abs(got - ra) <= TOL * ra).all(), "reddit edge softmax H8"
+    # u_mul_e on the oracle's fp32 alpha for the sampled rows
+    ra32 = ra.astype(np.float32)
+    s8[pos_d] = torch.from_numpy(ra32).cuda()
+    o = fgp.spmm(S.G, "u_mul_e", "sum", S.X["X256"], H=H, E=s8)
+    ro, rob, _, _ = oracle.spmm(rp, ci, "u_mul_e", "sum", X, H=H, E=ra32)
+    check_close(gpu_rows(o, rows), ro, rob, TOL, "reddit u_mul_e-sum H8 D32")
+
+
+def test_reddit_copy_u_max_F128_args(reddit):
+    g, host, S, rows, rp, ci, pos = reddit
+    ref, _, rau, rae = oracle.spmm(rp, ci, "copy_u", "max", host["X128"])
+    check_max(gpu_rows(S.o128, rows), gpu_rows(S.au128, rows), gpu_rows(S.ae128, rows), ref, rau, rae, pos,
+              "reddit copy_u-max F128")
+
+
+def test_reddit_mlp_max_args(reddit):
+    g, host, S, rows, rp, ci, pos = reddit
+    X8, W = host["X8"], host["W"]
+    ref, ab, _, _ = oracle.spmm(rp, ci, "mlp", "max", X8, W=W, X_dst=X8[rows])
+    check_mlp_valid(gpu_rows(S.omlp, rows), gpu_rows(S.aumlp, rows), gpu_rows(S.aemlp, rows), ref, ab, X8,
+                    X8[rows], W, g.col_idx, "reddit mlp-max d2=128")
+
+
+# ------------------------------------------------------------------ C5: reddit F=512 dst-row shards
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_reddit_shards_bit_identical(reddit, P):
+    import paper_2008_11359_b200 as fgp
+    from paper_2008_11359_b200.shard import make_shard
+    g, host, S, rows, rp, ci, pos = reddit
+    X = S.X["X512"]
+    parts_o, parts_s = [], []
+    for r in range(P):
+        sh = make_shard(g.row_ptr, g.col_idx, r, P)
+        L = fgp.Graph(torch.from_numpy(sh.row_ptr).cuda(), torch.from_numpy(sh.col_idx).cuda(), n_src=g.n_src)
+        parts_o.append(fgp.spmm(L, "copy_u", "sum", X))
+        parts_s.append(fgp.sddmm(L, X, X[sh.lo:sh.hi], H=1))
+        del L
+    assert torch.equal(torch.cat(parts_o), S.out512), f"P={P}: copy_u-sum shards differ from the 1-GPU output"
+    assert torch.equal(torch.cat(parts_s), S.s1), f"P={P}: u_dot_v shards differ from the 1-GPU output"
+
+
+# ------------------------------------------------------------------ C2: proteins GCN aggregation
+@pytest.mark.parametrize("F", [32, 128, 512])
+def test_proteins_copy_u_sum(cuda_ok, F):
+    import paper_2008_11359_b200 as fgp
+    g = gen.make_graph("proteins")
+    X = gen.features((g.n_src, F), gen.feature_seed("proteins"), F)
+    G = fgp.Graph(torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col_idx).cuda())
+    out = fgp.spmm(G, "copy_u", "sum", torch.from_numpy(X).cuda())
+    rows = sample(g, 202 + F)
+    rp, ci, _ = sub_csr(g, rows)
+    ref, ab, _, _ = oracle.spmm(rp, ci, "copy_u", "sum", X)
+    check_close(gpu_rows(out, rows), ref, ab, TOL, f"proteins copy_u-sum F={F}")
+
+
+# ------------------------------------------------------------------ C4: rand-100K MLP aggregation
+def test_rand100k_mlp_max_args(cuda_ok):
+    import paper_2008_11359_b200 as fgp
+    g = gen.make_graph("rand100k")
+    s = gen.feature_seed("rand100k")
+    X8 = gen.features((g.n_src, 8), s, 3)
+    W = gen.features((8, 128), s, 4, gen.SCALED, scale=1 / np.sqrt(8))
+    G = fgp.Graph(torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col_idx).cuda())
+    out, au, ae = fgp.spmm(G, "mlp", "max", torch.from_numpy(X8).cuda(), W=torch.from_numpy(W).cuda(),
+                           arg_u=True, arg_e=True)
+    rows = sample(g, 303)
+    rp, ci, _ = sub_csr(g, rows)
+    ref, ab, _, _ = oracle.spmm(rp, ci, "mlp", "max", X8, W=W, X_dst=X8[rows])
+    check_mlp_valid(gpu_rows(out, rows), gpu_rows(au, rows), gpu_rows(ae, rows), ref, ab, X8, X8[rows], W,
+                    g.col_idx, "rand100k mlp-max d2=128")

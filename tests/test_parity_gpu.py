@@ -310,7 +310,7 @@ def test_sddmm_int_exact(skewed):
 
 
 # ------------------------------------------------------------------ edge softmax
-@pytest.mark.parametrize("H", [1, 2, 8, 3])
+@pytest.mark.parametrize("H", [1, 2, 4, 8, 16, 3])
 @pytest.mark.parametrize("use_eid", [False, True])
 def test_edge_softmax(skewed, skewed_eid, H, use_eid):
     import paper_2008_11359_b200 as fgp
@@ -330,6 +330,24 @@ def test_edge_softmax(skewed, skewed_eid, H, use_eid):
     St = dev(S)
     fgp.edge_softmax(g.h, St, H=H, out=St)
     assert np.array_equal(St.cpu().numpy(), out)
+
+
+@pytest.mark.parametrize("H", [4, 8, 32])
+def test_edge_softmax_staging_boundaries(H):
+    """Row-length edge cases around the 8 KiB-of-scores mark (cap = 2048 / H
+    edges): rows of degree cap - 1, cap, cap + 1, a run of small rows, empty
+    rows, and a row several caps long."""
+    import paper_2008_11359_b200 as fgp
+    cap = 8 * 1024 // (4 * H)
+    rng = np.random.default_rng(H)
+    degs = [cap - 1, 0, cap, 1, cap + 1, 0, 0, 3 * cap + 7] + list(rng.integers(0, 40, 600)) + [cap, 2]
+    rp = np.concatenate([[0], np.cumsum(degs)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(4 * cap, size=d, replace=False)) for d in degs]).astype(np.int32)
+    g = G(rp, ci, n_src=4 * cap)
+    S = gen.features((g.nnz, H), 640 + H, 0, gen.REAL) * 8
+    out = fgp.edge_softmax(g.h, dev(S), H=H).cpu().numpy().astype(np.float64)
+    ref = oracle.edge_softmax(g.row_ptr, S, H=H)
+    assert (np.abs(out - ref) <= TOL * ref).all()
 
 
 def test_edge_softmax_special_values(skewed):
