@@ -55,7 +55,7 @@ struct State {
     float4 acc[NV];
 };
 
-template <int G, int NV>
+template <int G, int NV, int U, bool PIPE>
 __device__ __forceinline__ void attend_range(const Args& A, const float4* __restrict__ X, const float4 (&y)[NV],
                                              int64_t s, int64_t e, int gl, unsigned mask, State<NV>& st,
                                              float* __restrict__ scores, int* __restrict__ sidx) {
@@ -64,7 +64,6 @@ __device__ __forceinline__ void attend_range(const Args& A, const float4* __rest
     // the U x NV per-head scores (butterfly over the D/4 lanes of a head) and the
     // sequential online-softmax updates.
     constexpr int B = 32;
-    constexpr int U = NV >= 3 ? 2 : 4;
     const int F4 = A.F4, D4 = A.D4, H = A.H;
     for (int64_t p0 = s; p0 < e; p0 += B) {
         const int cnt = int(min((int64_t)B, e - p0));
@@ -84,14 +83,18 @@ __device__ __forceinline__ void attend_range(const Args& A, const float4* __rest
                 }
             }
         };
-        gather(0, xn);
+        if constexpr (PIPE) gather(0, xn);
         for (int t0 = 0; t0 < cnt; t0 += U) {
             float4 x[U][NV];
+            if constexpr (PIPE) {
 #pragma unroll
-            for (int uu = 0; uu < U; ++uu)
+                for (int uu = 0; uu < U; ++uu)
 #pragma unroll
-                for (int j = 0; j < NV; ++j) x[uu][j] = xn[uu][j];
-            if (t0 + U < cnt) gather(t0 + U, xn);
+                    for (int j = 0; j < NV; ++j) x[uu][j] = xn[uu][j];
+                if (t0 + U < cnt) gather(t0 + U, xn);
+            } else {
+                gather(t0, x);
+            }
             float sc[U][NV];
 #pragma unroll
             for (int uu = 0; uu < U; ++uu)
@@ -139,8 +142,8 @@ __device__ __forceinline__ void attend_range(const Args& A, const float4* __rest
     }
 }
 
-template <int G, int NV>
-__global__ void __launch_bounds__(THREADS, 2) gat_fused_kernel(const Args A, const float4* __restrict__ X,
+template <int G, int NV, int U, int MINB, bool PIPE>
+__global__ void __launch_bounds__(THREADS, MINB) gat_fused_kernel(const Args A, const float4* __restrict__ X,
                                                             const float4* __restrict__ Y, float4* __restrict__ out,
                                                             float* __restrict__ scores) {
     constexpr int NG = THREADS / G, TW = G * NV;
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(THREADS, 2) gat_fused_kernel(const Args A, con
     if (heavy) {
         const int64_t len = (e - s + NG - 1) / NG;
         const int64_t gs = min(e, s + gi * len), ge = min(e, gs + len);
-        attend_range<G, NV>(A, X, y, gs, ge, gl, mask, st, scores, s_idx[gi]);
+        attend_range<G, NV, U, PIPE>(A, X, y, gs, ge, gl, mask, st, scores, s_idx[gi]);
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
             const int c = gl + G * j;
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(THREADS, 2) gat_fused_kernel(const Args A, con
         }
         return;
     }
-    attend_range<G, NV>(A, X, y, s, e, gl, mask, st, scores, s_idx[gi]);
+    attend_range<G, NV, U, PIPE>(A, X, y, s, e, gl, mask, st, scores, s_idx[gi]);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const int c = gl + G * j;
@@ -219,14 +222,14 @@ __global__ void __launch_bounds__(THREADS, 2) gat_fused_kernel(const Args A, con
     }
 }
 
-template <int G, int NV>
+template <int G, int NV, int U = (NV >= 3 ? 2 : 4), int MINB = 2, bool PIPE = true>
 fg_status launch_t(Args A, const fg_graph* g, const float* X, const float* Y, float* out, float* scores,
                    cudaStream_t st) {
     constexpr int NG = THREADS / G;
     A.n_heavy = fgk::rows_with_degree_at_least(g, int64_t(NG) * 32);
     const int64_t blocks = A.n_heavy + (A.n_rows - A.n_heavy + NG - 1) / NG;
     if (blocks == 0) return FG_OK;
-    gat_fused_kernel<G, NV><<<unsigned(blocks), THREADS, 0, st>>>(A, reinterpret_cast<const float4*>(X),
+    gat_fused_kernel<G, NV, U, MINB, PIPE><<<unsigned(blocks), THREADS, 0, st>>>(A, reinterpret_cast<const float4*>(X),
                                                                   reinterpret_cast<const float4*>(Y),
                                                                   reinterpret_cast<float4*>(out), scores);
     return fgk::check_launch("gat_fused_kernel");
@@ -277,7 +280,11 @@ extern "C" fg_status fg_gat_attention(const fg_graph* g, int H, int D, const flo
         case 16: return launch_t<16, 1>(A, g, X, Y, out, scores, st);
         default:
             if (NV == 1) return launch_t<32, 1>(A, g, X, Y, out, scores, st);
-            if (NV == 2) return launch_t<32, 2>(A, g, X, Y, out, scores, st);
+            // H*D in (128, 256] (reddit GAT H = 8, D = 32): 2 edges in flight per lane,
+            // no software pipeline, 4 CTAs per SM (<= 64 registers).  Measured on
+            // reddit (tools/gat_exp.py): 14.9 ms vs 18.4 ms for 4 edges + pipeline at
+            // 2 CTAs/SM (128 registers); occupancy beats per-warp memory parallelism
+            if (NV == 2) return launch_t<32, 2, 2, 4, false>(A, g, X, Y, out, scores, st);
             if (NV == 3) return launch_t<32, 3>(A, g, X, Y, out, scores, st);
             return launch_t<32, 4>(A, g, X, Y, out, scores, st);
     }
