@@ -77,3 +77,31 @@ def test_allgather_rows_single_rank_nccl(cuda_ok):
     torch.cuda.synchronize()
     assert torch.equal(full2, X)
     c.close()
+
+
+def test_bench_step_overlapped_allgather_single_rank(cuda_ok):
+    """bench.Step's N > 1 schedule (all-gathers on their own stream, each op
+    waiting only for the tensor it reads) through a real 1-rank NCCL
+    communicator on a shard that is the whole graph: two steps back to back give
+    the same outputs as the unsharded step (the second step's gathers must wait
+    for the first step's ops)."""
+    import bench
+    import paper_2008_11359_b200 as fgp
+    from paper_2008_11359_b200.shard import make_shard
+    g = gen.random_graph(3000, 150000, 41, sigma=1.4, n_empty=20)
+    host = bench.make_inputs(g)
+    ref_stream = torch.cuda.Stream()
+    R = bench.Step(g, None, host, None, ref_stream)
+    with torch.cuda.stream(ref_stream):
+        R.enqueue()
+    torch.cuda.synchronize()
+    c = fgp.Comm(fgp.comm_unique_id(), 1, 0)
+    st = torch.cuda.Stream()
+    S = bench.Step(g, make_shard(g.row_ptr, g.col_idx, 0, 1), host, c, st)
+    with torch.cuda.stream(st):
+        S.enqueue()
+        S.enqueue()
+    torch.cuda.synchronize()
+    for a, b in zip(S.outputs(), R.outputs()):
+        assert torch.equal(a, b)
+    c.close()
