@@ -557,24 +557,50 @@ def main():
 
 def run_extras(S, args, sync_all, flush):
     """Next-row kernels measured beside the step (not part of it): f2 fused GAT
-    (u_dot_v -> softmax -> u_mul_e-sum in one pass) vs the 3-kernel chain."""
+    (u_dot_v -> softmax -> u_mul_e-sum in one pass) vs the 3-kernel chain, and
+    f4 bf16 feature storage (the same fp32 ops with the gathered X stored as
+    bf16: half the gather bytes) for the step's copy_u-sum / u_dot_v / GAT ops."""
     import torch
     st = S.stream
-    out = torch.empty_like(S.o256)
+    fgp = S.fgp
     k_steps = max(1, min(args.steps, 5))
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k_steps + 1)]
-    with torch.cuda.stream(st):
-        for k in range(k_steps + 1):
-            flush.fill_(float(k))
-            evs[k][0].record(st)
-            S.fgp.gat_attention(S.G, S.X["X256"], S.ydst("X256"), H=H_GAT, out=out, stream=st)
-            evs[k][1].record(st)
-    sync_all()
-    ms = float(np.mean([evs[k][0].elapsed_time(evs[k][1]) for k in range(1, k_steps + 1)]))
+
+    def timed(fn):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(k_steps + 1)]
+        with torch.cuda.stream(st):
+            for k in range(k_steps + 1):
+                flush.fill_(float(k))
+                evs[k][0].record(st)
+                fn()
+                evs[k][1].record(st)
+        sync_all()
+        return float(np.mean([evs[k][0].elapsed_time(evs[k][1]) for k in range(1, k_steps + 1)]))
+
+    out = torch.empty_like(S.o256)
+    ms = timed(lambda: fgp.gat_attention(S.G, S.X["X256"], S.ydst("X256"), H=H_GAT, out=out, stream=st))
     n, m, F = S.nl, S.m, H_GAT * D_GAT
     b = 8 * (n + 1) + 4 * m + 4 * m * F + 2 * 4 * n * F
-    return {"gat_fused_ms": round(ms, 4), "gat_fused_gbs": round(b / (ms * 1e-3) / 1e9, 1),
-            "gat_fused_bytes_model": "8(n+1) + 4m + 4mF + 8nF (X[u] gathered once; Y read, out written)"}
+    res = {"gat_fused_ms": round(ms, 4), "gat_fused_gbs": round(b / (ms * 1e-3) / 1e9, 1),
+           "gat_fused_bytes_model": "8(n+1) + 4m + 4mF + 8nF (X[u] gathered once; Y read, out written)"}
+    # bf16 storage (fg_spmm_x16 / fg_sddmm_x16): inputs converted once outside the timing
+    X16 = {k: S.X[k].to(torch.bfloat16) for k in ("X512", "X256")}
+    lo, nl = S.lo, S.nl
+    o512, s1, s8, o256 = (torch.empty_like(S.out512), torch.empty_like(S.s1), torch.empty_like(S.s8),
+                          torch.empty_like(S.o256))
+    bf = {
+        "spmm_copy_u_sum_F512": timed(lambda: fgp.spmm(S.G, "copy_u", "sum", X16["X512"], out=o512, stream=st)),
+        "sddmm_u_dot_v_H1_F512": timed(lambda: fgp.sddmm(S.G, X16["X512"], X16["X512"][lo:lo + nl], H=1, out=s1,
+                                                         stream=st)),
+        "sddmm_u_dot_v_H8_D32": timed(lambda: fgp.sddmm(S.G, X16["X256"], X16["X256"][lo:lo + nl], H=H_GAT,
+                                                        out=s8, stream=st)),
+        "spmm_u_mul_e_sum_H8_D32": timed(lambda: fgp.spmm(S.G, "u_mul_e", "sum", X16["X256"], H=H_GAT, E=S.s8,
+                                                          out=o256, stream=st)),
+    }
+    res["bf16_storage_ms"] = {k: round(v, 4) for k, v in bf.items()}
+    res["bf16_storage_note"] = ("row f4: same fp32 arithmetic and outputs, X (and Y) stored as bf16; "
+                                "parity vs the oracle on the decoded inputs in tests/test_parity_gpu.py")
+    return res
 
 
 def run_e2e(S, host, args, world, sync_all, flush):

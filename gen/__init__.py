@@ -189,3 +189,15 @@ def make_graph(name: str, uniform_sources: bool = False, scale: float = 1.0) -> 
 
 def feature_seed(graph_name: str) -> int:
     return SEED_BASE + CONFIGS[graph_name]["idx"] + 101
+
+
+def to_bf16(x: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Storage conversion for the bf16-feature inputs (row f4): fp32 -> bf16 by
+    round-to-nearest-even on the bit pattern (finite inputs).  Returns the
+    uint16 bits (what the GPU side receives) and their exact fp32 decoding
+    (what the oracle receives).  No method arithmetic: input preparation only."""
+    b = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    r = (b + 0x7FFF + ((b >> 16) & 1)) >> 16
+    bits = r.astype(np.uint16)
+    dec = (bits.astype(np.uint32) << 16).view(np.float32)
+    return bits, dec

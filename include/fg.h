@@ -206,6 +206,30 @@ fg_status fg_edge_softmax(const fg_graph* g, int H, const float* scores, float* 
 fg_status fg_gat_attention(const fg_graph* g, int H, int D, const float* X, const float* Y, float* out,
                            float* scores, fg_stream stream);
 
+/* ---------------------------------------------------------- bf16 features */
+/*
+ * Row f4: bf16 STORAGE of the vertex features, fp32 arithmetic.
+ * The messages and reductions are those of fg_spmm / fg_sddmm (Eq. (1), (4));
+ * only the gathered operand is narrower (8 bytes per 4 features instead of
+ * 16: the gathers -- the bound of these kernels, DESIGN.md §6 -- move half
+ * the bytes).  bf16 -> fp32 is exact, so the result is the fp32 computation on
+ * the bf16-representable inputs, to the same tolerance (1e-4 * sum|terms|
+ * against the fp64 oracle on the decoded inputs).
+ *
+ * fg_spmm_x16 -- msg in {FG_MSG_COPY_U, FG_MSG_U_MUL_E}, red in {FG_REDUCE_SUM,
+ *   FG_REDUCE_MAX} (else FG_EUNSUPPORTED).  X : bf16 bits [n_src][H*D]
+ *   (uint16, 8-byte aligned); E : fp32 [nnz][H] for u_mul_e, else NULL;
+ *   out fp32 [n_dst][H*D]; arg_u / arg_e as fg_spmm (max only).  Same
+ *   semantics, tie rules, empty-row conventions and errors as fg_spmm.
+ * fg_sddmm_x16 -- op FG_EDGE_U_DOT_V only.  X [n_src][H][D], Y [n_dst][H][D]
+ *   bf16 bits (8-byte aligned); out fp32 [nnz][H].  Shape rules as fg_sddmm.
+ */
+fg_status fg_spmm_x16(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D,
+                      const uint16_t* X, const float* E, float* out, int32_t* arg_u, int32_t* arg_e,
+                      fg_stream stream);
+fg_status fg_sddmm_x16(const fg_graph* g, fg_edge_op op, int H, int D, const uint16_t* X,
+                       const uint16_t* Y, float* out, fg_stream stream);
+
 /* ---------------------------------------------------------------- backward */
 /*
  * Gradients by the paper's gradient duality (the gradient

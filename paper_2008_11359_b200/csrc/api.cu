@@ -121,6 +121,46 @@ extern "C" fg_status fg_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, co
     return fgk::launch_sddmm(g, H, D, X, Y, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
+extern "C" fg_status fg_spmm_x16(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D,
+                                 const uint16_t* X, const float* E, float* out, int32_t* arg_u, int32_t* arg_e,
+                                 fg_stream stream) {
+    if (!g) return set_error(FG_EINVAL, "fg_spmm_x16: NULL graph");
+    if (msg != FG_MSG_COPY_U && msg != FG_MSG_U_MUL_E)
+        return set_error(FG_EUNSUPPORTED, "fg_spmm_x16: only copy_u and u_mul_e (got msg %d)", int(msg));
+    if (red != FG_REDUCE_SUM && red != FG_REDUCE_MAX)
+        return set_error(FG_EUNSUPPORTED, "fg_spmm_x16: only sum and max (got reduce %d)", int(red));
+    if (red == FG_REDUCE_SUM && (arg_u || arg_e)) return set_error(FG_EINVAL, "fg_spmm_x16: arg_u/arg_e with sum");
+    if (H < 1 || D < 1) return set_error(FG_ESHAPE, "fg_spmm_x16: H=%d D=%d must be >= 1", H, D);
+    const int64_t F = int64_t(H) * D;
+    if (F % 4 != 0 || F > (int64_t(1) << 20))
+        return set_error(FG_ESHAPE, "fg_spmm_x16: H*D=%lld must be a multiple of 4 (<= 2^20)", (long long)F);
+    if (!out && g->n_dst > 0) return set_error(FG_EINVAL, "fg_spmm_x16: out is NULL");
+    if (!X && g->nnz > 0) return set_error(FG_EINVAL, "fg_spmm_x16: X is NULL");
+    if (msg == FG_MSG_U_MUL_E && !E && g->nnz > 0) return set_error(FG_EINVAL, "fg_spmm_x16(u_mul_e): E is NULL");
+    if (msg == FG_MSG_COPY_U && E) return set_error(FG_EINVAL, "fg_spmm_x16(copy_u): E must be NULL");
+    if ((reinterpret_cast<uintptr_t>(X) & 7u) != 0 || !aligned16(out) || !aligned16(arg_u) || !aligned16(arg_e))
+        return set_error(FG_EINVAL, "fg_spmm_x16: X must be 8-byte, out/arg 16-byte aligned");
+    if (g->n_dst == 0) return FG_OK;
+    return fgk::launch_spmm_gather(g, msg, red, H, D, nullptr, E, out, arg_u, arg_e,
+                                   reinterpret_cast<cudaStream_t>(stream), X);
+}
+
+extern "C" fg_status fg_sddmm_x16(const fg_graph* g, fg_edge_op op, int H, int D, const uint16_t* X,
+                                  const uint16_t* Y, float* out, fg_stream stream) {
+    if (!g) return set_error(FG_EINVAL, "fg_sddmm_x16: NULL graph");
+    if (op != FG_EDGE_U_DOT_V) return set_error(FG_EUNSUPPORTED, "fg_sddmm_x16: only u_dot_v (got %d)", int(op));
+    if (H < 1 || D < 1) return set_error(FG_ESHAPE, "fg_sddmm_x16: H=%d D=%d must be >= 1", H, D);
+    const int64_t F = int64_t(H) * D;
+    if (F % 4 != 0 || F > (int64_t(1) << 20)) return set_error(FG_ESHAPE, "fg_sddmm_x16: H*D must be a multiple of 4");
+    if (H > 1 && (D % 4 != 0 || ((D / 4) & (D / 4 - 1)) != 0))
+        return set_error(FG_ESHAPE, "fg_sddmm_x16: with H > 1, D must be 4 * 2^k (got D=%d)", D);
+    if (g->nnz == 0) return FG_OK;
+    if (!X || !Y || !out) return set_error(FG_EINVAL, "fg_sddmm_x16: NULL tensor");
+    if ((reinterpret_cast<uintptr_t>(X) & 7u) != 0 || (reinterpret_cast<uintptr_t>(Y) & 7u) != 0 || !aligned16(out))
+        return set_error(FG_EINVAL, "fg_sddmm_x16: X/Y must be 8-byte, out 16-byte aligned");
+    return fgk::launch_sddmm(g, H, D, nullptr, nullptr, out, reinterpret_cast<cudaStream_t>(stream), X, Y);
+}
+
 extern "C" fg_status fg_edge_softmax(const fg_graph* g, int H, const float* scores, float* out, fg_stream stream) {
     if (!g) return set_error(FG_EINVAL, "fg_edge_softmax: NULL graph");
     if (H < 1 || H > 4096) return set_error(FG_ESHAPE, "fg_edge_softmax: H=%d out of range", H);

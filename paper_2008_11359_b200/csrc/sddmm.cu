@@ -52,6 +52,20 @@ struct Args {
     int persistent;   // != 0: persistent grid (resident CTAs per SM x #SMs; > 0 caps the CTAs per SM)
 };
 
+// 4 bf16 (one 8-byte chunk, feature 0 in the low half of .x) -> 4 fp32, exact
+__device__ __forceinline__ float4 bf16x4(uint2 w) {
+    return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y << 16),
+                       __uint_as_float(w.y & 0xffff0000u));
+}
+
+// chunk c (4 features) of row r of a feature matrix with F4 chunks per row;
+// XB: bf16 storage (the float4 pointer then addresses 8-byte chunks)
+template <bool XB>
+__device__ __forceinline__ float4 ld_chunk(const float4* __restrict__ M, int64_t r, int F4, int c) {
+    if constexpr (XB) return bf16x4(__ldg(reinterpret_cast<const uint2*>(M) + r * F4 + c));
+    else return __ldg(M + r * F4 + c);
+}
+
 __device__ __forceinline__ float dot4(const float4& a, const float4& b) {
     return fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, a.w * b.w)));
 }
@@ -98,7 +112,7 @@ __device__ __forceinline__ void reduce_scatter(float (&v)[K], int gl, unsigned m
 //                lane belongs to head c / D4; reduce over D4 lanes per chunk.
 // MODE_GENERAL : H == 1 with F > 4*G*NV (column tiles; Y re-read through L1), or
 //                H > 1 with D4 > G (a head spans several chunks of a lane).
-template <int G, int NV, int MODE, int DW>
+template <int G, int NV, int MODE, int DW, bool XB>
 __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const float4* __restrict__ X,
                                                            const float4* __restrict__ Y, float* __restrict__ out) {
     constexpr int TW = G * NV;
@@ -127,11 +141,10 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
     float* res = s_res[gi];
 
     float4 y0[NV];
-    const float4* yr = Y + v * F4;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const int c = A.c4base + gl + G * j;
-        y0[j] = (c < F4) ? __ldg(yr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        y0[j] = (c < F4) ? ld_chunk<XB>(Y, v, F4, c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
     constexpr int PF = (B + G - 1) / G;   // running sums per lane in a tiled pass (H == 1)
@@ -157,11 +170,10 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
             for (int uu = 0; uu < U; ++uu) {
                 const int t = t0 + uu;
                 us[uu] = (t < cnt) ? idx[t] : 0;
-                const float4* xr = X + int64_t(us[uu]) * F4;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     const int c = A.c4base + gl + G * j;
-                    x[uu][j] = (t < cnt && c < F4) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    x[uu][j] = (t < cnt && c < F4) ? ld_chunk<XB>(X, us[uu], F4, c) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
             if constexpr (MODE == MODE_H1 || MODE == MODE_HEADS) {
@@ -239,11 +251,10 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                         }
                     }
                     if (H == 1) {
-                        const float4* xr = X + int64_t(us[uu]) * F4;
                         for (int tile = 1; tile < ntiles; ++tile)
                             for (int j = 0; j < NV; ++j) {
                                 const int c = tile * TW + gl + G * j;
-                                if (c < F4) hs += dot4(__ldg(xr + c), __ldg(yr + c));
+                                if (c < F4) hs += dot4(ld_chunk<XB>(X, us[uu], F4, c), ld_chunk<XB>(Y, v, F4, c));
                             }
                         const float tot = group_sum<G>(hs, G, mask);
                         if (gl == 0) rr[0] = tot;
@@ -274,24 +285,24 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
     }   // units
 }
 
-template <int G, int NV>
+template <int G, int NV, bool XB = false>
 fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, cudaStream_t st) {
     using K = void (*)(const Args, const float4*, const float4*, float*);
     const int TW = G * NV;
     K k;
     if (A.H == 1 && (A.tile4 ? A.tile4 : A.F4) <= TW) {
-        k = sddmm_kernel<G, NV, MODE_H1, G>;
+        k = sddmm_kernel<G, NV, MODE_H1, G, XB>;
     } else if (A.H > 1 && A.D4 <= G && A.F4 <= TW) {
         switch (A.D4) {   // heads of D = 4*D4 floats reduce over D4 lanes
-            case 1: k = sddmm_kernel<G, NV, MODE_HEADS, 1>; break;
-            case 2: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 2 ? 2 : 1)>; break;
-            case 4: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 4 ? 4 : 1)>; break;
-            case 8: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 8 ? 8 : 1)>; break;
-            case 16: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 16 ? 16 : 1)>; break;
-            default: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 32 ? 32 : 1)>; break;
+            case 1: k = sddmm_kernel<G, NV, MODE_HEADS, 1, XB>; break;
+            case 2: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 2 ? 2 : 1), XB>; break;
+            case 4: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 4 ? 4 : 1), XB>; break;
+            case 8: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 8 ? 8 : 1), XB>; break;
+            case 16: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 16 ? 16 : 1), XB>; break;
+            default: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 32 ? 32 : 1), XB>; break;
         }
     } else {
-        k = sddmm_kernel<G, NV, MODE_GENERAL, 1>;
+        k = sddmm_kernel<G, NV, MODE_GENERAL, 1, XB>;
     }
     const int64_t per_block = THREADS / G;
     int64_t blocks = (A.n_units + per_block - 1) / per_block;
@@ -312,7 +323,8 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
 namespace fgk {
 
 fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const float* Y, float* out,
-                       cudaStream_t st) {
+                       cudaStream_t st, const uint16_t* Xbf16, const uint16_t* Ybf16) {
+    const bool xb = Xbf16 != nullptr;   // bf16 storage of X and Y (fg_sddmm_x16)
     Args A;
     A.unit_row = g->unit_row;
     A.unit_p0 = g->unit_p0;
@@ -330,8 +342,8 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     A.tile4 = 0;
     A.persistent = 0;
     int F4 = A.F4;
-    const float4* X4 = reinterpret_cast<const float4*>(X);
-    const float4* Y4 = reinterpret_cast<const float4*>(Y);
+    const float4* X4 = reinterpret_cast<const float4*>(xb ? static_cast<const void*>(Xbf16) : X);
+    const float4* Y4 = reinterpret_cast<const float4*>(xb ? static_cast<const void*>(Ybf16) : Y);
     // Feature-dimension tiling for L2 (as in spmm.cu): for H == 1 and
     // X larger than the L2 budget, pass k computes the partial dot over float4
     // columns [k*T4, (k+1)*T4) and accumulates into out (fixed pass order:
@@ -342,7 +354,7 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
         // (25.8 ms at 64 MB vs 21.3 untiled, even with the running sums prefetched;
         // the narrow-group per-edge reduction, not the traffic, is the limit)
         const char* on = getenv("FG_SDDMM_L2_TILE");
-        if (on && on[0] == '1' && H == 1 && budget > 0 && g->n_src * int64_t(F4) * 16 > budget) {
+        if (!xb && on && on[0] == '1' && H == 1 && budget > 0 && g->n_src * int64_t(F4) * 16 > budget) {
             int t4 = 32;
             while (t4 > 1 && g->n_src * int64_t(t4) * 16 > budget) t4 /= 2;
             A.tile4 = t4;
@@ -378,7 +390,7 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     {
         const char* mb = getenv("FG_SDDMM_SEG_MB");
         const int64_t budget = int64_t(mb ? atoi(mb) : 48) << 20;
-        const int64_t row_bytes = int64_t(F4) * 16;
+        const int64_t row_bytes = int64_t(F4) * (xb ? 8 : 16);
         if (A.tile4 == 0 && budget > 0 && g->n_src * row_bytes > budget) {
             int64_t seg_rows = budget / row_bytes;
             seg_rows = seg_rows < 32 ? 32 : seg_rows;
@@ -405,6 +417,20 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     }
     if (H > 1 && F4 > G * NV)
         return set_error(FG_EUNSUPPORTED, "fg_sddmm: multi-head with H*D > 512 not implemented");
+    if (xb) {
+        switch (G) {
+            case 1: return launch_t<1, 1, true>(A, X4, Y4, out, st);
+            case 2: return launch_t<2, 1, true>(A, X4, Y4, out, st);
+            case 4: return launch_t<4, 1, true>(A, X4, Y4, out, st);
+            case 8: return launch_t<8, 1, true>(A, X4, Y4, out, st);
+            case 16: return launch_t<16, 1, true>(A, X4, Y4, out, st);
+            default:
+                if (NV == 1) return launch_t<32, 1, true>(A, X4, Y4, out, st);
+                if (NV == 2) return launch_t<32, 2, true>(A, X4, Y4, out, st);
+                if (NV == 3) return launch_t<32, 3, true>(A, X4, Y4, out, st);
+                return launch_t<32, 4, true>(A, X4, Y4, out, st);
+        }
+    }
     switch (G) {
         case 1: return launch_t<1, 1>(A, X4, Y4, out, st);
         case 2: return launch_t<2, 1>(A, X4, Y4, out, st);

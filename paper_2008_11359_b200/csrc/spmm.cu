@@ -37,7 +37,8 @@
 namespace fgk {
 
 fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D, const float* X,
-                             const float* E, float* out, int32_t* arg_u, int32_t* arg_e, cudaStream_t st) {
+                             const float* E, float* out, int32_t* arg_u, int32_t* arg_e, cudaStream_t st,
+                             const uint16_t* Xbf16) {
     using namespace fgspmm;
     Args A;
     A.rows = g->rows_by_deg;
@@ -46,6 +47,8 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     A.col_idx = g->col_idx;
     A.eid = g->eid;
     A.X = reinterpret_cast<const float4*>(X);
+    A.Xh = reinterpret_cast<const uint2*>(Xbf16);
+    const int64_t chunk_bytes = Xbf16 ? 8 : 16;   // bytes of X per 4-feature chunk
     A.E = E;
     A.H = H;
     A.D = D;
@@ -71,9 +74,9 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
         const int64_t budget = fgk::l2_tile_budget();
         // copy_u only: u_mul_e re-reads E (m x H floats) on every pass, measured slower
         // at every budget (reddit H=8 D=32: 9.1-10.1 ms untiled vs 12.2-43.6 ms tiled)
-        if (msg == FG_MSG_COPY_U && budget > 0 && g->n_src * int64_t(F4) * 16 > budget) {
+        if (msg == FG_MSG_COPY_U && budget > 0 && g->n_src * int64_t(F4) * chunk_bytes > budget) {
             int64_t t4 = 32;
-            while (t4 > 1 && g->n_src * t4 * 16 > budget) t4 /= 2;
+            while (t4 > 1 && g->n_src * t4 * chunk_bytes > budget) t4 /= 2;
             F4 = int(t4);            // tile width drives (G, NV) below; the kernel tiles A.F4 by G*NV
         }
     }
@@ -92,6 +95,10 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     const int64_t NG = THREADS / G;
     A.n_heavy = rows_with_degree_at_least(g, NG * 32);
     const int opset = (op == OP_UADDE || op == OP_COPYE) ? 1 : 0;
+    if (Xbf16) {   // bf16 storage: copy_u / u_mul_e x {sum, max} (validated by the caller)
+        if (mx == R_MAX) return dispatch_x16<R_MAX>(A, G, NV, op, st);
+        return dispatch_x16<R_SUM>(A, G, NV, op, st);
+    }
     switch (mx) {
         case R_MAX: return opset ? dispatch_inst<R_MAX, 1>(A, G, NV, op, st) : dispatch_inst<R_MAX, 0>(A, G, NV, op, st);
         case R_MIN: return opset ? dispatch_inst<R_MIN, 1>(A, G, NV, op, st) : dispatch_inst<R_MIN, 0>(A, G, NV, op, st);

@@ -27,6 +27,7 @@ struct Args {
     const int32_t* col_idx;
     const int32_t* eid;
     const float4* X;
+    const uint2* Xh;            // bf16 storage of X (fg_spmm_x16): 4 features per 8-byte chunk
     const float* E;
     int H, D, F4;
     float4* out;
@@ -35,6 +36,11 @@ struct Args {
 };
 
 __device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); }
+// 4 bf16 (one 8-byte chunk, feature 0 in the low half of .x) -> 4 fp32, exact
+__device__ __forceinline__ float4 bf16x4(uint2 w) {
+    return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y << 16),
+                       __uint_as_float(w.y & 0xffff0000u));
+}
 __device__ __forceinline__ float comp(const float4& v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
 __device__ __forceinline__ void set_comp(float4& v, int k, float a) {
     if (k == 0) v.x = a; else if (k == 1) v.y = a; else if (k == 2) v.z = a; else v.w = a;
@@ -48,7 +54,7 @@ constexpr bool stage_e() {
 }
 
 // Accumulate edges [s, e) of one row into (acc, pos) for this lane's NV chunks.
-template <int G, int NV, int OP, int RED>
+template <int G, int NV, int OP, int RED, bool XB>
 __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e, int gl, unsigned mask,
                                              int c4base, float4 (&acc)[NV], int (&pos)[NV][4],
                                              float* __restrict__ etile) {
@@ -94,11 +100,13 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                 if constexpr (OP != OP_COPY) ed = __shfl_sync(mask, eix[t / G], t % G, G);
                 const float4* xr = (OP == OP_COPYE) ? reinterpret_cast<const float4*>(A.E) + int64_t(ed) * F4
                                                     : A.X + int64_t(u) * F4;
+                const uint2* xh = A.Xh + int64_t(u) * F4;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     const int c = c4base + gl + G * j;
                     const bool ok = (t < cnt) && (c < F4);
-                    x[uu][j] = ok ? __ldg(xr + c) : f4(0.f);
+                    if constexpr (XB) x[uu][j] = ok ? bf16x4(__ldg(xh + c)) : f4(0.f);
+                    else x[uu][j] = ok ? __ldg(xr + c) : f4(0.f);
                     if constexpr (OP == OP_UMULE) {
                         const int h = (4 * c) / A.D;
                         ev[uu][j][0] = !ok ? 0.f : (staged ? etile[t * A.H + h] : __ldg(A.E + int64_t(ed) * A.H + h));
@@ -205,7 +213,7 @@ __device__ __forceinline__ void store_elem(const Args& A, int64_t v, int c, floa
     }
 }
 
-template <int G, int NV, int OP, int RED>
+template <int G, int NV, int OP, int RED, bool XB>
 __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);
     constexpr int NG = THREADS / G;                 // groups per CTA
@@ -231,7 +239,7 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
         const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
         const int64_t len = (e - s + NG - 1) / NG;
         const int64_t gs = min(e, s + gi * len), ge = min(e, gs + len);
-        gather_range<G, NV, OP, RED>(A, gs, ge, gl, mask, c4base, acc, pos, s_etile[gi]);
+        gather_range<G, NV, OP, RED, XB>(A, gs, ge, gl, mask, c4base, acc, pos, s_etile[gi]);
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
             const int c = gl + G * j;
@@ -274,7 +282,7 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     if (r >= A.n_rows) return;
     const int64_t v = A.rows[r];
     const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
-    gather_range<G, NV, OP, RED>(A, s, e, gl, mask, c4base, acc, pos, s_etile[gi]);
+    gather_range<G, NV, OP, RED, XB>(A, s, e, gl, mask, c4base, acc, pos, s_etile[gi]);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const int c = c4base + gl + G * j;
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     }
 }
 
-template <int G, int NV, int OP, int RED>
+template <int G, int NV, int OP, int RED, bool XB = false>
 fg_status launch_t(const Args& A0, cudaStream_t st) {
     Args A = A0;
     constexpr int NG = THREADS / G;
@@ -292,7 +300,7 @@ fg_status launch_t(const Args& A0, cudaStream_t st) {
     const int tiles = (A.F4 + TW - 1) / TW;
     if (blocks == 0) return FG_OK;
     const dim3 grid{unsigned(blocks), unsigned(tiles), 1u};
-    spmm_gather_kernel<G, NV, OP, RED><<<grid, THREADS, 0, st>>>(A);
+    spmm_gather_kernel<G, NV, OP, RED, XB><<<grid, THREADS, 0, st>>>(A);
     return fgk::check_launch("spmm_gather_kernel");
 }
 
@@ -317,5 +325,12 @@ template <>
 fg_status dispatch_inst<R_MEAN, 0>(const Args& A, int G, int NV, int op, cudaStream_t st);
 template <>
 fg_status dispatch_inst<R_MEAN, 1>(const Args& A, int G, int NV, int op, cudaStream_t st);
+// bf16 storage of X (copy_u, u_mul_e; sum and max): spmm_inst_x16.cu
+template <int RED>
+fg_status dispatch_x16(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_x16<R_SUM>(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_x16<R_MAX>(const Args& A, int G, int NV, int op, cudaStream_t st);
 
 }  // namespace fgspmm

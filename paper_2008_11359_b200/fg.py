@@ -28,7 +28,7 @@ EDGE = {"u_dot_v": 0, "u_add_v": 1, "u_sub_v": 2, "u_mul_v": 3}
 SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
            "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
            "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
-           "fg_allgather_rows", "fg_status_string", "fg_last_error", "fg_abi_version"]
+           "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_status_string", "fg_last_error", "fg_abi_version"]
 
 
 class FGError(RuntimeError):
@@ -61,6 +61,8 @@ def lib() -> ctypes.CDLL:
     L.fg_spmm_workspace_size.argtypes = [vp, i32, i32, i32, i32, i32, ctypes.POINTER(sz)]
     L.fg_spmm.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]
     L.fg_sddmm.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
+    L.fg_spmm_x16.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]
+    L.fg_sddmm_x16.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
     L.fg_edge_softmax.argtypes = [vp, i32, vp, vp, vp]
     L.fg_gat_attention.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp]
     L.fg_graph_transpose.argtypes = [vp, vp, ctypes.POINTER(vp)]
@@ -74,7 +76,7 @@ def lib() -> ctypes.CDLL:
     for f in ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
               "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
               "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
-              "fg_allgather_rows"]:
+              "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16"]:
         getattr(L, f).restype = i32
     L.fg_status_string.argtypes = [i32]
     L.fg_status_string.restype = ctypes.c_char_p
@@ -180,7 +182,10 @@ def spmm(g: Graph, msg: str, reduce: str, X: torch.Tensor, *, H: int = 1, E: tor
          W: torch.Tensor | None = None, X_dst: torch.Tensor | None = None, out: torch.Tensor | None = None,
          arg_u: torch.Tensor | bool | None = None, arg_e: torch.Tensor | bool | None = None, stream=None):
     """featgraph.spmm (Eq. (1)).  Returns out, or (out, arg_u, arg_e) when args requested.
-    copy_e takes X=None and E [nnz][F]."""
+    copy_e takes X=None and E [nnz][F].  A torch.bfloat16 X selects bf16 feature
+    storage (fg_spmm_x16: copy_u / u_mul_e, sum / max; fp32 arithmetic and out)."""
+    if X is not None and X.dtype == torch.bfloat16:
+        return _spmm_x16(g, msg, reduce, X, H=H, E=E, out=out, arg_u=arg_u, arg_e=arg_e, stream=stream)
     X = _dev(X, torch.float32, "X")
     E, W, X_dst = _dev(E, torch.float32, "E"), _dev(W, torch.float32, "W"), _dev(X_dst, torch.float32, "X_dst")
     if msg == "copy_e":
@@ -213,11 +218,39 @@ def spmm(g: Graph, msg: str, reduce: str, X: torch.Tensor, *, H: int = 1, E: tor
     return out
 
 
+def _spmm_x16(g, msg, reduce, X, *, H, E, out, arg_u, arg_e, stream):
+    X = _dev(X, torch.bfloat16, "X")
+    E = _dev(E, torch.float32, "E")
+    F = X.numel() // max(X.shape[0], 1) if X.dim() > 1 else 1
+    if out is None:
+        out = torch.empty((g.n_dst, F), dtype=torch.float32, device=X.device)
+    want = reduce == "max" and (arg_u is not None or arg_e is not None)
+    if arg_u is True:
+        arg_u = torch.empty((g.n_dst, F), dtype=torch.int32, device=X.device)
+    if arg_e is True:
+        arg_e = torch.empty((g.n_dst, F), dtype=torch.int32, device=X.device)
+    arg_u = arg_u if isinstance(arg_u, torch.Tensor) else None
+    arg_e = arg_e if isinstance(arg_e, torch.Tensor) else None
+    _check(lib().fg_spmm_x16(g.handle, MSG[msg], REDUCE[reduce], H, F // H, _ptr(X), _ptr(E), _ptr(out),
+                             _ptr(arg_u), _ptr(arg_e), _stream(stream)), f"fg_spmm_x16({msg},{reduce})")
+    return (out, arg_u, arg_e) if want else out
+
+
 def sddmm(g: Graph, X: torch.Tensor, Y: torch.Tensor | None = None, *, H: int = 1, op: str = "u_dot_v",
           out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """featgraph.sddmm (Eq. (4), Fig. 5): out[eid][h] = <X[u,h,:], Y[v,h,:]> for
     op="u_dot_v"; the elementwise ops u_add_v / u_sub_v / u_mul_v give
-    out[eid][j] = X[u][j] OP Y[v][j] ([nnz][F])."""
+    out[eid][j] = X[u][j] OP Y[v][j] ([nnz][F]).  torch.bfloat16 X (and Y)
+    select bf16 feature storage (fg_sddmm_x16, u_dot_v; fp32 arithmetic and out)."""
+    if X.dtype == torch.bfloat16:
+        X = _dev(X, torch.bfloat16, "X")
+        Y = X if Y is None else _dev(Y, torch.bfloat16, "Y")
+        F = X.numel() // max(X.shape[0], 1)
+        if out is None:
+            out = torch.empty((g.nnz, H), dtype=torch.float32, device=X.device)
+        _check(lib().fg_sddmm_x16(g.handle, EDGE[op], H, F // H, _ptr(X), _ptr(Y), _ptr(out), _stream(stream)),
+               "fg_sddmm_x16")
+        return out
     X = _dev(X, torch.float32, "X")
     Y = X if Y is None else _dev(Y, torch.float32, "Y")
     F = X.numel() // max(X.shape[0], 1)

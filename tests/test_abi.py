@@ -20,7 +20,7 @@ def L():
 def header_functions():
     src = open(os.path.join(ROOT, "include", "fg.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_]+\*?\s+\*?(fg_[a-z_]+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_]+\*?\s+\*?(fg_[a-z0-9_]+)\s*\(", src, flags=re.M)))
 
 
 def test_exports_every_header_symbol(L):

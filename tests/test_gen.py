@@ -54,3 +54,15 @@ def test_rand100k_exact_edges():
 def test_lognormal_exact_sum_and_shape():
     d = gen.degrees_lognormal(232965 // 10, 114615892 // 10, 1.2, 21657, 7)
     assert d.sum() == 114615892 // 10 and d.min() >= 1 and d.max() <= 21657
+
+
+def test_to_bf16_round_to_nearest_even():
+    """gen.to_bf16 equals torch's fp32 -> bfloat16 conversion (RNE), and the
+    decoded values are exactly the bf16 values."""
+    import torch
+    x = gen.features((4096, 7), 5, 0) * np.float32(37.0)
+    x = np.concatenate([x.ravel(), np.float32([0.0, -0.0, 1.0, 1.00390625, 1.01171875, 3.0e38, -2.5e-38])])
+    bits, dec = gen.to_bf16(x)
+    t = torch.from_numpy(x).to(torch.bfloat16)
+    assert np.array_equal(bits, t.view(torch.int16).numpy().view(np.uint16))
+    assert np.array_equal(dec, t.to(torch.float32).numpy())

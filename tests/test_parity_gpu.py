@@ -540,3 +540,64 @@ def test_gat_fused(skewed, skewed_eid, H, D, use_eid):
     a = fgp.edge_softmax(g.h, s, H=H)
     o2 = fgp.spmm(g.h, "u_mul_e", "sum", dev(X), H=H, E=a).cpu().numpy()
     check_close(o2, ref, ab, TOL, "unfused chain")
+
+
+# ------------------------------------------------------------------ bf16 feature storage (row f4)
+def bf16_dev(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).cuda().view(torch.bfloat16)
+
+
+@pytest.mark.parametrize("F", [4, 32, 128, 200, 512, 640])
+@pytest.mark.parametrize("red", ["sum", "max"])
+def test_copy_u_bf16(skewed, F, red):
+    """fg_spmm_x16: the oracle runs on the exact fp32 decoding of the same bf16
+    inputs; sum to tolerance, max values and argmax exact."""
+    import paper_2008_11359_b200 as fgp
+    bits, dec = gen.to_bf16(feats((skewed.n_src, F), 700 + F, gen.REAL))
+    ref, ab, rau, rae = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", red, dec)
+    if red == "sum":
+        out = fgp.spmm(skewed.h, "copy_u", "sum", bf16_dev(bits)).cpu().numpy()
+        check_close(out, ref, ab, TOL, f"bf16 copy_u-sum F={F}")
+    else:
+        out, au, ae = fgp.spmm(skewed.h, "copy_u", "max", bf16_dev(bits), arg_u=True, arg_e=True)
+        assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+        assert np.array_equal(au.cpu().numpy(), rau) and np.array_equal(ae.cpu().numpy(), rae)
+
+
+@pytest.mark.parametrize("H,D", [(8, 32), (4, 2), (1, 512)])
+@pytest.mark.parametrize("red", ["sum", "max"])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_u_mul_e_bf16(skewed, skewed_eid, H, D, red, use_eid):
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    bits, dec = gen.to_bf16(feats((g.n_src, H * D), 710 + D, gen.REAL))
+    E = gen.features((g.nnz, H), 711, 0, gen.UNIT)
+    ref, ab, rau, rae = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", red, dec, H=H, E=E, eid=g.eid)
+    if red == "sum":
+        out = fgp.spmm(g.h, "u_mul_e", "sum", bf16_dev(bits), H=H, E=dev(E)).cpu().numpy()
+        check_close(out, ref, ab, TOL, f"bf16 u_mul_e-sum H={H} D={D}")
+    else:
+        out, au, ae = fgp.spmm(g.h, "u_mul_e", "max", bf16_dev(bits), H=H, E=dev(E), arg_u=True, arg_e=True)
+        assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+        assert np.array_equal(au.cpu().numpy(), rau) and np.array_equal(ae.cpu().numpy(), rae)
+
+
+@pytest.mark.parametrize("H,D", [(1, 16), (1, 128), (1, 512), (8, 32), (2, 4), (4, 64)])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_sddmm_bf16(skewed, skewed_eid, H, D, use_eid):
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    xb, xd = gen.to_bf16(feats((g.n_src, H * D), 720 + D, gen.REAL))
+    yb, yd = gen.to_bf16(feats((g.n_dst, H * D), 721 + D, gen.REAL))
+    out = fgp.sddmm(g.h, bf16_dev(xb), bf16_dev(yb), H=H).cpu().numpy()
+    ref, ab = oracle.sddmm(g.row_ptr, g.col_idx, xd, yd, H=H)
+    pos = np.arange(g.nnz) if g.eid is None else g.eid
+    check_close(out[pos], ref, ab, TOL, f"bf16 u_dot_v H={H} D={D}")
+
+
+def test_bf16_rejects_unsupported(skewed):
+    import paper_2008_11359_b200 as fgp
+    bits, _ = gen.to_bf16(feats((skewed.n_src, 32), 730, gen.REAL))
+    with pytest.raises(fgp.FGError) as e:
+        fgp.spmm(skewed.h, "copy_u", "mean", bf16_dev(bits))
+    assert e.value.status == 3   # FG_EUNSUPPORTED
