@@ -112,12 +112,31 @@ __device__ __forceinline__ void reduce_scatter(float (&v)[K], int gl, unsigned m
 //                lane belongs to head c / D4; reduce over D4 lanes per chunk.
 // MODE_GENERAL : H == 1 with F > 4*G*NV (column tiles; Y re-read through L1), or
 //                H > 1 with D4 > G (a head spans several chunks of a lane).
-template <int G, int NV, int MODE, int DW, bool XB>
+// Column (float4 index) of a lane's chunk j: PAIR (bf16 storage, H == 1) --
+// a lane owns pairs of adjacent chunks read with one 16-byte load (8 bf16);
+// otherwise chunk j of lane gl is column gl + G*j.
+template <int G, bool PAIR>
+__device__ __forceinline__ int colj(int gl, int j) {
+    if constexpr (PAIR) return 2 * (gl + G * (j >> 1)) + (j & 1);
+    else return gl + G * j;
+}
+
+// one 16-byte load of chunks c, c+1 (c even, bf16) -> two float4
+__device__ __forceinline__ void ld_pair(const float4* __restrict__ M, int64_t r, int F4, int c, float4& a,
+                                        float4& b) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint2*>(M) + r * F4 + c));
+    a = bf16x4(make_uint2(w.x, w.y));
+    b = bf16x4(make_uint2(w.z, w.w));
+}
+
+template <int G, int NV, int MODE, int DW, bool XB, bool PAIR = false>
 __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const float4* __restrict__ X,
                                                            const float4* __restrict__ Y, float* __restrict__ out) {
     constexpr int TW = G * NV;
     constexpr int B = G >= 4 ? 32 : 8;              // edges per batch
-    constexpr int U = NV >= 3 ? 2 : (NV == 2 ? 4 : 8);   // edges in flight per lane
+    // edges in flight per lane; PAIR keeps the raw bf16 pairs (half the registers of
+    // converted float4s), so it affords twice the edges -- the same bytes in flight
+    constexpr int U = PAIR ? (NV >= 4 ? 4 : 8) : (NV >= 3 ? 2 : (NV == 2 ? 4 : 8));
     constexpr int NGRP = THREADS / G;
     constexpr int CAP = 32 * G;                           // staged results per group
     __shared__ int s_idx[NGRP][B];
@@ -143,8 +162,15 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
     float4 y0[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-        const int c = A.c4base + gl + G * j;
-        y0[j] = (c < F4) ? ld_chunk<XB>(Y, v, F4, c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int c = A.c4base + colj<G, PAIR>(gl, j);
+        if constexpr (PAIR) {
+            if ((j & 1) == 0) {
+                if (c < F4) ld_pair(Y, v, F4, c, y0[j], y0[j + 1]);
+                else y0[j] = y0[j + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        } else {
+            y0[j] = (c < F4) ? ld_chunk<XB>(Y, v, F4, c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     }
 
     constexpr int PF = (B + G - 1) / G;   // running sums per lane in a tiled pass (H == 1)
@@ -164,7 +190,16 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
         }
         __syncwarp(mask);
         for (int t0 = 0; t0 < cnt; t0 += U) {
-            float4 x[U][NV];
+            float4 x[PAIR ? 1 : U][PAIR ? 1 : NV];
+            uint4 xw[PAIR ? U : 1][PAIR ? NV / 2 : 1];   // PAIR: raw bf16 chunk pairs
+            auto xv = [&](int uu, int j) -> float4 {
+                if constexpr (PAIR) {
+                    const uint4 w = xw[uu][j / 2];
+                    return (j & 1) ? bf16x4(make_uint2(w.z, w.w)) : bf16x4(make_uint2(w.x, w.y));
+                } else {
+                    return x[uu][j];
+                }
+            };
             int us[U];
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
@@ -172,8 +207,18 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                 us[uu] = (t < cnt) ? idx[t] : 0;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
-                    const int c = A.c4base + gl + G * j;
-                    x[uu][j] = (t < cnt && c < F4) ? ld_chunk<XB>(X, us[uu], F4, c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const int c = A.c4base + colj<G, PAIR>(gl, j);
+                    if constexpr (PAIR) {
+                        if ((j & 1) == 0) {
+                            xw[uu][j / 2] = (t < cnt && c < F4)
+                                                ? __ldg(reinterpret_cast<const uint4*>(
+                                                      reinterpret_cast<const uint2*>(X) + int64_t(us[uu]) * F4 + c))
+                                                : make_uint4(0, 0, 0, 0);
+                        }
+                    } else {
+                        x[uu][j] = (t < cnt && c < F4) ? ld_chunk<XB>(X, us[uu], F4, c)
+                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
                 }
             }
             if constexpr (MODE == MODE_H1 || MODE == MODE_HEADS) {
@@ -188,11 +233,11 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                         if constexpr (MODE == MODE_H1) {
                             float hs = 0.f;
 #pragma unroll
-                            for (int j = 0; j < NV; ++j) hs += dot4(x[uu][j], y0[j]);
+                            for (int j = 0; j < NV; ++j) hs += dot4(xv(uu, j), y0[j]);
                             pv[uu] = hs;
                         } else {
 #pragma unroll
-                            for (int j = 0; j < NV; ++j) pv[uu * NV + j] = dot4(x[uu][j], y0[j]);
+                            for (int j = 0; j < NV; ++j) pv[uu * NV + j] = dot4(xv(uu, j), y0[j]);
                         }
                     }
                     reduce_scatter<K, DW, G>(pv, gl, mask);
@@ -225,14 +270,14 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                 if constexpr (MODE == MODE_H1) {
                     float hs = 0.f;
 #pragma unroll
-                    for (int j = 0; j < NV; ++j) hs += dot4(x[uu][j], y0[j]);
+                    for (int j = 0; j < NV; ++j) hs += dot4(xv(uu, j), y0[j]);
                     hs = group_sum<G>(hs, G, mask);
                     if (gl == 0) rr[0] = hs;
                 } else if constexpr (MODE == MODE_HEADS) {
 #pragma unroll
                     for (int j = 0; j < NV; ++j) {
                         const int c = gl + G * j;
-                        const float part = group_sum<G>(dot4(x[uu][j], y0[j]), D4, mask);
+                        const float part = group_sum<G>(dot4(xv(uu, j), y0[j]), D4, mask);
                         if (c < F4 && (gl & (D4 - 1)) == 0) rr[c / D4] = part;
                     }
                 } else {
@@ -241,7 +286,7 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                     int head = 0;
 #pragma unroll
                     for (int j = 0; j < NV; ++j) {
-                        hs += dot4(x[uu][j], y0[j]);
+                        hs += dot4(xv(uu, j), y0[j]);
                         const int cend = G * (j + 1);
                         if (H > 1 && (j == NV - 1 || cend % D4 == 0)) {
                             const float tot = group_sum<G>(hs, G, mask);
@@ -285,24 +330,28 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
     }   // units
 }
 
-template <int G, int NV, bool XB = false>
+template <int G, int NV, bool XB = false, bool PAIR = false>
 fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, cudaStream_t st) {
     using K = void (*)(const Args, const float4*, const float4*, float*);
     const int TW = G * NV;
     K k;
-    if (A.H == 1 && (A.tile4 ? A.tile4 : A.F4) <= TW) {
-        k = sddmm_kernel<G, NV, MODE_H1, G, XB>;
-    } else if (A.H > 1 && A.D4 <= G && A.F4 <= TW) {
-        switch (A.D4) {   // heads of D = 4*D4 floats reduce over D4 lanes
-            case 1: k = sddmm_kernel<G, NV, MODE_HEADS, 1, XB>; break;
-            case 2: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 2 ? 2 : 1), XB>; break;
-            case 4: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 4 ? 4 : 1), XB>; break;
-            case 8: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 8 ? 8 : 1), XB>; break;
-            case 16: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 16 ? 16 : 1), XB>; break;
-            default: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 32 ? 32 : 1), XB>; break;
-        }
+    if constexpr (PAIR) {   // H == 1 only (launch_sddmm)
+        k = sddmm_kernel<G, NV, MODE_H1, G, XB, true>;
     } else {
-        k = sddmm_kernel<G, NV, MODE_GENERAL, 1, XB>;
+        if (A.H == 1 && (A.tile4 ? A.tile4 : A.F4) <= TW) {
+            k = sddmm_kernel<G, NV, MODE_H1, G, XB>;
+        } else if (A.H > 1 && A.D4 <= G && A.F4 <= TW) {
+            switch (A.D4) {   // heads of D = 4*D4 floats reduce over D4 lanes
+                case 1: k = sddmm_kernel<G, NV, MODE_HEADS, 1, XB>; break;
+                case 2: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 2 ? 2 : 1), XB>; break;
+                case 4: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 4 ? 4 : 1), XB>; break;
+                case 8: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 8 ? 8 : 1), XB>; break;
+                case 16: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 16 ? 16 : 1), XB>; break;
+                default: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 32 ? 32 : 1), XB>; break;
+            }
+        } else {
+            k = sddmm_kernel<G, NV, MODE_GENERAL, 1, XB>;
+        }
     }
     const int64_t per_block = THREADS / G;
     int64_t blocks = (A.n_units + per_block - 1) / per_block;
@@ -417,6 +466,27 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     }
     if (H > 1 && F4 > G * NV)
         return set_error(FG_EUNSUPPORTED, "fg_sddmm: multi-head with H*D > 512 not implemented");
+    // bf16, H == 1, one pass over an even number of chunks, 16-byte aligned X / Y:
+    // 16-byte loads of chunk pairs (G lanes x NV/2 pairs)
+    if (xb && H == 1 && F4 % 2 == 0 && F4 <= 256 && ((reinterpret_cast<uintptr_t>(Xbf16) |
+                                                    reinterpret_cast<uintptr_t>(Ybf16)) & 15u) == 0) {
+        const int F8 = F4 / 2;
+        if (F8 <= 32) {
+            int G2 = 1;
+            while (G2 < F8) G2 *= 2;
+            switch (G2) {
+                case 1: return launch_t<1, 2, true, true>(A, X4, Y4, out, st);
+                case 2: return launch_t<2, 2, true, true>(A, X4, Y4, out, st);
+                case 4: return launch_t<4, 2, true, true>(A, X4, Y4, out, st);
+                case 8: return launch_t<8, 2, true, true>(A, X4, Y4, out, st);
+                case 16: return launch_t<16, 2, true, true>(A, X4, Y4, out, st);
+                default: return launch_t<32, 2, true, true>(A, X4, Y4, out, st);
+            }
+        }
+        if (F8 <= 64) return launch_t<32, 4, true, true>(A, X4, Y4, out, st);
+        if (F8 <= 96) return launch_t<32, 6, true, true>(A, X4, Y4, out, st);
+        return launch_t<32, 8, true, true>(A, X4, Y4, out, st);
+    }
     if (xb) {
         switch (G) {
             case 1: return launch_t<1, 1, true>(A, X4, Y4, out, st);

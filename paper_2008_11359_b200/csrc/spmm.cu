@@ -92,12 +92,27 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     } else if (F4 <= 96) {
         NV = 3;
     }
+    // bf16 storage with an even number of 4-feature chunks per (tile) row and a
+    // 16-byte aligned X: lanes read PAIRS of chunks (8 features) with one 16-byte
+    // load -- half the load instructions of the 8-byte-per-chunk mapping
+    const bool pair = Xbf16 && A.F4 % 2 == 0 && F4 % 2 == 0 && (reinterpret_cast<uintptr_t>(Xbf16) & 15u) == 0;
+    if (pair) {
+        const int F8 = F4 / 2;
+        NV = 2;
+        if (F8 <= 32) {
+            G = 1;
+            while (G < F8) G *= 2;
+        } else {
+            G = 32;
+            NV = 4;   // 128 float4 columns per tile; wider rows take several tiles (grid.y)
+        }
+    }
     const int64_t NG = THREADS / G;
     A.n_heavy = rows_with_degree_at_least(g, NG * 32);
     const int opset = (op == OP_UADDE || op == OP_COPYE) ? 1 : 0;
     if (Xbf16) {   // bf16 storage: copy_u / u_mul_e x {sum, max} (validated by the caller)
-        if (mx == R_MAX) return dispatch_x16<R_MAX>(A, G, NV, op, st);
-        return dispatch_x16<R_SUM>(A, G, NV, op, st);
+        if (mx == R_MAX) return dispatch_x16<R_MAX>(A, G, NV, op, pair, st);
+        return dispatch_x16<R_SUM>(A, G, NV, op, pair, st);
     }
     switch (mx) {
         case R_MAX: return opset ? dispatch_inst<R_MAX, 1>(A, G, NV, op, st) : dispatch_inst<R_MAX, 0>(A, G, NV, op, st);

@@ -46,6 +46,15 @@ __device__ __forceinline__ void set_comp(float4& v, int k, float a) {
     if (k == 0) v.x = a; else if (k == 1) v.y = a; else if (k == 2) v.z = a; else v.w = a;
 }
 
+// Column (float4 index within the tile) of a lane's chunk j.  PAIR (bf16
+// storage, NV even): a lane owns pairs of adjacent chunks, read with ONE 16-byte
+// load (8 bf16 features); otherwise chunk j of lane gl is column gl + G*j.
+template <int G, bool PAIR>
+__device__ __forceinline__ int colj(int gl, int j) {
+    if constexpr (PAIR) return 2 * (gl + G * (j >> 1)) + (j & 1);
+    else return gl + G * j;
+}
+
 // u_mul_e stages each 32-edge batch's E rows in shared memory (NG x 512 floats)
 // when a whole warp owns the row (G == 32)
 template <int G, int OP, int RED>
@@ -54,13 +63,15 @@ constexpr bool stage_e() {
 }
 
 // Accumulate edges [s, e) of one row into (acc, pos) for this lane's NV chunks.
-template <int G, int NV, int OP, int RED, bool XB>
+template <int G, int NV, int OP, int RED, bool XB, bool PAIR>
 __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e, int gl, unsigned mask,
                                              int c4base, float4 (&acc)[NV], int (&pos)[NV][4],
                                              float* __restrict__ etile) {
     constexpr int B = 32;                                   // edges per index batch
     constexpr int R = B / G;                                // indices per lane per batch
-    constexpr int U = NV >= 4 ? 2 : (NV >= 2 ? 4 : 8);      // edges in flight per lane
+    // edges in flight per lane; PAIR keeps raw bf16 pairs (half the registers), so
+    // it affords twice the edges -- the same bytes in flight as the fp32 mapping
+    constexpr int U = PAIR ? (NV >= 4 ? 4 : 8) : (NV >= 4 ? 2 : (NV >= 2 ? 4 : 8));
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);     // select-type reducers
     const int F4 = A.F4;
     for (int64_t p0 = s; p0 < e; p0 += B) {
@@ -89,7 +100,8 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
 #pragma unroll
         for (int t0 = 0; t0 < B; t0 += U) {
             if (t0 >= cnt) break;                           // uniform within the group
-            float4 x[U][NV];
+            float4 x[PAIR ? 1 : U][PAIR ? 1 : NV];
+            uint4 xw[PAIR ? U : 1][PAIR ? NV / 2 : 1];   // PAIR: raw bf16 pairs, converted at use
             constexpr bool PERK = (OP == OP_UMULE_GEN || OP == OP_UADDE);   // head per component
             float ev[U][NV][PERK ? 4 : 1];
 #pragma unroll
@@ -103,10 +115,16 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                 const uint2* xh = A.Xh + int64_t(u) * F4;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
-                    const int c = c4base + gl + G * j;
+                    const int c = c4base + colj<G, PAIR>(gl, j);
                     const bool ok = (t < cnt) && (c < F4);
-                    if constexpr (XB) x[uu][j] = ok ? bf16x4(__ldg(xh + c)) : f4(0.f);
-                    else x[uu][j] = ok ? __ldg(xr + c) : f4(0.f);
+                    if constexpr (PAIR) {   // F4 even: c even, c + 1 < F4 with c
+                        if ((j & 1) == 0)
+                            xw[uu][j / 2] = ok ? __ldg(reinterpret_cast<const uint4*>(xh + c)) : make_uint4(0, 0, 0, 0);
+                    } else if constexpr (XB) {
+                        x[uu][j] = ok ? bf16x4(__ldg(xh + c)) : f4(0.f);
+                    } else {
+                        x[uu][j] = ok ? __ldg(xr + c) : f4(0.f);
+                    }
                     if constexpr (OP == OP_UMULE) {
                         const int h = (4 * c) / A.D;
                         ev[uu][j][0] = !ok ? 0.f : (staged ? etile[t * A.H + h] : __ldg(A.E + int64_t(ed) * A.H + h));
@@ -126,32 +144,39 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                 const int p = int(p0) + t;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
+                    float4 xv;
+                    if constexpr (PAIR) {
+                        const uint4 w = xw[uu][j / 2];
+                        xv = (j & 1) ? bf16x4(make_uint2(w.z, w.w)) : bf16x4(make_uint2(w.x, w.y));
+                    } else {
+                        xv = x[uu][j];
+                    }
                     if constexpr (!MAX) {
                         if constexpr (OP == OP_COPY) {
-                            acc[j].x += x[uu][j].x; acc[j].y += x[uu][j].y;
-                            acc[j].z += x[uu][j].z; acc[j].w += x[uu][j].w;
+                            acc[j].x += xv.x; acc[j].y += xv.y;
+                            acc[j].z += xv.z; acc[j].w += xv.w;
                         } else if constexpr (OP == OP_UMULE) {
                             const float w = ev[uu][j][0];
-                            acc[j].x = fmaf(x[uu][j].x, w, acc[j].x); acc[j].y = fmaf(x[uu][j].y, w, acc[j].y);
-                            acc[j].z = fmaf(x[uu][j].z, w, acc[j].z); acc[j].w = fmaf(x[uu][j].w, w, acc[j].w);
+                            acc[j].x = fmaf(xv.x, w, acc[j].x); acc[j].y = fmaf(xv.y, w, acc[j].y);
+                            acc[j].z = fmaf(xv.z, w, acc[j].z); acc[j].w = fmaf(xv.w, w, acc[j].w);
                         } else if constexpr (OP == OP_UADDE) {
-                            acc[j].x += __fadd_rn(x[uu][j].x, ev[uu][j][0]);
-                            acc[j].y += __fadd_rn(x[uu][j].y, ev[uu][j][1]);
-                            acc[j].z += __fadd_rn(x[uu][j].z, ev[uu][j][2]);
-                            acc[j].w += __fadd_rn(x[uu][j].w, ev[uu][j][3]);
+                            acc[j].x += __fadd_rn(xv.x, ev[uu][j][0]);
+                            acc[j].y += __fadd_rn(xv.y, ev[uu][j][1]);
+                            acc[j].z += __fadd_rn(xv.z, ev[uu][j][2]);
+                            acc[j].w += __fadd_rn(xv.w, ev[uu][j][3]);
                         } else if constexpr (OP == OP_COPYE) {
-                            acc[j].x += x[uu][j].x; acc[j].y += x[uu][j].y;
-                            acc[j].z += x[uu][j].z; acc[j].w += x[uu][j].w;
+                            acc[j].x += xv.x; acc[j].y += xv.y;
+                            acc[j].z += xv.z; acc[j].w += xv.w;
                         } else {
-                            acc[j].x = fmaf(x[uu][j].x, ev[uu][j][0], acc[j].x);
-                            acc[j].y = fmaf(x[uu][j].y, ev[uu][j][1], acc[j].y);
-                            acc[j].z = fmaf(x[uu][j].z, ev[uu][j][2], acc[j].z);
-                            acc[j].w = fmaf(x[uu][j].w, ev[uu][j][3], acc[j].w);
+                            acc[j].x = fmaf(xv.x, ev[uu][j][0], acc[j].x);
+                            acc[j].y = fmaf(xv.y, ev[uu][j][1], acc[j].y);
+                            acc[j].z = fmaf(xv.z, ev[uu][j][2], acc[j].z);
+                            acc[j].w = fmaf(xv.w, ev[uu][j][3], acc[j].w);
                         }
                     } else {
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
-                            float m = comp(x[uu][j], k);
+                            float m = comp(xv, k);
                             if constexpr (OP == OP_UMULE) m = __fmul_rn(m, ev[uu][j][0]);
                             else if constexpr (OP == OP_UMULE_GEN) m = __fmul_rn(m, ev[uu][j][k]);
                             else if constexpr (OP == OP_UADDE) m = __fadd_rn(m, ev[uu][j][k]);
@@ -213,7 +238,7 @@ __device__ __forceinline__ void store_elem(const Args& A, int64_t v, int c, floa
     }
 }
 
-template <int G, int NV, int OP, int RED, bool XB>
+template <int G, int NV, int OP, int RED, bool XB, bool PAIR>
 __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);
     constexpr int NG = THREADS / G;                 // groups per CTA
@@ -239,10 +264,10 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
         const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
         const int64_t len = (e - s + NG - 1) / NG;
         const int64_t gs = min(e, s + gi * len), ge = min(e, gs + len);
-        gather_range<G, NV, OP, RED, XB>(A, gs, ge, gl, mask, c4base, acc, pos, s_etile[gi]);
+        gather_range<G, NV, OP, RED, XB, PAIR>(A, gs, ge, gl, mask, c4base, acc, pos, s_etile[gi]);
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-            const int c = gl + G * j;
+            const int c = colj<G, PAIR>(gl, j);
             if constexpr (!MAX) {
                 s_acc[gi][c] = acc[j];
             } else {
@@ -282,15 +307,15 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     if (r >= A.n_rows) return;
     const int64_t v = A.rows[r];
     const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
-    gather_range<G, NV, OP, RED, XB>(A, s, e, gl, mask, c4base, acc, pos, s_etile[gi]);
+    gather_range<G, NV, OP, RED, XB, PAIR>(A, s, e, gl, mask, c4base, acc, pos, s_etile[gi]);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-        const int c = c4base + gl + G * j;
+        const int c = c4base + colj<G, PAIR>(gl, j);
         if (c < A.F4) store_elem<RED>(A, v, c, acc[j], pos[j], e - s);
     }
 }
 
-template <int G, int NV, int OP, int RED, bool XB = false>
+template <int G, int NV, int OP, int RED, bool XB = false, bool PAIR = false>
 fg_status launch_t(const Args& A0, cudaStream_t st) {
     Args A = A0;
     constexpr int NG = THREADS / G;
@@ -300,7 +325,7 @@ fg_status launch_t(const Args& A0, cudaStream_t st) {
     const int tiles = (A.F4 + TW - 1) / TW;
     if (blocks == 0) return FG_OK;
     const dim3 grid{unsigned(blocks), unsigned(tiles), 1u};
-    spmm_gather_kernel<G, NV, OP, RED, XB><<<grid, THREADS, 0, st>>>(A);
+    spmm_gather_kernel<G, NV, OP, RED, XB, PAIR><<<grid, THREADS, 0, st>>>(A);
     return fgk::check_launch("spmm_gather_kernel");
 }
 
@@ -326,11 +351,12 @@ fg_status dispatch_inst<R_MEAN, 0>(const Args& A, int G, int NV, int op, cudaStr
 template <>
 fg_status dispatch_inst<R_MEAN, 1>(const Args& A, int G, int NV, int op, cudaStream_t st);
 // bf16 storage of X (copy_u, u_mul_e; sum and max): spmm_inst_x16.cu
+// pair: 16-byte loads of adjacent chunk pairs (F4 even; NV even)
 template <int RED>
-fg_status dispatch_x16(const Args& A, int G, int NV, int op, cudaStream_t st);
+fg_status dispatch_x16(const Args& A, int G, int NV, int op, bool pair, cudaStream_t st);
 template <>
-fg_status dispatch_x16<R_SUM>(const Args& A, int G, int NV, int op, cudaStream_t st);
+fg_status dispatch_x16<R_SUM>(const Args& A, int G, int NV, int op, bool pair, cudaStream_t st);
 template <>
-fg_status dispatch_x16<R_MAX>(const Args& A, int G, int NV, int op, cudaStream_t st);
+fg_status dispatch_x16<R_MAX>(const Args& A, int G, int NV, int op, bool pair, cudaStream_t st);
 
 }  // namespace fgspmm

@@ -601,3 +601,26 @@ def test_bf16_rejects_unsupported(skewed):
     with pytest.raises(fgp.FGError) as e:
         fgp.spmm(skewed.h, "copy_u", "mean", bf16_dev(bits))
     assert e.value.status == 3   # FG_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("F", [128, 512])
+def test_copy_u_bf16_tiled_and_unaligned(skewed, monkeypatch, F):
+    """bf16 storage on the column-tiled copy_u path (a 1 MiB L2 budget forces
+    tiles on this graph) and with an X that is 8- but not 16-byte aligned (the
+    8-byte-per-chunk mapping instead of 16-byte pair loads)."""
+    import paper_2008_11359_b200 as fgp
+    bits, dec = gen.to_bf16(feats((skewed.n_src, F), 740 + F, gen.REAL))
+    ref, ab, _, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", "sum", dec)
+    monkeypatch.setenv("FG_L2_TILE_MB", "1")
+    out = fgp.spmm(skewed.h, "copy_u", "sum", bf16_dev(bits)).cpu().numpy()
+    check_close(out, ref, ab, TOL, f"bf16 copy_u-sum tiled F={F}")
+    monkeypatch.delenv("FG_L2_TILE_MB")
+    buf = torch.empty(skewed.n_src * F + 4, dtype=torch.bfloat16, device="cuda")
+    Xu = buf[4:].view(skewed.n_src, F)            # 8-byte aligned, not 16
+    Xu.copy_(bf16_dev(bits))
+    out = fgp.spmm(skewed.h, "copy_u", "sum", Xu).cpu().numpy()
+    check_close(out, ref, ab, TOL, f"bf16 copy_u-sum unaligned F={F}")
+    Yb, Yd = gen.to_bf16(feats((skewed.n_dst, F), 741 + F, gen.REAL))
+    s = fgp.sddmm(skewed.h, Xu, bf16_dev(Yb), H=1).cpu().numpy()
+    rs, rab = oracle.sddmm(skewed.row_ptr, skewed.col_idx, dec, Yd, H=1)
+    check_close(s, rs, rab, TOL, f"bf16 u_dot_v unaligned F={F}")
