@@ -25,6 +25,7 @@ OPS_BY_FILE = {
     "sddmm": ["sddmm_u_dot_v_H1_F512", "sddmm_u_dot_v_H8_D32"],
     "softmax": ["edge_softmax_H8"],
     "mlp": ["spmm_mlp_max_d8_d128_args"],
+    "gat": ["extra_gat_fused_H8_D32"],
 }
 
 
@@ -86,7 +87,8 @@ if os.path.exists(lp):
         if "FillFunctor" in k:
             segs.append(cur)
             cur = []
-        elif not k.startswith("void at::"):   # the flush's read-back reduction is not a step kernel
+        elif not k.startswith("void at::") and "::gather_kernel" not in k and "::stream_kernel" not in k:
+            # (the flush's read-back reduction and the L2 probe are not step kernels)
             cur.append((k, v))
     segs.append(cur)
     step = [sg for sg in segs if len(sg) >= 7][-1]   # last full step (extras follow it)
