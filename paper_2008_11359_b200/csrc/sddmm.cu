@@ -112,31 +112,12 @@ __device__ __forceinline__ void reduce_scatter(float (&v)[K], int gl, unsigned m
 //                lane belongs to head c / D4; reduce over D4 lanes per chunk.
 // MODE_GENERAL : H == 1 with F > 4*G*NV (column tiles; Y re-read through L1), or
 //                H > 1 with D4 > G (a head spans several chunks of a lane).
-// Column (float4 index) of a lane's chunk j: PAIR (bf16 storage, H == 1) --
-// a lane owns pairs of adjacent chunks read with one 16-byte load (8 bf16);
-// otherwise chunk j of lane gl is column gl + G*j.
-template <int G, bool PAIR>
-__device__ __forceinline__ int colj(int gl, int j) {
-    if constexpr (PAIR) return 2 * (gl + G * (j >> 1)) + (j & 1);
-    else return gl + G * j;
-}
-
-// one 16-byte load of chunks c, c+1 (c even, bf16) -> two float4
-__device__ __forceinline__ void ld_pair(const float4* __restrict__ M, int64_t r, int F4, int c, float4& a,
-                                        float4& b) {
-    const uint4 w = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint2*>(M) + r * F4 + c));
-    a = bf16x4(make_uint2(w.x, w.y));
-    b = bf16x4(make_uint2(w.z, w.w));
-}
-
-template <int G, int NV, int MODE, int DW, bool XB, bool PAIR = false>
+template <int G, int NV, int MODE, int DW, bool XB>
 __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const float4* __restrict__ X,
                                                            const float4* __restrict__ Y, float* __restrict__ out) {
     constexpr int TW = G * NV;
     constexpr int B = G >= 4 ? 32 : 8;              // edges per batch
-    // edges in flight per lane; PAIR keeps the raw bf16 pairs (half the registers of
-    // converted float4s), so it affords twice the edges -- the same bytes in flight
-    constexpr int U = PAIR ? (NV >= 4 ? 4 : 8) : (NV >= 3 ? 2 : (NV == 2 ? 4 : 8));
+    constexpr int U = NV >= 3 ? 2 : (NV == 2 ? 4 : 8);   // edges in flight per lane
     constexpr int NGRP = THREADS / G;
     constexpr int CAP = 32 * G;                           // staged results per group
     __shared__ int s_idx[NGRP][B];
@@ -162,15 +143,8 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
     float4 y0[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-        const int c = A.c4base + colj<G, PAIR>(gl, j);
-        if constexpr (PAIR) {
-            if ((j & 1) == 0) {
-                if (c < F4) ld_pair(Y, v, F4, c, y0[j], y0[j + 1]);
-                else y0[j] = y0[j + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        } else {
-            y0[j] = (c < F4) ? ld_chunk<XB>(Y, v, F4, c) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        const int c = A.c4base + gl + G * j;
+        y0[j] = (c < F4) ? ld_chunk<XB>(Y, v, F4, c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
     constexpr int PF = (B + G - 1) / G;   // running sums per lane in a tiled pass (H == 1)
@@ -190,16 +164,7 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
         }
         __syncwarp(mask);
         for (int t0 = 0; t0 < cnt; t0 += U) {
-            float4 x[PAIR ? 1 : U][PAIR ? 1 : NV];
-            uint4 xw[PAIR ? U : 1][PAIR ? NV / 2 : 1];   // PAIR: raw bf16 chunk pairs
-            auto xv = [&](int uu, int j) -> float4 {
-                if constexpr (PAIR) {
-                    const uint4 w = xw[uu][j / 2];
-                    return (j & 1) ? bf16x4(make_uint2(w.z, w.w)) : bf16x4(make_uint2(w.x, w.y));
-                } else {
-                    return x[uu][j];
-                }
-            };
+            float4 x[U][NV];
             int us[U];
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
@@ -207,18 +172,8 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                 us[uu] = (t < cnt) ? idx[t] : 0;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
-                    const int c = A.c4base + colj<G, PAIR>(gl, j);
-                    if constexpr (PAIR) {
-                        if ((j & 1) == 0) {
-                            xw[uu][j / 2] = (t < cnt && c < F4)
-                                                ? __ldg(reinterpret_cast<const uint4*>(
-                                                      reinterpret_cast<const uint2*>(X) + int64_t(us[uu]) * F4 + c))
-                                                : make_uint4(0, 0, 0, 0);
-                        }
-                    } else {
-                        x[uu][j] = (t < cnt && c < F4) ? ld_chunk<XB>(X, us[uu], F4, c)
-                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
+                    const int c = A.c4base + gl + G * j;
+                    x[uu][j] = (t < cnt && c < F4) ? ld_chunk<XB>(X, us[uu], F4, c) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
             if constexpr (MODE == MODE_H1 || MODE == MODE_HEADS) {
@@ -233,11 +188,11 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                         if constexpr (MODE == MODE_H1) {
                             float hs = 0.f;
 #pragma unroll
-                            for (int j = 0; j < NV; ++j) hs += dot4(xv(uu, j), y0[j]);
+                            for (int j = 0; j < NV; ++j) hs += dot4(x[uu][j], y0[j]);
                             pv[uu] = hs;
                         } else {
 #pragma unroll
-                            for (int j = 0; j < NV; ++j) pv[uu * NV + j] = dot4(xv(uu, j), y0[j]);
+                            for (int j = 0; j < NV; ++j) pv[uu * NV + j] = dot4(x[uu][j], y0[j]);
                         }
                     }
                     reduce_scatter<K, DW, G>(pv, gl, mask);
@@ -270,14 +225,14 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                 if constexpr (MODE == MODE_H1) {
                     float hs = 0.f;
 #pragma unroll
-                    for (int j = 0; j < NV; ++j) hs += dot4(xv(uu, j), y0[j]);
+                    for (int j = 0; j < NV; ++j) hs += dot4(x[uu][j], y0[j]);
                     hs = group_sum<G>(hs, G, mask);
                     if (gl == 0) rr[0] = hs;
                 } else if constexpr (MODE == MODE_HEADS) {
 #pragma unroll
                     for (int j = 0; j < NV; ++j) {
                         const int c = gl + G * j;
-                        const float part = group_sum<G>(dot4(xv(uu, j), y0[j]), D4, mask);
+                        const float part = group_sum<G>(dot4(x[uu][j], y0[j]), D4, mask);
                         if (c < F4 && (gl & (D4 - 1)) == 0) rr[c / D4] = part;
                     }
                 } else {
@@ -286,7 +241,7 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                     int head = 0;
 #pragma unroll
                     for (int j = 0; j < NV; ++j) {
-                        hs += dot4(xv(uu, j), y0[j]);
+                        hs += dot4(x[uu][j], y0[j]);
                         const int cend = G * (j + 1);
                         if (H > 1 && (j == NV - 1 || cend % D4 == 0)) {
                             const float tot = group_sum<G>(hs, G, mask);
@@ -330,28 +285,104 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
     }   // units
 }
 
-template <int G, int NV, bool XB = false, bool PAIR = false>
+// H == 1 with bf16 storage (fg_sddmm_x16): each lane reads PAIRS of 4-feature
+// chunks (8 bf16) with one 16-byte load and keeps them raw until the dot, so
+// U = 4 / 8 edges stay in flight -- the same bytes in flight per warp as the fp32
+// mapping, half the gathered bytes.  Same unit walk, batching and coalesced
+// result write-back as sddmm_kernel (MODE_H1).
+template <int G, int NP>
+__global__ void __launch_bounds__(THREADS, 3) sddmm_h1_pair_kernel(const Args A, const uint4* __restrict__ X,
+                                                                   const uint4* __restrict__ Y,
+                                                                   float* __restrict__ out) {
+    constexpr int B = G >= 4 ? 32 : 8;      // edges per batch
+    constexpr int U = NP >= 2 ? 4 : 8;      // edges in flight per lane
+    constexpr int NGRP = THREADS / G;
+    __shared__ int s_idx[NGRP][B];
+    __shared__ float s_res[NGRP][B];
+    const int lane = threadIdx.x & 31;
+    const int gl = threadIdx.x & (G - 1);
+    const int gi = threadIdx.x / G;
+    const unsigned mask = group_mask<G>(lane);
+    const int P8 = A.F4 / 2;                 // 8-feature pairs per row
+    const int64_t stride = int64_t(gridDim.x) * (THREADS / G);
+    for (int64_t unit = (int64_t(blockIdx.x) * THREADS + threadIdx.x) / G; unit < A.n_units; unit += stride) {
+        const int64_t v = A.unit_row[unit];
+        const int64_t s = A.unit_p0[unit];
+        const int64_t e = A.unit_p1 ? A.unit_p1[unit] : min(s + A.unit_chunk, A.row_ptr[v + 1]);
+        int* idx = s_idx[gi];
+        float* res = s_res[gi];
+        float4 ylo[NP], yhi[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            const int c = gl + G * j;
+            const uint4 w = (c < P8) ? __ldg(Y + v * P8 + c) : make_uint4(0, 0, 0, 0);
+            ylo[j] = bf16x4(make_uint2(w.x, w.y));
+            yhi[j] = bf16x4(make_uint2(w.z, w.w));
+        }
+        for (int64_t p0 = s; p0 < e; p0 += B) {
+            const int cnt = int(min((int64_t)B, e - p0));
+            __syncwarp(mask);
+            for (int t = gl; t < cnt; t += G) idx[t] = __ldg(A.col_idx + p0 + t);
+            __syncwarp(mask);
+            for (int t0 = 0; t0 < cnt; t0 += U) {
+                uint4 xw[U][NP];
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+                    const int t = t0 + uu;
+                    const int64_t u = (t < cnt) ? idx[t] : 0;
+#pragma unroll
+                    for (int j = 0; j < NP; ++j) {
+                        const int c = gl + G * j;
+                        xw[uu][j] = (t < cnt && c < P8) ? __ldg(X + u * P8 + c) : make_uint4(0, 0, 0, 0);
+                    }
+                }
+                float pv[U];
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+                    float hs = 0.f;
+#pragma unroll
+                    for (int j = 0; j < NP; ++j)
+                        hs += dot4(bf16x4(make_uint2(xw[uu][j].x, xw[uu][j].y)), ylo[j]) +
+                              dot4(bf16x4(make_uint2(xw[uu][j].z, xw[uu][j].w)), yhi[j]);
+                    pv[uu] = hs;
+                }
+                reduce_scatter<U, G, G>(pv, gl, mask);
+                constexpr int L = ilog2(U) < ilog2(G) ? ilog2(U) : ilog2(G);
+                constexpr int KEEP = U >> L;
+                const int bits = gl >> (ilog2(G) - L);
+                if ((gl & ((G >> L) - 1)) == 0) {
+#pragma unroll
+                    for (int i = 0; i < KEEP; ++i) res[t0 + bits * KEEP + i] = pv[i];
+                }
+            }
+            __syncwarp(mask);   // coalesced write-back of the batch's results
+            if (A.eid == nullptr) {
+                for (int q = gl; q < cnt; q += G) out[p0 + q] = res[q];
+            } else {
+                for (int q = gl; q < cnt; q += G) out[__ldg(A.eid + p0 + q)] = res[q];
+            }
+        }
+    }
+}
+
+template <int G, int NV, bool XB = false>
 fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, cudaStream_t st) {
     using K = void (*)(const Args, const float4*, const float4*, float*);
     const int TW = G * NV;
     K k;
-    if constexpr (PAIR) {   // H == 1 only (launch_sddmm)
-        k = sddmm_kernel<G, NV, MODE_H1, G, XB, true>;
-    } else {
-        if (A.H == 1 && (A.tile4 ? A.tile4 : A.F4) <= TW) {
-            k = sddmm_kernel<G, NV, MODE_H1, G, XB>;
-        } else if (A.H > 1 && A.D4 <= G && A.F4 <= TW) {
-            switch (A.D4) {   // heads of D = 4*D4 floats reduce over D4 lanes
-                case 1: k = sddmm_kernel<G, NV, MODE_HEADS, 1, XB>; break;
-                case 2: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 2 ? 2 : 1), XB>; break;
-                case 4: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 4 ? 4 : 1), XB>; break;
-                case 8: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 8 ? 8 : 1), XB>; break;
-                case 16: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 16 ? 16 : 1), XB>; break;
-                default: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 32 ? 32 : 1), XB>; break;
-            }
-        } else {
-            k = sddmm_kernel<G, NV, MODE_GENERAL, 1, XB>;
+    if (A.H == 1 && (A.tile4 ? A.tile4 : A.F4) <= TW) {
+        k = sddmm_kernel<G, NV, MODE_H1, G, XB>;
+    } else if (A.H > 1 && A.D4 <= G && A.F4 <= TW) {
+        switch (A.D4) {   // heads of D = 4*D4 floats reduce over D4 lanes
+            case 1: k = sddmm_kernel<G, NV, MODE_HEADS, 1, XB>; break;
+            case 2: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 2 ? 2 : 1), XB>; break;
+            case 4: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 4 ? 4 : 1), XB>; break;
+            case 8: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 8 ? 8 : 1), XB>; break;
+            case 16: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 16 ? 16 : 1), XB>; break;
+            default: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 32 ? 32 : 1), XB>; break;
         }
+    } else {
+        k = sddmm_kernel<G, NV, MODE_GENERAL, 1, XB>;
     }
     const int64_t per_block = THREADS / G;
     int64_t blocks = (A.n_units + per_block - 1) / per_block;
@@ -365,6 +396,23 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
     }
     k<<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
     return fgk::check_launch("sddmm_kernel");
+}
+
+template <int G, int NP>
+fg_status launch_pair(const Args& A, const uint4* X, const uint4* Y, float* out, cudaStream_t st) {
+    auto k = sddmm_h1_pair_kernel<G, NP>;
+    const int64_t per_block = THREADS / G;
+    int64_t blocks = (A.n_units + per_block - 1) / per_block;
+    if (blocks == 0) return FG_OK;
+    if (A.persistent) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, 0) != cudaSuccess || per_sm < 1)
+            per_sm = 1;
+        if (A.persistent > 0 && A.persistent < per_sm) per_sm = A.persistent;
+        blocks = std::min<int64_t>(blocks, int64_t(fgk::num_sms()) * per_sm);
+    }
+    k<<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
+    return fgk::check_launch("sddmm_h1_pair_kernel");
 }
 
 }  // namespace
@@ -466,26 +514,28 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     }
     if (H > 1 && F4 > G * NV)
         return set_error(FG_EUNSUPPORTED, "fg_sddmm: multi-head with H*D > 512 not implemented");
-    // bf16, H == 1, one pass over an even number of chunks, 16-byte aligned X / Y:
-    // 16-byte loads of chunk pairs (G lanes x NV/2 pairs)
-    if (xb && H == 1 && F4 % 2 == 0 && F4 <= 256 && ((reinterpret_cast<uintptr_t>(Xbf16) |
-                                                    reinterpret_cast<uintptr_t>(Ybf16)) & 15u) == 0) {
-        const int F8 = F4 / 2;
-        if (F8 <= 32) {
+    // bf16, H == 1, an even number of chunks, 16-byte aligned X / Y: 16-byte
+    // loads of 8-feature pairs (sddmm_h1_pair_kernel; G lanes x NP pairs)
+    if (xb && H == 1 && F4 % 2 == 0 && F4 <= 256 &&
+        ((reinterpret_cast<uintptr_t>(Xbf16) | reinterpret_cast<uintptr_t>(Ybf16)) & 15u) == 0) {
+        const uint4* Xp = reinterpret_cast<const uint4*>(Xbf16);
+        const uint4* Yp = reinterpret_cast<const uint4*>(Ybf16);
+        const int P8 = F4 / 2;
+        if (P8 <= 32) {
             int G2 = 1;
-            while (G2 < F8) G2 *= 2;
+            while (G2 < P8) G2 *= 2;
             switch (G2) {
-                case 1: return launch_t<1, 2, true, true>(A, X4, Y4, out, st);
-                case 2: return launch_t<2, 2, true, true>(A, X4, Y4, out, st);
-                case 4: return launch_t<4, 2, true, true>(A, X4, Y4, out, st);
-                case 8: return launch_t<8, 2, true, true>(A, X4, Y4, out, st);
-                case 16: return launch_t<16, 2, true, true>(A, X4, Y4, out, st);
-                default: return launch_t<32, 2, true, true>(A, X4, Y4, out, st);
+                case 1: return launch_pair<1, 1>(A, Xp, Yp, out, st);
+                case 2: return launch_pair<2, 1>(A, Xp, Yp, out, st);
+                case 4: return launch_pair<4, 1>(A, Xp, Yp, out, st);
+                case 8: return launch_pair<8, 1>(A, Xp, Yp, out, st);
+                case 16: return launch_pair<16, 1>(A, Xp, Yp, out, st);
+                default: return launch_pair<32, 1>(A, Xp, Yp, out, st);
             }
         }
-        if (F8 <= 64) return launch_t<32, 4, true, true>(A, X4, Y4, out, st);
-        if (F8 <= 96) return launch_t<32, 6, true, true>(A, X4, Y4, out, st);
-        return launch_t<32, 8, true, true>(A, X4, Y4, out, st);
+        if (P8 <= 64) return launch_pair<32, 2>(A, Xp, Yp, out, st);
+        if (P8 <= 96) return launch_pair<32, 3>(A, Xp, Yp, out, st);
+        return launch_pair<32, 4>(A, Xp, Yp, out, st);
     }
     if (xb) {
         switch (G) {
