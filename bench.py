@@ -270,7 +270,7 @@ class Step:
                  arg_e=self.aemlp, stream=st)
         rec(8)
 
-    LAUNCHES_PER_STEP = 8   # libfg kernels per step: one per fg_* call, plus mlp's tf32 pre-split
+    LAUNCHES_PER_STEP = 9   # libfg kernels per step: one per fg_* call, plus mlp's tf32 pre-split and q_v = x_v W
 
     def enqueue_pipelined(self, ins_h, w_h, outs_h, h2d, d2h):
         """The same step for the end-to-end leg, with the host copies overlapped:
