@@ -285,25 +285,32 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
     }   // units
 }
 
-// H == 1 with bf16 storage (fg_sddmm_x16): each lane reads PAIRS of 4-feature
-// chunks (8 bf16) with one 16-byte load and keeps them raw until the dot, so
-// U = 4 / 8 edges stay in flight -- the same bytes in flight per warp as the fp32
-// mapping, half the gathered bytes.  Same unit walk, batching and coalesced
-// result write-back as sddmm_kernel (MODE_H1).
-template <int G, int NP>
-__global__ void __launch_bounds__(THREADS, 3) sddmm_h1_pair_kernel(const Args A, const uint4* __restrict__ X,
-                                                                   const uint4* __restrict__ Y,
-                                                                   float* __restrict__ out) {
+// bf16 storage (fg_sddmm_x16): each lane reads PAIRS of 4-feature chunks (8
+// bf16) with one 16-byte load and keeps them raw until the dot, so U = 4 / 8
+// edges stay in flight -- the same bytes in flight per warp as the fp32
+// mapping, half the gathered bytes.  Lane gl owns pairs gl + G*j (j < NP).
+//   DWP == G (H == 1): one dot per edge over all G lanes;
+//   DWP <  G (H > 1): a head spans D/8 = DWP consecutive pairs, i.e. DWP lanes;
+//                     pair j of lane gl belongs to head gl/DWP + j*(G/DWP).
+// Same unit walk, batching, reduce-scatter and coalesced result write-back as
+// sddmm_kernel (MODE_H1 / MODE_HEADS).
+template <int G, int NP, int DWP>
+__global__ void __launch_bounds__(THREADS, 3) sddmm_pair_kernel(const Args A, const uint4* __restrict__ X,
+                                                                const uint4* __restrict__ Y,
+                                                                float* __restrict__ out) {
+    constexpr bool H1 = (DWP == G);
     constexpr int B = G >= 4 ? 32 : 8;      // edges per batch
     constexpr int U = NP >= 2 ? 4 : 8;      // edges in flight per lane
     constexpr int NGRP = THREADS / G;
+    constexpr int CAP = 32 * G;             // staged results per group (B * H <= CAP, checked by the host)
     __shared__ int s_idx[NGRP][B];
-    __shared__ float s_res[NGRP][B];
+    __shared__ float s_res[NGRP][CAP];
     const int lane = threadIdx.x & 31;
     const int gl = threadIdx.x & (G - 1);
     const int gi = threadIdx.x / G;
     const unsigned mask = group_mask<G>(lane);
     const int P8 = A.F4 / 2;                 // 8-feature pairs per row
+    const int H = A.H;
     const int64_t stride = int64_t(gridDim.x) * (THREADS / G);
     for (int64_t unit = (int64_t(blockIdx.x) * THREADS + threadIdx.x) / G; unit < A.n_units; unit += stride) {
         const int64_t v = A.unit_row[unit];
@@ -336,30 +343,49 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_h1_pair_kernel(const Args A,
                         xw[uu][j] = (t < cnt && c < P8) ? __ldg(X + u * P8 + c) : make_uint4(0, 0, 0, 0);
                     }
                 }
-                float pv[U];
+                constexpr int K = H1 ? U : U * NP;
+                float pv[K];
 #pragma unroll
                 for (int uu = 0; uu < U; ++uu) {
                     float hs = 0.f;
 #pragma unroll
-                    for (int j = 0; j < NP; ++j)
-                        hs += dot4(bf16x4(make_uint2(xw[uu][j].x, xw[uu][j].y)), ylo[j]) +
-                              dot4(bf16x4(make_uint2(xw[uu][j].z, xw[uu][j].w)), yhi[j]);
-                    pv[uu] = hs;
+                    for (int j = 0; j < NP; ++j) {
+                        const float d = dot4(bf16x4(make_uint2(xw[uu][j].x, xw[uu][j].y)), ylo[j]) +
+                                        dot4(bf16x4(make_uint2(xw[uu][j].z, xw[uu][j].w)), yhi[j]);
+                        if constexpr (H1) hs += d;
+                        else pv[uu * NP + j] = d;
+                    }
+                    if constexpr (H1) pv[uu] = hs;
                 }
-                reduce_scatter<U, G, G>(pv, gl, mask);
-                constexpr int L = ilog2(U) < ilog2(G) ? ilog2(U) : ilog2(G);
-                constexpr int KEEP = U >> L;
-                const int bits = gl >> (ilog2(G) - L);
-                if ((gl & ((G >> L) - 1)) == 0) {
+                reduce_scatter<K, DWP, G>(pv, gl, mask);
+                constexpr int L = ilog2(K) < ilog2(DWP) ? ilog2(K) : ilog2(DWP);
+                constexpr int KEEP = K >> L;
+                const int sub = gl & (DWP - 1);
+                const int bits = sub >> (ilog2(DWP) - L);
+                if ((sub & ((DWP >> L) - 1)) == 0) {
 #pragma unroll
-                    for (int i = 0; i < KEEP; ++i) res[t0 + bits * KEEP + i] = pv[i];
+                    for (int i = 0; i < KEEP; ++i) {
+                        const int id = bits * KEEP + i;
+                        if constexpr (H1) {
+                            res[t0 + id] = pv[i];
+                        } else {
+                            const int uu = id / NP, j = id % NP;
+                            const int head = gl / DWP + j * (G / DWP);
+                            if (head < H) res[(t0 + uu) * H + head] = pv[i];
+                        }
+                    }
                 }
             }
             __syncwarp(mask);   // coalesced write-back of the batch's results
+            const int tot = cnt * H;
             if (A.eid == nullptr) {
-                for (int q = gl; q < cnt; q += G) out[p0 + q] = res[q];
+                float* o = out + p0 * H;
+                for (int q = gl; q < tot; q += G) o[q] = res[q];
             } else {
-                for (int q = gl; q < cnt; q += G) out[__ldg(A.eid + p0 + q)] = res[q];
+                for (int q = gl; q < tot; q += G) {
+                    const int t = q / H, h = q - t * H;
+                    out[int64_t(__ldg(A.eid + p0 + t)) * H + h] = res[q];
+                }
             }
         }
     }
@@ -398,9 +424,9 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
     return fgk::check_launch("sddmm_kernel");
 }
 
-template <int G, int NP>
+template <int G, int NP, int DWP = G>
 fg_status launch_pair(const Args& A, const uint4* X, const uint4* Y, float* out, cudaStream_t st) {
-    auto k = sddmm_h1_pair_kernel<G, NP>;
+    auto k = sddmm_pair_kernel<G, NP, DWP>;
     const int64_t per_block = THREADS / G;
     int64_t blocks = (A.n_units + per_block - 1) / per_block;
     if (blocks == 0) return FG_OK;
@@ -412,7 +438,7 @@ fg_status launch_pair(const Args& A, const uint4* X, const uint4* Y, float* out,
         blocks = std::min<int64_t>(blocks, int64_t(fgk::num_sms()) * per_sm);
     }
     k<<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
-    return fgk::check_launch("sddmm_h1_pair_kernel");
+    return fgk::check_launch("sddmm_pair_kernel");
 }
 
 }  // namespace
@@ -514,28 +540,46 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     }
     if (H > 1 && F4 > G * NV)
         return set_error(FG_EUNSUPPORTED, "fg_sddmm: multi-head with H*D > 512 not implemented");
-    // bf16, H == 1, an even number of chunks, 16-byte aligned X / Y: 16-byte
-    // loads of 8-feature pairs (sddmm_h1_pair_kernel; G lanes x NP pairs)
-    if (xb && H == 1 && F4 % 2 == 0 && F4 <= 256 &&
-        ((reinterpret_cast<uintptr_t>(Xbf16) | reinterpret_cast<uintptr_t>(Ybf16)) & 15u) == 0) {
+    // bf16 storage, 16-byte aligned X / Y, whole 8-feature pairs: 16-byte loads of
+    // pairs (sddmm_pair_kernel; G lanes x NP pairs).  H == 1: any even F4 <= 256;
+    // H > 1: D = 8 * 2^k with D/8 <= 32 lanes per head, H*D <= 512 and the batch's
+    // H results per edge fitting the group's staging buffer (H * 32 <= 32 * G).
+    if (xb && ((reinterpret_cast<uintptr_t>(Xbf16) | reinterpret_cast<uintptr_t>(Ybf16)) & 15u) == 0) {
         const uint4* Xp = reinterpret_cast<const uint4*>(Xbf16);
         const uint4* Yp = reinterpret_cast<const uint4*>(Ybf16);
         const int P8 = F4 / 2;
-        if (P8 <= 32) {
-            int G2 = 1;
-            while (G2 < P8) G2 *= 2;
-            switch (G2) {
-                case 1: return launch_pair<1, 1>(A, Xp, Yp, out, st);
-                case 2: return launch_pair<2, 1>(A, Xp, Yp, out, st);
-                case 4: return launch_pair<4, 1>(A, Xp, Yp, out, st);
-                case 8: return launch_pair<8, 1>(A, Xp, Yp, out, st);
-                case 16: return launch_pair<16, 1>(A, Xp, Yp, out, st);
-                default: return launch_pair<32, 1>(A, Xp, Yp, out, st);
+        if (H == 1 && F4 % 2 == 0 && F4 <= 256) {
+            if (P8 <= 32) {
+                int G2 = 1;
+                while (G2 < P8) G2 *= 2;
+                switch (G2) {
+                    case 1: return launch_pair<1, 1>(A, Xp, Yp, out, st);
+                    case 2: return launch_pair<2, 1>(A, Xp, Yp, out, st);
+                    case 4: return launch_pair<4, 1>(A, Xp, Yp, out, st);
+                    case 8: return launch_pair<8, 1>(A, Xp, Yp, out, st);
+                    case 16: return launch_pair<16, 1>(A, Xp, Yp, out, st);
+                    default: return launch_pair<32, 1>(A, Xp, Yp, out, st);
+                }
+            }
+            if (P8 <= 64) return launch_pair<32, 2>(A, Xp, Yp, out, st);
+            if (P8 <= 96) return launch_pair<32, 3>(A, Xp, Yp, out, st);
+            return launch_pair<32, 4>(A, Xp, Yp, out, st);
+        }
+        const int DP = D / 8;   // pairs (= lanes) per head
+        if (H > 1 && D % 8 == 0 && (DP & (DP - 1)) == 0 && DP <= 32 && F4 <= 128) {
+            // G = 32 lanes x NP pairs covers P8 <= 32 * NP; heads need H * 32 <= 32 * 32
+            const int NP = P8 <= 32 ? 1 : 2;
+            if (H <= 32) {
+                switch (DP) {
+                    case 1: return NP == 1 ? launch_pair<32, 1, 1>(A, Xp, Yp, out, st) : launch_pair<32, 2, 1>(A, Xp, Yp, out, st);
+                    case 2: return NP == 1 ? launch_pair<32, 1, 2>(A, Xp, Yp, out, st) : launch_pair<32, 2, 2>(A, Xp, Yp, out, st);
+                    case 4: return NP == 1 ? launch_pair<32, 1, 4>(A, Xp, Yp, out, st) : launch_pair<32, 2, 4>(A, Xp, Yp, out, st);
+                    case 8: return NP == 1 ? launch_pair<32, 1, 8>(A, Xp, Yp, out, st) : launch_pair<32, 2, 8>(A, Xp, Yp, out, st);
+                    case 16: return NP == 1 ? launch_pair<32, 1, 16>(A, Xp, Yp, out, st) : launch_pair<32, 2, 16>(A, Xp, Yp, out, st);
+                    default: break;   // DP == 32: one head per 32 lanes = the H1 reduction per head; use the chunk path
+                }
             }
         }
-        if (P8 <= 64) return launch_pair<32, 2>(A, Xp, Yp, out, st);
-        if (P8 <= 96) return launch_pair<32, 3>(A, Xp, Yp, out, st);
-        return launch_pair<32, 4>(A, Xp, Yp, out, st);
     }
     if (xb) {
         switch (G) {

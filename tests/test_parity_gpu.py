@@ -582,7 +582,7 @@ def test_u_mul_e_bf16(skewed, skewed_eid, H, D, red, use_eid):
         assert np.array_equal(au.cpu().numpy(), rau) and np.array_equal(ae.cpu().numpy(), rae)
 
 
-@pytest.mark.parametrize("H,D", [(1, 16), (1, 128), (1, 512), (8, 32), (2, 4), (4, 64)])
+@pytest.mark.parametrize("H,D", [(1, 16), (1, 128), (1, 512), (8, 32), (2, 4), (4, 64), (2, 16), (16, 8), (4, 128), (2, 256)])
 @pytest.mark.parametrize("use_eid", [False, True])
 def test_sddmm_bf16(skewed, skewed_eid, H, D, use_eid):
     import paper_2008_11359_b200 as fgp
