@@ -501,7 +501,20 @@ __global__ void __launch_bounds__(THREADS, ILP == 2 ? 3 : CTAS_PER_SM) mlp_tcgen
         uint32_t lane_base;
         asm volatile("mov.b32 %0, %1;" : "=r"(lane_base) : "r"(tmem + (uint32_t(warp * 32) << 16)));
         const int nnz_cta = int(E1 - E0);
-        for (int t = 0; t < ntiles; ++t) {
+        // a warp whose 32 features all lie beyond d2 (d2 < 128: the W^T rows are
+        // zero padding) only keeps the TMEM buffers cycling: no tcgen05.ld -- the
+        // TMEM reads are this kernel's bound
+        const bool warp_active = mbase + warp * 32 < A.d2;
+        if (!warp_active) {
+            for (int t = 0; t < ntiles; ++t) {
+                const int b = t % NBUF;
+                mbar_wait_backoff(&S.tfull[b], (t / NBUF) & 1, A.backoff_ns);
+                tc_fence_after();
+                tc_fence_before();
+                mbar_arrive(&S.tempty[b]);
+            }
+        }
+        for (int t = 0; warp_active && t < ntiles; ++t) {
             const int b = t % NBUF;
             if (A.epi_backoff_ns > 0) mbar_wait_backoff(&S.tfull[b], (t / NBUF) & 1, A.epi_backoff_ns);
             else mbar_wait(&S.tfull[b], (t / NBUF) & 1);
@@ -529,7 +542,8 @@ __global__ void __launch_bounds__(THREADS, ILP == 2 ? 3 : CTAS_PER_SM) mlp_tcgen
             tc_fence_before();
             mbar_arrive(&S.tempty[b]);
         }
-        while (ep.r < ep.r_hi) ep.advance();   // trailing rows (empty rows after the last edge)
+        if (warp_active)
+            while (ep.r < ep.r_hi) ep.advance();   // trailing rows (empty rows after the last edge)
     }
     tc_fence_before();
     __syncthreads();

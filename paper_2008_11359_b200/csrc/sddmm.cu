@@ -509,12 +509,19 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
     // slice stays L2-resident.  Measured on reddit u_dot_v F = 512: 19.7 ms -> 16.4
     // ms (DRAM 115 -> 29 GB); non-persistent segmentation was slower (23.8 ms: one
     // CTA launch per 8 short units caps the active warps at 15 %).
-    // FG_SDDMM_SEG_MB: segment budget (default 48; 0 disables).
+    // FG_SDDMM_SEG_MB: segment size (default 48; 0 disables); segmentation only when X
+    // exceeds FG_SDDMM_SEG_MIN_MB (default 96).  Swept on reddit / proteins
+    // (tools/seg_sweep.py, tools/var_exp.py): X of 60 MB (F = 64) runs 3.00 ms
+    // unsegmented vs 3.61 ms in 48 MB segments, 119 MB (F = 128) ties, and the
+    // 238 / 477 MB cases (H = 8 D = 32, H = 1 F = 512) prefer 48 MB segments over
+    // 96 MB ones (9.39 vs 9.79 ms, 16.46 vs 16.72 ms).
     {
         const char* mb = getenv("FG_SDDMM_SEG_MB");
+        const char* mn = getenv("FG_SDDMM_SEG_MIN_MB");
         const int64_t budget = int64_t(mb ? atoi(mb) : 48) << 20;
+        const int64_t min_x = int64_t(mn ? atoi(mn) : 96) << 20;
         const int64_t row_bytes = int64_t(F4) * (xb ? 8 : 16);
-        if (A.tile4 == 0 && budget > 0 && g->n_src * row_bytes > budget) {
+        if (A.tile4 == 0 && budget > 0 && g->n_src * row_bytes > std::max(budget, min_x)) {
             int64_t seg_rows = budget / row_bytes;
             seg_rows = seg_rows < 32 ? 32 : seg_rows;
             const fg_graph::SegUnits* su = nullptr;

@@ -510,6 +510,7 @@ def test_sddmm_source_segmented(skewed, skewed_eid, H, D, use_eid, monkeypatch):
     import paper_2008_11359_b200 as fgp
     g = skewed_eid if use_eid else skewed
     monkeypatch.setenv("FG_SDDMM_SEG_MB", "1")
+    monkeypatch.setenv("FG_SDDMM_SEG_MIN_MB", "0")
     X = feats((g.n_src, H * D), 980 + D, gen.REAL)
     Y = feats((g.n_dst, H * D), 981 + D, gen.REAL)
     out = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
@@ -519,6 +520,13 @@ def test_sddmm_source_segmented(skewed, skewed_eid, H, D, use_eid, monkeypatch):
     monkeypatch.setenv("FG_SDDMM_PERSIST", "1")   # one CTA per SM: every group walks many units
     out1 = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
     assert np.array_equal(out1, out)              # same per-edge arithmetic, any schedule
+    if H * D % 8 == 0:   # the bf16 pair kernel on the same segmented units
+        monkeypatch.delenv("FG_SDDMM_PERSIST")
+        xb, xd = gen.to_bf16(X)
+        yb, yd = gen.to_bf16(Y)
+        outb = fgp.sddmm(g.h, bf16_dev(xb), bf16_dev(yb), H=H).cpu().numpy()
+        rb, rbb = oracle.sddmm(g.row_ptr, g.col_idx, xd, yd, H=H)
+        check_close(outb[pos], rb, rbb, TOL, f"segmented bf16 u_dot_v H={H} D={D}")
 
 
 # ------------------------------------------------------------------ fused GAT (f2)
