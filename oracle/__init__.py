@@ -7,7 +7,8 @@ the PAPER.md passages each routine follows.  Pins: tests/test_oracle_pins.py.
 
 Parity status per function:
   spmm copy_u sum/max, u_mul_e sum/max, mlp max/sum, sddmm u_dot_v,
-  edge_softmax -- all pinned (no "parity unpinned" functions).
+  sddmm u_dot_v-then-e_mul, edge_softmax -- all pinned (no "parity unpinned"
+  functions).
 """
 from __future__ import annotations
 
@@ -48,6 +49,8 @@ def _L():
         lib.or_edge_softmax.restype = None
         lib.or_sddmm_binary.argtypes = [i64, vp, vp, vp, i32, i64, vp, vp, vp, vp]
         lib.or_sddmm_binary.restype = None
+        lib.or_sddmm_emul.argtypes = [i64, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]
+        lib.or_sddmm_emul.restype = None
         _lib = lib
     return _lib
 
@@ -117,6 +120,27 @@ def sddmm(row_ptr, col_idx, X, Y=None, *, H: int = 1, rows=None):
     ref = np.empty((ne, H), np.float64)
     ab = np.empty((ne, H), np.float64)
     _L().or_sddmm(n_rows, _p(rows_a), _p(row_ptr), _p(col_idx), H, D, _p(X), _p(Y), _p(ref), _p(ab))
+    return ref, ab
+
+
+def sddmm_emul(row_ptr, col_idx, X, Y, E, *, H: int = 1, eid=None, rows=None):
+    """u_dot_v then e_mul (oracle.c or_sddmm_emul): (Eq. (4) score) * E[eid][h]
+    for the edges of the listed rows, in CSR order of the listed rows.  Returns
+    (ref, abssum) fp64 [edges][H]."""
+    row_ptr, col_idx = _c(row_ptr, np.int64), _c(col_idx, np.int32)
+    X = _c(X, np.float32)
+    Y = X if Y is None else _c(Y, np.float32)
+    E = _c(E, np.float32)
+    eid = _c(eid, np.int32)
+    F = X.reshape(X.shape[0], -1).shape[1]
+    D = F // H
+    n_rows, rows_a = _rows(rows, row_ptr.size - 1)
+    ne = int((row_ptr[1:] - row_ptr[:-1]).sum()) if rows_a is None else \
+        int((row_ptr[rows_a + 1] - row_ptr[rows_a]).sum())
+    ref = np.empty((ne, H), np.float64)
+    ab = np.empty((ne, H), np.float64)
+    _L().or_sddmm_emul(n_rows, _p(rows_a), _p(row_ptr), _p(col_idx), _p(eid), H, D, _p(X), _p(Y), _p(E),
+                       _p(ref), _p(ab))
     return ref, ab
 
 

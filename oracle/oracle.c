@@ -171,6 +171,46 @@ void or_sddmm(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr, const
 }
 
 /*
+ * u_dot_v followed by e_mul (row f4: the DGL builtin pair the paper's SDDMM
+ * template covers): the per-edge, per-head score of Eq. (4) scaled by
+ * an edge tensor, as written:
+ *     out[e][h] = ( sum_{d<D} X[u][h][d] * Y[v][h][d] ) * E[e][h],  e = eid(p)
+ * fp64; abssum = (sum_d |X*Y|) * |E[e][h]|.  Emitted at the listed-row CSR
+ * position like or_sddmm (E is indexed by edge id: eid[p], or p when eid is NULL).
+ */
+void or_sddmm_emul(int64_t n_rows, const int64_t* rows, const int64_t* row_ptr, const int32_t* col_idx,
+                   const int32_t* eid, int H, int D, const float* X, const float* Y, const float* E,
+                   double* ref, double* abssum) {
+    const int64_t F = (int64_t)H * D;
+    int64_t* off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_rows + 1));
+    off[0] = 0;
+    for (int64_t r = 0; r < n_rows; ++r) {
+        int64_t v = rows ? rows[r] : r;
+        off[r + 1] = off[r] + (row_ptr[v + 1] - row_ptr[v]);
+    }
+    #pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t r = 0; r < n_rows; ++r) {
+        const int64_t v = rows ? rows[r] : r;
+        for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {
+            const int64_t u = col_idx[p];
+            const int64_t e = eid ? (int64_t)eid[p] : p;
+            const int64_t o = off[r] + (p - row_ptr[v]);
+            for (int h = 0; h < H; ++h) {
+                double s = 0.0, a = 0.0;
+                for (int d = 0; d < D; ++d) {
+                    double t = (double)X[u * F + (int64_t)h * D + d] * (double)Y[v * F + (int64_t)h * D + d];
+                    s += t; a += fabs(t);
+                }
+                const double w = (double)E[e * H + h];
+                ref[o * H + h] = s * w;
+                abssum[o * H + h] = a * fabs(w);
+            }
+        }
+    }
+    free(off);
+}
+
+/*
  * Elementwise SDDMM edge functions (the u_OP_v members of the DGL builtin
  * family the paper plugs into): Eq. (2) with
  *   psi(x_u, x_v)[j] = X[u][j] OP Y[v][j],  OP in {add (0), sub (1), mul (2)}

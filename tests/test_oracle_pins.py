@@ -423,6 +423,49 @@ def test_u_dot_v_complete_graph_is_dense(H, D):
         np.testing.assert_allclose(ab[:, h].reshape(n, n), dabs, rtol=1e-12, atol=1e-13)
 
 
+@pytest.mark.parametrize("H,D", [(1, 7), (4, 4), (8, 2)])
+def test_u_dot_v_e_mul_complete_graph_is_dense_hadamard(H, D):
+    """u_dot_v-then-e_mul on the complete graph (self-loops included) equals the
+    dense per-head (Y X^T) (.) E_dense (numpy BLAS), with a permuted edge-id map so
+    E is read through eid; |terms| likewise.  Integer regime: bit-exact."""
+    n = 29
+    rp = np.arange(n + 1, dtype=np.int64) * n
+    ci = np.tile(np.arange(n, dtype=np.int32), n)
+    eid = gen.permutation(n * n, 77).astype(np.int32)
+    for regime in (gen.REAL, gen.INT):
+        X = gen.features((n, H * D), 52, 0, regime)
+        Y = gen.features((n, H * D), 52, 1, regime)
+        E = gen.features((n * n, H), 52, 2, regime, lo=-3, hi=3)
+        ref, ab = oracle.sddmm_emul(rp, ci, X, Y, E, H=H, eid=eid)
+        for h in range(H):
+            blk = slice(h * D, (h + 1) * D)
+            dense = Y[:, blk].astype(np.float64) @ X[:, blk].astype(np.float64).T        # [v, u]
+            Eh = E[eid, h].astype(np.float64).reshape(n, n)                             # CSR position -> E[eid]
+            dabs = np.abs(Y[:, blk].astype(np.float64)) @ np.abs(X[:, blk].astype(np.float64)).T
+            if regime == gen.INT:
+                assert np.array_equal(ref[:, h].reshape(n, n), dense * Eh)
+            else:
+                np.testing.assert_allclose(ref[:, h].reshape(n, n), dense * Eh, rtol=1e-12, atol=1e-13)
+            np.testing.assert_allclose(ab[:, h].reshape(n, n), dabs * np.abs(Eh), rtol=1e-12, atol=1e-13)
+
+
+def test_u_dot_v_e_mul_special_cases():
+    """E == 1 gives the plain score (Eq. (4)); E == 0 gives +-0; a single edge
+    with hand-computed values (2*3 + 1*(-4)) * 0.5 = 1."""
+    g = small_graph()
+    X = gen.features((g.n_src, 8), 53, 0)
+    ones = np.ones((g.nnz, 2), np.float32)
+    r1, a1 = oracle.sddmm_emul(g.row_ptr, g.col_idx, X, X, ones, H=2)
+    r0, a0 = oracle.sddmm(g.row_ptr, g.col_idx, X, X, H=2)
+    assert np.array_equal(r1, r0) and np.array_equal(a1, a0)
+    rz, az = oracle.sddmm_emul(g.row_ptr, g.col_idx, X, X, np.zeros((g.nnz, 2), np.float32), H=2)
+    assert (rz == 0).all() and (az == 0).all()
+    rp, ci = csr_from_edges(2, [[0, 1]])
+    X2 = np.array([[2, 1], [3, -4]], np.float32)
+    r, _ = oracle.sddmm_emul(rp, ci, X2, X2, np.array([[0.5]], np.float32), H=1)
+    assert r.tolist() == [[1.0]]
+
+
 def test_spec_dot_examples():
     ex = GOLD["dot"]
     rp, ci = csr_from_edges(ex["n"], ex["edges"])
