@@ -598,6 +598,10 @@ def run_extras(S, args, sync_all, flush):
                                                           out=o256, stream=st)),
     }
     res["bf16_storage_ms"] = {k: round(v, 4) for k, v in bf.items()}
+    # f4: u_dot_v then e_mul (scores scaled by the step's alpha, fused into the write-back)
+    s8w = torch.empty_like(S.s8)
+    res["sddmm_u_dot_v_e_mul_H8_D32_ms"] = round(timed(
+        lambda: fgp.sddmm(S.G, S.X["X256"], S.ydst("X256"), H=H_GAT, E=S.s8, out=s8w, stream=st)), 4)
     res["bf16_storage_note"] = ("row f4: same fp32 arithmetic and outputs, X (and Y) stored as bf16; "
                                 "parity vs the oracle on the decoded inputs in tests/test_parity_gpu.py")
     return res

@@ -206,6 +206,18 @@ fg_status fg_edge_softmax(const fg_graph* g, int H, const float* scores, float* 
 fg_status fg_gat_attention(const fg_graph* g, int H, int D, const float* X, const float* Y, float* out,
                            float* scores, fg_stream stream);
 
+/*
+ * fg_sddmm_emul -- u_dot_v followed by e_mul (row f4: the DGL builtin pair the
+ *   SDDMM template covers), the edge function inlined into the
+ *   template:
+ *     out[eid(p)][h] = ( sum_{d<D} X[u][h][d] * Y[v][h][d] ) * E[eid(p)][h]
+ *   X, Y, out as fg_sddmm (u_dot_v); E : fp32 [nnz][H] indexed by edge id;
+ *   out must not overlap E (FG_EINVAL).  The scale is applied at the kernel's
+ *   result write-back; shape rules and errors as fg_sddmm.
+ */
+fg_status fg_sddmm_emul(const fg_graph* g, int H, int D, const float* X, const float* Y, const float* E,
+                        float* out, fg_stream stream);
+
 /* ---------------------------------------------------------- bf16 features */
 /*
  * Row f4: bf16 STORAGE of the vertex features, fp32 arithmetic.

@@ -121,6 +121,26 @@ extern "C" fg_status fg_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, co
     return fgk::launch_sddmm(g, H, D, X, Y, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
+extern "C" fg_status fg_sddmm_emul(const fg_graph* g, int H, int D, const float* X, const float* Y, const float* E,
+                                   float* out, fg_stream stream) {
+    if (!g) return set_error(FG_EINVAL, "fg_sddmm_emul: NULL graph");
+    if (H < 1 || D < 1) return set_error(FG_ESHAPE, "fg_sddmm_emul: H=%d D=%d must be >= 1", H, D);
+    const int64_t F = int64_t(H) * D;
+    if (F % 4 != 0 || F > (int64_t(1) << 20)) return set_error(FG_ESHAPE, "fg_sddmm_emul: H*D must be a multiple of 4");
+    if (H > 1 && (D % 4 != 0 || ((D / 4) & (D / 4 - 1)) != 0))
+        return set_error(FG_ESHAPE, "fg_sddmm_emul: with H > 1, D must be 4 * 2^k (got D=%d)", D);
+    if (g->nnz == 0) return FG_OK;
+    if (!X || !Y || !E || !out) return set_error(FG_EINVAL, "fg_sddmm_emul: NULL tensor");
+    if (!aligned16(X) || !aligned16(Y) || !aligned16(out))
+        return set_error(FG_EINVAL, "fg_sddmm_emul: X/Y/out must be 16-byte aligned");
+    {
+        const uintptr_t o0 = reinterpret_cast<uintptr_t>(out), e0 = reinterpret_cast<uintptr_t>(E);
+        const uintptr_t nb = uintptr_t(g->nnz) * uintptr_t(H) * 4u;
+        if (o0 < e0 + nb && e0 < o0 + nb) return set_error(FG_EINVAL, "fg_sddmm_emul: out must not overlap E");
+    }
+    return fgk::launch_sddmm(g, H, D, X, Y, out, reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, E);
+}
+
 extern "C" fg_status fg_spmm_x16(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D,
                                  const uint16_t* X, const float* E, float* out, int32_t* arg_u, int32_t* arg_e,
                                  fg_stream stream) {

@@ -69,7 +69,8 @@ fg_status launch_spmm_mlp_simt(const fg_graph* g, fg_reduce_op red, int d2, cons
                                int d_in, const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e,
                                cudaStream_t st);
 fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const float* Y, float* out,
-                       cudaStream_t st, const uint16_t* Xbf16 = nullptr, const uint16_t* Ybf16 = nullptr);
+                       cudaStream_t st, const uint16_t* Xbf16 = nullptr, const uint16_t* Ybf16 = nullptr,
+                       const float* E = nullptr);
 fg_status launch_sddmm_binary(const fg_graph* g, int op, int F, const float* X, const float* Y, float* out,
                               cudaStream_t st);
 fg_status launch_edge_softmax(const fg_graph* g, int H, const float* S, float* out, cudaStream_t st);

@@ -50,6 +50,7 @@ struct Args {
     int accumulate;   // pass > 0: out += partial
     int tile4;        // float4 columns per pass (0: one pass over all F4)
     int persistent;   // != 0: persistent grid (resident CTAs per SM x #SMs; > 0 caps the CTAs per SM)
+    const float* E;   // u_dot_v-then-e_mul (fg_sddmm_emul): scores scaled by E[eid][h] at the write-back
 };
 
 // 4 bf16 (one 8-byte chunk, feature 0 in the low half of .x) -> 4 fp32, exact
@@ -273,11 +274,17 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                 }
             } else if (A.eid == nullptr) {
                 float* o = out + p0 * H;
-                for (int q = gl; q < tot; q += G) o[q] = res[q];
+                if (A.E) {
+                    const float* ew = A.E + p0 * H;
+                    for (int q = gl; q < tot; q += G) o[q] = res[q] * __ldg(ew + q);
+                } else {
+                    for (int q = gl; q < tot; q += G) o[q] = res[q];
+                }
             } else {
                 for (int q = gl; q < tot; q += G) {
                     const int t = q / H, h = q - t * H;
-                    out[int64_t(__ldg(A.eid + p0 + t)) * H + h] = res[q];
+                    const int64_t oi = int64_t(__ldg(A.eid + p0 + t)) * H + h;
+                    out[oi] = A.E ? res[q] * __ldg(A.E + oi) : res[q];
                 }
             }
         }
@@ -380,11 +387,17 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_pair_kernel(const Args A, co
             const int tot = cnt * H;
             if (A.eid == nullptr) {
                 float* o = out + p0 * H;
-                for (int q = gl; q < tot; q += G) o[q] = res[q];
+                if (A.E) {
+                    const float* ew = A.E + p0 * H;
+                    for (int q = gl; q < tot; q += G) o[q] = res[q] * __ldg(ew + q);
+                } else {
+                    for (int q = gl; q < tot; q += G) o[q] = res[q];
+                }
             } else {
                 for (int q = gl; q < tot; q += G) {
                     const int t = q / H, h = q - t * H;
-                    out[int64_t(__ldg(A.eid + p0 + t)) * H + h] = res[q];
+                    const int64_t oi = int64_t(__ldg(A.eid + p0 + t)) * H + h;
+                    out[oi] = A.E ? res[q] * __ldg(A.E + oi) : res[q];
                 }
             }
         }
@@ -445,10 +458,16 @@ fg_status launch_pair(const Args& A, const uint4* X, const uint4* Y, float* out,
 
 namespace fgk {
 
-fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const float* Y, float* out,
-                       cudaStream_t st, const uint16_t* Xbf16, const uint16_t* Ybf16) {
+__global__ void scale_by_kernel(float* __restrict__ out, const float* __restrict__ E, int64_t n) {
+    const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+    if (i < n) out[i] *= E[i];
+}
+
+static fg_status launch_sddmm_core(const fg_graph* g, int H, int D, const float* X, const float* Y, float* out,
+                                   cudaStream_t st, const uint16_t* Xbf16, const uint16_t* Ybf16, const float* E) {
     const bool xb = Xbf16 != nullptr;   // bf16 storage of X and Y (fg_sddmm_x16)
     Args A;
+    A.E = E;
     A.unit_row = g->unit_row;
     A.unit_p0 = g->unit_p0;
     A.n_units = g->n_units;
@@ -614,6 +633,33 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
             if (NV == 3) return launch_t<32, 3>(A, X4, Y4, out, st);
             return launch_t<32, 4>(A, X4, Y4, out, st);
     }
+}
+
+// u_dot_v, optionally followed by e_mul (E != NULL: out[e][h] = score * E[e][h]).
+// The scale is fused into the kernels' staged result write-back; configurations
+// that write results directly (more heads than a group stages: H > G, or the
+// opt-in column-tiled pass) scale in a second, elementwise pass instead.
+fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const float* Y, float* out,
+                       cudaStream_t st, const uint16_t* Xbf16, const uint16_t* Ybf16, const float* E) {
+    if (E) {
+        const int F4 = H * D / 4;
+        int G = 32;
+        if (F4 <= 32) {
+            G = 1;
+            while (G < F4) G *= 2;
+        }
+        const int B = G >= 4 ? 32 : 8;
+        const char* on = getenv("FG_SDDMM_L2_TILE");
+        const bool tiled = !Xbf16 && on && on[0] == '1' && H == 1;
+        if (H * B > 32 * G || tiled) {   // (the bf16 pair kernels stage whenever this holds)
+            fg_status s = launch_sddmm_core(g, H, D, X, Y, out, st, Xbf16, Ybf16, nullptr);
+            if (s != FG_OK) return s;
+            const int64_t n = g->nnz * H;
+            scale_by_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(out, E, n);
+            return check_launch("scale_by_kernel");
+        }
+    }
+    return launch_sddmm_core(g, H, D, X, Y, out, st, Xbf16, Ybf16, E);
 }
 
 }  // namespace fgk

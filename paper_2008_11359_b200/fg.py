@@ -28,7 +28,7 @@ EDGE = {"u_dot_v": 0, "u_add_v": 1, "u_sub_v": 2, "u_mul_v": 3}
 SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
            "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
            "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
-           "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_status_string", "fg_last_error", "fg_abi_version"]
+           "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_sddmm_emul", "fg_status_string", "fg_last_error", "fg_abi_version"]
 
 
 class FGError(RuntimeError):
@@ -63,6 +63,7 @@ def lib() -> ctypes.CDLL:
     L.fg_sddmm.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
     L.fg_spmm_x16.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]
     L.fg_sddmm_x16.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
+    L.fg_sddmm_emul.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp]
     L.fg_edge_softmax.argtypes = [vp, i32, vp, vp, vp]
     L.fg_gat_attention.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp]
     L.fg_graph_transpose.argtypes = [vp, vp, ctypes.POINTER(vp)]
@@ -76,7 +77,7 @@ def lib() -> ctypes.CDLL:
     for f in ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
               "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
               "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
-              "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16"]:
+              "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_sddmm_emul"]:
         getattr(L, f).restype = i32
     L.fg_status_string.argtypes = [i32]
     L.fg_status_string.restype = ctypes.c_char_p
@@ -237,11 +238,25 @@ def _spmm_x16(g, msg, reduce, X, *, H, E, out, arg_u, arg_e, stream):
 
 
 def sddmm(g: Graph, X: torch.Tensor, Y: torch.Tensor | None = None, *, H: int = 1, op: str = "u_dot_v",
-          out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+          out: torch.Tensor | None = None, E: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """featgraph.sddmm (Eq. (4), Fig. 5): out[eid][h] = <X[u,h,:], Y[v,h,:]> for
     op="u_dot_v"; the elementwise ops u_add_v / u_sub_v / u_mul_v give
     out[eid][j] = X[u][j] OP Y[v][j] ([nnz][F]).  torch.bfloat16 X (and Y)
-    select bf16 feature storage (fg_sddmm_x16, u_dot_v; fp32 arithmetic and out)."""
+    select bf16 feature storage (fg_sddmm_x16, u_dot_v; fp32 arithmetic and out).
+    E [nnz][H] (op="u_dot_v", fp32 X): u_dot_v-then-e_mul, out = score * E
+    (fg_sddmm_emul)."""
+    if E is not None:
+        if op != "u_dot_v":
+            raise FGError(FG_EINVAL, "sddmm: E (e_mul) applies to u_dot_v only")
+        X = _dev(X, torch.float32, "X")
+        Y = X if Y is None else _dev(Y, torch.float32, "Y")
+        E = _dev(E, torch.float32, "E")
+        F = X.numel() // max(X.shape[0], 1)
+        if out is None:
+            out = torch.empty((g.nnz, H), dtype=torch.float32, device=X.device)
+        _check(lib().fg_sddmm_emul(g.handle, H, F // H, _ptr(X), _ptr(Y), _ptr(E), _ptr(out), _stream(stream)),
+               "fg_sddmm_emul")
+        return out
     if X.dtype == torch.bfloat16:
         X = _dev(X, torch.bfloat16, "X")
         Y = X if Y is None else _dev(Y, torch.bfloat16, "Y")

@@ -632,3 +632,35 @@ def test_copy_u_bf16_tiled_and_unaligned(skewed, monkeypatch, F):
     s = fgp.sddmm(skewed.h, Xu, bf16_dev(Yb), H=1).cpu().numpy()
     rs, rab = oracle.sddmm(skewed.row_ptr, skewed.col_idx, dec, Yd, H=1)
     check_close(s, rs, rab, TOL, f"bf16 u_dot_v unaligned F={F}")
+
+
+# ------------------------------------------------------------------ u_dot_v then e_mul (row f4)
+@pytest.mark.parametrize("H,D", [(1, 512), (1, 16), (8, 32), (2, 4), (64, 4)])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_sddmm_emul(skewed, skewed_eid, H, D, use_eid):
+    """fg_sddmm_emul vs the oracle (score * E[eid][h]); (64, 4) has more heads than
+    a group stages, so the scale runs as a second pass."""
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    X = feats((g.n_src, H * D), 990 + D, gen.REAL)
+    Y = feats((g.n_dst, H * D), 991 + D, gen.REAL)
+    E = gen.features((g.nnz, H), 992, 0, gen.REAL) * np.float32(3)
+    out = fgp.sddmm(g.h, dev(X), dev(Y), H=H, E=dev(E)).cpu().numpy()
+    ref, ab = oracle.sddmm_emul(g.row_ptr, g.col_idx, X, Y, E, H=H, eid=g.eid)
+    pos = np.arange(g.nnz) if g.eid is None else g.eid
+    check_close(out[pos], ref, ab, TOL, f"u_dot_v-e_mul H={H} D={D}")
+    # integer regime: exact
+    Xi, Yi = feats((g.n_src, H * D), 993, gen.INT), feats((g.n_dst, H * D), 994, gen.INT)
+    Ei = gen.features((g.nnz, H), 995, 0, gen.INT, lo=-3, hi=3)
+    out = fgp.sddmm(g.h, dev(Xi), dev(Yi), H=H, E=dev(Ei)).cpu().numpy()
+    ref, _ = oracle.sddmm_emul(g.row_ptr, g.col_idx, Xi, Yi, Ei, H=H, eid=g.eid)
+    assert np.array_equal(out[pos].astype(np.float64), ref)
+
+
+def test_sddmm_emul_rejects_overlap(skewed):
+    import paper_2008_11359_b200 as fgp
+    X = dev(feats((skewed.n_src, 32), 996, gen.REAL))
+    E = dev(gen.features((skewed.nnz, 1), 997, 0, gen.REAL))
+    with pytest.raises(fgp.FGError) as e:
+        fgp.sddmm(skewed.h, X, H=1, E=E, out=E)
+    assert e.value.status == 1   # FG_EINVAL
