@@ -284,7 +284,7 @@ class Step:
         G, X, lo, nl = self.G, self.X, self.lo, self.nl
         arrived = {}
         with torch.cuda.stream(h2d):
-            for key in ("X8", "X128", "X512", "X256"):
+            for key in ("X8", "X128", "X256", "X512"):   # in the order the ops below first need them
                 X[key][lo:lo + nl].copy_(ins_h[key], non_blocking=True)
                 if key == "X8":
                     self.W.copy_(w_h, non_blocking=True)
@@ -304,6 +304,10 @@ class Step:
                 for o in outs:
                     outs_h[id(o)].copy_(o, non_blocking=True)
 
+        # op order: the smallest input first (X8, 7.5 MB), and the GAT scores +
+        # softmax (X256) before copy_u-sum so that X512's 477 MB copy is hidden
+        # behind them; the GAT aggregation last -- its n x 256 result is the
+        # smallest D2H tail
         ready("X8")
         fgp.spmm(G, "mlp", "max", X["X8"], W=self.W, X_dst=self.ydst("X8"), out=self.omlp, arg_u=self.aumlp,
                  arg_e=self.aemlp, stream=st)
@@ -311,14 +315,14 @@ class Step:
         ready("X128")
         fgp.spmm(G, "copy_u", "max", X["X128"], out=self.o128, arg_u=self.au128, arg_e=self.ae128, stream=st)
         ship([self.o128, self.au128, self.ae128])
+        ready("X256")
+        fgp.sddmm(G, X["X256"], self.ydst("X256"), H=H_GAT, out=self.s8, stream=st)
+        fgp.edge_softmax(G, self.s8, H=H_GAT, out=self.s8, stream=st)
         ready("X512")
         fgp.spmm(G, "copy_u", "sum", X["X512"], out=self.out512, stream=st)
         ship([self.out512])
         fgp.sddmm(G, X["X512"], self.ydst("X512"), H=1, out=self.s1, stream=st)
         ship([self.s1])
-        ready("X256")   # the GAT chain last: the smallest result (n x 256) is the D2H tail
-        fgp.sddmm(G, X["X256"], self.ydst("X256"), H=H_GAT, out=self.s8, stream=st)
-        fgp.edge_softmax(G, self.s8, H=H_GAT, out=self.s8, stream=st)
         fgp.spmm(G, "u_mul_e", "sum", X["X256"], H=H_GAT, E=self.s8, out=self.o256, stream=st)
         ship([self.o256])
 
