@@ -29,5 +29,18 @@ for g in (gen.make_graph("tiny"), gen.random_graph(600, 30000, 3, sigma=1.5, n_e
     W = dev(gen.features((8, 128), 3, 1))
     fgp.spmm(G, "mlp", "max", X8, W=W, arg_u=True, arg_e=True)
     fgp.spmm(G, "mlp", "sum", X8, W=W)
+    fgp.spmm(G, "mlp", "max", X8, W=W[:, :32].contiguous(), arg_u=True)   # d2 < 128: idle epilogue warps
+    # bf16 feature storage (16-byte pairs and 8-byte chunks) and u_dot_v-then-e_mul
+    for F in (8, 32, 128, 512):
+        Xb = dev(gen.features((g.n_src, F), 4, 0)).to(torch.bfloat16)
+        fgp.spmm(G, "copy_u", "sum", Xb)
+        fgp.spmm(G, "copy_u", "max", Xb, arg_u=True, arg_e=True)
+        fgp.sddmm(G, Xb)
+    Xb = X.to(torch.bfloat16)
+    fgp.sddmm(G, Xb, H=H)
+    fgp.spmm(G, "u_mul_e", "sum", Xb, H=H, E=a)
+    fgp.sddmm(G, X, H=H, E=a)
+    X64 = dev(gen.features((g.n_src, 256), 5, 0))
+    fgp.sddmm(G, X64, H=64, E=dev(gen.features((g.nnz, 64), 5, 1)))   # H > G: the second-pass scale
 torch.cuda.synchronize()
 print("sanitize_run: OK")
