@@ -345,23 +345,8 @@ struct Epi {
     }
 };
 
-// mark v as written after a preceding tcgen05.wait::ld (for a second buffer loaded
-// before that wait): keeps uses of v from being scheduled above the wait
-__device__ __forceinline__ void tmem_after_wait(uint32_t (&v)[32]) {
-    asm volatile(""
-                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
-                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
-                   "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
-                   "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
-                   "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
-                 :
-                 : "memory");
-}
-
-// ILP = TMEM chunks loaded per wait (1: 4 CTAs/SM at <= 80 registers; 2: both
-// 32-column chunks of a tile in flight, 3 CTAs/SM)
-template <int KS, bool MAX, int ILP>
-__global__ void __launch_bounds__(THREADS, ILP == 2 ? 3 : CTAS_PER_SM) mlp_tcgen05_kernel(const __grid_constant__ Args A) {
+template <int KS, bool MAX>
+__global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const __grid_constant__ Args A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem<KS>& S = *reinterpret_cast<Smem<KS>*>(smem_raw);
     const int tid = threadIdx.x;
@@ -521,23 +506,14 @@ __global__ void __launch_bounds__(THREADS, ILP == 2 ? 3 : CTAS_PER_SM) mlp_tcgen
             tc_fence_after();
             const int tb = t * NT;                       // relative to E0
             const int nv_tile = min(NT, nnz_cta - tb);
-            if constexpr (ILP == 2) {
-                static_assert(NT == 64, "ILP 2 loads the tile's two chunks");
-                uint32_t v0[32], v1[32];
-                tmem_ld32(lane_base + uint32_t(b * NT), v0);
-                tmem_ld32(lane_base + uint32_t(b * NT + 32), v1);
-                tmem_wait_ld(v0);
-                tmem_after_wait(v1);
-                ep.consume(v0, tb, max(0, min(32, nv_tile)));
-                ep.consume(v1, tb + 32, max(0, min(32, nv_tile - 32)));
-            } else {
+            // one 32-column chunk per tcgen05.ld (loading both chunks of the tile at once
+            // needs 3 CTAs/SM for the registers and measured slower: 4.29 vs 4.07 ms)
 #pragma unroll 1
-                for (int ch = 0; ch < NT / 32; ++ch) {   // single-buffered: 4 CTAs per SM supply the overlap
-                    uint32_t v0[32];
-                    tmem_ld32(lane_base + uint32_t(b * NT + ch * 32), v0);
-                    tmem_wait_ld(v0);
-                    ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)));
-                }
+            for (int ch = 0; ch < NT / 32; ++ch) {
+                uint32_t v0[32];
+                tmem_ld32(lane_base + uint32_t(b * NT + ch * 32), v0);
+                tmem_wait_ld(v0);
+                ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)));
             }
             tc_fence_before();
             mbar_arrive(&S.tempty[b]);
@@ -553,10 +529,10 @@ __global__ void __launch_bounds__(THREADS, ILP == 2 ? 3 : CTAS_PER_SM) mlp_tcgen
     }
 }
 
-template <int KS, bool MAX, int ILP>
+template <int KS, bool MAX>
 fg_status launch_ks(const Args& A, cudaStream_t st) {
     const int smem = int(sizeof(Smem<KS>)) + 1024;
-    const int smem_min = (ILP == 2 ? 72 : 56) * 1024;             // bounds residency (TMEM columns)
+    const int smem_min = 56 * 1024;                              // bounds residency (TMEM columns)
     const int smem_req = smem < smem_min ? smem_min : smem;
     {   // pre-split X into tf32 hi / lo rows (the producers' cp.async source)
         const int64_t tot = A.n_src * KS * 8;
@@ -574,13 +550,13 @@ fg_status launch_ks(const Args& A, cudaStream_t st) {
         fg_status s = fgk::check_launch("mlp_q_kernel");
         if (s != FG_OK) return s;
     }
-    auto kfn = mlp_tcgen05_kernel<KS, MAX, ILP>;
+    auto kfn = mlp_tcgen05_kernel<KS, MAX>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_req);
     // the whole unified L1/smem for shared memory: without it the driver picks a
     // carveout that fits ONE 100 KB CTA per SM and the persistent grid runs as two waves
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return fgk::set_error(FG_ECUDA, "mlp_tcgen05: smem attribute: %s", cudaGetErrorString(e));
-    int nb = (ILP == 2 ? 3 : CTAS_PER_SM) * fgk::num_sms();
+    int nb = CTAS_PER_SM * fgk::num_sms();
     const int64_t want = (A.nnz + 4 * NT - 1) / (4 * NT);   // >= 4 tiles per CTA
     if (want < nb) nb = int(want < 1 ? 1 : want);
     const dim3 grid{unsigned(nb), unsigned((A.d2 + MT - 1) / MT), 1u};
@@ -632,23 +608,11 @@ fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, c
     A.d2 = d2;
     const bool mx = red == FG_REDUCE_MAX;
     const int ks = (d_in + 7) / 8;
-    static const int ilp = [] {
-        const char* e = getenv("FG_MLP_ILP");
-        return (e && e[0] == '2') ? 2 : 1;
-    }();
-    if (ilp == 2) {
-        switch (ks) {
-            case 1: return mx ? launch_ks<1, true, 2>(A, st) : launch_ks<1, false, 2>(A, st);
-            case 2: return mx ? launch_ks<2, true, 2>(A, st) : launch_ks<2, false, 2>(A, st);
-            case 3: return mx ? launch_ks<3, true, 2>(A, st) : launch_ks<3, false, 2>(A, st);
-            default: return mx ? launch_ks<4, true, 2>(A, st) : launch_ks<4, false, 2>(A, st);
-        }
-    }
     switch (ks) {
-        case 1: return mx ? launch_ks<1, true, 1>(A, st) : launch_ks<1, false, 1>(A, st);
-        case 2: return mx ? launch_ks<2, true, 1>(A, st) : launch_ks<2, false, 1>(A, st);
-        case 3: return mx ? launch_ks<3, true, 1>(A, st) : launch_ks<3, false, 1>(A, st);
-        default: return mx ? launch_ks<4, true, 1>(A, st) : launch_ks<4, false, 1>(A, st);
+        case 1: return mx ? launch_ks<1, true>(A, st) : launch_ks<1, false>(A, st);
+        case 2: return mx ? launch_ks<2, true>(A, st) : launch_ks<2, false>(A, st);
+        case 3: return mx ? launch_ks<3, true>(A, st) : launch_ks<3, false>(A, st);
+        default: return mx ? launch_ks<4, true>(A, st) : launch_ks<4, false>(A, st);
     }
 }
 
