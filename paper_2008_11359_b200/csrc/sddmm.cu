@@ -113,7 +113,7 @@ __device__ __forceinline__ void reduce_scatter(float (&v)[K], int gl, unsigned m
 //                lane belongs to head c / D4; reduce over D4 lanes per chunk.
 // MODE_GENERAL : H == 1 with F > 4*G*NV (column tiles; Y re-read through L1), or
 //                H > 1 with D4 > G (a head spans several chunks of a lane).
-template <int G, int NV, int MODE, int DW, bool XB>
+template <int G, int NV, int MODE, int DW, bool XB, bool EM = false>
 __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const float4* __restrict__ X,
                                                            const float4* __restrict__ Y, float* __restrict__ out) {
     constexpr int TW = G * NV;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                 }
             } else if (A.eid == nullptr) {
                 float* o = out + p0 * H;
-                if (A.E) {
+                if constexpr (EM) {   // u_dot_v then e_mul: scale at the write-back
                     const float* ew = A.E + p0 * H;
                     for (int q = gl; q < tot; q += G) o[q] = res[q] * __ldg(ew + q);
                 } else {
@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                 for (int q = gl; q < tot; q += G) {
                     const int t = q / H, h = q - t * H;
                     const int64_t oi = int64_t(__ldg(A.eid + p0 + t)) * H + h;
-                    out[oi] = A.E ? res[q] * __ldg(A.E + oi) : res[q];
+                    if constexpr (EM) out[oi] = res[q] * __ldg(A.E + oi);
+                    else out[oi] = res[q];
                 }
             }
         }
@@ -387,17 +388,11 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_pair_kernel(const Args A, co
             const int tot = cnt * H;
             if (A.eid == nullptr) {
                 float* o = out + p0 * H;
-                if (A.E) {
-                    const float* ew = A.E + p0 * H;
-                    for (int q = gl; q < tot; q += G) o[q] = res[q] * __ldg(ew + q);
-                } else {
-                    for (int q = gl; q < tot; q += G) o[q] = res[q];
-                }
+                for (int q = gl; q < tot; q += G) o[q] = res[q];
             } else {
                 for (int q = gl; q < tot; q += G) {
                     const int t = q / H, h = q - t * H;
-                    const int64_t oi = int64_t(__ldg(A.eid + p0 + t)) * H + h;
-                    out[oi] = A.E ? res[q] * __ldg(A.E + oi) : res[q];
+                    out[int64_t(__ldg(A.eid + p0 + t)) * H + h] = res[q];
                 }
             }
         }
@@ -422,6 +417,24 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
         }
     } else {
         k = sddmm_kernel<G, NV, MODE_GENERAL, 1, XB>;
+    }
+    if constexpr (!XB) {   // u_dot_v then e_mul (fg_sddmm_emul, fp32 only): the staged modes
+        if (A.E) {
+            if (A.H == 1 && (A.tile4 ? A.tile4 : A.F4) <= TW) {
+                k = sddmm_kernel<G, NV, MODE_H1, G, false, true>;
+            } else if (A.H > 1 && A.D4 <= G && A.F4 <= TW) {
+                switch (A.D4) {
+                    case 1: k = sddmm_kernel<G, NV, MODE_HEADS, 1, false, true>; break;
+                    case 2: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 2 ? 2 : 1), false, true>; break;
+                    case 4: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 4 ? 4 : 1), false, true>; break;
+                    case 8: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 8 ? 8 : 1), false, true>; break;
+                    case 16: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 16 ? 16 : 1), false, true>; break;
+                    default: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 32 ? 32 : 1), false, true>; break;
+                }
+            } else {
+                k = sddmm_kernel<G, NV, MODE_GENERAL, 1, false, true>;
+            }
+        }
     }
     const int64_t per_block = THREADS / G;
     int64_t blocks = (A.n_units + per_block - 1) / per_block;
