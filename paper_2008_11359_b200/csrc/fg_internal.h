@@ -81,14 +81,15 @@ fg_status check_launch(const char* what);
 // first use; the handle owns it)
 fg_status get_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t st, const fg_graph::SegUnits** out);
 
-// L2 budget (bytes) for feature-dimension tiling of the gathered operand;
-// FG_L2_TILE_MB overrides the default (64 MiB, half the 126 MB L2), 0 disables.
-// column-tile budget of the copy_u gather (FG_L2_TILE_MB, default 32: on reddit
-// 32 MB tiles beat 64 MB for F = 128 sum / max (3.49 / 4.79 vs 3.63 / 5.46 ms) and
-// tie at F = 512; 24 MB and below drop to 4-lane groups and lose)
-inline int64_t l2_tile_budget() {
+// column-tile budget (bytes of the gathered operand per pass) of the copy_u
+// gather, the paper's feature-dimension tiling retargeted to the L2.
+// FG_L2_TILE_MB overrides; 0 disables.  Defaults measured on reddit (one B200):
+// select reducers (max / min + argmax) 32 MB (F=128 max + args 4.79 ms vs 5.46 at
+// 64 MB), sum / mean 64 MB (F=512 13.4-13.6 ms vs 14.0-14.1 at 32 MB); 24 MB and
+// below fall to 4-lane groups and lose.
+inline int64_t l2_tile_budget(bool select_reducer = false) {
     const char* e = getenv("FG_L2_TILE_MB");
-    return int64_t(e ? atoi(e) : 32) << 20;
+    return int64_t(e ? atoi(e) : (select_reducer ? 32 : 64)) << 20;
 }
 
 inline int num_sms() {

@@ -71,7 +71,7 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     int G = 32, NV = 4;
     int F4 = A.F4;
     {
-        const int64_t budget = fgk::l2_tile_budget();
+        const int64_t budget = fgk::l2_tile_budget(red == FG_REDUCE_MAX || red == FG_REDUCE_MIN);
         // copy_u only: u_mul_e re-reads E (m x H floats) on every pass, measured slower
         // at every budget (reddit H=8 D=32: 9.1-10.1 ms untiled vs 12.2-43.6 ms tiled)
         if (msg == FG_MSG_COPY_U && budget > 0 && g->n_src * int64_t(F4) * chunk_bytes > budget) {
