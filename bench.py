@@ -186,6 +186,7 @@ class Step:
     def __init__(self, g, shard, host, comm, stream):
         import torch
         import paper_2008_11359_b200 as fgp
+        from paper_2008_11359_b200.shard import make_shard as make_shard_fn
         self.fgp, self.torch = fgp, torch
         self.shard, self.comm, self.stream = shard, comm, stream
         self.n = g.n_dst
@@ -215,6 +216,14 @@ class Step:
         # N > 1: the source-feature all-gathers run on their own stream, in the
         # order the ops consume them, overlapped with the ops on the earlier tensors
         self.comm_stream = torch.cuda.Stream() if comm is not None else None
+        # e2e leg: the last op (GAT aggregation) runs on two row halves of this
+        # rank's graph (two fg_graph handles over contiguous row ranges, global
+        # source ids) so the first half's result ships while the second computes
+        self.halves = []
+        for r in range(2):
+            h = make_shard_fn(rp, ci, r, 2)
+            self.halves.append((fgp.Graph(torch.from_numpy(h.row_ptr).to(dev), torch.from_numpy(h.col_idx).to(dev),
+                                          n_src=g.n_src), h.lo, h.hi, h.edge_lo, h.edge_lo + h.nnz))
 
     def ydst(self, k):
         return self.X[k][self.lo:self.lo + self.nl]
@@ -296,13 +305,16 @@ class Step:
             if self.comm is not None:
                 self.comm.allgather_rows(self.shard.offsets, X[key][lo:lo + nl], X[key], stream=st)
 
-        def ship(outs):
+        def ship(outs, rows=None):
             done = torch.cuda.Event()
             done.record(st)
             d2h.wait_event(done)
             with torch.cuda.stream(d2h):
                 for o in outs:
-                    outs_h[id(o)].copy_(o, non_blocking=True)
+                    if rows is None:
+                        outs_h[id(o)].copy_(o, non_blocking=True)
+                    else:
+                        outs_h[id(o)][rows[0]:rows[1]].copy_(o[rows[0]:rows[1]], non_blocking=True)
 
         # op order: the smallest input first (X8, 7.5 MB), and the GAT scores +
         # softmax (X256) before copy_u-sum so that X512's 477 MB copy is hidden
@@ -323,8 +335,9 @@ class Step:
         ship([self.out512])
         fgp.sddmm(G, X["X512"], self.ydst("X512"), H=1, out=self.s1, stream=st)
         ship([self.s1])
-        fgp.spmm(G, "u_mul_e", "sum", X["X256"], H=H_GAT, E=self.s8, out=self.o256, stream=st)
-        ship([self.o256])
+        for Gh, rlo, rhi, elo, ehi in self.halves:   # halves: the first half's D2H overlaps the second
+            fgp.spmm(Gh, "u_mul_e", "sum", X["X256"], H=H_GAT, E=self.s8[elo:ehi], out=self.o256[rlo:rhi], stream=st)
+            ship([self.o256], rows=(rlo, rhi))
 
     def outputs(self):
         return [self.out512, self.s1, self.o256, self.o128, self.au128, self.ae128, self.omlp, self.aumlp,
