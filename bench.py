@@ -144,6 +144,32 @@ def gpu_id_for_smi(local_rank: int) -> str:
     return str(local_rank)
 
 
+def mlp_tmem_floor(S, flush, sync_all, reps: int = 5) -> float:
+    """The MLP kernel's own ceiling, measured live: the same launch with the
+    gathers and the MMAs disabled (FG_MLP_DBG=6: the epilogue still reads every
+    accumulator element out of TMEM -- m x d2 x 4 bytes -- but the results are
+    garbage), i.e. the TMEM-read-bound skeleton."""
+    import torch
+    st = S.stream
+    os.environ["FG_MLP_DBG"] = "6"
+    try:
+        ts = []
+        for k in range(reps + 1):
+            with torch.cuda.stream(st):
+                flush.fill_(float(k))
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                S.fgp.spmm(S.G, "mlp", "max", S.X["X8"], W=S.W, X_dst=S.ydst("X8"), out=S.omlp, arg_u=S.aumlp,
+                           arg_e=S.aemlp, stream=st)
+                b.record(st)
+            sync_all()
+            if k:
+                ts.append(a.elapsed_time(b))
+    finally:
+        os.environ.pop("FG_MLP_DBG", None)
+    return float(np.mean(ts))
+
+
 def l2_gather_ceiling(torch, buf) -> dict | None:
     """The L2 gather ceiling of this GPU, measured live (libfgprobe.so,
     paper_2008_11359_b200/probe/l2_probe.cu): random whole-row reads of an
@@ -485,6 +511,7 @@ def main():
         e2e = run_e2e(S, host, args, world, sync_all, flush)
 
     l2peak = l2_gather_ceiling(torch, flush.buf) if rank == 0 else None
+    mlp_floor_ms = mlp_tmem_floor(S, flush, sync_all) if rank == 0 else None
 
     total_bytes = sum(op_bytes(g.n_dst, g.nnz).values())
     local_bytes = op_bytes(S.nl, S.m)
@@ -551,6 +578,14 @@ def main():
         {k: round(local_bytes[k] / (op_ms[k] * 1e-3) / 1e9, 1) for k in OPS},
         "allgather_ms": round(ag_ms, 4) if world > 1 else 0.0,
         "mlp_tflops": round(mlp_flops(S.m) / (op_ms["spmm_mlp_max_d8_d128_args"] * 1e-3) / 1e12, 2),
+        "mlp_roofline": ({"kernel": "spmm_mlp_max_d8_d128_args", "bound": "tmem-read", "unit": "GB/s",
+                          "achieved": round(4 * S.m * D2 / (op_ms["spmm_mlp_max_d8_d128_args"] * 1e-3) / 1e9, 1),
+                          "peak": round(4 * S.m * D2 / (mlp_floor_ms * 1e-3) / 1e9, 1),
+                          "frac": round(mlp_floor_ms / op_ms["spmm_mlp_max_d8_d128_args"], 4),
+                          "note": "bytes = every fp32 accumulator element read out of TMEM (m x d2 x 4); peak = "
+                                  "those bytes / the same launch with gathers and MMAs disabled "
+                                  "(FG_MLP_DBG=6), measured live in this run"}
+                         if mlp_floor_ms else None),
         "roofline": {"kernel": dom, "share": round(dom_ms / sum(op_ms.values()), 4), "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",

@@ -76,3 +76,13 @@ def test_probe_lib_loads_and_rejects_bad_args(L):
     out = (ctypes.c_double * 5)()
     assert P.fgprobe_l2(None, 0, out) != 0
     assert P.fgprobe_l2(ctypes.c_void_p(256), 1 << 20, out) != 0
+
+
+def test_host_validation_new_entry_points_no_gpu(L):
+    """fg_spmm_x16 / fg_sddmm_x16 / fg_sddmm_emul reject bad arguments on the
+    host before any launch (include/fg.h)."""
+    from paper_2008_11359_b200 import fg
+    assert L.fg_spmm_x16(None, 0, 0, 1, 4, None, None, None, None, None, None) == fg.FG_EINVAL
+    assert L.fg_sddmm_x16(None, 0, 1, 4, None, None, None, None) == fg.FG_EINVAL
+    assert L.fg_sddmm_emul(None, 1, 4, None, None, None, None, None) == fg.FG_EINVAL
+    assert b"NULL graph" in L.fg_last_error()
