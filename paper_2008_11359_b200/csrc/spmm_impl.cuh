@@ -69,9 +69,9 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                                              float* __restrict__ etile) {
     constexpr int B = 32;                                   // edges per index batch
     constexpr int R = B / G;                                // indices per lane per batch
-    // edges in flight per lane; PAIR keeps raw bf16 pairs (half the registers), so
-    // it affords twice the edges -- the same bytes in flight as the fp32 mapping
-    constexpr int U = PAIR ? (NV >= 4 ? 4 : 8) : (NV >= 4 ? 2 : (NV >= 2 ? 4 : 8));
+    // edges in flight per lane; PAIR (raw bf16 pairs): 4 -- 8 measured slower
+    // (reddit bf16 copy_u-sum F=512 9.37 vs 8.49 ms, u_mul_e H=8 10.1 vs 7.5 ms)
+    constexpr int U = PAIR ? 4 : (NV >= 4 ? 2 : (NV >= 2 ? 4 : 8));
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);     // select-type reducers
     const int F4 = A.F4;
     for (int64_t p0 = s; p0 < e; p0 += B) {
