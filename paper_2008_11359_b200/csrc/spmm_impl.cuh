@@ -70,8 +70,10 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
     constexpr int B = 32;                                   // edges per index batch
     constexpr int R = B / G;                                // indices per lane per batch
     // edges in flight per lane; PAIR (raw bf16 pairs): 4 -- 8 measured slower
-    // (reddit bf16 copy_u-sum F=512 9.37 vs 8.49 ms, u_mul_e H=8 10.1 vs 7.5 ms)
-    constexpr int U = PAIR ? 4 : (NV >= 4 ? 2 : (NV >= 2 ? 4 : 8));
+    // (reddit bf16 copy_u-sum F=512 9.37 vs 8.49 ms, u_mul_e H=8 10.1 vs 7.5 ms);
+    // one chunk per lane: 8 for sum, 4 for the select reducers (reddit copy_u-max
+    // F=128 + args 4.84 -> 4.63 ms; sum F=512 unchanged)
+    constexpr int U = PAIR ? 4 : (NV >= 4 ? 2 : (NV >= 2 ? 4 : ((RED == R_MAX || RED == R_MIN) ? 4 : 8)));
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);     // select-type reducers
     const int F4 = A.F4;
     for (int64_t p0 = s; p0 < e; p0 += B) {
