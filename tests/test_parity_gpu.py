@@ -717,3 +717,17 @@ def test_bipartite_all_ops(bipartite):
     gat = fgp.gat_attention(g.h, dev(X), dev(Y), H=H).cpu().numpy()
     rg, rgb = oracle.gat(g.row_ptr, g.col_idx, X, Y, H=H)
     check_close(gat, rg, rgb, TOL, "bipartite fused GAT")
+
+
+@pytest.mark.parametrize("chunk", ["32", "256"])
+def test_sddmm_unit_sizes(skewed, monkeypatch, chunk):
+    """The SDDMM work-unit size (edges per unit, fixed at graph creation;
+    default 64) does not change any result: same per-edge arithmetic."""
+    import paper_2008_11359_b200 as fgp
+    monkeypatch.setenv("FG_SDDMM_CHUNK", chunk)
+    g2 = G(skewed.row_ptr, skewed.col_idx, skewed.n_src)
+    for H, D in ((1, 512), (8, 32)):
+        X = feats((skewed.n_src, H * D), 1200 + D, gen.REAL)
+        a = fgp.sddmm(g2.h, dev(X), H=H).cpu().numpy()
+        b = fgp.sddmm(skewed.h, dev(X), H=H).cpu().numpy()
+        assert np.array_equal(a, b)
