@@ -107,8 +107,12 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
             NV = 4;   // 128 float4 columns per tile; wider rows take several tiles (grid.y)
         }
     }
-    const int64_t NG = THREADS / G;
-    A.n_heavy = rows_with_degree_at_least(g, NG * 32);
+    {   // rows with degree >= FG_SPMM_HEAVY_DEG run CTA-per-row (default 4096 for every
+        // G; reddit: the former NG * 32 = 256..1024 cost copy_u-sum F=512 14.1 vs 12.5 ms,
+        // u_mul_e H=8 9.4 vs 7.8 ms, copy_u-max F=128 4.7 vs 4.35 ms; 2048 / 8192 lose 1-6 %)
+        const char* hv = getenv("FG_SPMM_HEAVY_DEG");
+        A.n_heavy = rows_with_degree_at_least(g, hv ? std::max<int64_t>(1, atoll(hv)) : 4096);
+    }
     const int opset = (op == OP_UADDE || op == OP_COPYE) ? 1 : 0;
     if (Xbf16) {   // bf16 storage: copy_u / u_mul_e x {sum, max} (validated by the caller)
         if (mx == R_MAX) return dispatch_x16<R_MAX>(A, G, NV, op, pair, st);

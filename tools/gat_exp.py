@@ -18,7 +18,7 @@ def t(fn, reps=5):
     return np.median(ts)
 ref = None
 for v in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0"]):
-    os.environ["FG_GAT_VARIANT"] = v
+    os.environ["FG_GAT_HEAVY_DEG"] = v
     ms = t(lambda: fgp.gat_attention(G, X, X, H=H, out=out))
     o = out.clone()
     if ref is None: ref = o
