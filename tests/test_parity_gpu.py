@@ -731,3 +731,40 @@ def test_sddmm_unit_sizes(skewed, monkeypatch, chunk):
         a = fgp.sddmm(g2.h, dev(X), H=H).cpu().numpy()
         b = fgp.sddmm(skewed.h, dev(X), H=H).cpu().numpy()
         assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ CTA-per-row path on the small graphs
+@pytest.mark.parametrize("deg", ["1", "200", "1024"])
+def test_cta_per_row_thresholds(skewed, skewed_eid, monkeypatch, deg):
+    """Rows of degree >= FG_SPMM_HEAVY_DEG / FG_GAT_HEAVY_DEG (default 4096, above
+    this graph's maximum) run CTA-per-row with the fixed-order combine: force it
+    for most rows and check sum / max (argmax ties across the CTA's chunks) / min /
+    mean, u_mul_e and u_add_e with edge ids, bf16 storage and the fused GAT."""
+    import paper_2008_11359_b200 as fgp
+    monkeypatch.setenv("FG_SPMM_HEAVY_DEG", deg)
+    monkeypatch.setenv("FG_GAT_HEAVY_DEG", deg)
+    g = skewed
+    for F, regime in ((512, gen.REAL), (32, gen.INT), (128, gen.INT)):
+        X = feats((g.n_src, F), 1300 + F, regime, lo=-2, hi=2)   # integers in [-2, 2]: many ties
+        for red in ("sum", "max", "min", "mean"):
+            ref, ab, rau, rae = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", red, X)
+            if red in ("max", "min"):
+                o, au, ae = fgp.spmm(g.h, "copy_u", red, dev(X), arg_u=True, arg_e=True)
+                assert np.array_equal(o.cpu().numpy().astype(np.float64), ref), (red, F)
+                assert np.array_equal(au.cpu().numpy(), rau) and np.array_equal(ae.cpu().numpy(), rae), (red, F)
+            else:
+                check_close(fgp.spmm(g.h, "copy_u", red, dev(X)).cpu().numpy(), ref, ab, TOL, f"{red} F={F}")
+    ge = skewed_eid
+    H, D = 8, 32
+    X = feats((ge.n_src, H * D), 1310, gen.REAL)
+    E = gen.features((ge.nnz, H), 1311, 0, gen.UNIT)
+    for op in ("u_mul_e", "u_add_e"):
+        ref, ab, _, _ = oracle.spmm(ge.row_ptr, ge.col_idx, op, "sum", X, H=H, E=E, eid=ge.eid)
+        check_close(fgp.spmm(ge.h, op, "sum", dev(X), H=H, E=dev(E)).cpu().numpy(), ref, ab, TOL, op)
+    bits, dec = gen.to_bf16(X)
+    ref, ab, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", "sum", dec)
+    check_close(fgp.spmm(g.h, "copy_u", "sum", bf16_dev(bits)).cpu().numpy(), ref, ab, TOL, "bf16 copy_u")
+    Y = feats((g.n_dst, H * D), 1312, gen.REAL)
+    out = fgp.gat_attention(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+    rg, rgb = oracle.gat(g.row_ptr, g.col_idx, X, Y, H=H)
+    check_close(out, rg, rgb, TOL, "fused GAT")
