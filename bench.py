@@ -246,8 +246,14 @@ class Step:
         # rank's graph (two fg_graph handles over contiguous row ranges, global
         # source ids) so the first half's result ships while the second computes
         self.halves = []
+        # split row: nnz-balanced, moved to the nearest row whose first edge is a
+        # multiple of 4 (the per-edge H=1 scores s1[e0:e1] must stay 16-byte aligned)
+        mid = int(np.searchsorted(rp, rp[-1] // 2))
+        cand = [r for r in range(max(1, mid - 64), min(len(rp) - 1, mid + 64)) if rp[r] % 4 == 0]
+        split = min(cand, key=lambda r: abs(r - mid)) if cand else 0
+        offs = np.array([0, split, len(rp) - 1], np.int64)
         for r in range(2):
-            h = make_shard_fn(rp, ci, r, 2)
+            h = make_shard_fn(rp, ci, r, 2, offsets=offs)
             self.halves.append((fgp.Graph(torch.from_numpy(h.row_ptr).to(dev), torch.from_numpy(h.col_idx).to(dev),
                                           n_src=g.n_src), h.lo, h.hi, h.edge_lo, h.edge_lo + h.nnz))
 
@@ -357,10 +363,14 @@ class Step:
         fgp.sddmm(G, X["X256"], self.ydst("X256"), H=H_GAT, out=self.s8, stream=st)
         fgp.edge_softmax(G, self.s8, H=H_GAT, out=self.s8, stream=st)
         ready("X512")
-        fgp.spmm(G, "copy_u", "sum", X["X512"], out=self.out512, stream=st)
-        ship([self.out512])
-        fgp.sddmm(G, X["X512"], self.ydst("X512"), H=1, out=self.s1, stream=st)
-        ship([self.s1])
+        # the two X512 ops on the row halves too: each half's result ships while
+        # the next half computes (the D2H stream is the e2e tail's bottleneck)
+        for Gh, rlo, rhi, elo, ehi in self.halves:
+            fgp.spmm(Gh, "copy_u", "sum", X["X512"], out=self.out512[rlo:rhi], stream=st)
+            ship([self.out512], rows=(rlo, rhi))
+        for Gh, rlo, rhi, elo, ehi in self.halves:
+            fgp.sddmm(Gh, X["X512"], self.ydst("X512")[rlo:rhi], H=1, out=self.s1[elo:ehi], stream=st)
+            ship([self.s1], rows=(elo, ehi))
         for Gh, rlo, rhi, elo, ehi in self.halves:   # halves: the first half's D2H overlaps the second
             fgp.spmm(Gh, "u_mul_e", "sum", X["X256"], H=H_GAT, E=self.s8[elo:ehi], out=self.o256[rlo:rhi], stream=st)
             ship([self.o256], rows=(rlo, rhi))
