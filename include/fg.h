@@ -302,6 +302,23 @@ fg_status fg_comm_init(const void* unique_id_128, int nranks, int rank, fg_comm*
 fg_status fg_comm_destroy(fg_comm* c);
 fg_status fg_allgather_rows(fg_comm* c, const int64_t* shard_offsets, int64_t row_elems,
                             const float* X_local, float* X_full, fg_stream stream);
+/*
+ * fg_dist_spmm / fg_dist_sddmm -- the sharded ops: fg_allgather_rows of this
+ *   rank's source-feature block X_local into X_full (device, [n_src][row]; the
+ *   row is H*D floats, d_in for mlp), then fg_spmm / fg_sddmm on `local` (this
+ *   rank's destination rows, GLOBAL source ids) reading X_full, both enqueued on
+ *   `stream`.  Y_local / X_dst / out_local / arg_* / E are this rank's rows /
+ *   edges; every other argument, shape rule and error as fg_spmm / fg_sddmm
+ *   (copy_e: FG_EUNSUPPORTED, it gathers no source rows).  Per-row results are
+ *   bit-identical to the unsharded op.
+ */
+fg_status fg_dist_spmm(const fg_graph* local, fg_comm* c, const int64_t* shard_offsets, fg_msg_op msg,
+                       fg_reduce_op red, int H, int D, const float* X_local, float* X_full, const float* E,
+                       const float* W, int d_in, const float* X_dst, float* out_local, int32_t* arg_u,
+                       int32_t* arg_e, void* workspace, size_t workspace_bytes, fg_stream stream);
+fg_status fg_dist_sddmm(const fg_graph* local, fg_comm* c, const int64_t* shard_offsets, fg_edge_op op, int H,
+                        int D, const float* X_local, float* X_full, const float* Y_local, float* out_local,
+                        fg_stream stream);
 
 /* ---------------------------------------------------------------- errors */
 const char* fg_status_string(fg_status s);

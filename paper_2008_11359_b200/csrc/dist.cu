@@ -124,3 +124,29 @@ extern "C" fg_status fg_allgather_rows(fg_comm* c, const int64_t* off, int64_t r
     if (r != ncclSuccess) return nccl_fail("ncclGroupEnd", r);
     return FG_OK;
 }
+
+// ---------------------------------------------------------------- sharded ops
+// The dst-row-sharded forms of gSpMM / gSDDMM: the one
+// exchange step (all-gather of the source-feature row blocks over NVLink) then
+// the unchanged local kernel on this rank's rows, both enqueued on `stream`.
+extern "C" fg_status fg_dist_spmm(const fg_graph* local, fg_comm* c, const int64_t* shard_offsets, fg_msg_op msg,
+                                  fg_reduce_op red, int H, int D, const float* X_local, float* X_full, const float* E,
+                                  const float* W, int d_in, const float* X_dst, float* out_local, int32_t* arg_u,
+                                  int32_t* arg_e, void* workspace, size_t workspace_bytes, fg_stream stream) {
+    if (!local || !c || !shard_offsets || !X_full) return fgk::set_error(FG_EINVAL, "fg_dist_spmm: NULL argument");
+    if (msg == FG_MSG_COPY_E) return fgk::set_error(FG_EUNSUPPORTED, "fg_dist_spmm: copy_e gathers no source rows");
+    const int64_t row_elems = (msg == FG_MSG_MLP) ? int64_t(d_in) : int64_t(H) * D;
+    fg_status s = fg_allgather_rows(c, shard_offsets, row_elems, X_local, X_full, stream);
+    if (s != FG_OK) return s;
+    return fg_spmm(local, msg, red, H, D, X_full, E, W, d_in, X_dst, out_local, arg_u, arg_e, workspace,
+                   workspace_bytes, stream);
+}
+
+extern "C" fg_status fg_dist_sddmm(const fg_graph* local, fg_comm* c, const int64_t* shard_offsets, fg_edge_op op,
+                                   int H, int D, const float* X_local, float* X_full, const float* Y_local,
+                                   float* out_local, fg_stream stream) {
+    if (!local || !c || !shard_offsets || !X_full) return fgk::set_error(FG_EINVAL, "fg_dist_sddmm: NULL argument");
+    fg_status s = fg_allgather_rows(c, shard_offsets, int64_t(H) * D, X_local, X_full, stream);
+    if (s != FG_OK) return s;
+    return fg_sddmm(local, op, H, D, X_full, Y_local, out_local, stream);
+}

@@ -28,7 +28,7 @@ EDGE = {"u_dot_v": 0, "u_add_v": 1, "u_sub_v": 2, "u_mul_v": 3}
 SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
            "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
            "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
-           "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_sddmm_emul", "fg_status_string", "fg_last_error", "fg_abi_version"]
+           "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_sddmm_emul", "fg_dist_spmm", "fg_dist_sddmm", "fg_status_string", "fg_last_error", "fg_abi_version"]
 
 
 class FGError(RuntimeError):
@@ -64,6 +64,8 @@ def lib() -> ctypes.CDLL:
     L.fg_spmm_x16.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]
     L.fg_sddmm_x16.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
     L.fg_sddmm_emul.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp]
+    L.fg_dist_spmm.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]
+    L.fg_dist_sddmm.argtypes = [vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp]
     L.fg_edge_softmax.argtypes = [vp, i32, vp, vp, vp]
     L.fg_gat_attention.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp]
     L.fg_graph_transpose.argtypes = [vp, vp, ctypes.POINTER(vp)]
@@ -77,7 +79,8 @@ def lib() -> ctypes.CDLL:
     for f in ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
               "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
               "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
-              "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_sddmm_emul"]:
+              "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_sddmm_emul", "fg_dist_spmm",
+              "fg_dist_sddmm"]:
         getattr(L, f).restype = i32
     L.fg_status_string.argtypes = [i32]
     L.fg_status_string.restype = ctypes.c_char_p
@@ -361,6 +364,38 @@ class Comm:
         _check(lib().fg_allgather_rows(self.handle, ctypes.c_void_p(off.ctypes.data), row_elems, _ptr(X_local),
                                        _ptr(X_full), _stream(stream)), "fg_allgather_rows")
         return X_full
+
+    def dist_spmm(self, g_local: "Graph", shard_offsets, msg: str, reduce: str, X_local: torch.Tensor,
+                  X_full: torch.Tensor, *, H: int = 1, E: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                  stream=None) -> torch.Tensor:
+        """fg_dist_spmm (sum / mean reducers of copy_u / u_mul_e / u_add_e): all-gather
+        X_local into X_full, then the local gSpMM on this rank's rows."""
+        import numpy as np
+        off = np.ascontiguousarray(np.asarray(shard_offsets, dtype=np.int64))
+        X_full = _dev(X_full, torch.float32, "X_full")
+        E = _dev(E, torch.float32, "E")
+        F = X_full.numel() // max(X_full.shape[0], 1)
+        if out is None:
+            out = torch.empty((g_local.n_dst, F), dtype=torch.float32, device=X_full.device)
+        _check(lib().fg_dist_spmm(g_local.handle, self.handle, ctypes.c_void_p(off.ctypes.data), MSG[msg],
+                                  REDUCE[reduce], H, F // H, _ptr(X_local), _ptr(X_full), _ptr(E), None, 0, None,
+                                  _ptr(out), None, None, None, 0, _stream(stream)), "fg_dist_spmm")
+        return out
+
+    def dist_sddmm(self, g_local: "Graph", shard_offsets, X_local: torch.Tensor, X_full: torch.Tensor,
+                   Y_local: torch.Tensor, *, H: int = 1, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """fg_dist_sddmm (u_dot_v): all-gather X_local into X_full, then the local gSDDMM."""
+        import numpy as np
+        off = np.ascontiguousarray(np.asarray(shard_offsets, dtype=np.int64))
+        X_full = _dev(X_full, torch.float32, "X_full")
+        Y_local = _dev(Y_local, torch.float32, "Y_local")
+        F = X_full.numel() // max(X_full.shape[0], 1)
+        if out is None:
+            out = torch.empty((g_local.nnz, H), dtype=torch.float32, device=X_full.device)
+        _check(lib().fg_dist_sddmm(g_local.handle, self.handle, ctypes.c_void_p(off.ctypes.data), EDGE["u_dot_v"], H,
+                                   F // H, _ptr(X_local), _ptr(X_full), _ptr(Y_local), _ptr(out), _stream(stream)),
+               "fg_dist_sddmm")
+        return out
 
     def close(self):
         if self.handle:

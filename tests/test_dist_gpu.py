@@ -135,3 +135,29 @@ def test_bench_e2e_pipeline_matches_step(cuda_ok):
     torch.cuda.synchronize()
     for o, r in zip(S.outputs(), ref):
         assert torch.equal(outs_h[id(o)], r.cpu())
+
+
+def test_dist_spmm_sddmm_single_rank(cuda_ok, graph):
+    """fg_dist_spmm / fg_dist_sddmm through a 1-rank NCCL communicator (the shard
+    is the whole graph): the all-gather fills X_full from a separate X_local and
+    the local ops equal the unsharded fg_spmm / fg_sddmm bit for bit."""
+    import paper_2008_11359_b200 as fgp
+    g = graph
+    G = fgp.Graph(dev(g.row_ptr), dev(g.col_idx))
+    c = fgp.Comm(fgp.comm_unique_id(), 1, 0)
+    off = [0, g.n_dst]
+    H, D = 8, 32
+    X = dev(gen.features((g.n_src, H * D), 17, 0))
+    E = dev(gen.features((g.nnz, H), 17, 1, gen.UNIT))
+    Xf = torch.zeros_like(X)
+    o = c.dist_spmm(G, off, "copy_u", "sum", X, Xf)
+    torch.cuda.synchronize()
+    assert torch.equal(Xf, X)
+    assert torch.equal(o, fgp.spmm(G, "copy_u", "sum", X))
+    Xf.zero_()
+    o = c.dist_spmm(G, off, "u_mul_e", "sum", X, Xf, H=H, E=E)
+    assert torch.equal(o, fgp.spmm(G, "u_mul_e", "sum", X, H=H, E=E))
+    Xf.zero_()
+    s = c.dist_sddmm(G, off, X, Xf, X, H=H)
+    assert torch.equal(s, fgp.sddmm(G, X, H=H))
+    c.close()
