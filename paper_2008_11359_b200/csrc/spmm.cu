@@ -107,11 +107,22 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
             NV = 4;   // 128 float4 columns per tile; wider rows take several tiles (grid.y)
         }
     }
-    {   // rows with degree >= FG_SPMM_HEAVY_DEG run CTA-per-row (default 4096 for every
-        // G; reddit: the former NG * 32 = 256..1024 cost copy_u-sum F=512 14.1 vs 12.5 ms,
-        // u_mul_e H=8 9.4 vs 7.8 ms, copy_u-max F=128 4.7 vs 4.35 ms; 2048 / 8192 lose 1-6 %)
+    {   // rows with degree >= the heavy threshold run CTA-per-row.  Threshold = the fair
+        // share of edges per group in flight, m / (SMs x 2048 / G), clamped to
+        // [1024, 4096] (FG_SPMM_HEAVY_DEG overrides).  Measured on reddit: a constant
+        // NG x 32 = 256..1024 cost copy_u-sum F=512 14.1 vs 12.5 ms, u_mul_e H=8 9.4 vs
+        // 7.8 ms (a group per long row keeps more gathers in flight than a CTA per
+        // row); a constant 4096 cost the short F = 32 kernels their tail (rand-100K
+        // 0.37 -> 0.52 ms: a 4,000-edge row on one 8-lane group outlasts the rest).
         const char* hv = getenv("FG_SPMM_HEAVY_DEG");
-        A.n_heavy = rows_with_degree_at_least(g, hv ? std::max<int64_t>(1, atoll(hv)) : 4096);
+        int64_t thr;
+        if (hv) {
+            thr = std::max<int64_t>(1, atoll(hv));
+        } else {
+            const int64_t groups = int64_t(fgk::num_sms()) * (2048 / G);
+            thr = std::min<int64_t>(4096, std::max<int64_t>(1024, g->nnz / std::max<int64_t>(1, groups)));
+        }
+        A.n_heavy = rows_with_degree_at_least(g, thr);
     }
     const int opset = (op == OP_UADDE || op == OP_COPYE) ? 1 : 0;
     if (Xbf16) {   // bf16 storage: copy_u / u_mul_e x {sum, max} (validated by the caller)
