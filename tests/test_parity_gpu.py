@@ -768,3 +768,84 @@ def test_cta_per_row_thresholds(skewed, skewed_eid, monkeypatch, deg):
     out = fgp.gat_attention(g.h, dev(X), dev(Y), H=H).cpu().numpy()
     rg, rgb = oracle.gat(g.row_ptr, g.col_idx, X, Y, H=H)
     check_close(out, rg, rgb, TOL, "fused GAT")
+
+
+# ------------------------------------------------------------------ randomized equivalence
+def test_random_equivalence_200_cases():
+    """200 seeded random cases -- graph size and skew, feature shape, message,
+    reducer, edge-id permutation, regime -- each GPU op against the oracle, with
+    every output pre-filled with NaN / garbage (outputs must be fully overwritten)."""
+    import paper_2008_11359_b200 as fgp
+    rng = np.random.default_rng(20081135)
+    shapes = [(1, 4), (1, 12), (1, 32), (1, 100), (1, 512), (2, 4), (4, 8), (8, 32), (2, 64), (3, 12)]
+    for case in range(200):
+        n = int(rng.integers(1, 400))
+        n_src = n if rng.random() < 0.7 else int(rng.integers(1, 500))
+        m = int(rng.integers(0, min(n * n_src, 6000) + 1))
+        deg = rng.multinomial(m, rng.dirichlet(np.full(n, float(rng.choice([0.2, 1.0, 5.0]))))) if m else np.zeros(n, int)
+        deg = np.minimum(deg, n_src)
+        rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+        ci = np.concatenate([np.sort(rng.choice(n_src, size=int(d), replace=False)) for d in deg]
+                            + [np.zeros(0, np.int64)]).astype(np.int32)
+        eid = rng.permutation(int(rp[-1])).astype(np.int32) if rng.random() < 0.3 else None
+        g = G(rp, ci, n_src=n_src, eid=eid)
+        H, D = shapes[int(rng.integers(len(shapes)))]
+        F = H * D
+        regime = gen.INT if rng.random() < 0.3 else gen.REAL
+        X = feats((n_src, F), 5000 + case, regime)
+        what = f"case {case}: n={n} n_src={n_src} m={g.nnz} H={H} D={D} eid={eid is not None}"
+        kind = case % 4
+        if kind == 0:   # copy_u / u_mul_e with a random reducer
+            msg = "copy_u" if rng.random() < 0.5 else "u_mul_e"
+            red = str(rng.choice(["sum", "max", "min", "mean"]))
+            E = gen.features((max(g.nnz, 1), H), 6000 + case, 0, gen.UNIT)[: g.nnz] if msg == "u_mul_e" else None
+            out = torch.full((n, F), float("nan"), device="cuda")
+            kw = dict(H=H, out=out)
+            if E is not None:
+                kw["E"] = dev(E) if g.nnz else torch.zeros((0, H), device="cuda")
+            if red in ("max", "min"):
+                au = torch.full((n, F), 12345, dtype=torch.int32, device="cuda")
+                fgp.spmm(g.h, msg, red, dev(X), arg_u=au, **kw)
+            else:
+                fgp.spmm(g.h, msg, red, dev(X), **kw)
+            ref, ab, rau, _ = oracle.spmm(g.row_ptr, g.col_idx, msg, red, X, H=H, E=E, eid=g.eid)
+            if red in ("max", "min"):
+                assert np.array_equal(out.cpu().numpy().astype(np.float64), ref), what
+                assert np.array_equal(au.cpu().numpy(), rau), what
+            else:
+                check_close(out.cpu().numpy(), ref, ab, TOL, what)
+        elif kind == 1:   # u_dot_v
+            if D % 4 or (H > 1 and (D // 4) & (D // 4 - 1)):
+                H, D = 1, F
+            Y = feats((n, F), 7000 + case, regime)
+            out = torch.full((max(g.nnz, 1), H), float("nan"), device="cuda")[: g.nnz]
+            fgp.sddmm(g.h, dev(X), dev(Y), H=H, out=out)
+            ref, ab = oracle.sddmm(g.row_ptr, g.col_idx, X, Y, H=H)
+            pos = np.arange(g.nnz) if g.eid is None else g.eid
+            check_close(out.cpu().numpy()[pos], ref, ab, TOL, what)
+        elif kind == 2:   # edge softmax on oracle scores
+            S = gen.features((max(g.nnz, 1), H), 8000 + case, 0, gen.REAL)[: g.nnz] * np.float32(6)
+            if g.nnz == 0:
+                continue
+            out = torch.full((g.nnz, H), float("nan"), device="cuda")
+            fgp.edge_softmax(g.h, dev(S), H=H, out=out)
+            ref = oracle.edge_softmax(g.row_ptr, S, H=H, eid=g.eid)
+            pos = np.arange(g.nnz) if g.eid is None else g.eid
+            got = out.cpu().numpy()[pos].astype(np.float64)
+            assert (np.abs(got - ref) <= TOL * ref).all(), what
+        else:   # mlp max / sum (integer regime: exact)
+            d2 = int(rng.choice([16, 32, 128, 200]))
+            X8 = feats((n_src, 8), 9000 + case, gen.INT)
+            Xd = feats((n, 8), 9100 + case, gen.INT)
+            W = gen.features((8, d2), 9200 + case, 1, gen.INT, lo=-4, hi=4)
+            red = "max" if rng.random() < 0.6 else "sum"
+            out = torch.full((n, d2), float("nan"), device="cuda")
+            if red == "max":
+                au = torch.full((n, d2), 12345, dtype=torch.int32, device="cuda")
+                fgp.spmm(g.h, "mlp", "max", dev(X8), W=dev(W), X_dst=dev(Xd), out=out, arg_u=au)
+            else:
+                fgp.spmm(g.h, "mlp", "sum", dev(X8), W=dev(W), X_dst=dev(Xd), out=out)
+            ref, _, rau, _ = oracle.spmm(g.row_ptr, g.col_idx, "mlp", red, X8, W=W, X_dst=Xd, eid=g.eid)
+            assert np.array_equal(out.cpu().numpy().astype(np.float64), ref), what
+            if red == "max":
+                assert np.array_equal(au.cpu().numpy(), rau), what
