@@ -7,7 +7,7 @@
 // The paper parallelises edges across a CUDA block and tree-reduces each dot
 // product through shared memory (Fig. 7b; up to 2x).  On
 // sm_100a the reduction is a register butterfly (__shfl_xor_sync) inside a
-// group of G lanes, and the traversal is ROW-major in work units of <= 256
+// group of G lanes, and the traversal is ROW-major in work units of <= 64
 // edges of one destination row (fg_graph unit table): the group loads Y[v]
 // into registers once per unit and then only gathers X[u] (coalesced LDG.128
 // per lane), so the kernel is bound by the gather bytes m*F*4.  Heads are
