@@ -14,8 +14,9 @@
 // rescaled when the max grows, so one pass over the row suffices.
 //
 // Mapping as in spmm.cu: a group of G lanes owns a destination row, each lane
-// NV float4 columns (head of column chunk c = c / (D/4)); the per-edge score is
-// a butterfly all-reduce over the D/4 lanes of a head.  Rows of degree >= T run
+// NV float4 columns (head of column chunk c = c / (D/4)); the per-edge scores are
+// reduced over the D/4 lanes of a head (a reduce-scatter of the U x NV partial
+// dots + one gather shuffle per score when NV = 2, else a butterfly).  Rows of degree >= T run
 // CTA-per-row: the groups take contiguous edge ranges and their (m, l, acc)
 // partials are merged in a fixed order (deterministic, no atomics).
 #include <algorithm>
@@ -42,6 +43,34 @@ struct Args {
     int H, D4, F4;
 };
 
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+
+// Recursive-halving reduce-scatter of K values over W aligned lanes (as in
+// sddmm.cu): at offset o a lane keeps the half of its values selected by
+// (gl & o) and adds the partner's copy of that half; the last levels are a plain
+// butterfly.  Afterwards lane gl holds the W-lane sum of value index
+// ((gl mod W) >> (log2 W - L)) * (K >> L) + i, L = min(log2 K, log2 W).
+template <int K, int W, int G>
+__device__ __forceinline__ void reduce_scatter(float (&v)[K], int gl, unsigned mask) {
+    if constexpr (W > 1) {
+        constexpr int o = W / 2;
+        if constexpr (K > 1) {
+            const bool up = (gl & o) != 0;
+#pragma unroll
+            for (int i = 0; i < K / 2; ++i) {
+                const float send = up ? v[i] : v[i + K / 2];
+                const float keep = up ? v[i + K / 2] : v[i];
+                v[i] = keep + __shfl_xor_sync(mask, send, o, G);
+            }
+            float (&h)[K / 2] = *reinterpret_cast<float(*)[K / 2]>(&v[0]);
+            reduce_scatter<K / 2, W / 2, G>(h, gl, mask);
+        } else {
+#pragma unroll
+            for (int oo = o; oo >= 1; oo >>= 1) v[0] += __shfl_xor_sync(mask, v[0], oo, G);
+        }
+    }
+}
+
 __device__ __forceinline__ float dot4(const float4& a, const float4& b) {
     return fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, a.w * b.w)));
 }
@@ -58,7 +87,10 @@ struct State {
     float4 acc[NV];
 };
 
-template <int G, int NV, int U, bool PIPE>
+// DWT > 0: the head width D/4 is DWT lanes (compile time): the U x NV per-head
+// scores are reduced with one reduce-scatter over the DWT lanes and gathered back
+// with U*NV shuffles (fewer shuffles and adds than a butterfly per score)
+template <int G, int NV, int U, bool PIPE, int DWT>
 __device__ __forceinline__ void attend_range(const Args& A, const float4* __restrict__ X, const float4 (&y)[NV],
                                              int64_t s, int64_t e, int gl, unsigned mask, State<NV>& st,
                                              float* __restrict__ scores, int* __restrict__ sidx) {
@@ -103,14 +135,29 @@ __device__ __forceinline__ void attend_range(const Args& A, const float4* __rest
             for (int uu = 0; uu < U; ++uu)
 #pragma unroll
                 for (int j = 0; j < NV; ++j) sc[uu][j] = dot4(x[uu][j], y[j]);
+            if constexpr (DWT > 0) {
+                constexpr int K = U * NV;
+                static_assert(K <= DWT, "one reduced score per lane");
+                float pv[K];
 #pragma unroll
-            for (int o = 16; o >= 1; o >>= 1)
-                if (o < D4 && o < G) {
+                for (int uu = 0; uu < U; ++uu)
 #pragma unroll
-                    for (int uu = 0; uu < U; ++uu)
+                    for (int j = 0; j < NV; ++j) pv[uu * NV + j] = sc[uu][j];
+                reduce_scatter<K, DWT, G>(pv, gl, mask);
+                constexpr int SH = ilog2(DWT) - ilog2(K);   // lane of value id: base | (id << SH)
+                const int base = gl & ~(DWT - 1);
 #pragma unroll
-                        for (int j = 0; j < NV; ++j) sc[uu][j] += __shfl_xor_sync(mask, sc[uu][j], o, G);
-                }
+                for (int id = 0; id < K; ++id) sc[id / NV][id % NV] = __shfl_sync(mask, pv[0], base | (id << SH), G);
+            } else {
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1)
+                    if (o < D4 && o < G) {
+#pragma unroll
+                        for (int uu = 0; uu < U; ++uu)
+#pragma unroll
+                            for (int j = 0; j < NV; ++j) sc[uu][j] += __shfl_xor_sync(mask, sc[uu][j], o, G);
+                    }
+            }
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
                 const int t = t0 + uu;
@@ -145,7 +192,7 @@ __device__ __forceinline__ void attend_range(const Args& A, const float4* __rest
     }
 }
 
-template <int G, int NV, int U, int MINB, bool PIPE>
+template <int G, int NV, int U, int MINB, bool PIPE, int DWT>
 __global__ void __launch_bounds__(THREADS, MINB) gat_fused_kernel(const Args A, const float4* __restrict__ X,
                                                             const float4* __restrict__ Y, float4* __restrict__ out,
                                                             float* __restrict__ scores) {
@@ -184,7 +231,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gat_fused_kernel(const Args A, 
     if (heavy) {
         const int64_t len = (e - s + NG - 1) / NG;
         const int64_t gs = min(e, s + gi * len), ge = min(e, gs + len);
-        attend_range<G, NV, U, PIPE>(A, X, y, gs, ge, gl, mask, st, scores, s_idx[gi]);
+        attend_range<G, NV, U, PIPE, DWT>(A, X, y, gs, ge, gl, mask, st, scores, s_idx[gi]);
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
             const int c = gl + G * j;
@@ -211,7 +258,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gat_fused_kernel(const Args A, 
         }
         return;
     }
-    attend_range<G, NV, U, PIPE>(A, X, y, s, e, gl, mask, st, scores, s_idx[gi]);
+    attend_range<G, NV, U, PIPE, DWT>(A, X, y, s, e, gl, mask, st, scores, s_idx[gi]);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const int c = gl + G * j;
@@ -225,7 +272,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gat_fused_kernel(const Args A, 
     }
 }
 
-template <int G, int NV, int U = (NV >= 3 ? 2 : 4), int MINB = 2, bool PIPE = true>
+template <int G, int NV, int U = (NV >= 3 ? 2 : 4), int MINB = 2, bool PIPE = true, int DWT = 0>
 fg_status launch_t(Args A, const fg_graph* g, const float* X, const float* Y, float* out, float* scores,
                    cudaStream_t st) {
     constexpr int NG = THREADS / G;
@@ -236,7 +283,7 @@ fg_status launch_t(Args A, const fg_graph* g, const float* X, const float* Y, fl
     }
     const int64_t blocks = A.n_heavy + (A.n_rows - A.n_heavy + NG - 1) / NG;
     if (blocks == 0) return FG_OK;
-    gat_fused_kernel<G, NV, U, MINB, PIPE><<<unsigned(blocks), THREADS, 0, st>>>(A, reinterpret_cast<const float4*>(X),
+    gat_fused_kernel<G, NV, U, MINB, PIPE, DWT><<<unsigned(blocks), THREADS, 0, st>>>(A, reinterpret_cast<const float4*>(X),
                                                                   reinterpret_cast<const float4*>(Y),
                                                                   reinterpret_cast<float4*>(out), scores);
     return fgk::check_launch("gat_fused_kernel");
@@ -291,7 +338,17 @@ extern "C" fg_status fg_gat_attention(const fg_graph* g, int H, int D, const flo
             // no software pipeline, 4 CTAs per SM (<= 64 registers).  Measured on
             // reddit (tools/gat_exp.py): 14.9 ms vs 18.4 ms for 4 edges + pipeline at
             // 2 CTAs/SM (128 registers); occupancy beats per-warp memory parallelism
-            if (NV == 2) return launch_t<32, 2, 2, 4, false>(A, g, X, Y, out, scores, st);
+            if (NV == 2) {
+                // per-head scores by one reduce-scatter over the head's D/4 lanes +
+                // a gather (reddit H=8 D=32: 14.0 -> 11.8 ms vs a butterfly per score)
+                switch (A.D4) {
+                    case 4: return launch_t<32, 2, 2, 4, false, 4>(A, g, X, Y, out, scores, st);
+                    case 8: return launch_t<32, 2, 2, 4, false, 8>(A, g, X, Y, out, scores, st);
+                    case 16: return launch_t<32, 2, 2, 4, false, 16>(A, g, X, Y, out, scores, st);
+                    case 32: return launch_t<32, 2, 2, 4, false, 32>(A, g, X, Y, out, scores, st);
+                    default: return launch_t<32, 2, 2, 4, false>(A, g, X, Y, out, scores, st);
+                }
+            }
             if (NV == 3) return launch_t<32, 3>(A, g, X, Y, out, scores, st);
             return launch_t<32, 4>(A, g, X, Y, out, scores, st);
     }
