@@ -144,7 +144,7 @@ def gpu_id_for_smi(local_rank: int) -> str:
     return str(local_rank)
 
 
-def mlp_tmem_floor(S, flush, sync_all, reps: int = 5) -> float:
+def mlp_tmem_floor(S, flush, reps: int = 5) -> float:
     """The MLP kernel's own ceiling, measured live: the same launch with the
     gathers and the MMAs disabled (FG_MLP_DBG=6: the epilogue still reads every
     accumulator element out of TMEM -- m x d2 x 4 bytes -- but the results are
@@ -162,7 +162,7 @@ def mlp_tmem_floor(S, flush, sync_all, reps: int = 5) -> float:
                 S.fgp.spmm(S.G, "mlp", "max", S.X["X8"], W=S.W, X_dst=S.ydst("X8"), out=S.omlp, arg_u=S.aumlp,
                            arg_e=S.aemlp, stream=st)
                 b.record(st)
-            sync_all()
+            torch.cuda.synchronize()   # rank 0 only (no barrier: the other ranks are done)
             if k:
                 ts.append(a.elapsed_time(b))
     finally:
@@ -521,7 +521,7 @@ def main():
         e2e = run_e2e(S, host, args, world, sync_all, flush)
 
     l2peak = l2_gather_ceiling(torch, flush.buf) if rank == 0 else None
-    mlp_floor_ms = mlp_tmem_floor(S, flush, sync_all) if rank == 0 else None
+    mlp_floor_ms = mlp_tmem_floor(S, flush) if rank == 0 else None
 
     total_bytes = sum(op_bytes(g.n_dst, g.nnz).values())
     local_bytes = op_bytes(S.nl, S.m)
