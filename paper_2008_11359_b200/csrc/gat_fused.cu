@@ -333,7 +333,15 @@ extern "C" fg_status fg_gat_attention(const fg_graph* g, int H, int D, const flo
         case 8: return launch_t<8, 1>(A, g, X, Y, out, scores, st);
         case 16: return launch_t<16, 1>(A, g, X, Y, out, scores, st);
         default:
-            if (NV == 1) return launch_t<32, 1>(A, g, X, Y, out, scores, st);
+            if (NV == 1) {   // reduce-scatter scores too (K = 4 edges x 1 chunk <= D/4 lanes)
+                switch (A.D4) {
+                    case 4: return launch_t<32, 1, 4, 2, true, 4>(A, g, X, Y, out, scores, st);
+                    case 8: return launch_t<32, 1, 4, 2, true, 8>(A, g, X, Y, out, scores, st);
+                    case 16: return launch_t<32, 1, 4, 2, true, 16>(A, g, X, Y, out, scores, st);
+                    case 32: return launch_t<32, 1, 4, 2, true, 32>(A, g, X, Y, out, scores, st);
+                    default: return launch_t<32, 1>(A, g, X, Y, out, scores, st);
+                }
+            }
             // H*D in (128, 256] (reddit GAT H = 8, D = 32): 2 edges in flight per lane,
             // no software pipeline, 4 CTAs per SM (<= 64 registers).  Measured on
             // reddit (tools/gat_exp.py): 14.9 ms vs 18.4 ms for 4 edges + pipeline at
