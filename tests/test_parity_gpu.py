@@ -531,7 +531,7 @@ def test_sddmm_source_segmented(skewed, skewed_eid, H, D, use_eid, monkeypatch):
 
 # ------------------------------------------------------------------ fused GAT (f2)
 @pytest.mark.parametrize("H,D", [(8, 32), (4, 16), (2, 4), (1, 128), (8, 64), (1, 16), (16, 16), (4, 64), (2, 128),
-                                 (6, 32), (4, 32), (8, 16), (2, 64), (3, 32)])
+                                 (6, 32), (4, 32), (8, 16), (2, 64), (3, 32), (16, 32), (4, 128)])
 @pytest.mark.parametrize("use_eid", [False, True])
 def test_gat_fused(skewed, skewed_eid, H, D, use_eid):
     import paper_2008_11359_b200 as fgp
