@@ -358,10 +358,12 @@ extern "C" fg_status fg_gat_attention(const fg_graph* g, int H, int D, const flo
                 }
             }
             if (NV == 3) return launch_t<32, 3>(A, g, X, Y, out, scores, st);
-            switch (A.D4) {   // reduce-scatter scores (K = 2 edges x 4 chunks <= D/4 lanes)
-                case 8: return launch_t<32, 4, 2, 2, true, 8>(A, g, X, Y, out, scores, st);
-                case 16: return launch_t<32, 4, 2, 2, true, 16>(A, g, X, Y, out, scores, st);
-                case 32: return launch_t<32, 4, 2, 2, true, 32>(A, g, X, Y, out, scores, st);
+            // reduce-scatter scores (K = 2 edges x 4 chunks <= D/4 lanes), no software
+            // pipeline (reddit H=8 D=64: 32.2 vs 34.3 ms with it; 3 CTAs/SM or 1 edge: 38+)
+            switch (A.D4) {
+                case 8: return launch_t<32, 4, 2, 2, false, 8>(A, g, X, Y, out, scores, st);
+                case 16: return launch_t<32, 4, 2, 2, false, 16>(A, g, X, Y, out, scores, st);
+                case 32: return launch_t<32, 4, 2, 2, false, 32>(A, g, X, Y, out, scores, st);
                 default: return launch_t<32, 4>(A, g, X, Y, out, scores, st);
             }
     }
