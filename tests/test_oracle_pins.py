@@ -384,6 +384,36 @@ def test_mlp_sum_brute_force():
         np.testing.assert_allclose(ref[v], acc, rtol=1e-12, atol=1e-13)
 
 
+@pytest.mark.parametrize("regime", [gen.INT, gen.UNIT])
+def test_mlp_sum_closed_form_nonnegative(regime):
+    """With X, X_dst >= 0 and W >= 0 every pre-activation is >= 0, so ReLU is the
+    identity and Fig. 3b's sum aggregation is linear:
+        out[v] = sum_{u in N(v)} (x_u + x_v) W = (A . (X W))[v] + deg(v) (X_dst W)[v].
+    Dense A times a BLAS product -- no per-edge loop, no ReLU -- so a dropped
+    x_v term, a wrong sign or a transposed W fails it.  Integer regime: exact."""
+    g = small_graph(n=120, m=1500, seed=13)
+    d1, d2 = 8, 24
+    if regime == gen.INT:
+        X = gen.features((g.n_src, d1), 44, 0, gen.INT, lo=0, hi=8)
+        Xd = gen.features((g.n_dst, d1), 44, 2, gen.INT, lo=0, hi=8)
+        W = gen.features((d1, d2), 44, 1, gen.INT, lo=0, hi=4)
+    else:
+        X = gen.features((g.n_src, d1), 44, 0, gen.UNIT)
+        Xd = gen.features((g.n_dst, d1), 44, 2, gen.UNIT)
+        W = gen.features((d1, d2), 44, 1, gen.UNIT)
+    ref, ab, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "mlp", "sum", X, W=W, X_dst=Xd)
+    A = dense_adjacency(g.row_ptr, g.col_idx, g.n_src)
+    XW = X.astype(np.float64) @ W.astype(np.float64)
+    XdW = Xd.astype(np.float64) @ W.astype(np.float64)
+    closed = A @ XW + g.degrees()[:, None] * XdW
+    if regime == gen.INT:
+        assert np.array_equal(ref, closed)
+    else:
+        np.testing.assert_allclose(ref, closed, rtol=1e-12, atol=0)
+    # every term is non-negative, so the tolerance scale equals the value itself
+    np.testing.assert_allclose(ab, closed, rtol=1e-12, atol=0)
+
+
 def test_mlp_x_dst_separate():
     """X_dst enters only through x_v: mlp with W = I, X_dst = 0 is ReLU(copy_u max)."""
     g = small_graph(n=60, m=500, seed=8)
