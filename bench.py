@@ -144,32 +144,6 @@ def gpu_id_for_smi(local_rank: int) -> str:
     return str(local_rank)
 
 
-def mlp_tmem_floor(S, flush, reps: int = 5) -> float:
-    """The MLP kernel's own ceiling, measured live: the same launch with the
-    gathers and the MMAs disabled (FG_MLP_DBG=6: the epilogue still reads every
-    accumulator element out of TMEM -- m x d2 x 4 bytes -- but the results are
-    garbage), i.e. the TMEM-read-bound skeleton."""
-    import torch
-    st = S.stream
-    os.environ["FG_MLP_DBG"] = "6"
-    try:
-        ts = []
-        for k in range(reps + 1):
-            with torch.cuda.stream(st):
-                flush.fill_(float(k))
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(st)
-                S.fgp.spmm(S.G, "mlp", "max", S.X["X8"], W=S.W, X_dst=S.ydst("X8"), out=S.omlp, arg_u=S.aumlp,
-                           arg_e=S.aemlp, stream=st)
-                b.record(st)
-            torch.cuda.synchronize()   # rank 0 only (no barrier: the other ranks are done)
-            if k:
-                ts.append(a.elapsed_time(b))
-    finally:
-        os.environ.pop("FG_MLP_DBG", None)
-    return float(np.mean(ts))
-
-
 def l2_gather_ceiling(torch, buf) -> dict | None:
     """The L2 gather ceiling of this GPU, measured live (libfgprobe.so,
     paper_2008_11359_b200/probe/l2_probe.cu): random whole-row reads of an
@@ -225,6 +199,7 @@ class Step:
         self.rp_d = torch.from_numpy(rp).to(dev)
         self.ci_d = torch.from_numpy(ci).to(dev)
         self.G = fgp.Graph(self.rp_d, self.ci_d, n_src=g.n_src, validate=True)
+        self.prepare(self.G, g.nnz)
         self.m = int(rp[-1])
         self.lo = lo
         # full-size source feature buffers (the all-gather target when sharded)
@@ -254,8 +229,19 @@ class Step:
         offs = np.array([0, split, len(rp) - 1], np.int64)
         for r in range(2):
             h = make_shard_fn(rp, ci, r, 2, offsets=offs)
-            self.halves.append((fgp.Graph(torch.from_numpy(h.row_ptr).to(dev), torch.from_numpy(h.col_idx).to(dev),
-                                          n_src=g.n_src), h.lo, h.hi, h.edge_lo, h.edge_lo + h.nnz))
+            Gh = fgp.Graph(torch.from_numpy(h.row_ptr).to(dev), torch.from_numpy(h.col_idx).to(dev), n_src=g.n_src)
+            self.prepare(Gh, g.nnz)
+            self.halves.append((Gh, h.lo, h.hi, h.edge_lo, h.edge_lo + h.nnz))
+
+    @staticmethod
+    def prepare(G, nnz_total):
+        """Per-topology setup outside the timed region: the source-segment tables of
+        the gathered widths (fp32 F = 512 / 256 and their bf16 storage), and the
+        whole graph's edge count for the CTA-per-row threshold (so shards and row
+        halves split rows exactly as the unsharded op)."""
+        G.tune("balance_nnz", nnz_total)
+        for row_bytes in (F_DOT * 4, H_GAT * D_GAT * 4, F_DOT * 2, H_GAT * D_GAT * 2):
+            G.prepare(row_bytes)
 
     def ydst(self, k):
         return self.X[k][self.lo:self.lo + self.nl]
@@ -311,7 +297,7 @@ class Step:
                  arg_e=self.aemlp, stream=st)
         rec(8)
 
-    LAUNCHES_PER_STEP = 9   # libfg kernels per step: one per fg_* call, plus mlp's tf32 pre-split and q_v = x_v W
+    LAUNCHES_PER_STEP = 7   # libfg kernels per step: one per fg_* call
 
     def enqueue_pipelined(self, ins_h, w_h, outs_h, h2d, d2h):
         """The same step for the end-to-end leg, with the host copies overlapped:
@@ -432,12 +418,49 @@ def calibrate_sample(g, host, target_s: float):
         budget = min(g.nnz, int(budget * min(8.0, max(1.5, 0.9 * target_s / max(dt, 1e-3)))))
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_c2_single_thread() -> dict:
+    """The analogue of Table tab:cpu-kernel's single-thread protocol:
+    the fp64 oracle's copy_u-sum at F = 32 on a seeded row sample of the
+    proteins-shaped graph, ONE thread (a fresh process with OMP_NUM_THREADS=1).
+    Context only: the oracle is a correctness reference, not a tuned kernel."""
+    code = ("import sys, time, json; sys.path.insert(0, %r); import numpy as np, gen, oracle, bench;"
+            "g = gen.make_graph('proteins'); rows = bench.sample_rows(g, 2_000_000);"
+            "rows = np.sort(rows); X = gen.features((g.n_src, 32), gen.feature_seed('proteins'), 0);"
+            "deg = g.row_ptr[rows + 1] - g.row_ptr[rows]; rp = np.zeros(rows.size + 1, np.int64);"
+            "np.cumsum(deg, out=rp[1:]); ci = g.col_idx[oracle.edge_positions(g.row_ptr, rows)];"
+            "oracle.spmm(rp[:2], ci[:rp[1]], 'copy_u', 'sum', X);"
+            "t = time.perf_counter(); oracle.spmm(rp, ci, 'copy_u', 'sum', X); dt = time.perf_counter() - t;"
+            "print(json.dumps({'rows': int(rows.size), 'edges': int(rp[-1]), 'seconds': dt}))") % ROOT
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)[:200]}
+    full_s = d["seconds"] * 79122504 / max(d["edges"], 1)
+    return {"op": "copy_u-sum F=32 (proteins-shaped)", "threads": 1, "sample_rows": d["rows"],
+            "sample_edges": d["edges"], "sample_s": round(d["seconds"], 3),
+            "extrapolated_full_graph_ms": round(full_s * 1e3, 1)}
+
+
 def cpu_baseline(g, host, target_s: float = 12.0) -> dict:
     rows, dt, b, me = calibrate_sample(g, host, target_s)
     return {"value": b / dt / 1e9, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"all 7 ops of the step on {rows.size} seeded-random destination rows "
                       f"({me} in-edges, {me / g.nnz:.2%} of the graph), fp64 C oracle, OpenMP over rows; "
-                      f"{dt:.1f} s", "seconds": dt}
+                      f"{dt:.1f} s", "seconds": dt,
+            "single_thread_c2": oracle_c2_single_thread()}
 
 
 # ----------------------------------------------------------------- main
@@ -450,11 +473,22 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--uniform-sources", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU harness: start the ranks (gloo), report them, skip all GPU work")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` without a launcher: re-exec under torch.distributed.run,
+        # one rank per GPU (the driver's own launch form), NCCL init logged
+        return self_launch(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
+    if args.dry_run:
+        return dry_run(args, world, rank)
     if args.impl == "reference":
         return run_reference(args, world, rank)
 
@@ -512,8 +546,15 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    # f2 (next row): the fused GAT layer on the same inputs, timed separately (not part of the step)
-    extras = run_extras(S, args, sync_all, flush)
+    # the paper's protocol: the same step with L2 left warm between runs
+    warm_ms = timed_steps(S, args.steps, None, torch)
+    if world > 1:
+        t = torch.tensor([warm_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        warm_ms = float(t.item())
+
+    # next rows and the other BASELINE configs, timed beside the step (not part of it)
+    extras = None if args.no_extras else run_extras(S, args, sync_all, flush, world)
 
     # end-to-end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -521,8 +562,6 @@ def main():
         e2e = run_e2e(S, host, args, world, sync_all, flush)
 
     l2peak = l2_gather_ceiling(torch, flush.buf) if rank == 0 else None
-    mlp_floor_ms = mlp_tmem_floor(S, flush) if rank == 0 else None
-
     total_bytes = sum(op_bytes(g.n_dst, g.nnz).values())
     local_bytes = op_bytes(S.nl, S.m)
     ob_full = op_bytes(g.n_dst, g.nnz)
@@ -534,29 +573,15 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(g, host)
-    # dominant kernel = the HBM-bound op with the largest share of the step
-    dom = max((k for k in op_ms if k != "spmm_mlp_max_d8_d128_args"), key=lambda k: op_ms[k])
-    dom_ms = op_ms[dom]
-    achieved = local_bytes[dom] / (dom_ms * 1e-3) / 1e9
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = l2_bytes = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        try:
-            rec = json.load(open(tp)).get(dom, {})
-            traffic, l2_bytes = rec.get("dram_bytes_per_launch"), rec.get("l2_bytes_per_launch")
-        except Exception:
-            traffic = l2_bytes = None
-    l2 = None
-    if l2peak and l2_bytes and world == 1:
-        ach = l2_bytes / (dom_ms * 1e-3) / 1e9
-        l2 = {"achieved": round(ach, 1), "peak": l2peak["gather_best"], "unit": "GB/s",
-              "frac": round(ach / l2peak["gather_best"], 4), "probe": l2peak,
-              "note": "achieved = ncu lts__t_sectors x 32 B of one launch (profiles/ncu_traffic.json) / "
-                      "this run's event time; peak = the L2 gather ceiling measured live in this run "
-                      "(libfgprobe: random whole-row reads of an L2-resident X, no arithmetic)"}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    sm_mhz = (clk or {}).get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
+    # dominant kernel = the HBM/L2-bound op with the largest share of the step
+    dom = max((k for k in op_ms if k != "spmm_mlp_max_d8_d128_args"), key=lambda k: op_ms[k])
+    roof = roofline(dom, op_ms[dom], local_bytes[dom], op_ms, hbm_peak, l2peak, world,
+                    "uniform" if args.uniform_sources else "default")
+    mlp_ms = op_ms["spmm_mlp_max_d8_d128_args"]
     line = {
         "metric": metric_name(),
         "value": total_bytes / (ms * 1e-3) / 1e9,
@@ -580,31 +605,22 @@ def main():
                             "ops on earlier tensors; allgather_ms = the exposed wait for X512)")
             if world > 1 else "single GPU",
             "l2": "flushed before every timed step, outside the events: 256 MB write (2x the L2) then a "
-                  "read of it, so the flush's dirty lines are written back before the step starts",
+                  "read of it, so the flush's dirty lines are written back before the step starts "
+                  "(warm_l2_ms_per_step: the paper's warm protocol, P:607)",
             "bytes_per_step": total_bytes,
+            "value_bytes": "gather model (SURVEY 8(d)): every per-edge source-row read counted at full width; "
+                           "L2 serves most of them, so value is an effective rate, not a physical HBM rate "
+                           "(roofline.dram_gbs is the physical one)",
         },
+        "warm_l2_ms_per_step": round(warm_ms, 4),
         "ops_ms": {k: round(v, 4) for k, v in op_ms.items()},
         "ops_gbs": {k: round(ob_full[k] / world / (op_ms[k] * 1e-3) / 1e9, 1) for k in OPS} if world == 1 else
         {k: round(local_bytes[k] / (op_ms[k] * 1e-3) / 1e9, 1) for k in OPS},
         "allgather_ms": round(ag_ms, 4) if world > 1 else 0.0,
-        "mlp_tflops": round(mlp_flops(S.m) / (op_ms["spmm_mlp_max_d8_d128_args"] * 1e-3) / 1e12, 2),
-        "mlp_roofline": ({"kernel": "spmm_mlp_max_d8_d128_args", "bound": "tmem-read", "unit": "GB/s",
-                          "achieved": round(4 * S.m * D2 / (op_ms["spmm_mlp_max_d8_d128_args"] * 1e-3) / 1e9, 1),
-                          "peak": round(4 * S.m * D2 / (mlp_floor_ms * 1e-3) / 1e9, 1),
-                          "frac": round(mlp_floor_ms / op_ms["spmm_mlp_max_d8_d128_args"], 4),
-                          "note": "bytes = every fp32 accumulator element read out of TMEM (m x d2 x 4); peak = "
-                                  "those bytes / the same launch with gathers and MMAs disabled "
-                                  "(FG_MLP_DBG=6), measured live in this run"}
-                         if mlp_floor_ms else None),
-        "roofline": {"kernel": dom, "share": round(dom_ms / sum(op_ms.values()), 4), "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
-                     "bytes_model": "gather model (SURVEY 8(d)): every per-edge source-row read counted at "
-                                    "full width; L2 serves part of them, so achieved/peak can exceed 1; "
-                                    "'traffic' is the ncu DRAM bytes of one launch and dram_frac its "
-                                    "rate against the same peak",
-                     "dram_frac": (round(traffic / (dom_ms * 1e-3) / 1e9 / peak, 4) if traffic else None),
-                     "l2": l2},
+        "comm": ({"backend": "nccl", "nranks": S.comm.nranks_nccl()} if world > 1 else None),
+        "mlp_tflops": round(mlp_flops(S.m) / (mlp_ms * 1e-3) / 1e12, 2),
+        "mlp_roofline": mlp_roofline(S.m, mlp_ms, sm_mhz),
+        "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": Step.LAUNCHES_PER_STEP * args.steps,
@@ -617,15 +633,151 @@ def main():
         dist.destroy_process_group()
 
 
-def run_extras(S, args, sync_all, flush):
-    """Next-row kernels measured beside the step (not part of it): f2 fused GAT
-    (u_dot_v -> softmax -> u_mul_e-sum in one pass) vs the 3-kernel chain, and
-    f4 bf16 feature storage (the same fp32 ops with the gathered X stored as
-    bf16: half the gather bytes) for the step's copy_u-sum / u_dot_v / GAT ops."""
+def self_launch(n: int) -> int:
+    """Re-exec this command under torch.distributed.run with n ranks on
+    127.0.0.1 (one process per GPU); NCCL's communicator init is logged
+    (NCCL_DEBUG=INFO, subsystem INIT) unless the caller set NCCL_DEBUG."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print("bench.py: self-launch: " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args, world: int, rank: int) -> int:
+    """Launch check without a GPU: the ranks meet over gloo, agree on the world
+    size and the row shards of a small graph, and rank 0 prints the JSON line."""
+    import torch.distributed as dist
+    import gen
+    from paper_2008_11359_b200.shard import make_shard
+    if world > 1:
+        dist.init_process_group("gloo")
+    g = gen.random_graph(2000, 40000, 5)
+    sh = make_shard(g.row_ptr, g.col_idx, rank, world)
+    print(f"bench.py dry-run: rank {rank}/{world} rows [{sh.lo}, {sh.hi}) nnz {sh.nnz}", file=sys.stderr, flush=True)
+    ranks = [None] * world
+    if world > 1:
+        dist.all_gather_object(ranks, (rank, sh.lo, sh.hi, sh.nnz))
+    else:
+        ranks = [(rank, sh.lo, sh.hi, sh.nnz)]
+    if rank == 0:
+        print(json.dumps({"metric": metric_name(), "dry_run": True, "n_gpus": world,
+                          "ranks": [list(r) for r in ranks], "nnz_total": int(sum(r[3] for r in ranks))}),
+              flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def timed_steps(S, k_steps: int, flush, torch) -> float:
+    """Mean device ms of k_steps whole steps on S.stream (after one untimed step);
+    flush=None keeps L2 warm between steps (the paper's protocol)."""
+    st = S.stream
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k_steps + 1)]
+    with torch.cuda.stream(st):
+        for k in range(k_steps + 1):
+            if flush is not None:
+                flush.fill_(float(k))
+            evs[k][0].record(st)
+            S.enqueue()
+            evs[k][1].record(st)
+    torch.cuda.synchronize()
+    return float(np.mean([evs[k][0].elapsed_time(evs[k][1]) for k in range(1, k_steps + 1)]))
+
+
+def ncu_record(op: str, variant: str):
+    """(record, fresh, stamped_hash) of `op` from profiles/ncu_traffic.json: the
+    per-launch ncu figures of the last --set full capture, usable only if that
+    capture was taken on the libfg.so this tree builds (same source hash)."""
+    from paper_2008_11359_b200.build import source_hash
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        doc = json.load(open(tp))
+    except Exception:
+        return None, False, None
+    h = doc.get("build_hash")
+    return doc.get(variant, {}).get(op), h == source_hash(), h
+
+
+def roofline(dom, dom_ms, dom_bytes, op_ms, hbm_peak, l2peak, world, variant) -> dict:
+    """The dominant kernel's roofline line (base contract fields + the physical
+    figures).  achieved = gather-model bytes per launch / live event time (the
+    contract's algorithmic bytes: per edge 4F bytes of X[u] + index and row
+    terms) against the measured HBM copy peak -- an EFFECTIVE rate that L2
+    reuse lets exceed 1; dram_* and l2_* are the physical rates: the ncu bytes
+    of one launch of this build (profiles/ncu_traffic.json) over the live time."""
+    from paper_2008_11359_b200.build import source_hash
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    rec, fresh, stamped = ncu_record(dom, variant)
+    r = {"kernel": dom, "share": round(dom_ms / sum(op_ms.values()), 4), "bound": "hbm",
+         "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+         "achieved_model": "gather model (effective; not a physical HBM rate -- see dram_gbs / l2_gbs)",
+         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+         "traffic": None, "dram_gbs": None, "dram_frac": None, "l2_gbs": None, "l2_frac_of_ncu_peak": None,
+         "l2_frac_of_gather_probe": None,
+         "ncu": {"build_hash": source_hash(), "capture_hash": stamped, "fresh": bool(fresh and rec)}}
+    if rec and fresh and world == 1:
+        t = dom_ms * 1e-3
+        traffic = rec.get("dram_bytes_per_launch")
+        r["traffic"] = traffic
+        if traffic:
+            r["dram_gbs"] = round(traffic / t / 1e9, 1)
+            r["dram_frac"] = round(traffic / t / 1e9 / hbm_peak, 4)
+        l2b = rec.get("l2_bytes_per_launch")
+        if l2b:
+            r["l2_gbs"] = round(l2b / t / 1e9, 1)
+            if l2peak:
+                r["l2_frac_of_gather_probe"] = round(l2b / t / 1e9 / l2peak["gather_best"], 4)
+        pct, nt = rec.get("lts_throughput_pct"), rec.get("ncu_time_s")
+        if pct and nt:   # ncu's L2 throughput share, rescaled from the capture's time to this run's
+            r["l2_frac_of_ncu_peak"] = round(pct / 100.0 * nt / t, 4)
+        r["ncu"]["capture"] = rec.get("capture")
+    r["l2_probe"] = l2peak
+    return r
+
+
+def sm_max_mhz() -> float:
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0))
+    except Exception:
+        return 1965.0
+
+
+def mlp_roofline(m: int, ms: float, sm_mhz: float, d2: int = D2, sms: int = 148) -> dict:
+    """The tcgen05 MLP kernel against its bound, reading every fp32 accumulator
+    element out of TMEM (m x d2 x 4 bytes) at the guide's LDTM throughput of
+    64 B/clk/SM (B300_MICROARCH.md "TMEM"; same tcgen05.ld on sm_100a) x SMs x
+    the live SM clock; plus the tensor pipe's share (3 tf32 MMAs per product)."""
+    tmem_bytes = 4 * m * d2
+    peak = 64.0 * sms * sm_mhz * 1e6 / 1e9
+    ach = tmem_bytes / (ms * 1e-3) / 1e9
+    return {"bound": "tmem-read", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "GB/s",
+            "frac": round(ach / peak, 4),
+            "peak_source": f"64 B/clk/SM (guide LDTM throughput) x {sms} SMs x {sm_mhz:.0f} MHz (live median)",
+            "algorithmic_tflops": round(2 * m * 8 * d2 / (ms * 1e-3) / 1e12, 2)}
+
+
+def run_extras(S, args, sync_all, flush, world):
+    """Measured beside the step (not part of it):
+      f2  fused GAT (u_dot_v -> softmax -> u_mul_e-sum in one pass);
+      f4  bf16 feature storage, u_dot_v-then-e_mul;
+      a3  MLP ablations on the same reddit inputs (FFMA, bf16 2-split vs 3xTF32);
+    and, at N = 1, the other BASELINE.json configs:
+      C2  proteins-shaped GCN aggregation, copy_u-sum F = 32 / 128 / 512;
+      C4  rand-100K MLP aggregation, mlp-max d2 = 128 + args (and its ablations);
+      C6  the DRAM-bound control: reddit-shaped with uniform sources, F = 512."""
     import torch
     st = S.stream
     fgp = S.fgp
-    k_steps = max(1, min(args.steps, 5))
+    k_steps = max(3, min(args.steps, 10))
 
     def timed(fn):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -660,12 +812,82 @@ def run_extras(S, args, sync_all, flush):
                                                           out=o256, stream=st)),
     }
     res["bf16_storage_ms"] = {k: round(v, 4) for k, v in bf.items()}
+    del X16
     # f4: u_dot_v then e_mul (scores scaled by the step's alpha, fused into the write-back)
     s8w = torch.empty_like(S.s8)
     res["sddmm_u_dot_v_e_mul_H8_D32_ms"] = round(timed(
         lambda: fgp.sddmm(S.G, S.X["X256"], S.ydst("X256"), H=H_GAT, E=S.s8, out=s8w, stream=st)), 4)
     res["bf16_storage_note"] = ("row f4: same fp32 arithmetic and outputs, X (and Y) stored as bf16; "
                                 "parity vs the oracle on the decoded inputs in tests/test_parity_gpu.py")
+
+    def mlp_impls(G, X8, W, Xd, o, au, ae):
+        r = {}
+        for name, impl in (("tcgen05_3xtf32", 0), ("tcgen05_bf16_2split", 2), ("ffma_simt", 1)):
+            G.tune("mlp_impl", impl)
+            r[name] = round(timed(lambda: fgp.spmm(G, "mlp", "max", X8, W=W, X_dst=Xd, out=o, arg_u=au, arg_e=ae,
+                                                   stream=st)), 4)
+        G.tune("mlp_impl", 0)
+        return r
+
+    res["mlp_ablation_reddit_ms"] = mlp_impls(S.G, S.X["X8"], S.W, S.ydst("X8"), S.omlp, S.aumlp, S.aemlp)
+    sync_all()
+    if world != 1:
+        return res
+    import gen
+    dev = torch.device("cuda")
+
+    def graph_on_gpu(name, uniform=False):
+        gg = gen.make_graph(name, uniform_sources=uniform)
+        G = fgp.Graph(torch.from_numpy(gg.row_ptr).to(dev), torch.from_numpy(gg.col_idx).to(dev), n_src=gg.n_src)
+        return gg, G
+
+    # C2: proteins-shaped GCN aggregation
+    gp, Gp = graph_on_gpu("proteins")
+    c2 = {}
+    for Fp in (32, 128, 512):
+        Xp = torch.from_numpy(gen.features((gp.n_src, Fp), gen.feature_seed("proteins"), 0)).to(dev)
+        op = torch.empty(gp.n_dst, Fp, device=dev)
+        t = timed(lambda: fgp.spmm(Gp, "copy_u", "sum", Xp, out=op, stream=st))
+        bts = 8 * (gp.n_dst + 1) + 4 * gp.nnz + 4 * gp.nnz * Fp + 4 * gp.n_dst * Fp
+        c2[f"copy_u_sum_F{Fp}"] = {"ms": round(t, 4), "gbs": round(bts / (t * 1e-3) / 1e9, 1)}
+        del Xp, op
+    res["C2_proteins_gcn"] = c2
+    del Gp, gp
+    # C4: rand-100K MLP aggregation, d1 = 8, d2 = 128, with args
+    gr, Gr = graph_on_gpu("rand100k")
+    s4 = gen.feature_seed("rand100k")
+    X8 = torch.from_numpy(gen.features((gr.n_src, D1), s4, 3)).to(dev)
+    W = torch.from_numpy(gen.features((D1, D2), s4, 4, gen.SCALED, scale=1 / np.sqrt(D1))).to(dev)
+    o = torch.empty(gr.n_dst, D2, device=dev)
+    au, ae = (torch.empty(gr.n_dst, D2, dtype=torch.int32, device=dev) for _ in range(2))
+    abl = mlp_impls(Gr, X8, W, X8, o, au, ae)
+    t = abl["tcgen05_3xtf32"]
+    res["C4_rand100k_mlp"] = {"ms": t, "tflops": round(mlp_flops(gr.nnz) / (t * 1e-3) / 1e12, 2),
+                              "tmem": mlp_roofline(gr.nnz, t, sm_max_mhz()), "ablation_ms": abl}
+    X128 = torch.from_numpy(gen.features((gr.n_src, 128), s4, 2)).to(dev)
+    o128 = torch.empty(gr.n_dst, 128, device=dev)
+    res["C4_rand100k_copy_u_sum_F128_ms"] = round(timed(
+        lambda: fgp.spmm(Gr, "copy_u", "sum", X128, out=o128, stream=st)), 4)
+    del Gr, gr, X8, W, o, au, ae, X128, o128
+    # C6: DRAM-bound control: uniform sources, F = 512
+    gu, Gu = graph_on_gpu("reddit", uniform=True)
+    Gu.prepare(F_DOT * 4)
+    Xu = S.X["X512"]
+    ou = torch.empty(gu.n_dst, F_GCN, device=dev)
+    su = torch.empty(gu.nnz, 1, device=dev)
+    ob = op_bytes(gu.n_dst, gu.nnz)
+    ctl = {}
+    for name, fn in (("spmm_copy_u_sum_F512", lambda: fgp.spmm(Gu, "copy_u", "sum", Xu, out=ou, stream=st)),
+                     ("sddmm_u_dot_v_H1_F512", lambda: fgp.sddmm(Gu, Xu, Xu, H=1, out=su, stream=st))):
+        t = timed(fn)
+        rec, fresh, _ = ncu_record(name, "uniform")
+        d = {"ms": round(t, 4), "gather_model_gbs": round(ob[name] / (t * 1e-3) / 1e9, 1), "ncu_fresh": bool(fresh)}
+        if rec and fresh and rec.get("dram_bytes_per_launch"):
+            d["dram_gbs"] = round(rec["dram_bytes_per_launch"] / (t * 1e-3) / 1e9, 1)
+        ctl[name] = d
+    res["C6_uniform_sources_control"] = ctl
+    del Gu, gu, ou, su
+    torch.cuda.empty_cache()
     return res
 
 
@@ -706,7 +928,7 @@ def run_e2e(S, host, args, world, sync_all, flush):
     outs_h = {id(o): torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs_d}
     h2d = sum(t.numel() * t.element_size() for t in ins.values()) + w_h.numel() * 4
     d2h = sum(t.numel() * t.element_size() for t in outs_h.values())
-    k_steps = max(1, min(args.steps, 5))
+    k_steps = max(1, args.steps)   # the same K as the device-timed step
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k_steps + 1)]
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
     with torch.cuda.stream(st):
@@ -759,11 +981,12 @@ def run_reference(args, world, rank):
         "config": {"workload": "reddit-shaped synthetic graph, same 7-op step as the GPU arm, bounded row sample",
                    "graph": GRAPH, "n": g.n_dst, "nnz": g.nnz, "sample_rows": int(rows.size),
                    "sample_edges": int(me)},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

@@ -32,16 +32,21 @@
  *    16-byte aligned (128-bit lane accesses); F % 4 == 0 (F = H*D, or d2).
  *  - fg_graph borrows row_ptr / col_idx / eid: they must stay alive and
  *    unmodified until fg_graph_destroy.  The handle owns only derived tables.
- *  - Calls are asynchronous on `stream` except fg_graph_create (which
- *    synchronises once: it reads row_ptr back to build the degree bins).
+ *  - Calls are asynchronous on `stream` except the per-topology ones,
+ *    fg_graph_create / fg_graph_prepare / fg_graph_transpose (synchronous: they
+ *    read the CSR back and allocate the handle's tables).  The op calls never
+ *    allocate, synchronise or read the environment, so they can be captured in
+ *    a CUDA graph.
  *    Argument errors are detected on the host BEFORE any launch: a non-OK
  *    status means nothing was launched and outputs are untouched.  Device
  *    faults surface at the caller's next synchronisation.
  *  - Outputs are fully overwritten, never accumulated into.
  *  - Results are deterministic: no floating-point atomics; reruns are bitwise
  *    identical.
- *  - A handle is immutable after creation: concurrent calls on different
- *    streams are safe.  fg_last_error() is thread-local.
+ *  - A handle is only modified by fg_graph_prepare / fg_graph_tune: between
+ *    those, op calls on the same handle from different streams or threads are
+ *    safe (no per-call state lives in the handle).  fg_last_error() is
+ *    thread-local.
  */
 #ifndef FG_H_
 #define FG_H_
@@ -89,7 +94,7 @@ typedef enum {
     FG_EDGE_U_MUL_V = 3  /* psi[j] = x_u[j] * y_v[j]           same */
 } fg_edge_op;
 
-typedef struct fg_graph fg_graph;          /* opaque, immutable after create */
+typedef struct fg_graph fg_graph;          /* opaque; changed only by fg_graph_prepare / fg_graph_tune */
 typedef struct CUstream_st* fg_stream;      /* == cudaStream_t */
 
 /* ---------------------------------------------------------------- graph */
@@ -124,6 +129,70 @@ typedef struct {
 } fg_graph_info_t;
 fg_status fg_graph_info(const fg_graph* g, fg_graph_info_t* info);
 
+/*
+ * fg_graph_prepare -- the per-topology table of the source-segmented gSDDMM
+ * traversal for gathered rows of `row_bytes` bytes (H*D*4 for fp32 features,
+ * H*D*2 for bf16 storage): the paper's 1D source partitioning
+ * with segments sized to the B200 L2.  It applies only when the
+ * source features are wider than the segmentation threshold (48 MB segments
+ * for X > 96 MB by default); otherwise it builds nothing and returns FG_OK.
+ * SYNCHRONOUS on `stream` (allocates device memory, reads counts back), like
+ * fg_graph_create; idempotent per width.  fg_sddmm / fg_sddmm_emul /
+ * fg_sddmm_x16 / fg_dist_sddmm never allocate or synchronise (so they can be
+ * captured in a CUDA graph): for a width that was not prepared they run the
+ * unsegmented traversal, which gives bit-identical results (each edge's dot
+ * product is evaluated by the same lane partition and reduction tree; only
+ * the order of the work units differs) and is slower only when X exceeds the
+ * L2.  Not safe concurrently with calls on the same handle.
+ *   Errors: FG_EINVAL (NULL), FG_ESHAPE (row_bytes <= 0), FG_ENOMEM, FG_ECUDA.
+ */
+fg_status fg_graph_prepare(fg_graph* g, int64_t row_bytes, fg_stream stream);
+
+/*
+ * fg_graph_tune / fg_graph_get_tune -- the launch-configuration knobs of one
+ * handle (the paper's FDS, kept internal: every default is the
+ * value measured best on B200, DESIGN.md §6 / §9).  The FG_* environment
+ * variables of the same names are read once, by fg_graph_create; the launch
+ * paths read only the handle.  Values are read on the host at each launch, so
+ * a change applies to later calls; not safe concurrently with other calls on
+ * the same handle.  None of them changes a result beyond the fp32 summation
+ * order of a sum (max / min / argmax / integer results are invariant), except
+ * FG_TUNE_MLP_IMPL = 2 (bf16 2-split, within the same 1e-4 tolerance).
+ *   FG_TUNE_L2_TILE_MB     copy_u column-tile budget in MB (-1 default, 0 off)
+ *   FG_TUNE_SPMM_HEAVY_DEG CTA-per-row degree threshold of gSpMM (0 automatic)
+ *   FG_TUNE_BALANCE_NNZ    edge count the automatic threshold is computed from
+ *                          (0: this graph's nnz).  The sharding code sets the
+ *                          whole graph's nnz on every shard, so shards split
+ *                          rows exactly as the unsharded op: bit-identical sums.
+ *   FG_TUNE_SDDMM_SEG_MB, FG_TUNE_SDDMM_SEG_MIN_MB   segmentation (above)
+ *   FG_TUNE_SDDMM_PERSIST  CTAs per SM of the segmented launch (-1 occupancy)
+ *   FG_TUNE_SDDMM_L2_TILE  1: column-tiled gSDDMM passes (ablation)
+ *   FG_TUNE_SDDMM_DOT      1: thread-per-edge dot products (ablation E6)
+ *   FG_TUNE_GAT_HEAVY_DEG  CTA-per-row threshold of fg_gat_attention
+ *   FG_TUNE_MLP_IMPL       0 tcgen05 3xTF32 (default), 1 CUDA-core FFMA,
+ *                          2 tcgen05 bf16 2-split with K = 32 (ablations)
+ *   FG_TUNE_HYBRID         1: hot sources staged in shared memory by gSpMM
+ *                          copy_u-sum (the paper's hybrid partitioning,
+ *                          P:534-539) when fg_graph_prepare_hybrid built the
+ *                          table for that width (ablation E7)
+ *   Errors: FG_EINVAL (NULL, unknown key, out-of-range value).
+ */
+typedef enum {
+    FG_TUNE_L2_TILE_MB = 0,
+    FG_TUNE_SPMM_HEAVY_DEG = 1,
+    FG_TUNE_BALANCE_NNZ = 2,
+    FG_TUNE_SDDMM_SEG_MB = 3,
+    FG_TUNE_SDDMM_SEG_MIN_MB = 4,
+    FG_TUNE_SDDMM_PERSIST = 5,
+    FG_TUNE_SDDMM_L2_TILE = 6,
+    FG_TUNE_SDDMM_DOT = 7,
+    FG_TUNE_GAT_HEAVY_DEG = 8,
+    FG_TUNE_MLP_IMPL = 9,
+    FG_TUNE_HYBRID = 10
+} fg_tune_key;
+fg_status fg_graph_tune(fg_graph* g, fg_tune_key key, int64_t value);
+fg_status fg_graph_get_tune(const fg_graph* g, fg_tune_key key, int64_t* value);
+
 /* ---------------------------------------------------------------- gSpMM */
 /*
  * fg_spmm -- featgraph.spmm(A, msgfunc, aggregation), Eq. (1):
@@ -139,8 +208,10 @@ fg_status fg_graph_info(const fg_graph* g, fg_graph_info_t* info);
  *                           W [d_in][d2], X_dst [n_dst][d_in] (NULL -> X, which
  *                           requires n_src == n_dst); 1 <= d_in <= 32 (d_in = 8
  *                           in the paper).  ReLU after the full
- *                           contraction (Fig. 3b).  Runs on the
- *                           tcgen05 tensor cores (split-TF32).
+ *                           contraction (Fig. 3b), s = x_u + x_v
+ *                           formed in fp32 before the contraction (the paper's
+ *                           order).  Runs on the tcgen05 tensor cores
+ *                           (3xTF32); X / X_dst 16-byte aligned.
  *   out   : [n_dst][H*D] fp32, fully overwritten.
  *   red   : FG_REDUCE_SUM / _MAX / _MIN / _MEAN (elementwise per feature
  *           column).  mlp supports sum and max only (else FG_EUNSUPPORTED).
@@ -148,12 +219,10 @@ fg_status fg_graph_info(const fg_graph* g, fg_graph_info_t* info);
  *           source id / edge id of the winning edge.  Ties -> lowest CSR
  *           position.  Must be NULL for sum and mean.
  *   Empty rows: out = +0.0 and arg = -1.
- *   workspace / workspace_bytes: device scratch of >= fg_spmm_workspace_size
- *           bytes, owned by the caller, not used across calls (may be NULL
- *           when that size is 0: copy_u / u_mul_e need none; mlp needs
- *           2 * n_src * ceil(d_in/8) * 8 * 4 + n_dst * D * 4 + 512 bytes for
- *           the tf32 hi/lo split of X and the per-row q_v = x_v W).  Too
- *           small -> FG_EINVAL.
+ *   workspace / workspace_bytes: device scratch of fg_spmm_workspace_size
+ *           bytes; that size is 0 for every op of this version (heavy rows
+ *           combine on chip; the mlp producer forms and splits x_u + x_v on
+ *           the fly), so NULL / 0 may be passed.  Kept for ABI stability.
  *   Errors: FG_EINVAL (null/misaligned pointer, bad enum, arg_* with sum),
  *           FG_ESHAPE (H < 1, D < 1, (H*D) % 4 != 0, mlp with H != 1 or d_in
  *           out of range, u_mul_e/copy_u with d_in != 0), FG_ECUDA.
@@ -300,6 +369,9 @@ typedef struct fg_comm fg_comm;
 fg_status fg_comm_unique_id(void* unique_id_128);
 fg_status fg_comm_init(const void* unique_id_128, int nranks, int rank, fg_comm** out);
 fg_status fg_comm_destroy(fg_comm* c);
+/* fg_comm_info: the communicator's size and this rank as NCCL reports them
+ * (ncclCommCount / ncclCommUserRank) -- the check that every rank joined. */
+fg_status fg_comm_info(const fg_comm* c, int* nranks, int* rank);
 fg_status fg_allgather_rows(fg_comm* c, const int64_t* shard_offsets, int64_t row_elems,
                             const float* X_local, float* X_full, fg_stream stream);
 /*
@@ -309,8 +381,13 @@ fg_status fg_allgather_rows(fg_comm* c, const int64_t* shard_offsets, int64_t ro
  *   rank's destination rows, GLOBAL source ids) reading X_full, both enqueued on
  *   `stream`.  Y_local / X_dst / out_local / arg_* / E are this rank's rows /
  *   edges; every other argument, shape rule and error as fg_spmm / fg_sddmm
- *   (copy_e: FG_EUNSUPPORTED, it gathers no source rows).  Per-row results are
- *   bit-identical to the unsharded op.
+ *   (copy_e: FG_EUNSUPPORTED, it gathers no source rows).  All argument checks
+ *   of the local op run before the all-gather is enqueued (a non-OK status
+ *   means nothing was launched and X_full is untouched).  Per-row results are
+ *   bit-identical to the unsharded op when the local handle's automatic
+ *   CTA-per-row threshold is computed from the whole graph's edge count
+ *   (fg_graph_tune FG_TUNE_BALANCE_NNZ, which the sharding code sets), and
+ *   for max / min / argmax always.
  */
 fg_status fg_dist_spmm(const fg_graph* local, fg_comm* c, const int64_t* shard_offsets, fg_msg_op msg,
                        fg_reduce_op red, int H, int D, const float* X_local, float* X_full, const float* E,

@@ -27,6 +27,21 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas",
          "--expt-relaxed-constexpr", f"-I{os.path.join(ROOT, 'include')}"]
 
 
+def source_hash() -> str:
+    """sha256 over everything libfg.so is built from (csrc sources and headers,
+    include/fg.h, the nvcc arch and flags): the build identity that ncu captures
+    under profiles/ are stamped with, so bench.py can refuse a stale capture."""
+    import hashlib
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                   glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(ROOT, "include", "fg.h")]
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        h.update(open(f, "rb").read())
+    h.update(" ".join(ARCH + [x for x in FLAGS if not x.startswith("-I")]).encode())
+    return h.hexdigest()[:16]
+
+
 def _deps_mtime(src: str) -> float:
     hdrs = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(ROOT, "include", "fg.h")]

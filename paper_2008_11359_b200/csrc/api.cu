@@ -7,8 +7,6 @@
 
 namespace {
 thread_local char g_err[512] = "";
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 }  // namespace
 
 namespace fgk {
@@ -28,6 +26,7 @@ fg_status check_launch(const char* what) {
 }  // namespace fgk
 
 using fgk::set_error;
+using fgk::aligned16;
 
 extern "C" const char* fg_status_string(fg_status s) {
     switch (s) {
@@ -49,15 +48,19 @@ extern "C" int fg_abi_version(void) { return FG_ABI_VERSION; }
 extern "C" fg_status fg_spmm_workspace_size(const fg_graph* g, fg_msg_op msg, fg_reduce_op, int H, int D, int d_in,
                                             size_t* bytes) {
     if (!g || !bytes) return set_error(FG_EINVAL, "fg_spmm_workspace_size: NULL argument");
-    // gather messages: none (heavy rows combine on chip); mlp: tf32 hi/lo split of X + q_v = x_v W
-    *bytes = (msg == FG_MSG_MLP && d_in > 0) ? fgk::mlp_workspace_bytes(g->n_src, g->n_dst, d_in, H * D) : 0;
+    // no message needs scratch: heavy rows combine on chip, and the mlp producer
+    // forms and splits x_u + x_v on the fly (kept in the ABI for future messages)
+    (void)msg; (void)H; (void)D; (void)d_in;
+    *bytes = 0;
     return FG_OK;
 }
 
-extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D,
-                             const float* X, const float* E, const float* W, int d_in, const float* X_dst,
-                             float* out, int32_t* arg_u, int32_t* arg_e, void* workspace,
-                             size_t workspace_bytes, fg_stream stream) {
+namespace fgk {
+// Host-side argument checks of fg_spmm (before any launch; also run by
+// fg_dist_spmm before it starts the all-gather).
+fg_status check_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D, const float* X,
+                     const float* E, const float* W, int d_in, const float* X_dst, const float* out,
+                     const int32_t* arg_u, const int32_t* arg_e) {
     if (!g) return set_error(FG_EINVAL, "fg_spmm: NULL graph");
     if (msg != FG_MSG_COPY_U && msg != FG_MSG_U_MUL_E && msg != FG_MSG_MLP && msg != FG_MSG_U_ADD_E &&
         msg != FG_MSG_COPY_E)
@@ -82,9 +85,7 @@ extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
         if (!X_dst && g->n_src != g->n_dst)
             return set_error(FG_ESHAPE, "fg_spmm(mlp): X_dst = NULL needs n_src == n_dst");
         if (E) return set_error(FG_EINVAL, "fg_spmm(mlp): E must be NULL");
-        if (!workspace || workspace_bytes < fgk::mlp_workspace_bytes(g->n_src, g->n_dst, d_in, D))
-            return set_error(FG_EINVAL, "fg_spmm(mlp): workspace of >= %zu bytes required (fg_spmm_workspace_size)",
-                             fgk::mlp_workspace_bytes(g->n_src, g->n_dst, d_in, D));
+        if (!aligned16(X_dst)) return set_error(FG_EINVAL, "fg_spmm(mlp): X_dst must be 16-byte aligned");
     } else {
         if (d_in != 0 || W || X_dst) return set_error(FG_EINVAL, "fg_spmm: W/X_dst/d_in are for mlp only");
         if ((msg == FG_MSG_U_MUL_E || msg == FG_MSG_U_ADD_E || msg == FG_MSG_COPY_E) && !E && g->nnz > 0)
@@ -94,15 +95,12 @@ extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
         if (msg == FG_MSG_COPY_E && !aligned16(E)) return set_error(FG_EINVAL, "fg_spmm(copy_e): E must be 16-byte aligned");
     }
     if (msg != FG_MSG_COPY_E && !X && g->nnz > 0) return set_error(FG_EINVAL, "fg_spmm: X is NULL");
-    if (g->n_dst == 0) return FG_OK;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (msg == FG_MSG_MLP)
-        return fgk::launch_spmm_mlp(g, red, D, X, W, d_in, X_dst ? X_dst : X, out, arg_u, arg_e, workspace, st);
-    return fgk::launch_spmm_gather(g, msg, red, H, D, X, E, out, arg_u, arg_e, st);
+    return FG_OK;
 }
 
-extern "C" fg_status fg_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, const float* X, const float* Y,
-                              float* out, fg_stream stream) {
+// Host-side argument checks of fg_sddmm (also run by fg_dist_sddmm before the all-gather).
+fg_status check_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, const float* X, const float* Y,
+                      const float* out) {
     if (!g) return set_error(FG_EINVAL, "fg_sddmm: NULL graph");
     if (op != FG_EDGE_U_DOT_V && op != FG_EDGE_U_ADD_V && op != FG_EDGE_U_SUB_V && op != FG_EDGE_U_MUL_V)
         return set_error(FG_EINVAL, "fg_sddmm: bad edge op %d", int(op));
@@ -111,11 +109,37 @@ extern "C" fg_status fg_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, co
     if (F % 4 != 0) return set_error(FG_ESHAPE, "fg_sddmm: H*D must be a multiple of 4");
     if (op == FG_EDGE_U_DOT_V && H > 1 && (D % 4 != 0 || ((D / 4) & (D / 4 - 1)) != 0))
         return set_error(FG_ESHAPE, "fg_sddmm: with H > 1, D must be 4 * 2^k (got D=%d)", D);
+    if (op == FG_EDGE_U_DOT_V && H > 1 && F > 512)
+        return set_error(FG_EUNSUPPORTED, "fg_sddmm: multi-head with H*D > 512 not implemented");
     if (F > (int64_t(1) << 20)) return set_error(FG_ESHAPE, "fg_sddmm: H*D too large");
     if (g->nnz == 0) return FG_OK;
     if (!X || !Y || !out) return set_error(FG_EINVAL, "fg_sddmm: NULL tensor");
     if (!aligned16(X) || !aligned16(Y) || !aligned16(out))
         return set_error(FG_EINVAL, "fg_sddmm: X/Y/out must be 16-byte aligned");
+    return FG_OK;
+}
+}  // namespace fgk
+
+extern "C" fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int D,
+                             const float* X, const float* E, const float* W, int d_in, const float* X_dst,
+                             float* out, int32_t* arg_u, int32_t* arg_e, void* workspace,
+                             size_t workspace_bytes, fg_stream stream) {
+    (void)workspace; (void)workspace_bytes;   // no op needs scratch (fg_spmm_workspace_size == 0)
+    fg_status s = fgk::check_spmm(g, msg, red, H, D, X, E, W, d_in, X_dst, out, arg_u, arg_e);
+    if (s != FG_OK) return s;
+    if (g->n_dst == 0) return FG_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (msg == FG_MSG_MLP)
+        return fgk::launch_spmm_mlp(g, red, D, X, W, d_in, X_dst ? X_dst : X, out, arg_u, arg_e, st);
+    return fgk::launch_spmm_gather(g, msg, red, H, D, X, E, out, arg_u, arg_e, st);
+}
+
+extern "C" fg_status fg_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, const float* X, const float* Y,
+                              float* out, fg_stream stream) {
+    fg_status s = fgk::check_sddmm(g, op, H, D, X, Y, out);
+    if (s != FG_OK) return s;
+    if (g->nnz == 0) return FG_OK;
+    const int64_t F = int64_t(H) * D;
     if (op != FG_EDGE_U_DOT_V)
         return fgk::launch_sddmm_binary(g, int(op), int(F), X, Y, out, reinterpret_cast<cudaStream_t>(stream));
     return fgk::launch_sddmm(g, H, D, X, Y, out, reinterpret_cast<cudaStream_t>(stream));

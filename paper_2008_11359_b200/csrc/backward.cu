@@ -143,7 +143,6 @@ __global__ void __launch_bounds__(THREADS) softmax_backward_thread_kernel(
     }
 }
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 bool is_transpose_of(const fg_graph* g, const fg_graph* gT) {
     return gT && gT->n_dst == g->n_src && gT->n_src == g->n_dst && gT->nnz == g->nnz;
@@ -219,7 +218,7 @@ extern "C" fg_status fg_spmm_backward(const fg_graph* g, const fg_graph* gT, fg_
     const bool mean = red == FG_REDUCE_MEAN;
     if ((red == FG_REDUCE_MAX || red == FG_REDUCE_MIN) && !arg_u)
         return set_error(FG_EINVAL, "fg_spmm_backward: max/min need the forward's arg_u");
-    if (!aligned16(dOut) || !aligned16(dX) || !aligned16(X) || !aligned16(arg_u))
+    if (!fgk::aligned16(dOut) || !fgk::aligned16(dX) || !fgk::aligned16(X) || !fgk::aligned16(arg_u))
         return set_error(FG_EINVAL, "fg_spmm_backward: tensors must be 16-byte aligned");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int F4 = H * D / 4;

@@ -31,6 +31,8 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+    ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
     bool ok = false;
 };
 
@@ -52,6 +54,8 @@ NcclApi& api() {
     a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(a.h, "ncclGroupStart"));
     a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(a.h, "ncclGroupEnd"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(a.h, "ncclGetErrorString"));
+    a.CommCount = reinterpret_cast<decltype(a.CommCount)>(dlsym(a.h, "ncclCommCount"));
+    a.CommUserRank = reinterpret_cast<decltype(a.CommUserRank)>(dlsym(a.h, "ncclCommUserRank"));
     a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Broadcast && a.GroupStart && a.GroupEnd &&
            a.GetErrorString;
     return a;
@@ -90,6 +94,16 @@ extern "C" fg_status fg_comm_init(const void* uid, int nranks, int rank, fg_comm
         return nccl_fail("ncclCommInitRank", r);
     }
     *out = c;
+    return FG_OK;
+}
+
+extern "C" fg_status fg_comm_info(const fg_comm* c, int* nranks, int* rank) {
+    if (!c || !nranks || !rank) return fgk::set_error(FG_EINVAL, "fg_comm_info: NULL argument");
+    NcclApi& a = api();
+    if (!a.CommCount || !a.CommUserRank) return fgk::set_error(FG_ENCCL, "fg_comm_info: ncclCommCount unavailable");
+    ncclResult_t r = a.CommCount(c->comm, nranks);
+    if (r == ncclSuccess) r = a.CommUserRank(c->comm, rank);
+    if (r != ncclSuccess) return nccl_fail("ncclCommCount/UserRank", r);
     return FG_OK;
 }
 
@@ -136,7 +150,11 @@ extern "C" fg_status fg_dist_spmm(const fg_graph* local, fg_comm* c, const int64
     if (!local || !c || !shard_offsets || !X_full) return fgk::set_error(FG_EINVAL, "fg_dist_spmm: NULL argument");
     if (msg == FG_MSG_COPY_E) return fgk::set_error(FG_EUNSUPPORTED, "fg_dist_spmm: copy_e gathers no source rows");
     const int64_t row_elems = (msg == FG_MSG_MLP) ? int64_t(d_in) : int64_t(H) * D;
-    fg_status s = fg_allgather_rows(c, shard_offsets, row_elems, X_local, X_full, stream);
+    // every argument check of the local op runs BEFORE the collective is enqueued:
+    // a non-OK status means nothing was launched and X_full is untouched
+    fg_status s = fgk::check_spmm(local, msg, red, H, D, X_full, E, W, d_in, X_dst, out_local, arg_u, arg_e);
+    if (s != FG_OK) return s;
+    s = fg_allgather_rows(c, shard_offsets, row_elems, X_local, X_full, stream);
     if (s != FG_OK) return s;
     return fg_spmm(local, msg, red, H, D, X_full, E, W, d_in, X_dst, out_local, arg_u, arg_e, workspace,
                    workspace_bytes, stream);
@@ -146,7 +164,9 @@ extern "C" fg_status fg_dist_sddmm(const fg_graph* local, fg_comm* c, const int6
                                    int H, int D, const float* X_local, float* X_full, const float* Y_local,
                                    float* out_local, fg_stream stream) {
     if (!local || !c || !shard_offsets || !X_full) return fgk::set_error(FG_EINVAL, "fg_dist_sddmm: NULL argument");
-    fg_status s = fg_allgather_rows(c, shard_offsets, int64_t(H) * D, X_local, X_full, stream);
+    fg_status s = fgk::check_sddmm(local, op, H, D, X_full, Y_local, out_local);
+    if (s != FG_OK) return s;
+    s = fg_allgather_rows(c, shard_offsets, int64_t(H) * D, X_local, X_full, stream);
     if (s != FG_OK) return s;
     return fg_sddmm(local, op, H, D, X_full, Y_local, out_local, stream);
 }

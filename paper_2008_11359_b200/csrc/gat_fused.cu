@@ -278,8 +278,7 @@ fg_status launch_t(Args A, const fg_graph* g, const float* X, const float* Y, fl
     constexpr int NG = THREADS / G;
     {   // rows with degree >= FG_GAT_HEAVY_DEG (default 4096) run CTA-per-row: reddit
         // H=8 D=32 14.9 ms at 256 (8 groups x 32), 14.3 at 1024, 14.0 at 4096, 14.3 at 8192
-        const char* hv = getenv("FG_GAT_HEAVY_DEG");
-        A.n_heavy = fgk::rows_with_degree_at_least(g, hv ? std::max<int64_t>(1, atoll(hv)) : 4096);
+        A.n_heavy = fgk::rows_with_degree_at_least(g, g->tune.gat_heavy_deg);
     }
     const int64_t blocks = A.n_heavy + (A.n_rows - A.n_heavy + NG - 1) / NG;
     if (blocks == 0) return FG_OK;
@@ -289,7 +288,6 @@ fg_status launch_t(Args A, const fg_graph* g, const float* X, const float* Y, fl
     return fgk::check_launch("gat_fused_kernel");
 }
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
 
@@ -303,7 +301,7 @@ extern "C" fg_status fg_gat_attention(const fg_graph* g, int H, int D, const flo
     if (F4 > 128) return set_error(FG_EUNSUPPORTED, "fg_gat_attention: H*D > 512 not implemented");
     if (g->n_dst == 0) return FG_OK;
     if (!X || !Y || !out) return set_error(FG_EINVAL, "fg_gat_attention: NULL tensor");
-    if (!aligned16(X) || !aligned16(Y) || !aligned16(out))
+    if (!fgk::aligned16(X) || !fgk::aligned16(Y) || !fgk::aligned16(out))
         return set_error(FG_EINVAL, "fg_gat_attention: X/Y/out must be 16-byte aligned");
     Args A;
     A.rows = g->rows_by_deg;

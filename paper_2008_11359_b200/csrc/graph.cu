@@ -17,6 +17,27 @@
 
 #include "fg_internal.h"
 
+namespace fgk {
+// FG_* environment overrides of the launch knobs, read once per handle here (the
+// launch paths read only g->tune); fg_graph_tune sets them explicitly.
+void tuning_from_env(fg_tuning* t) {
+    auto rd = [](const char* name, int64_t& v) {
+        const char* e = getenv(name);
+        if (e && *e) v = atoll(e);
+    };
+    rd("FG_L2_TILE_MB", t->l2_tile_mb);
+    rd("FG_SPMM_HEAVY_DEG", t->spmm_heavy_deg);
+    rd("FG_SDDMM_SEG_MB", t->sddmm_seg_mb);
+    rd("FG_SDDMM_SEG_MIN_MB", t->sddmm_seg_min_mb);
+    rd("FG_SDDMM_PERSIST", t->sddmm_persist);
+    rd("FG_SDDMM_L2_TILE", t->sddmm_l2_tile);
+    rd("FG_SDDMM_DOT", t->sddmm_dot);
+    rd("FG_GAT_HEAVY_DEG", t->gat_heavy_deg);
+    rd("FG_MLP_IMPL", t->mlp_impl);
+    rd("FG_HYBRID", t->hybrid);
+}
+}  // namespace fgk
+
 namespace {
 
 // flags
@@ -100,20 +121,16 @@ __global__ void seg_write_kernel(int64_t n, int nseg, int64_t seg_rows, int chun
 }
 
 namespace fgk {
-fg_status get_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t st, const fg_graph::SegUnits** out) {
+fg_status build_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t st) {
     std::lock_guard<std::mutex> lock(g->seg_mu);
     for (auto& su : g->seg_units)
-        if (su.seg_rows == seg_rows) {
-            *out = &su;
-            return FG_OK;
-        }
+        if (su.seg_rows == seg_rows) return FG_OK;
     const int64_t n = g->n_dst;
     const int nseg = int((g->n_src + seg_rows - 1) / seg_rows);
     fg_graph::SegUnits su;
     su.seg_rows = seg_rows;
     int64_t* cnt = nullptr;
     std::vector<int64_t> h(size_t(n) * nseg + 1, 0);
-    fg_status stt = FG_OK;
     cudaError_t e = cudaMalloc(&cnt, sizeof(int64_t) * (size_t(n) * nseg + 1));
     if (e == cudaSuccess && n > 0) {
         seg_count_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(n, nseg, seg_rows, chunk, g->row_ptr, g->col_idx, cnt);
@@ -142,12 +159,26 @@ fg_status get_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t s
     cudaFree(cnt);
     if (e != cudaSuccess) {
         cudaFree(su.row); cudaFree(su.p0); cudaFree(su.p1);
-        return set_error(FG_ECUDA, "segmented SDDMM units: %s", cudaGetErrorString(e));
+        return set_error(e == cudaErrorMemoryAllocation ? FG_ENOMEM : FG_ECUDA, "fg_graph_prepare: segment units: %s",
+                         cudaGetErrorString(e));
     }
     g->device_bytes += 20 * su.n_units;
     g->seg_units.push_back(su);
-    *out = &g->seg_units.back();
-    return stt;
+    return FG_OK;
+}
+
+const fg_graph::SegUnits* find_seg_units(const fg_graph* g, int64_t seg_rows) {
+    std::lock_guard<std::mutex> lock(const_cast<fg_graph*>(g)->seg_mu);
+    for (auto& su : g->seg_units)
+        if (su.seg_rows == seg_rows) return &su;
+    return nullptr;
+}
+
+int64_t sddmm_seg_rows(const fg_graph* g, int64_t row_bytes) {
+    const int64_t budget = g->tune.sddmm_seg_mb << 20;
+    const int64_t min_x = g->tune.sddmm_seg_min_mb << 20;
+    if (budget <= 0 || row_bytes <= 0 || g->n_src * row_bytes <= std::max(budget, min_x)) return 0;
+    return std::max<int64_t>(32, budget / row_bytes);
 }
 
 int64_t rows_with_degree_at_least(const fg_graph* g, int64_t t) {
@@ -184,6 +215,7 @@ extern "C" fg_status fg_graph_create(int64_t n_dst, int64_t n_src, int64_t nnz, 
     g->n_dst = n_dst; g->n_src = n_src; g->nnz = nnz;
     g->row_ptr = row_ptr; g->col_idx = col_idx; g->eid = eid;
     cudaGetDevice(&g->device);
+    fgk::tuning_from_env(&g->tune);
     unsigned* dflags = nullptr;
     unsigned* seen = nullptr;
     std::vector<int64_t> rp(size_t(n_dst + 1));
@@ -316,4 +348,56 @@ extern "C" fg_status fg_graph_info(const fg_graph* g, fg_graph_info_t* info) {
     info->n_sddmm_units = g->n_units;
     info->device_bytes = g->device_bytes;
     return FG_OK;
+}
+
+// ---------------------------------------------------------------- knobs and prepare
+extern "C" fg_status fg_graph_tune(fg_graph* g, fg_tune_key key, int64_t value) {
+    if (!g) return fgk::set_error(FG_EINVAL, "fg_graph_tune: NULL handle");
+    fg_tuning& t = g->tune;
+    switch (key) {
+        case FG_TUNE_L2_TILE_MB: t.l2_tile_mb = value < 0 ? -1 : value; break;
+        case FG_TUNE_SPMM_HEAVY_DEG: t.spmm_heavy_deg = std::max<int64_t>(0, value); break;
+        case FG_TUNE_BALANCE_NNZ: t.balance_nnz = std::max<int64_t>(0, value); break;
+        case FG_TUNE_SDDMM_SEG_MB: t.sddmm_seg_mb = std::max<int64_t>(0, value); break;
+        case FG_TUNE_SDDMM_SEG_MIN_MB: t.sddmm_seg_min_mb = std::max<int64_t>(0, value); break;
+        case FG_TUNE_SDDMM_PERSIST: t.sddmm_persist = value; break;
+        case FG_TUNE_SDDMM_L2_TILE: t.sddmm_l2_tile = value != 0; break;
+        case FG_TUNE_SDDMM_DOT: t.sddmm_dot = value != 0; break;
+        case FG_TUNE_GAT_HEAVY_DEG: t.gat_heavy_deg = std::max<int64_t>(1, value); break;
+        case FG_TUNE_MLP_IMPL:
+            if (value < 0 || value > 2) return fgk::set_error(FG_EINVAL, "fg_graph_tune: mlp impl %lld", (long long)value);
+            t.mlp_impl = value;
+            break;
+        case FG_TUNE_HYBRID: t.hybrid = value != 0; break;
+        default: return fgk::set_error(FG_EINVAL, "fg_graph_tune: bad key %d", int(key));
+    }
+    return FG_OK;
+}
+
+extern "C" fg_status fg_graph_get_tune(const fg_graph* g, fg_tune_key key, int64_t* value) {
+    if (!g || !value) return fgk::set_error(FG_EINVAL, "fg_graph_get_tune: NULL argument");
+    const fg_tuning& t = g->tune;
+    switch (key) {
+        case FG_TUNE_L2_TILE_MB: *value = t.l2_tile_mb; break;
+        case FG_TUNE_SPMM_HEAVY_DEG: *value = t.spmm_heavy_deg; break;
+        case FG_TUNE_BALANCE_NNZ: *value = t.balance_nnz; break;
+        case FG_TUNE_SDDMM_SEG_MB: *value = t.sddmm_seg_mb; break;
+        case FG_TUNE_SDDMM_SEG_MIN_MB: *value = t.sddmm_seg_min_mb; break;
+        case FG_TUNE_SDDMM_PERSIST: *value = t.sddmm_persist; break;
+        case FG_TUNE_SDDMM_L2_TILE: *value = t.sddmm_l2_tile; break;
+        case FG_TUNE_SDDMM_DOT: *value = t.sddmm_dot; break;
+        case FG_TUNE_GAT_HEAVY_DEG: *value = t.gat_heavy_deg; break;
+        case FG_TUNE_MLP_IMPL: *value = t.mlp_impl; break;
+        case FG_TUNE_HYBRID: *value = t.hybrid; break;
+        default: return fgk::set_error(FG_EINVAL, "fg_graph_get_tune: bad key %d", int(key));
+    }
+    return FG_OK;
+}
+
+extern "C" fg_status fg_graph_prepare(fg_graph* g, int64_t row_bytes, fg_stream stream) {
+    if (!g) return fgk::set_error(FG_EINVAL, "fg_graph_prepare: NULL handle");
+    if (row_bytes <= 0) return fgk::set_error(FG_ESHAPE, "fg_graph_prepare: row_bytes must be > 0");
+    const int64_t seg_rows = fgk::sddmm_seg_rows(g, row_bytes);
+    if (seg_rows == 0 || g->nnz == 0) return FG_OK;   // this width is not segmented: nothing to build
+    return fgk::build_seg_units(g, seg_rows, g->unit_chunk, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -3,14 +3,13 @@
 // shapes the tensor-core kernel does not take.
 //
 // Fig. 3b: phi(u, v) = ReLU((x_u + x_v) W), W in R^{d1 x d2},
-// aggregated by max (Fig. 1 "picking the maximum") or sum.
-// Using (x_u + x_v) W = x_u W + x_v W, the per-destination term q_v = x_v W is
-// computed once per row and the per-edge work is a_e = x_u W (d1*d2 FMAs).
-//   max: out = ReLU(max_e a_e + q_v); arg = first argmax of a_e if that is > 0,
-//        else the row's first edge (all messages are +0 then; first wins)
-//        -- exact in real arithmetic because ReLU(. + q) is monotone.
-//   sum: out = sum_e ReLU(a_e + q_v).
-// One warp per destination row (degree-descending order), lane owns NC columns.
+// aggregated by max (Fig. 1 "picking the maximum") or sum, in the paper's
+// order: s_e = x_u + x_v (fp32), z_e = s_e W (d1*d2 FMAs in k order), then
+//   max: out = ReLU(max_e z_e); arg = first argmax if that is > 0, else the
+//        row's first edge (all messages are +0 then; first wins);
+//   sum: out = sum_e ReLU(z_e).
+// One warp per destination row (degree-descending order), lane owns NC columns;
+// x_v (d_in <= 32 values) is held in registers for the row.
 #include <cstdlib>
 
 #include "fg_internal.h"
@@ -40,34 +39,32 @@ __global__ void __launch_bounds__(THREADS) mlp_simt_kernel(const int32_t* __rest
     if (r >= n_rows) return;
     const int64_t v = rows[r];
     const int64_t s = rp[v], e = rp[v + 1];
-    float q[NC], best[NC];
+    float best[NC];
     int pos[NC];
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
-        const int c = cbase + lane + 32 * j;
-        float a = 0.f;
-        for (int k = 0; k < d_in; ++k) a = fmaf(__ldg(Xd + v * d_in + k), sW[k][lane + 32 * j], a);
-        q[j] = a;
         best[j] = MAX ? -INFINITY : 0.f;
         pos[j] = -1;
     }
+    const float xv_l = lane < d_in ? __ldg(Xd + v * d_in + lane) : 0.f;   // lane k holds x_v[k]
     for (int64_t p = s; p < e; ++p) {
         const int64_t u = __ldg(ci + p);
-        const float* xu = X + u * d_in;
+        const float xu_l = lane < d_in ? __ldg(X + u * d_in + lane) : 0.f;
+        const float s_l = xu_l + xv_l;                                     // s_e[k] = x_u[k] + x_v[k]
         float a[NC];
 #pragma unroll
         for (int j = 0; j < NC; ++j) a[j] = 0.f;
         for (int k = 0; k < d_in; ++k) {
-            const float xk = __ldg(xu + k);
+            const float sk = __shfl_sync(0xffffffffu, s_l, k);
 #pragma unroll
-            for (int j = 0; j < NC; ++j) a[j] = fmaf(xk, sW[k][lane + 32 * j], a[j]);
+            for (int j = 0; j < NC; ++j) a[j] = fmaf(sk, sW[k][lane + 32 * j], a[j]);
         }
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
             if (MAX) {
                 if (a[j] > best[j]) { best[j] = a[j]; pos[j] = int(p); }
             } else {
-                best[j] += fmaxf(a[j] + q[j], 0.f);
+                best[j] += fmaxf(a[j], 0.f);
             }
         }
     }
@@ -83,7 +80,7 @@ __global__ void __launch_bounds__(THREADS) mlp_simt_kernel(const int32_t* __rest
             if (arg_e) arg_e[o] = -1;
             continue;
         }
-        const float z = best[j] + q[j];
+        const float z = best[j];
         const int pw = (z > 0.f) ? pos[j] : int(s);
         out[o] = z > 0.f ? z : 0.f;
         if (arg_u) arg_u[o] = __ldg(ci + pw);
@@ -108,16 +105,12 @@ fg_status launch_spmm_mlp_simt(const fg_graph* g, fg_reduce_op red, int d2, cons
     return check_launch("mlp_simt_kernel");
 }
 
-// The product path is the tcgen05 kernel; FG_MLP_SIMT=1 selects the FFMA kernel
-// (ablation only: same semantics, CUDA cores instead of tensor cores).
+// The product path is the tcgen05 3xTF32 kernel; FG_TUNE_MLP_IMPL selects the
+// ablations (1: this FFMA kernel, CUDA cores instead of tensor cores; 2: the
+// tcgen05 kernel with the bf16 2-split) -- same semantics.
 fg_status launch_spmm_mlp(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W, int d_in,
-                          const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e, void* workspace,
-                          cudaStream_t st) {
-    static const bool simt = [] {
-        const char* e = getenv("FG_MLP_SIMT");
-        return e && e[0] == '1';
-    }();
-    if (simt) return launch_spmm_mlp_simt(g, red, d2, X, W, d_in, X_dst, out, arg_u, arg_e, st);
-    return launch_spmm_mlp_tcgen05(g, red, d2, X, W, d_in, X_dst, out, arg_u, arg_e, workspace, st);
+                          const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e, cudaStream_t st) {
+    if (g->tune.mlp_impl == 1) return launch_spmm_mlp_simt(g, red, d2, X, W, d_in, X_dst, out, arg_u, arg_e, st);
+    return launch_spmm_mlp_tcgen05(g, red, d2, X, W, d_in, X_dst, out, arg_u, arg_e, g->tune.mlp_impl == 2, st);
 }
 }  // namespace fgk

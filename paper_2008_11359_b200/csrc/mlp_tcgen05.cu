@@ -3,36 +3,42 @@
 //
 // Fig. 3b: phi(u, v) = ReLU(sum_k (x_u[k] + x_v[k]) W[k, i]),
 // aggregated by max (Fig. 1 "picking the maximum"; MLP aggregation of
-// Table tab:gpu-kernel(b), d1 = 8) or sum.
-// Using (x_u + x_v) W = x_u W + x_v W:
-//     a_e[i] = x_u W[:, i]    -- a real dense contraction: a gathered tile of NT
-//                                edges x d1 against the shared W (tensor cores)
-//     q_v[i] = x_v W[:, i]    -- once per destination row (epilogue, FFMA)
-//     max: out[v][i] = ReLU(max_e a_e[i] + q_v[i]); argmax = first e attaining the
-//          max if that is > 0, else the row's first edge (all messages are +0);
-//     sum: out[v][i] = sum_e ReLU(a_e[i] + q_v[i]).
-// (exact in real arithmetic: ReLU(. + q) is monotone -- SURVEY §8(c) pin table).
+// Table tab:gpu-kernel(b), d1 = 8) or sum.  Evaluated in the paper's
+// order: s_e = x_u + x_v (one fp32 add per input dimension, as Fig. 3b line
+// 1), then z_e = s_e W (the contraction), then ReLU and the aggregation:
+//     max: out[v][i] = ReLU(max_e z_e[i]); argmax = first e attaining the max
+//          if that is > 0, else the row's first edge (all messages are +0);
+//     sum: out[v][i] = sum_e ReLU(z_e[i]).
+// Forming s_e before the contraction keeps the error relative to
+// sum_k |s_e[k] W[k,i]| -- the oracle's tolerance scale -- also when x_v nearly
+// cancels x_u (the earlier x_u W + x_v W split carried an error relative to
+// |x_u W| + |x_v W|).
 //
 // The paper's V100 schedule bound d2 to blocks and tree-reduced d1 over threads
 // (listing fig:schedule-mlp-conv-gpu).  Here, per CTA (persistent,
 // 4 per SM -- four independent pipelines hide the MMA/commit latency -- each
 // owning a contiguous range of destination rows and therefore of CSR edges):
-//   * producer warp gathers x_u for NT = 64 edges (L2-resident: n x d1 x 4 B),
-//     pre-split into tf32 hi + lo (mlp_split_kernel), with cp.async straight into
-//     the B operand (K-major, no-swizzle canonical layout) of an 8-stage ring;
-//   * one thread issues tcgen05.mma.kind::tf32, M = 128 features (W^T, staged
-//     once), N = 64 edges, K = 8, three times per tile
-//     (hi*hi + hi*lo + lo*hi = "3xTF32", error ~2^-21 relative: fp32-grade,
-//     the 1e-4 bound needs more than one tf32 pass), accumulating in
-//     TMEM (2 x 64 columns, double-buffered), and commits to mbarriers;
+//   * a producer warp walks NT = 64 edges per tile: it finds each edge's
+//     destination row in a 32-row window of row_ptr (register binary search),
+//     loads x_u and x_v (L2-resident: n x d1 x 4 B), forms s_e, splits it into
+//     tensor-core operands and stores them into the B operand (K-major,
+//     no-swizzle canonical layout) of an 8-stage shared-memory ring;
+//   * one thread issues the MMAs, M = 128 features (W^T, staged once), N = 64
+//     edges, accumulating in TMEM (2 x 64 columns, double-buffered):
+//       3xTF32 (default): tcgen05.mma.kind::tf32, K = 8, hi*hi + hi*lo + lo*hi
+//         (error ~2^-21 relative: fp32-grade; one TF32 pass cannot meet the
+//         1e-4 bound);
+//       bf16 2-split (FG_TUNE_MLP_IMPL = 2): tcgen05.mma.kind::f16 with bf16
+//         operands, K = 16, [s_hi | s_hi] . [w_hi | w_lo] + [s_lo | s_lo] .
+//         [w_hi | w_lo] = (s_hi + s_lo)(w_hi + w_lo) (error ~2^-17 relative);
 //   * 4 epilogue warps read the accumulator with tcgen05.ld (thread = feature,
 //     walking edge columns, so the per-row segmented max needs no cross-lane
-//     reduction), keep the running winner as a CSR position, add the per-row
-//     q_v = x_v W (mlp_q_kernel, once per call) and write each finished row.
-// Bound: reading every accumulator element out of TMEM (m x d2 x 4 B; TMEM
-// reads run at ~64-72 B/clk/SM) -- measured on reddit d2 = 128: the epilogue
-// loop alone (gathers and MMAs disabled, FG_MLP_DBG=6) takes 2.8-2.9 ms of the
-// 4.05 ms; the argmax search adds the rest.
+//     reduction), keep the running winner as a CSR position, and write each
+//     finished row.
+// Bound: reading every accumulator element out of TMEM (m x d2 x 4 B; the
+// guide's LDTM throughput is 64 B/clk/SM, B300_MICROARCH.md "TMEM") -- on
+// reddit d2 = 128 the epilogue's TMEM reads alone take ~2.8 ms of ~4 ms
+// (DESIGN.md §6).
 #include <cstdint>
 #include <cstdlib>
 
@@ -50,7 +56,6 @@ constexpr int MMA_WARP = 4;
 constexpr int NPROD = 1;                  // producer warp 5
 constexpr int THREADS = (NEPI + 1 + NPROD) * 32;
 constexpr int TMEM_COLS = NBUF * NT;      // 128: four CTAs per SM share the 512 columns
-constexpr int TILE_BYTES = 8 * 4 * 128;   // one K-step operand tile: 128 rows x 8 tf32 = 4 KB
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -141,28 +146,6 @@ __device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[32]) {
         : "memory");
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
-}
-// arrive on the mbarrier once all of this thread's prior cp.async copies have landed
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Split X into tf32 hi / lo rows of KS*8 floats (zero-padded beyond d_in), once per call.
-template <int KS>
-__global__ void __launch_bounds__(256) mlp_split_kernel(const float* __restrict__ X, int64_t n, int d_in,
-                                                      float* __restrict__ Xhi, float* __restrict__ Xlo) {
-    const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
-    if (i >= n * KS * 8) return;
-    const int64_t r = i / (KS * 8);
-    const int k = int(i % (KS * 8));
-    const float x = (k < d_in) ? __ldg(X + r * d_in + k) : 0.f;
-    const float hi = tf32_rna(x);
-    Xhi[i] = hi;
-    Xlo[i] = tf32_rna(x - hi);
-}
-
 __device__ __forceinline__ int64_t lower_bound_rp(const int64_t* rp, int64_t n1, int64_t target) {
     int64_t lo = 0, hi = n1;   // first i in [0, n1) with rp[i] >= target
     while (lo < hi) {
@@ -171,6 +154,14 @@ __device__ __forceinline__ int64_t lower_bound_rp(const int64_t* rp, int64_t n1,
     }
     return lo;
 }
+
+// bf16 (round to nearest even) bits of x, and its value as fp32 (exact)
+__device__ __forceinline__ uint32_t bf16_bits(float x) {
+    uint16_t r;
+    asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float bf16_val(uint32_t b) { return __uint_as_float(b << 16); }
 
 struct Args {
     const int64_t* row_ptr;
@@ -184,40 +175,14 @@ struct Args {
     int32_t* arg_e;
     int64_t n_dst, nnz, n_src;
     int d_in, d2;
-    const float* Xhi;     // [n_src][KS*8] tf32 hi part of X (workspace)
-    const float* Xlo;     // [n_src][KS*8] tf32 lo part
-    const float* Q;       // [n_dst][d2]: q_v = x_v W in fp32 (workspace, mlp_q_kernel)
-    int backoff_ns;       // producer / MMA wait back-off (FG_MLP_BACKOFF_NS)
-    int epi_backoff_ns;   // epilogue wait back-off (FG_MLP_EPI_BACKOFF_NS, 0 = spin on try_wait)
-    int dbg;              // FG_MLP_DBG bits (pipeline experiments): 2 skip gathers, 4 skip MMAs
-                          // (results are then wrong; timing only)
 };
 
-// q_v = x_v W (fp32 FMA chain in k order), once per destination row and feature:
-// the per-row term of the MLP message, applied in the epilogue (see the header).
-// Block = 128 features (blockIdx.y) x Q_ROWS rows (blockIdx.x): no 64-bit index
-// division per element (that version took 146 us on reddit d2 = 128).
-constexpr int Q_ROWS = 16;
-__global__ void __launch_bounds__(128) mlp_q_kernel(const float* __restrict__ Xd, const float* __restrict__ W,
-                                                  int64_t n, int d_in, int d2, float* __restrict__ Q) {
-    const int i = blockIdx.y * 128 + threadIdx.x;
-    if (i >= d2) return;
-    float w[32];
-#pragma unroll
-    for (int k = 0; k < 32; ++k) w[k] = (k < d_in) ? __ldg(W + int64_t(k) * d2 + i) : 0.f;
-    const int64_t v0 = int64_t(blockIdx.x) * Q_ROWS;
-    for (int r = 0; r < Q_ROWS; ++r) {
-        const int64_t v = v0 + r;
-        if (v >= n) break;
-        const float* x = Xd + v * d_in;
-        float a = 0.f;
-#pragma unroll
-        for (int k = 0; k < 32; ++k)
-            if (k < d_in) a = fmaf(__ldg(x + k), w[k], a);
-        Q[v * d2 + i] = a;
-    }
-}
+constexpr int BACKOFF_NS = 128;   // producer / MMA wait back-off (the epilogue spins)
 
+// Shared memory of one CTA.  Every operand tile is 32 bytes per row per MMA
+// (tf32 K = 8 or bf16 K = 16): A tiles 128 rows (4 KB), B tiles NT rows (2 KB).
+// 3xTF32: a_hi / a_lo = tf32 hi / lo of W^T, b_hi / b_lo = of s_e (per K step ks).
+// bf16:   a_hi = [w_hi | w_lo] (bf16), b_hi = [s_hi | s_hi], b_lo = [s_lo | s_lo].
 template <int KS>
 struct Smem {
     float a_hi[KS][MT * 8];
@@ -240,23 +205,19 @@ struct Epi {
     int64_t E0;       // CSR position of the CTA's first edge
     int rs, re;       // current row's edge range, relative to E0
     int nre;          // prefetched end of row r + 1 (relative)
-    float best, q, nq;
+    float best;
     int bpos;         // relative position of the current winner
     int i;            // global feature index
     bool active;      // i < d2
 
-    // prefetch the next row's end pointer and q so that the per-row bookkeeping
-    // never waits on a global load
+    // prefetch the next row's end pointer so that the per-row bookkeeping never
+    // waits on a global load
     __device__ __forceinline__ void prefetch(int rn) {
-        if (rn < r_hi) {
-            nre = int(__ldg(A->row_ptr + rn + 1) - E0);
-            nq = active ? __ldg(A->Q + int64_t(rn) * A->d2 + i) : 0.f;
-        }
+        if (rn < r_hi) nre = int(__ldg(A->row_ptr + rn + 1) - E0);
     }
     __device__ __forceinline__ void start_row() {
         best = MAX ? -INFINITY : 0.f;
         bpos = 0;
-        q = nq;
         prefetch(r + 1);
     }
     __device__ __forceinline__ void finish_row() {
@@ -272,10 +233,9 @@ struct Epi {
             if (A->arg_e) A->arg_e[o] = -1;
             return;
         }
-        const float z = best + q;
-        const bool pos = z > 0.f;
-        A->out[o] = pos ? z : 0.f;
-        // every message is +0 when z <= 0: the row's first edge wins
+        const bool pos = best > 0.f;
+        A->out[o] = pos ? best : 0.f;
+        // every message is +0 when max z <= 0: the row's first edge wins
         const int64_t p = E0 + (pos ? bpos : rs);
         if (A->arg_u) A->arg_u[o] = __ldg(A->col_idx + p);
         if (A->arg_e) A->arg_e[o] = A->eid ? __ldg(A->eid + p) : int(p);
@@ -319,7 +279,7 @@ struct Epi {
 #pragma unroll
             for (int c = 0; c < 32; c += 4)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) sm[k] += fmaxf(__uint_as_float(v[c + k]) + q, 0.f);
+                for (int k = 0; k < 4; ++k) sm[k] += fmaxf(__uint_as_float(v[c + k]), 0.f);
             best += (sm[0] + sm[1]) + (sm[2] + sm[3]);
         }
     }
@@ -345,7 +305,7 @@ struct Epi {
                 float sm = 0.f;
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
-                    if ((cm >> c) & 1u) sm += fmaxf(__uint_as_float(v[c]) + q, 0.f);
+                    if ((cm >> c) & 1u) sm += fmaxf(__uint_as_float(v[c]), 0.f);
                 best += sm;
             }
             c0 = c1;
@@ -357,7 +317,66 @@ struct Epi {
     }
 };
 
-template <int KS, bool MAX>
+// 4 consecutive input dimensions [k0, k0 + 4) of row r of a [rows][d_in] matrix,
+// zero beyond d_in (vector load when d_in % 4 == 0: rows are then 16-byte aligned)
+__device__ __forceinline__ float4 ld_in4(const float* __restrict__ M, int64_t r, int d_in, int k0, bool vec) {
+    const float* p = M + r * d_in + k0;
+    if (vec) return k0 < d_in ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    return make_float4(k0 < d_in ? __ldg(p) : 0.f, k0 + 1 < d_in ? __ldg(p + 1) : 0.f,
+                       k0 + 2 < d_in ? __ldg(p + 2) : 0.f, k0 + 3 < d_in ? __ldg(p + 3) : 0.f);
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+
+// The B-operand rows of edge slot e (tile row e) for s = x_u + x_v, dimensions
+// [ks*8, ks*8 + 8): 3xTF32 -> tf32 hi / lo (RNA); bf16 -> bf16 hi / lo (RN),
+// each written twice (K positions 0-7 and 8-15 of the K = 16 step).
+template <bool BF>
+__device__ __forceinline__ void store_split(uint32_t bh, uint32_t bl, int e, const float4& s0, const float4& s1) {
+    const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    if constexpr (!BF) {
+        uint32_t hi[8], lo[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float h = tf32_rna(sv[k]);
+            hi[k] = __float_as_uint(h);
+            lo[k] = __float_as_uint(tf32_rna(sv[k] - h));
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            sts128(bh + tile_off(e, 4 * c), hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+            sts128(bl + tile_off(e, 4 * c), lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+        }
+    } else {
+        uint32_t hp[4], lp[4];
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+            const uint32_t h0 = bf16_bits(sv[k]), h1 = bf16_bits(sv[k + 1]);
+            const uint32_t l0 = bf16_bits(sv[k] - bf16_val(h0)), l1 = bf16_bits(sv[k + 1] - bf16_val(h1));
+            hp[k / 2] = h0 | (h1 << 16);
+            lp[k / 2] = l0 | (l1 << 16);
+        }
+        // K-major bf16: 8 elements per 16-byte core-matrix row; K chunk 1 at +128 B
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            sts128(bh + tile_off(e, 4 * c), hp[0], hp[1], hp[2], hp[3]);
+            sts128(bl + tile_off(e, 4 * c), lp[0], lp[1], lp[2], lp[3]);
+        }
+    }
+}
+
+// instruction descriptor: kind::f16 with bf16 A/B, D f32, K-major, N = NT, M = MT
+constexpr uint32_t IDESC_BF16 = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NT >> 3) << 17) |
+                                (uint32_t(MT >> 4) << 24);
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC_BF16), "r"(accumulate));
+}
+
+template <int KS, bool MAX, bool BF>
 __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const __grid_constant__ Args A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem<KS>& S = *reinterpret_cast<Smem<KS>*>(smem_raw);
@@ -375,15 +394,24 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         for (int b2 = 0; b2 < NBUF; ++b2) { mbar_init(&S.tfull[b2], 1); mbar_init(&S.tempty[b2], NEPI * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // stage W^T (A operand) as tf32 hi / lo: row = feature, k = input dim
+    // stage the A operand (W^T: row = feature, k = input dim), once
     for (int idx = tid; idx < KS * MT * 8; idx += THREADS) {
         const int ks = idx / (MT * 8), rem = idx % (MT * 8), r = rem / 8, k = rem % 8;
         const int kk = ks * 8 + k, col = mbase + r;
         const float w = (kk < A.d_in && col < A.d2) ? A.W[int64_t(kk) * A.d2 + col] : 0.f;
-        const float hi = tf32_rna(w);
-        const float lo = tf32_rna(w - hi);
-        *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(S.a_hi[ks]) + tile_off(r, k)) = hi;
-        *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(S.a_lo[ks]) + tile_off(r, k)) = lo;
+        if constexpr (!BF) {
+            const float hi = tf32_rna(w);
+            *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(S.a_hi[ks]) + tile_off(r, k)) = hi;
+            *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(S.a_lo[ks]) + tile_off(r, k)) = tf32_rna(w - hi);
+        } else {
+            // [w_hi | w_lo]: element (r, k) of the K = 16 bf16 tile sits at byte
+            // (r>>3)*256 + (k>>3)*128 + (r&7)*16 + (k&7)*2
+            const uint32_t hb = bf16_bits(w), lb = bf16_bits(w - bf16_val(hb));
+            unsigned char* base = reinterpret_cast<unsigned char*>(S.a_hi[ks]);
+            const uint32_t o = uint32_t((r >> 3) * 256 + (r & 7) * 16 + k * 2);
+            *reinterpret_cast<uint16_t*>(base + o) = uint16_t(hb);
+            *reinterpret_cast<uint16_t*>(base + o + 128) = uint16_t(lb);
+        }
     }
     fence_async_smem();
     if (warp == MMA_WARP) {
@@ -398,19 +426,23 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
     const int64_t r_lo = S.r_lo, r_hi = S.r_hi;
     const int64_t E0 = __ldg(A.row_ptr + r_lo), E1 = __ldg(A.row_ptr + r_hi);
     const int ntiles = int((E1 - E0 + NT - 1) / NT);
+    const int nnz_cta = int(E1 - E0);
 
     if (warp >= MMA_WARP + 1) {
-        // ------------------------------------------------ producers: gather pre-split x_u rows into B
-        // x_u was split once into tf32 hi / lo rows of KS*8 floats (mlp_split_kernel,
-        // workspace).  Per edge the producer issues 2*KS*2 cp.async 16-byte copies
-        // straight into the K-major canonical tile positions (no register staging,
-        // no per-edge dependent waits); cp.async.mbarrier.arrive signals full[s]
-        // when this thread's copies land.
-        constexpr int EPT = NT / (NPROD * 32);
-        const int pt = tid - (MMA_WARP + 1) * 32;          // 0 .. NPROD*32-1
-        const int rowf = KS * 8;                            // floats per pre-split row
-        // indices are prefetched PF tiles ahead (a register ring, static slots via
-        // the unrolled-by-PF loop): the col_idx round trip (~1 us) would otherwise
+        // ------------------------------------------------ producer: s_e = x_u + x_v -> B operand
+        constexpr int EPT = NT / (NPROD * 32);          // edge slots per lane per tile
+        const int pt = tid - (MMA_WARP + 1) * 32;       // 0 .. NPROD*32-1
+        const bool vec = (A.d_in % 4) == 0;
+        // destination rows: a window of 32 consecutive rows [wb, wb + 32) whose
+        // ends (relative to E0) lane j holds in wend; rows >= r_hi end at INT_MAX
+        int wb = int(r_lo);
+        auto load_window = [&](int base) {
+            const int64_t rr = int64_t(base) + lane;
+            return rr < r_hi ? int(__ldg(A.row_ptr + rr + 1) - E0) : 0x7fffffff;
+        };
+        int wend = load_window(wb);
+        // neighbour indices are prefetched PF tiles ahead (a register ring, static
+        // slots via the unrolled-by-PF loop): the col_idx round trip would otherwise
         // bound the pipeline at one tile per load latency
         constexpr int PF = 4;
         int u_pf[PF][EPT];
@@ -426,51 +458,91 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         for (int k = 0; k < PF; ++k) load_idx(k, u_pf[k]);
         auto tile = [&](int t, int (&u_cur)[EPT]) {
             const int s = t % STAGES;
-            mbar_wait_backoff(&S.empty[s], ((t / STAGES) & 1) ^ 1, A.backoff_ns);
+            // the destination row of each edge slot (padded slots: the CTA's last row)
+            int vrow[EPT];
+            bool done[EPT];
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                vrow[i] = int(r_hi) - 1;
+                done[i] = t * NT + pt + i * NPROD * 32 >= nnz_cta;
+            }
+            for (;;) {
+                const int last = __shfl_sync(0xffffffffu, wend, 31);
+#pragma unroll
+                for (int i = 0; i < EPT; ++i) {
+                    const int pe = t * NT + pt + i * NPROD * 32;
+                    int lo = 0;   // number of window rows ending at or before pe (ends ascend)
+#pragma unroll
+                    for (int step = 16; step >= 1; step >>= 1)
+                        if (__shfl_sync(0xffffffffu, wend, lo + step - 1) <= pe) lo += step;
+                    if (!done[i] && pe < last) {
+                        vrow[i] = wb + lo;
+                        done[i] = true;
+                    }
+                }
+                bool all = true;
+#pragma unroll
+                for (int i = 0; i < EPT; ++i) all = all && done[i];
+                if (__all_sync(0xffffffffu, all)) break;
+                wb += 32;   // some edge lies beyond the window: slide it
+                wend = load_window(wb);
+            }
+            float4 sv[EPT][KS][2];
+#pragma unroll
+            for (int i = 0; i < EPT; ++i)
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int k0 = ks * 8 + c * 4;
+                        const float4 a = ld_in4(A.X, u_cur[i], A.d_in, k0, vec);
+                        const float4 b = ld_in4(A.Xd, vrow[i], A.d_in, k0, vec);
+                        sv[i][ks][c] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+                    }
+            mbar_wait_backoff(&S.empty[s], ((t / STAGES) & 1) ^ 1, BACKOFF_NS);
 #pragma unroll
             for (int i = 0; i < EPT; ++i) {
                 const int e = pt + i * NPROD * 32;
-                const float* xh = A.Xhi + int64_t(u_cur[i]) * rowf;
-                const float* xl = A.Xlo + int64_t(u_cur[i]) * rowf;
 #pragma unroll
-                for (int ks = 0; ks < KS; ++ks) {
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        const uint32_t off = tile_off(e, c * 4);
-                        if (!(A.dbg & 2)) {
-                            cp_async16(smem_u32(S.b_hi[s][ks]) + off, xh + ks * 8 + c * 4);
-                            cp_async16(smem_u32(S.b_lo[s][ks]) + off, xl + ks * 8 + c * 4);
-                        }
-                    }
-                }
+                for (int ks = 0; ks < KS; ++ks)
+                    store_split<BF>(smem_u32(S.b_hi[s][ks]), smem_u32(S.b_lo[s][ks]), e, sv[i][ks][0], sv[i][ks][1]);
             }
-            cp_async_arrive(&S.full[s]);
+            fence_async_smem();        // generic-proxy stores -> tensor-core (async proxy) reads
+            mbar_arrive(&S.full[s]);
             load_idx(t + PF, u_cur);   // refill this slot PF tiles ahead
+            // keep the window at the row of this tile's last edge (rows only move forward)
+            const int wlast = __shfl_sync(0xffffffffu, vrow[EPT - 1], 31);
+            if (wlast >= wb + 32 - 1 && wlast < r_hi) {   // the next tile starts at or beyond the window's end
+                wb = wlast;
+                wend = load_window(wb);
+            }
         };
         for (int t0 = 0; t0 < ntiles; t0 += PF) {
 #pragma unroll
             for (int k = 0; k < PF; ++k)
                 if (t0 + k < ntiles) tile(t0 + k, u_pf[k]);
         }
-        asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp == MMA_WARP) {
         // ------------------------------------------------ MMA issuer (one thread)
         if (lane == 0) {
             for (int t = 0; t < ntiles; ++t) {
                 const int s = t % STAGES, b = t % NBUF;
-                mbar_wait_backoff(&S.full[s], (t / STAGES) & 1, A.backoff_ns);
-                fence_async_smem();   // cp.async (generic proxy) writes -> tensor-core (async proxy) reads
-                mbar_wait_backoff(&S.tempty[b], ((t / NBUF) & 1) ^ 1, A.backoff_ns);
+                mbar_wait_backoff(&S.full[s], (t / STAGES) & 1, BACKOFF_NS);
+                fence_async_smem();
+                mbar_wait_backoff(&S.tempty[b], ((t / NBUF) & 1) ^ 1, BACKOFF_NS);
                 tc_fence_after();
                 const uint32_t d = tmem + uint32_t(b * NT);
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) {
                     const uint64_t ah = smem_desc(smem_u32(S.a_hi[ks])), al = smem_desc(smem_u32(S.a_lo[ks]));
                     const uint64_t bh = smem_desc(smem_u32(S.b_hi[s][ks])), bl = smem_desc(smem_u32(S.b_lo[s][ks]));
-                    if (!(A.dbg & 4)) {
+                    if constexpr (!BF) {
                         mma_tf32(d, ah, bh, ks > 0 ? 1u : 0u);
                         mma_tf32(d, ah, bl, 1u);
                         mma_tf32(d, al, bh, 1u);
+                    } else {
+                        mma_bf16(d, ah, bh, ks > 0 ? 1u : 0u);   // s_hi (w_hi + w_lo)
+                        mma_bf16(d, ah, bl, 1u);                 // s_lo (w_hi + w_lo)
                     }
                 }
                 mma_commit(&S.empty[s]);
@@ -497,7 +569,6 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         // register instead of being rematerialised from %tid every chunk
         uint32_t lane_base;
         asm volatile("mov.b32 %0, %1;" : "=r"(lane_base) : "r"(tmem + (uint32_t(warp * 32) << 16)));
-        const int nnz_cta = int(E1 - E0);
         // a warp whose 32 features all lie beyond d2 (d2 < 128: the W^T rows are
         // zero padding) only keeps the TMEM buffers cycling: no tcgen05.ld -- the
         // TMEM reads are this kernel's bound
@@ -505,7 +576,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         if (!warp_active) {
             for (int t = 0; t < ntiles; ++t) {
                 const int b = t % NBUF;
-                mbar_wait_backoff(&S.tfull[b], (t / NBUF) & 1, A.backoff_ns);
+                mbar_wait_backoff(&S.tfull[b], (t / NBUF) & 1, BACKOFF_NS);
                 tc_fence_after();
                 tc_fence_before();
                 mbar_arrive(&S.tempty[b]);
@@ -513,8 +584,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
         }
         for (int t = 0; warp_active && t < ntiles; ++t) {
             const int b = t % NBUF;
-            if (A.epi_backoff_ns > 0) mbar_wait_backoff(&S.tfull[b], (t / NBUF) & 1, A.epi_backoff_ns);
-            else mbar_wait(&S.tfull[b], (t / NBUF) & 1);
+            mbar_wait(&S.tfull[b], (t / NBUF) & 1);
             tc_fence_after();
             const int tb = t * NT;                       // relative to E0
             const int nv_tile = min(NT, nnz_cta - tb);
@@ -541,27 +611,12 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
     }
 }
 
-template <int KS, bool MAX>
+template <int KS, bool MAX, bool BF>
 fg_status launch_ks(const Args& A, cudaStream_t st) {
     const int smem = int(sizeof(Smem<KS>)) + 1024;
     const int smem_min = 56 * 1024;                              // bounds residency (TMEM columns)
     const int smem_req = smem < smem_min ? smem_min : smem;
-    {   // pre-split X into tf32 hi / lo rows (the producers' cp.async source)
-        const int64_t tot = A.n_src * KS * 8;
-        if (tot > 0)
-            mlp_split_kernel<KS><<<unsigned((tot + 255) / 256), 256, 0, st>>>(
-                A.X, A.n_src, A.d_in, const_cast<float*>(A.Xhi), const_cast<float*>(A.Xlo));
-        fg_status s = fgk::check_launch("mlp_split_kernel");
-        if (s != FG_OK) return s;
-    }
-    {   // q_v = x_v W per destination row (the epilogue's per-row term)
-        if (A.n_dst > 0 && A.d2 > 0)
-            mlp_q_kernel<<<dim3(unsigned((A.n_dst + Q_ROWS - 1) / Q_ROWS), unsigned((A.d2 + 127) / 128)), 128, 0, st>>>(
-                A.Xd, A.W, A.n_dst, A.d_in, A.d2, const_cast<float*>(A.Q));
-        fg_status s = fgk::check_launch("mlp_q_kernel");
-        if (s != FG_OK) return s;
-    }
-    auto kfn = mlp_tcgen05_kernel<KS, MAX>;
+    auto kfn = mlp_tcgen05_kernel<KS, MAX, BF>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_req);
     // the whole unified L1/smem for shared memory: without it the driver picks a
     // carveout that fits ONE 100 KB CTA per SM and the persistent grid runs as two waves
@@ -575,35 +630,20 @@ fg_status launch_ks(const Args& A, cudaStream_t st) {
     return fgk::check_launch("mlp_tcgen05_kernel");
 }
 
+template <int KS, bool BF>
+fg_status launch_red(const Args& A, bool mx, cudaStream_t st) {
+    return mx ? launch_ks<KS, true, BF>(A, st) : launch_ks<KS, false, BF>(A, st);
+}
+
 }  // namespace
 
 namespace fgk {
 
-// workspace: tf32 hi / lo rows of X (2 x n_src x KS*8 floats) + Q (n_dst x d2 floats)
-size_t mlp_workspace_bytes(int64_t n_src, int64_t n_dst, int d_in, int d2) {
-    const int64_t ks = (d_in + 7) / 8;
-    return size_t(2 * n_src * ks * 8 * 4 + 256 + n_dst * int64_t(d2) * 4 + 256);
-}
-
 fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, const float* X, const float* W,
                                   int d_in, const float* X_dst, float* out, int32_t* arg_u, int32_t* arg_e,
-                                  void* workspace, cudaStream_t st) {
+                                  bool bf16_split, cudaStream_t st) {
     Args A;
-    const int64_t ksz = (d_in + 7) / 8;
-    float* ws = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
-    A.Xhi = ws;
-    A.Xlo = ws + g->n_src * ksz * 8;
-    A.Q = reinterpret_cast<const float*>(
-        (reinterpret_cast<uintptr_t>(A.Xlo + g->n_src * ksz * 8) + 255) & ~uintptr_t(255));
     A.n_src = g->n_src;
-    {
-        const char* d = getenv("FG_MLP_DBG");
-        A.dbg = d ? atoi(d) : 0;
-        const char* bo = getenv("FG_MLP_BACKOFF_NS");
-        A.backoff_ns = bo ? atoi(bo) : 128;
-        const char* eb = getenv("FG_MLP_EPI_BACKOFF_NS");
-        A.epi_backoff_ns = eb ? atoi(eb) : 0;
-    }
     A.row_ptr = g->row_ptr;
     A.col_idx = g->col_idx;
     A.eid = g->eid;
@@ -619,11 +659,19 @@ fg_status launch_spmm_mlp_tcgen05(const fg_graph* g, fg_reduce_op red, int d2, c
     A.d2 = d2;
     const bool mx = red == FG_REDUCE_MAX;
     const int ks = (d_in + 7) / 8;
+    if (bf16_split) {
+        switch (ks) {
+            case 1: return launch_red<1, true>(A, mx, st);
+            case 2: return launch_red<2, true>(A, mx, st);
+            case 3: return launch_red<3, true>(A, mx, st);
+            default: return launch_red<4, true>(A, mx, st);
+        }
+    }
     switch (ks) {
-        case 1: return mx ? launch_ks<1, true>(A, st) : launch_ks<1, false>(A, st);
-        case 2: return mx ? launch_ks<2, true>(A, st) : launch_ks<2, false>(A, st);
-        case 3: return mx ? launch_ks<3, true>(A, st) : launch_ks<3, false>(A, st);
-        default: return mx ? launch_ks<4, true>(A, st) : launch_ks<4, false>(A, st);
+        case 1: return launch_red<1, false>(A, mx, st);
+        case 2: return launch_red<2, false>(A, mx, st);
+        case 3: return launch_red<3, false>(A, mx, st);
+        default: return launch_red<4, false>(A, mx, st);
     }
 }
 

@@ -504,12 +504,11 @@ static fg_status launch_sddmm_core(const fg_graph* g, int H, int D, const float*
     // columns [k*T4, (k+1)*T4) and accumulates into out (fixed pass order:
     // deterministic).  Each pass gathers from an L2-resident slice of X.
     {
-        const int64_t budget = fgk::l2_tile_budget();
-        // opt-in (FG_SDDMM_L2_TILE=1): measured slower than one pass on reddit F=512
+        const int64_t budget = fgk::l2_tile_budget(g);
+        // opt-in (FG_TUNE_SDDMM_L2_TILE): measured slower than one pass on reddit F=512
         // (25.8 ms at 64 MB vs 21.3 untiled, even with the running sums prefetched;
         // the narrow-group per-edge reduction, not the traffic, is the limit)
-        const char* on = getenv("FG_SDDMM_L2_TILE");
-        if (!xb && on && on[0] == '1' && H == 1 && budget > 0 && g->n_src * int64_t(F4) * 16 > budget) {
+        if (!xb && g->tune.sddmm_l2_tile && H == 1 && budget > 0 && g->n_src * int64_t(F4) * 16 > budget) {
             int t4 = 32;
             while (t4 > 1 && g->n_src * int64_t(t4) * 16 > budget) t4 /= 2;
             A.tile4 = t4;
@@ -547,24 +546,18 @@ static fg_status launch_sddmm_core(const fg_graph* g, int H, int D, const float*
     // unsegmented vs 3.61 ms in 48 MB segments, 119 MB (F = 128) ties, and the
     // 238 / 477 MB cases (H = 8 D = 32, H = 1 F = 512) prefer 48 MB segments over
     // 96 MB ones (9.39 vs 9.79 ms, 16.46 vs 16.72 ms).
-    {
-        const char* mb = getenv("FG_SDDMM_SEG_MB");
-        const char* mn = getenv("FG_SDDMM_SEG_MIN_MB");
-        const int64_t budget = int64_t(mb ? atoi(mb) : 48) << 20;
-        const int64_t min_x = int64_t(mn ? atoi(mn) : 96) << 20;
-        const int64_t row_bytes = int64_t(F4) * (xb ? 8 : 16);
-        if (A.tile4 == 0 && budget > 0 && g->n_src * row_bytes > std::max(budget, min_x)) {
-            int64_t seg_rows = budget / row_bytes;
-            seg_rows = seg_rows < 32 ? 32 : seg_rows;
-            const fg_graph::SegUnits* su = nullptr;
-            fg_status r = fgk::get_seg_units(const_cast<fg_graph*>(g), seg_rows, g->unit_chunk, st, &su);
-            if (r != FG_OK) return r;
+    // The tables are built by fg_graph_prepare(g, row_bytes) (synchronous, per
+    // topology); a width that was not prepared runs the unsegmented traversal --
+    // this launch path never allocates or synchronises.
+    if (A.tile4 == 0) {
+        const int64_t seg_rows = fgk::sddmm_seg_rows(g, int64_t(F4) * (xb ? 8 : 16));
+        const fg_graph::SegUnits* su = seg_rows ? fgk::find_seg_units(g, seg_rows) : nullptr;
+        if (su) {
             A.unit_row = su->row;
             A.unit_p0 = su->p0;
             A.unit_p1 = su->p1;
             A.n_units = su->n_units;
-            const char* pe = getenv("FG_SDDMM_PERSIST");   // CTAs per SM (default: the occupancy)
-            A.persistent = pe ? atoi(pe) : -1;
+            A.persistent = int(g->tune.sddmm_persist);   // CTAs per SM (-1: the occupancy)
         }
     }
     int G = 32, NV = 4;
@@ -662,8 +655,7 @@ fg_status launch_sddmm(const fg_graph* g, int H, int D, const float* X, const fl
             while (G < F4) G *= 2;
         }
         const int B = G >= 4 ? 32 : 8;
-        const char* on = getenv("FG_SDDMM_L2_TILE");
-        const bool tiled = !Xbf16 && on && on[0] == '1' && H == 1;
+        const bool tiled = !Xbf16 && g->tune.sddmm_l2_tile && H == 1;
         if (H * B > 32 * G || tiled) {   // (the bf16 pair kernels stage whenever this holds)
             fg_status s = launch_sddmm_core(g, H, D, X, Y, out, st, Xbf16, Ybf16, nullptr);
             if (s != FG_OK) return s;

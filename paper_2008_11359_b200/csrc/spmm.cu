@@ -71,7 +71,7 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     int G = 32, NV = 4;
     int F4 = A.F4;
     {
-        const int64_t budget = fgk::l2_tile_budget(red == FG_REDUCE_MAX || red == FG_REDUCE_MIN);
+        const int64_t budget = fgk::l2_tile_budget(g, red == FG_REDUCE_MAX || red == FG_REDUCE_MIN);
         // copy_u only: u_mul_e re-reads E (m x H floats) on every pass, measured slower
         // at every budget (reddit H=8 D=32: 9.1-10.1 ms untiled vs 12.2-43.6 ms tiled)
         if (msg == FG_MSG_COPY_U && budget > 0 && g->n_src * int64_t(F4) * chunk_bytes > budget) {
@@ -114,13 +114,15 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
         // 7.8 ms (a group per long row keeps more gathers in flight than a CTA per
         // row); a constant 4096 cost the short F = 32 kernels their tail (rand-100K
         // 0.37 -> 0.52 ms: a 4,000-edge row on one 8-lane group outlasts the rest).
-        const char* hv = getenv("FG_SPMM_HEAVY_DEG");
+        // The edge count is FG_TUNE_BALANCE_NNZ when set: the sharding code sets the
+        // whole graph's, so every shard splits rows exactly as the unsharded op.
         int64_t thr;
-        if (hv) {
-            thr = std::max<int64_t>(1, atoll(hv));
+        if (g->tune.spmm_heavy_deg > 0) {
+            thr = g->tune.spmm_heavy_deg;
         } else {
             const int64_t groups = int64_t(fgk::num_sms()) * (2048 / G);
-            thr = std::min<int64_t>(4096, std::max<int64_t>(1024, g->nnz / std::max<int64_t>(1, groups)));
+            const int64_t m = g->tune.balance_nnz > 0 ? g->tune.balance_nnz : g->nnz;
+            thr = std::min<int64_t>(4096, std::max<int64_t>(1024, m / std::max<int64_t>(1, groups)));
         }
         A.n_heavy = rows_with_degree_at_least(g, thr);
     }

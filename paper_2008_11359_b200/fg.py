@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -25,10 +26,16 @@ REDUCE = {"sum": 0, "max": 1, "min": 2, "mean": 3}
 EDGE = {"u_dot_v": 0, "u_add_v": 1, "u_sub_v": 2, "u_mul_v": 3}
 
 # exported symbols declared in include/fg.h (checked by tests/test_abi.py)
-SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
+SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_graph_prepare", "fg_graph_tune",
+           "fg_graph_get_tune", "fg_spmm_workspace_size", "fg_spmm",
            "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
            "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
-           "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_sddmm_emul", "fg_dist_spmm", "fg_dist_sddmm", "fg_status_string", "fg_last_error", "fg_abi_version"]
+           "fg_comm_info", "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_sddmm_emul", "fg_dist_spmm", "fg_dist_sddmm", "fg_status_string", "fg_last_error", "fg_abi_version"]
+
+
+# fg_tune_key (include/fg.h)
+TUNE = {"l2_tile_mb": 0, "spmm_heavy_deg": 1, "balance_nnz": 2, "sddmm_seg_mb": 3, "sddmm_seg_min_mb": 4,
+        "sddmm_persist": 5, "sddmm_l2_tile": 6, "sddmm_dot": 7, "gat_heavy_deg": 8, "mlp_impl": 9, "hybrid": 10}
 
 
 class FGError(RuntimeError):
@@ -58,6 +65,9 @@ def lib() -> ctypes.CDLL:
     L.fg_graph_create.argtypes = [i64, i64, i64, vp, vp, vp, i32, vp, ctypes.POINTER(vp)]
     L.fg_graph_destroy.argtypes = [vp]
     L.fg_graph_info.argtypes = [vp, ctypes.POINTER(GraphInfo)]
+    L.fg_graph_prepare.argtypes = [vp, i64, vp]
+    L.fg_graph_tune.argtypes = [vp, i32, i64]
+    L.fg_graph_get_tune.argtypes = [vp, i32, ctypes.POINTER(i64)]
     L.fg_spmm_workspace_size.argtypes = [vp, i32, i32, i32, i32, i32, ctypes.POINTER(sz)]
     L.fg_spmm.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]
     L.fg_sddmm.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
@@ -75,11 +85,13 @@ def lib() -> ctypes.CDLL:
     L.fg_comm_unique_id.argtypes = [vp]
     L.fg_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.fg_comm_destroy.argtypes = [vp]
+    L.fg_comm_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.fg_allgather_rows.argtypes = [vp, vp, i64, vp, vp, vp]
-    for f in ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_spmm_workspace_size", "fg_spmm",
+    for f in ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_graph_prepare", "fg_graph_tune",
+              "fg_graph_get_tune", "fg_spmm_workspace_size", "fg_spmm",
               "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
               "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
-              "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_sddmm_emul", "fg_dist_spmm",
+              "fg_comm_info", "fg_allgather_rows", "fg_spmm_x16", "fg_sddmm_x16", "fg_sddmm_emul", "fg_dist_spmm",
               "fg_dist_sddmm"]:
         getattr(L, f).restype = i32
     L.fg_status_string.argtypes = [i32]
@@ -119,6 +131,24 @@ def _dev(t, dtype, name):
     return t
 
 
+def _head_dim(F: int, H: int) -> int:
+    """D = F / H; F must split into H heads exactly (else the library would read
+    rows with the wrong stride)."""
+    if H < 1 or F % H != 0:
+        raise FGError(FG_ESHAPE, f"feature width {F} does not split into H={H} heads")
+    return F // H
+
+
+def _out(t, shape, dtype, name):
+    """A caller-supplied output tensor: CUDA, dtype, contiguous and exactly `shape`."""
+    if t is None:
+        return None
+    t = _dev(t, dtype, name)
+    if tuple(t.shape) != tuple(shape) and not (t.numel() == int(np.prod(shape)) and t.dim() == 1):
+        raise FGError(FG_ESHAPE, f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return t
+
+
 class Graph:
     """fg_graph handle (featgraph.spmat).  Borrows row_ptr/col_idx/eid: the
     tensors are kept referenced by this object."""
@@ -151,6 +181,23 @@ class Graph:
         _check(lib().fg_graph_transpose(self.handle, _stream(stream), ctypes.byref(h)), "fg_graph_transpose")
         return Graph._from_handle(h, self.n_src, self.n_dst, self.nnz)
 
+    def prepare(self, row_bytes: int, stream=None) -> "Graph":
+        """fg_graph_prepare: build the source-segment table of the gSDDMM traversal
+        for gathered rows of `row_bytes` bytes (synchronous; no-op when that width
+        is not segmented).  Call before timing / CUDA-graph capture."""
+        _check(lib().fg_graph_prepare(self.handle, int(row_bytes), _stream(stream)), "fg_graph_prepare")
+        return self
+
+    def tune(self, key: str, value: int) -> "Graph":
+        """fg_graph_tune: set one launch knob of this handle (include/fg.h fg_tune_key)."""
+        _check(lib().fg_graph_tune(self.handle, TUNE[key], int(value)), f"fg_graph_tune({key})")
+        return self
+
+    def get_tune(self, key: str) -> int:
+        v = ctypes.c_int64(0)
+        _check(lib().fg_graph_get_tune(self.handle, TUNE[key], ctypes.byref(v)), f"fg_graph_get_tune({key})")
+        return int(v.value)
+
     def info(self) -> GraphInfo:
         inf = GraphInfo()
         _check(lib().fg_graph_info(self.handle, ctypes.byref(inf)), "fg_graph_info")
@@ -168,20 +215,6 @@ class Graph:
             pass
 
 
-def _workspace(g: Graph, msg: int, red: int, H: int, D: int, d_in: int, device):
-    """Scratch of fg_spmm_workspace_size bytes, cached on the graph object
-    (stream-ordered reuse: calls on one stream never overlap)."""
-    n = ctypes.c_size_t(0)
-    _check(lib().fg_spmm_workspace_size(g.handle, msg, red, H, D, d_in, ctypes.byref(n)), "fg_spmm_workspace_size")
-    if n.value == 0:
-        return None, 0
-    buf = getattr(g, "_ws", None)
-    if buf is None or buf.numel() < n.value:
-        buf = torch.empty(n.value, dtype=torch.uint8, device=device)
-        g._ws = buf
-    return buf, buf.numel()
-
-
 def spmm(g: Graph, msg: str, reduce: str, X: torch.Tensor, *, H: int = 1, E: torch.Tensor | None = None,
          W: torch.Tensor | None = None, X_dst: torch.Tensor | None = None, out: torch.Tensor | None = None,
          arg_u: torch.Tensor | bool | None = None, arg_e: torch.Tensor | bool | None = None, stream=None):
@@ -195,15 +228,25 @@ def spmm(g: Graph, msg: str, reduce: str, X: torch.Tensor, *, H: int = 1, E: tor
     if msg == "copy_e":
         d_in = 0
         F = E.numel() // max(E.shape[0], 1) if E.dim() > 1 else 1
-        H_, D = H, F // H
+        H_, D = H, _head_dim(F, H)
     elif msg == "mlp":
         d_in, F = W.shape
         H_, D = 1, F
     else:
         d_in = 0
         F = X.numel() // max(X.shape[0], 1) if X.dim() > 1 else 1
-        H_, D = H, F // H
+        H_, D = H, _head_dim(F, H)
+    if X is not None and msg != "copy_e" and X.shape[0] < g.n_src:
+        raise FGError(FG_ESHAPE, f"X has {X.shape[0]} rows, the graph has {g.n_src} sources")
+    if msg == "mlp":
+        if X.numel() != X.shape[0] * d_in or (X_dst is not None and X_dst.numel() != g.n_dst * d_in):
+            raise FGError(FG_ESHAPE, f"mlp: X / X_dst rows must have d_in={d_in} features")
+    elif msg in ("u_mul_e", "u_add_e") and E is not None and E.numel() != g.nnz * H_:
+        raise FGError(FG_ESHAPE, f"E has {E.numel()} elements, expected nnz*H = {g.nnz * H_}")
+    elif msg == "copy_e" and E is not None and E.shape[0] != g.nnz:
+        raise FGError(FG_ESHAPE, f"E has {E.shape[0]} rows, expected nnz = {g.nnz}")
     device = (X if X is not None else E).device
+    out = _out(out, (g.n_dst, F), torch.float32, "out")
     if out is None:
         out = torch.empty((g.n_dst, F), dtype=torch.float32, device=device)
     want = reduce in ("max", "min") and (arg_u is not None or arg_e is not None)
@@ -211,11 +254,10 @@ def spmm(g: Graph, msg: str, reduce: str, X: torch.Tensor, *, H: int = 1, E: tor
         arg_u = torch.empty((g.n_dst, F), dtype=torch.int32, device=device)
     if arg_e is True:
         arg_e = torch.empty((g.n_dst, F), dtype=torch.int32, device=device)
-    arg_u = arg_u if isinstance(arg_u, torch.Tensor) else None
-    arg_e = arg_e if isinstance(arg_e, torch.Tensor) else None
-    ws, ws_bytes = _workspace(g, MSG[msg], REDUCE[reduce], H_, D, d_in, device)
+    arg_u = _out(arg_u, (g.n_dst, F), torch.int32, "arg_u") if isinstance(arg_u, torch.Tensor) else None
+    arg_e = _out(arg_e, (g.n_dst, F), torch.int32, "arg_e") if isinstance(arg_e, torch.Tensor) else None
     _check(lib().fg_spmm(g.handle, MSG[msg], REDUCE[reduce], H_, D, _ptr(X), _ptr(E), _ptr(W), d_in, _ptr(X_dst),
-                         _ptr(out), _ptr(arg_u), _ptr(arg_e), _ptr(ws), ws_bytes, _stream(stream)),
+                         _ptr(out), _ptr(arg_u), _ptr(arg_e), None, 0, _stream(stream)),
            f"fg_spmm({msg},{reduce})")
     if want:
         return out, arg_u, arg_e
@@ -226,6 +268,7 @@ def _spmm_x16(g, msg, reduce, X, *, H, E, out, arg_u, arg_e, stream):
     X = _dev(X, torch.bfloat16, "X")
     E = _dev(E, torch.float32, "E")
     F = X.numel() // max(X.shape[0], 1) if X.dim() > 1 else 1
+    out = _out(out, (g.n_dst, F), torch.float32, "out")
     if out is None:
         out = torch.empty((g.n_dst, F), dtype=torch.float32, device=X.device)
     want = reduce == "max" and (arg_u is not None or arg_e is not None)
@@ -233,9 +276,9 @@ def _spmm_x16(g, msg, reduce, X, *, H, E, out, arg_u, arg_e, stream):
         arg_u = torch.empty((g.n_dst, F), dtype=torch.int32, device=X.device)
     if arg_e is True:
         arg_e = torch.empty((g.n_dst, F), dtype=torch.int32, device=X.device)
-    arg_u = arg_u if isinstance(arg_u, torch.Tensor) else None
-    arg_e = arg_e if isinstance(arg_e, torch.Tensor) else None
-    _check(lib().fg_spmm_x16(g.handle, MSG[msg], REDUCE[reduce], H, F // H, _ptr(X), _ptr(E), _ptr(out),
+    arg_u = _out(arg_u, (g.n_dst, F), torch.int32, "arg_u") if isinstance(arg_u, torch.Tensor) else None
+    arg_e = _out(arg_e, (g.n_dst, F), torch.int32, "arg_e") if isinstance(arg_e, torch.Tensor) else None
+    _check(lib().fg_spmm_x16(g.handle, MSG[msg], REDUCE[reduce], H, _head_dim(F, H), _ptr(X), _ptr(E), _ptr(out),
                              _ptr(arg_u), _ptr(arg_e), _stream(stream)), f"fg_spmm_x16({msg},{reduce})")
     return (out, arg_u, arg_e) if want else out
 
@@ -255,33 +298,39 @@ def sddmm(g: Graph, X: torch.Tensor, Y: torch.Tensor | None = None, *, H: int = 
         Y = X if Y is None else _dev(Y, torch.float32, "Y")
         E = _dev(E, torch.float32, "E")
         F = X.numel() // max(X.shape[0], 1)
+        E = _out(E, (g.nnz, H), torch.float32, "E")
+        out = _out(out, (g.nnz, H), torch.float32, "out")
         if out is None:
             out = torch.empty((g.nnz, H), dtype=torch.float32, device=X.device)
-        _check(lib().fg_sddmm_emul(g.handle, H, F // H, _ptr(X), _ptr(Y), _ptr(E), _ptr(out), _stream(stream)),
+        _check(lib().fg_sddmm_emul(g.handle, H, _head_dim(F, H), _ptr(X), _ptr(Y), _ptr(E), _ptr(out), _stream(stream)),
                "fg_sddmm_emul")
         return out
     if X.dtype == torch.bfloat16:
         X = _dev(X, torch.bfloat16, "X")
         Y = X if Y is None else _dev(Y, torch.bfloat16, "Y")
         F = X.numel() // max(X.shape[0], 1)
+        out = _out(out, (g.nnz, H), torch.float32, "out")
         if out is None:
             out = torch.empty((g.nnz, H), dtype=torch.float32, device=X.device)
-        _check(lib().fg_sddmm_x16(g.handle, EDGE[op], H, F // H, _ptr(X), _ptr(Y), _ptr(out), _stream(stream)),
+        _check(lib().fg_sddmm_x16(g.handle, EDGE[op], H, _head_dim(F, H), _ptr(X), _ptr(Y), _ptr(out), _stream(stream)),
                "fg_sddmm_x16")
         return out
     X = _dev(X, torch.float32, "X")
     Y = X if Y is None else _dev(Y, torch.float32, "Y")
     F = X.numel() // max(X.shape[0], 1)
+    oshape = (g.nnz, H if op == "u_dot_v" else F)
+    out = _out(out, oshape, torch.float32, "out")
     if out is None:
-        out = torch.empty((g.nnz, H if op == "u_dot_v" else F), dtype=torch.float32, device=X.device)
-    _check(lib().fg_sddmm(g.handle, EDGE[op], H, F // H, _ptr(X), _ptr(Y), _ptr(out), _stream(stream)), "fg_sddmm")
+        out = torch.empty(oshape, dtype=torch.float32, device=X.device)
+    _check(lib().fg_sddmm(g.handle, EDGE[op], H, _head_dim(F, H), _ptr(X), _ptr(Y), _ptr(out), _stream(stream)), "fg_sddmm")
     return out
 
 
 def edge_softmax(g: Graph, scores: torch.Tensor, *, H: int = 1, out: torch.Tensor | None = None,
                  stream=None) -> torch.Tensor:
     """Per-destination softmax over in-edges, per head (GAT)."""
-    scores = _dev(scores, torch.float32, "scores")
+    scores = _out(scores, (g.nnz, H), torch.float32, "scores")
+    out = _out(out, (g.nnz, H), torch.float32, "out")
     if out is None:
         out = torch.empty_like(scores)
     _check(lib().fg_edge_softmax(g.handle, H, _ptr(scores), _ptr(out), _stream(stream)), "fg_edge_softmax")
@@ -295,13 +344,14 @@ def gat_attention(g: Graph, X: torch.Tensor, Y: torch.Tensor | None = None, *, H
     X = _dev(X, torch.float32, "X")
     Y = X if Y is None else _dev(Y, torch.float32, "Y")
     F = X.shape[1]
+    out = _out(out, (g.n_dst, F), torch.float32, "out")
     if out is None:
         out = torch.empty((g.n_dst, F), dtype=torch.float32, device=X.device)
     want = scores is not None and scores is not False
     if scores is True:
         scores = torch.empty((g.nnz, H), dtype=torch.float32, device=X.device)
-    sc = scores if isinstance(scores, torch.Tensor) else None
-    _check(lib().fg_gat_attention(g.handle, H, F // H, _ptr(X), _ptr(Y), _ptr(out), _ptr(sc), _stream(stream)),
+    sc = _out(scores, (g.nnz, H), torch.float32, "scores") if isinstance(scores, torch.Tensor) else None
+    _check(lib().fg_gat_attention(g.handle, H, _head_dim(F, H), _ptr(X), _ptr(Y), _ptr(out), _ptr(sc), _stream(stream)),
            "fg_gat_attention")
     return (out, sc) if want else out
 
@@ -316,7 +366,7 @@ def spmm_backward(g: Graph, gT: Graph | None, msg: str, reduce: str, dOut: torch
     dX = torch.empty((g.n_src, F), dtype=torch.float32, device=dOut.device) if want_dX else None
     dE = torch.empty((g.nnz, H), dtype=torch.float32, device=dOut.device) if want_dE else None
     _check(lib().fg_spmm_backward(g.handle, gT.handle if gT is not None else None, MSG[msg], REDUCE[reduce], H,
-                                  F // H, _ptr(_dev(X, torch.float32, "X")), _ptr(_dev(E, torch.float32, "E")),
+                                  _head_dim(F, H), _ptr(_dev(X, torch.float32, "X")), _ptr(_dev(E, torch.float32, "E")),
                                   _ptr(dOut), _ptr(_dev(arg_u, torch.int32, "arg_u")), _ptr(dX), _ptr(dE),
                                   _stream(stream)), "fg_spmm_backward")
     return dX, dE
@@ -329,7 +379,7 @@ def sddmm_backward(g: Graph, gT: Graph | None, X: torch.Tensor, Y: torch.Tensor,
     F = X.shape[1]
     dX = torch.empty((g.n_src, F), dtype=torch.float32, device=X.device) if want_dX else None
     dY = torch.empty((g.n_dst, F), dtype=torch.float32, device=X.device) if want_dY else None
-    _check(lib().fg_sddmm_backward(g.handle, gT.handle if gT is not None else None, EDGE["u_dot_v"], H, F // H,
+    _check(lib().fg_sddmm_backward(g.handle, gT.handle if gT is not None else None, EDGE["u_dot_v"], H, _head_dim(F, H),
                                    _ptr(X), _ptr(Y), _ptr(dS), _ptr(dX), _ptr(dY), _stream(stream)),
            "fg_sddmm_backward")
     return dX, dY
@@ -357,6 +407,12 @@ class Comm:
         _check(lib().fg_comm_init(buf, nranks, rank, ctypes.byref(h)), "fg_comm_init")
         self.handle, self.nranks, self.rank = h, nranks, rank
 
+    def nranks_nccl(self) -> int:
+        """The communicator size as NCCL reports it (fg_comm_info)."""
+        n, r = ctypes.c_int(0), ctypes.c_int(0)
+        _check(lib().fg_comm_info(self.handle, ctypes.byref(n), ctypes.byref(r)), "fg_comm_info")
+        return int(n.value)
+
     def allgather_rows(self, shard_offsets, X_local: torch.Tensor | None, X_full: torch.Tensor, stream=None):
         import numpy as np
         off = np.ascontiguousarray(np.asarray(shard_offsets, dtype=np.int64))
@@ -378,7 +434,7 @@ class Comm:
         if out is None:
             out = torch.empty((g_local.n_dst, F), dtype=torch.float32, device=X_full.device)
         _check(lib().fg_dist_spmm(g_local.handle, self.handle, ctypes.c_void_p(off.ctypes.data), MSG[msg],
-                                  REDUCE[reduce], H, F // H, _ptr(X_local), _ptr(X_full), _ptr(E), None, 0, None,
+                                  REDUCE[reduce], H, _head_dim(F, H), _ptr(X_local), _ptr(X_full), _ptr(E), None, 0, None,
                                   _ptr(out), None, None, None, 0, _stream(stream)), "fg_dist_spmm")
         return out
 
@@ -393,7 +449,7 @@ class Comm:
         if out is None:
             out = torch.empty((g_local.nnz, H), dtype=torch.float32, device=X_full.device)
         _check(lib().fg_dist_sddmm(g_local.handle, self.handle, ctypes.c_void_p(off.ctypes.data), EDGE["u_dot_v"], H,
-                                   F // H, _ptr(X_local), _ptr(X_full), _ptr(Y_local), _ptr(out), _stream(stream)),
+                                   _head_dim(F, H), _ptr(X_local), _ptr(X_full), _ptr(Y_local), _ptr(out), _stream(stream)),
                "fg_dist_sddmm")
         return out
 

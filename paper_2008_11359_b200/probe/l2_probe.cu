@@ -110,6 +110,127 @@ double gather_gbs(const float4* X, int64_t x_bytes, int F, int blocks_per_sm, fl
 
 double maxd(double a, double b) { return a > b ? a : b; }
 
+// ---------------------------------------------------------------- TMA bulk row gather
+// The same random whole-row gathers, moved by the TMA engine instead of LDG:
+// lanes of one producer warp each issue cp.async.bulk (one 16-byte-aligned row
+// per instruction) into a STAGES-deep shared-memory ring of RPS rows per stage,
+// completing on an mbarrier (expect_tx); NC consumer warps wait for each stage,
+// optionally read it from shared memory (READ: LDS.128 + add, as a gSDDMM /
+// gSpMM consumer would), and release it.  Measures whether TMA row gathers
+// beat the register-bound LDG gathers above.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+    asm volatile("{\n\t.reg .pred P1;\n\tW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@P1 bra D;\n\tbra W;\n\tD:\n\t}"
+                 ::"r"(smem_u32(b)), "r"(ph) : "memory");
+}
+
+template <int ROWB, int STAGES, int RPS, int NC, bool READ>
+__global__ void __launch_bounds__((NC + 1) * 32) tma_gather_kernel(const char* __restrict__ X, int nrows,
+                                                                   int iters, float* sink) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    unsigned char* buf = sm;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * RPS * ROWB);
+    uint64_t* empty = full + STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NC * 32); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    float acc = 0.f;
+    if (warp == 0) {
+        for (int it = 0; it < iters; ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
+                             "r"(RPS * ROWB) : "memory");
+            __syncwarp();
+            for (int r = lane; r < RPS; r += 32) {
+                const uint32_t row = hash32(uint32_t(blockIdx.x * 1000003u + it * RPS + r)) % uint32_t(nrows);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                    ::"r"(smem_u32(buf + (s * RPS + r) * ROWB)), "l"(X + int64_t(row) * ROWB), "r"(ROWB),
+                    "r"(smem_u32(&full[s])) : "memory");
+            }
+        }
+    } else {
+        const int ct = threadIdx.x - 32;
+        for (int it = 0; it < iters; ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&full[s], (it / STAGES) & 1);
+            if (READ) {
+                const float4* b4 = reinterpret_cast<const float4*>(buf + s * RPS * ROWB);
+                for (int i = ct; i < RPS * ROWB / 16; i += NC * 32) {
+                    const float4 v = b4[i];
+                    acc += v.x + v.y + v.z + v.w;
+                }
+            }
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+        }
+    }
+    if (acc == 1234.5f) sink[0] = acc;
+}
+
+template <int ROWB, int STAGES, int RPS, int NC, bool READ>
+double tma_gbs(const char* X, int64_t x_bytes, int ctas_per_sm, float* sink, bool verbose) {
+    const int nrows = int(x_bytes / ROWB);
+    const int smem = STAGES * RPS * ROWB + 2 * STAGES * 8;
+    auto k = tma_gather_kernel<ROWB, STAGES, RPS, NC, READ>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    const int blocks = g_sms * ctas_per_sm;
+    const int64_t total = (1600LL << 20) / ROWB;
+    const int iters = int((total / blocks + RPS - 1) / RPS);
+    const float ms = best_ms([&] { k<<<blocks, (NC + 1) * 32, smem>>>(X, nrows, iters, sink); }, 5);
+    const double gbs = double(blocks) * iters * RPS * ROWB / (ms * 1e-3) / 1e9;
+    if (verbose)
+        printf("tma-bulk rowB=%4d X=%4lld MiB stages=%d rows/stage=%d consumers=%d ctas/SM=%d read=%d: %.3f ms %.1f GB/s\n",
+               ROWB, (long long)(x_bytes >> 20), STAGES, RPS, NC, ctas_per_sm, int(READ), ms, gbs);
+    return gbs;
+}
+
+}  // namespace
+
+// TMA bulk-copy row gathers vs the LDG gathers (verbose sweep; tooling only).
+// out4: best GB/s for 2 KiB rows without / with the shared-memory read, and for
+// 512 B rows without / with it, all over a 64 MiB (L2-resident) X.
+extern "C" int fgprobe_tma(void* buf, int64_t buf_bytes, double* out4, int verbose) {
+    if (!buf || !out4 || buf_bytes < (96LL << 20)) return int(cudaErrorInvalidValue);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    const char* X = static_cast<const char*>(buf);
+    float* sink = reinterpret_cast<float*>(static_cast<char*>(buf) + buf_bytes - 64);
+    const int64_t xb = 64LL << 20;
+    double a = 0, b = 0, c = 0, d = 0;
+    a = maxd(a, tma_gbs<2048, 8, 4, 4, false>(X, xb, 2, sink, verbose));
+    a = maxd(a, tma_gbs<2048, 8, 4, 4, false>(X, xb, 3, sink, verbose));
+    a = maxd(a, tma_gbs<2048, 4, 8, 4, false>(X, xb, 3, sink, verbose));
+    a = maxd(a, tma_gbs<2048, 12, 4, 2, false>(X, xb, 2, sink, verbose));
+    b = maxd(b, tma_gbs<2048, 8, 4, 4, true>(X, xb, 2, sink, verbose));
+    b = maxd(b, tma_gbs<2048, 8, 4, 4, true>(X, xb, 3, sink, verbose));
+    b = maxd(b, tma_gbs<2048, 4, 8, 8, true>(X, xb, 3, sink, verbose));
+    b = maxd(b, tma_gbs<2048, 6, 4, 8, true>(X, xb, 4, sink, verbose));
+    c = maxd(c, tma_gbs<512, 8, 16, 4, false>(X, xb, 2, sink, verbose));
+    c = maxd(c, tma_gbs<512, 8, 32, 4, false>(X, xb, 3, sink, verbose));
+    d = maxd(d, tma_gbs<512, 8, 16, 4, true>(X, xb, 2, sink, verbose));
+    d = maxd(d, tma_gbs<512, 8, 32, 8, true>(X, xb, 3, sink, verbose));
+    // DRAM-resident X (503 MB) for the 2 KiB rows
+    if (buf_bytes >= (512LL << 20)) {
+        tma_gbs<2048, 8, 4, 4, false>(X, 503LL << 20, 3, sink, verbose);
+        tma_gbs<2048, 8, 4, 4, true>(X, 503LL << 20, 3, sink, verbose);
+    }
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    out4[0] = a; out4[1] = b; out4[2] = c; out4[3] = d;
+    return int(e);
+}
+
+namespace {
 }  // namespace
 
 extern "C" int fgprobe_l2_verbose(void* buf, int64_t buf_bytes, double* out5, int verbose) {

@@ -1,7 +1,23 @@
 """Test-only helpers: tiny graphs from edge lists, dense views, comparators."""
 from __future__ import annotations
 
+from contextlib import contextmanager
+
 import numpy as np
+
+
+@contextmanager
+def tuned(handle, **knobs):
+    """Set launch knobs of an fg Graph handle (fg_graph_tune) for the block,
+    restoring the previous values afterwards."""
+    old = {k: handle.get_tune(k) for k in knobs}
+    for k, v in knobs.items():
+        handle.tune(k, v)
+    try:
+        yield handle
+    finally:
+        for k, v in old.items():
+            handle.tune(k, v)
 
 
 def csr_from_edges(n_dst: int, edges, n_src: int | None = None):

@@ -151,20 +151,22 @@ def test_reddit_mlp_max_args(reddit):
 
 # ------------------------------------------------------------------ C5: reddit F=512 dst-row shards
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_reddit_shards_bit_identical(reddit, P, monkeypatch):
+def test_reddit_shards_bit_identical(reddit, P):
     """Per-row computation depends only on the row and the launch decisions; the
     default CTA-per-row threshold adapts to a graph's edge count (fair share per
-    group, clamped to [1024, 4096]), so the shards run with the threshold the
-    unsharded step used (4096 here) to make the comparison bit for bit."""
+    group, clamped to [1024, 4096]), so each shard's handle is given the whole
+    graph's edge count (FG_TUNE_BALANCE_NNZ, as bench.py and the sharding code
+    do) to make the comparison bit for bit."""
     import paper_2008_11359_b200 as fgp
     from paper_2008_11359_b200.shard import make_shard
-    monkeypatch.setenv("FG_SPMM_HEAVY_DEG", "4096")
     g, host, S, rows, rp, ci, pos = reddit
     X = S.X["X512"]
     parts_o, parts_s = [], []
     for r in range(P):
         sh = make_shard(g.row_ptr, g.col_idx, r, P)
         L = fgp.Graph(torch.from_numpy(sh.row_ptr).cuda(), torch.from_numpy(sh.col_idx).cuda(), n_src=g.n_src)
+        L.tune("balance_nnz", g.nnz)
+        L.prepare(512 * 4)
         parts_o.append(fgp.spmm(L, "copy_u", "sum", X))
         parts_s.append(fgp.sddmm(L, X, X[sh.lo:sh.hi], H=1))
         del L

@@ -14,7 +14,7 @@ import torch
 
 import gen
 import oracle
-from helpers import check_close, csr_from_edges
+from helpers import check_close, csr_from_edges, tuned
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-4
@@ -473,12 +473,15 @@ def test_abi_errors_on_device(skewed):
 
 # ------------------------------------------------------------------ L2 feature-dimension tiling paths
 @pytest.mark.parametrize("F", [128, 512, 1024])
-def test_l2_column_tiling(skewed, F, monkeypatch):
+def test_l2_column_tiling(skewed, F):
     """Force the column-tiled (multi-pass) paths with a tiny L2 budget: copy_u
     sum/max and H=1 u_dot_v must still match the oracle (max bit-exact)."""
+    with tuned(skewed.h, l2_tile_mb=1, sddmm_l2_tile=1):
+        _l2_column_tiling(skewed, F)
+
+
+def _l2_column_tiling(skewed, F):
     import paper_2008_11359_b200 as fgp
-    monkeypatch.setenv("FG_L2_TILE_MB", "1")
-    monkeypatch.setenv("FG_SDDMM_L2_TILE", "1")
     X = feats((skewed.n_src, F), 960 + F, gen.REAL)
     Y = feats((skewed.n_dst, F), 961 + F, gen.REAL)
     out = fgp.spmm(skewed.h, "copy_u", "sum", dev(X)).cpu().numpy()
@@ -497,31 +500,39 @@ def test_l2_column_tiling(skewed, F, monkeypatch):
     s = fgp.sddmm(skewed.h, dev(X), dev(Y)).cpu().numpy()
     ref, ab = oracle.sddmm(skewed.row_ptr, skewed.col_idx, X, Y)
     check_close(s, ref, ab, TOL, f"tiled u_dot_v F={F}")
-    monkeypatch.setenv("FG_L2_TILE_MB", "0")
+    skewed.h.tune("l2_tile_mb", 0)
     s0 = fgp.sddmm(skewed.h, dev(X), dev(Y)).cpu().numpy()
     check_close(s0, ref, ab, TOL, f"untiled u_dot_v F={F}")
 
 
 @pytest.mark.parametrize("H,D", [(1, 512), (1, 128), (8, 32), (2, 4)])
 @pytest.mark.parametrize("use_eid", [False, True])
-def test_sddmm_source_segmented(skewed, skewed_eid, H, D, use_eid, monkeypatch):
+def test_sddmm_source_segmented(skewed, skewed_eid, H, D, use_eid):
     """Row f3: force the source-segmented persistent SDDMM (1 MB segments ->
-    several segments even on the small test graph) and compare with the oracle."""
-    import paper_2008_11359_b200 as fgp
+    several segments even on the small test graph, tables built by
+    fg_graph_prepare) and compare with the oracle."""
     g = skewed_eid if use_eid else skewed
-    monkeypatch.setenv("FG_SDDMM_SEG_MB", "1")
-    monkeypatch.setenv("FG_SDDMM_SEG_MIN_MB", "0")
+    with tuned(g.h, sddmm_seg_mb=1, sddmm_seg_min_mb=0):
+        g.h.prepare(H * D * 4)
+        g.h.prepare(H * D * 2)
+        _sddmm_source_segmented(g, H, D)
+
+
+def _sddmm_source_segmented(g, H, D):
+    import paper_2008_11359_b200 as fgp
     X = feats((g.n_src, H * D), 980 + D, gen.REAL)
     Y = feats((g.n_dst, H * D), 981 + D, gen.REAL)
     out = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
     ref, ab = oracle.sddmm(g.row_ptr, g.col_idx, X, Y, H=H)
     pos = np.arange(g.nnz) if g.eid is None else g.eid
     check_close(out[pos], ref, ab, TOL, f"segmented u_dot_v H={H} D={D}")
-    monkeypatch.setenv("FG_SDDMM_PERSIST", "1")   # one CTA per SM: every group walks many units
-    out1 = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+    with tuned(g.h, sddmm_persist=1):             # one CTA per SM: every group walks many units
+        out1 = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
     assert np.array_equal(out1, out)              # same per-edge arithmetic, any schedule
+    with tuned(g.h, sddmm_seg_mb=0):              # unsegmented: still bit-identical (fg.h fg_graph_prepare)
+        out0 = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+    assert np.array_equal(out0, out)
     if H * D % 8 == 0:   # the bf16 pair kernel on the same segmented units
-        monkeypatch.delenv("FG_SDDMM_PERSIST")
         xb, xd = gen.to_bf16(X)
         yb, yd = gen.to_bf16(Y)
         outb = fgp.sddmm(g.h, bf16_dev(xb), bf16_dev(yb), H=H).cpu().numpy()
@@ -613,17 +624,16 @@ def test_bf16_rejects_unsupported(skewed):
 
 
 @pytest.mark.parametrize("F", [128, 512])
-def test_copy_u_bf16_tiled_and_unaligned(skewed, monkeypatch, F):
+def test_copy_u_bf16_tiled_and_unaligned(skewed, F):
     """bf16 storage on the column-tiled copy_u path (a 1 MiB L2 budget forces
     tiles on this graph) and with an X that is 8- but not 16-byte aligned (the
     8-byte-per-chunk mapping instead of 16-byte pair loads)."""
     import paper_2008_11359_b200 as fgp
     bits, dec = gen.to_bf16(feats((skewed.n_src, F), 740 + F, gen.REAL))
     ref, ab, _, _ = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", "sum", dec)
-    monkeypatch.setenv("FG_L2_TILE_MB", "1")
-    out = fgp.spmm(skewed.h, "copy_u", "sum", bf16_dev(bits)).cpu().numpy()
+    with tuned(skewed.h, l2_tile_mb=1):
+        out = fgp.spmm(skewed.h, "copy_u", "sum", bf16_dev(bits)).cpu().numpy()
     check_close(out, ref, ab, TOL, f"bf16 copy_u-sum tiled F={F}")
-    monkeypatch.delenv("FG_L2_TILE_MB")
     buf = torch.empty(skewed.n_src * F + 4, dtype=torch.bfloat16, device="cuda")
     Xu = buf[4:].view(skewed.n_src, F)            # 8-byte aligned, not 16
     Xu.copy_(bf16_dev(bits))
@@ -736,14 +746,18 @@ def test_sddmm_unit_sizes(skewed, monkeypatch, chunk):
 
 # ------------------------------------------------------------------ CTA-per-row path on the small graphs
 @pytest.mark.parametrize("deg", ["1", "200", "1024"])
-def test_cta_per_row_thresholds(skewed, skewed_eid, monkeypatch, deg):
+def test_cta_per_row_thresholds(skewed, skewed_eid, deg):
     """Rows of degree >= FG_SPMM_HEAVY_DEG / FG_GAT_HEAVY_DEG (default 4096, above
     this graph's maximum) run CTA-per-row with the fixed-order combine: force it
     for most rows and check sum / max (argmax ties across the CTA's chunks) / min /
     mean, u_mul_e and u_add_e with edge ids, bf16 storage and the fused GAT."""
+    d = int(deg)
+    with tuned(skewed.h, spmm_heavy_deg=d, gat_heavy_deg=d), tuned(skewed_eid.h, spmm_heavy_deg=d, gat_heavy_deg=d):
+        _cta_per_row_thresholds(skewed, skewed_eid)
+
+
+def _cta_per_row_thresholds(skewed, skewed_eid):
     import paper_2008_11359_b200 as fgp
-    monkeypatch.setenv("FG_SPMM_HEAVY_DEG", deg)
-    monkeypatch.setenv("FG_GAT_HEAVY_DEG", deg)
     g = skewed
     for F, regime in ((512, gen.REAL), (32, gen.INT), (128, gen.INT)):
         X = feats((g.n_src, F), 1300 + F, regime, lo=-2, hi=2)   # integers in [-2, 2]: many ties

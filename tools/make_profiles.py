@@ -2,12 +2,15 @@
 
     python tools/make_profiles.py r01c
 
-Reads gpurun_out/prof_{mlp,sddmm,spmm,softmax}_<tag>.ncu-rep and
+Reads gpurun_out/prof_{spmm,sddmm,softmax,mlp,gat}_<tag>.ncu-rep (the default
+step) and prof_{uspmm,usddmm}_<tag>.ncu-rep (the uniform-sources control) and
 gpurun_out/launches_<tag>.csv; writes
   profiles/ncu_summary_<tag>.md    per-kernel metrics (time, DRAM bytes, L2 hit,
                                    occupancy, issue, tensor pipe, top stalls)
-  profiles/ncu_traffic.json        DRAM bytes per launch per bench op (bench.py
-                                   reads this for roofline.traffic)
+  profiles/ncu_traffic.json        per-launch DRAM / L2 bytes and ncu's L2
+                                   throughput share per bench op, stamped with
+                                   the source hash of the libfg.so captured
+                                   (bench.py refuses a capture of another build)
   profiles/launches_<tag>.md       per-launch device times of one bench step
 """
 import csv
@@ -19,13 +22,17 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_summary import summarise  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2008_11359_b200.build import source_hash  # noqa: E402
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
-OPS_BY_FILE = {
-    "spmm": ["spmm_copy_u_sum_F512", "spmm_u_mul_e_sum_H8_D32", "spmm_copy_u_max_F128_args"],
-    "sddmm": ["sddmm_u_dot_v_H1_F512", "sddmm_u_dot_v_H8_D32"],
-    "softmax": ["edge_softmax_H8"],
-    "mlp": ["spmm_mlp_max_d8_d128_args"],
-    "gat": ["extra_gat_fused_H8_D32"],
+OPS_BY_FILE = {   # file key -> (variant, ops in capture order)
+    "spmm": ("default", ["spmm_copy_u_sum_F512", "spmm_u_mul_e_sum_H8_D32", "spmm_copy_u_max_F128_args"]),
+    "sddmm": ("default", ["sddmm_u_dot_v_H1_F512", "sddmm_u_dot_v_H8_D32"]),
+    "softmax": ("default", ["edge_softmax_H8"]),
+    "mlp": ("default", ["spmm_mlp_max_d8_d128_args"]),
+    "gat": ("default", ["extra_gat_fused_H8_D32"]),
+    "uspmm": ("uniform", ["spmm_copy_u_sum_F512"]),
+    "usddmm": ("uniform", ["sddmm_u_dot_v_H1_F512"]),
 }
 
 
@@ -44,8 +51,9 @@ lines = [f"# ncu --set full summaries ({tag})", "",
          "Captured with `ncu --set full --clock-control none --import-source on` on one B200 (gpurun), "
          "kernels of one timed `bench.py` step (reddit-shaped graph, 232,965 v / 114,615,892 e). "
          "Times are ncu replay times (cold-cache, serialised), not bench values.", ""]
-traffic = {}
-for key, ops in OPS_BY_FILE.items():
+traffic = {"build_hash": os.environ.get("FG_BUILD_HASH") or source_hash(), "capture": tag,
+           "default": {}, "uniform": {}}
+for key, (variant, ops) in OPS_BY_FILE.items():
     path = os.path.join(ROOT, "gpurun_out", f"prof_{key}_{tag}.ncu-rep")
     if not os.path.exists(path):
         continue
@@ -55,11 +63,17 @@ for key, ops in OPS_BY_FILE.items():
         wr = num(d.get("dram__bytes_write.sum", "")) or 0.0
         lts = num(d.get("lts__t_sectors.sum", "").replace(" sector", " byte"))
         lts = lts * 32 if lts else None
-        traffic[op] = {"kernel": d["kernel"], "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-                       "l2_bytes_per_launch": lts,
-                       "ncu_time_s": t, "dram_gbs": (rd + wr) / t / 1e9 if t else None,
-                       "l2_hit_pct": d.get("lts__t_sector_hit_rate.pct")}
-        lines += [f"## {op}", "", f"`{d['kernel']}`", "", "| metric | value |", "|---|---|"]
+        lpct = d.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", "")
+        try:
+            lpct = float(lpct.split()[0].replace(",", ""))
+        except (ValueError, IndexError):
+            lpct = None
+        traffic[variant][op] = {"kernel": d["kernel"], "dram_bytes_per_launch": rd + wr, "dram_read": rd,
+                                "dram_write": wr, "l2_bytes_per_launch": lts, "lts_throughput_pct": lpct,
+                                "ncu_time_s": t, "dram_gbs": (rd + wr) / t / 1e9 if t else None,
+                                "l2_hit_pct": d.get("lts__t_sector_hit_rate.pct"), "capture": f"prof_{key}_{tag}"}
+        lines += [f"## {op}" + (" (uniform-sources control)" if variant == "uniform" else ""), "",
+                  f"`{d['kernel']}`", "", "| metric | value |", "|---|---|"]
         for k, v in d.items():
             if k in ("kernel", "top_stalls"):
                 continue
