@@ -177,6 +177,25 @@ fg_status fg_graph_prepare(fg_graph* g, int64_t row_bytes, fg_stream stream);
  *                          table for that width (ablation E7)
  *   Errors: FG_EINVAL (NULL, unknown key, out-of-range value).
  */
+/*
+ * fg_graph_prepare_hybrid -- the table of the GPU hybrid partitioning (PAPER.md
+ * "reorders the vertices into a low-degree part and a high-degree
+ * part according to a threshold; it only partitions high-degree vertices and
+ * loads them to shared memory"): the k = smem_bytes / row_bytes sources of
+ * highest out-degree (ties: lower id) form the shared-memory partition, and
+ * every edge gets a source code (u, or the staged slot) in a copy of col_idx
+ * owned by the handle (4 * nnz bytes).  Used by fg_spmm copy_u-sum for rows of
+ * exactly row_bytes (fp32 F = row_bytes / 4 <= 128, untiled) when
+ * FG_TUNE_HYBRID is 1; results are bit-identical to the plain kernel (same
+ * values, same order).  SYNCHRONOUS; replaces any previous hybrid table.
+ *   row_bytes  : bytes per source row (multiple of 16)
+ *   smem_bytes : shared memory per CTA for the staged rows (row_bytes .. 200 KiB)
+ *   Errors: FG_EINVAL, FG_ESHAPE, FG_ENOMEM, FG_ECUDA.
+ * fg_graph_hybrid_info -- k and the fraction of edges whose source is staged.
+ */
+fg_status fg_graph_prepare_hybrid(fg_graph* g, int64_t row_bytes, int64_t smem_bytes, fg_stream stream);
+fg_status fg_graph_hybrid_info(const fg_graph* g, int64_t* k, double* hot_edge_share);
+
 typedef enum {
     FG_TUNE_L2_TILE_MB = 0,
     FG_TUNE_SPMM_HEAVY_DEG = 1,

@@ -48,31 +48,38 @@ def _deps_mtime(src: str) -> float:
     return max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in hdrs])
 
 
-def _compile(src: str, force: bool) -> tuple[str, str]:
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+def _compile(src: str, force: bool, defines=(), objdir: str = OBJ) -> tuple[str, str]:
+    obj = os.path.join(objdir, os.path.basename(src) + ".o")
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= _deps_mtime(src):
         return obj, ""
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str | None = None) -> str:
+    """Build libfg.so; `defines` / `lib` build a development VARIANT (kernel
+    constants overridden with -D, objects under build/<tag>/) at another path --
+    experiments only, never the product library (tools/variants.py)."""
+    objdir = OBJ if not defines else os.path.join(OBJ, "v_" + "_".join(d.replace("=", "") for d in defines))
+    out = LIB if lib is None else lib
+    os.makedirs(objdir, exist_ok=True)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        results = list(ex.map(lambda s: _compile(s, force), srcs))
+        results = list(ex.map(lambda s: _compile(s, force, defines, objdir), srcs))
     objs = [o for o, _ in results]
     if verbose:
         for _, log in results:
             if log:
                 print(log, file=sys.stderr)
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ldl"]
+    if force or not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(o) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-ldl"]
         subprocess.check_call(cmd)
+    if lib is not None:
+        return out
     # measurement utility for bench.py's roofline (L2 gather ceiling); not libfg
     if force or not os.path.exists(PROBE_LIB) or os.path.getmtime(PROBE_LIB) < os.path.getmtime(PROBE_SRC):
         subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "-o", PROBE_LIB,

@@ -60,6 +60,16 @@ struct fg_graph {
     std::deque<SegUnits> seg_units;      // deque: references stay valid as it grows
     std::mutex seg_mu;                   // guards seg_units against concurrent fg_graph_prepare calls
 
+    // hybrid partitioning table (fg_graph_prepare_hybrid): per-edge
+    // source codes (u, or -(slot+1) when source u is staged in shared memory)
+    // and the staged sources -- the hyb_k of highest out-degree
+    struct Hybrid {
+        int64_t row_bytes = 0, k = 0;
+        int32_t* code = nullptr;   // [nnz]
+        int32_t* hot = nullptr;    // [k]
+        double hot_edge_share = 0; // fraction of edges whose source is staged
+    } hyb;
+
     // derived (owned, host)
     std::vector<int64_t> deg_sorted;    // degrees in rows_by_deg order (descending)
     int64_t n_nonempty = 0;

@@ -22,17 +22,13 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "device_common.cuh"
 #include "fg_internal.h"
 
 namespace {
+using namespace fgdev;
 
 constexpr int THREADS = 256;
-
-template <int G>
-__device__ __forceinline__ unsigned group_mask(int lane) {
-    if constexpr (G == 32) return 0xffffffffu;
-    else return ((1u << G) - 1u) << (lane & ~(G - 1));
-}
 
 struct Args {
     const int32_t* rows;
@@ -42,38 +38,6 @@ struct Args {
     const int32_t* eid;
     int H, D4, F4;
 };
-
-constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
-
-// Recursive-halving reduce-scatter of K values over W aligned lanes (as in
-// sddmm.cu): at offset o a lane keeps the half of its values selected by
-// (gl & o) and adds the partner's copy of that half; the last levels are a plain
-// butterfly.  Afterwards lane gl holds the W-lane sum of value index
-// ((gl mod W) >> (log2 W - L)) * (K >> L) + i, L = min(log2 K, log2 W).
-template <int K, int W, int G>
-__device__ __forceinline__ void reduce_scatter(float (&v)[K], int gl, unsigned mask) {
-    if constexpr (W > 1) {
-        constexpr int o = W / 2;
-        if constexpr (K > 1) {
-            const bool up = (gl & o) != 0;
-#pragma unroll
-            for (int i = 0; i < K / 2; ++i) {
-                const float send = up ? v[i] : v[i + K / 2];
-                const float keep = up ? v[i + K / 2] : v[i];
-                v[i] = keep + __shfl_xor_sync(mask, send, o, G);
-            }
-            float (&h)[K / 2] = *reinterpret_cast<float(*)[K / 2]>(&v[0]);
-            reduce_scatter<K / 2, W / 2, G>(h, gl, mask);
-        } else {
-#pragma unroll
-            for (int oo = o; oo >= 1; oo >>= 1) v[0] += __shfl_xor_sync(mask, v[0], oo, G);
-        }
-    }
-}
-
-__device__ __forceinline__ float dot4(const float4& a, const float4& b) {
-    return fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, a.w * b.w)));
-}
 
 __device__ __forceinline__ float ex2(float x) {   // 2^x, MUFU.EX2 (rel. error ~2^-22)
     float y;

@@ -331,6 +331,8 @@ extern "C" fg_status fg_graph_destroy(fg_graph* g) {
         cudaFree(su.p0);
         cudaFree(su.p1);
     }
+    if (g->hyb.code) cudaFree(g->hyb.code);
+    if (g->hyb.hot) cudaFree(g->hyb.hot);
     if (g->owned_row_ptr) cudaFree(g->owned_row_ptr);
     if (g->owned_col_idx) cudaFree(g->owned_col_idx);
     if (g->owned_eid) cudaFree(g->owned_eid);
@@ -400,4 +402,92 @@ extern "C" fg_status fg_graph_prepare(fg_graph* g, int64_t row_bytes, fg_stream 
     const int64_t seg_rows = fgk::sddmm_seg_rows(g, row_bytes);
     if (seg_rows == 0 || g->nnz == 0) return FG_OK;   // this width is not segmented: nothing to build
     return fgk::build_seg_units(g, seg_rows, g->unit_chunk, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- hybrid partitioning
+namespace {
+__global__ void out_degree_kernel(int64_t nnz, const int32_t* __restrict__ ci, int32_t* __restrict__ cnt) {
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < nnz; p += int64_t(gridDim.x) * blockDim.x)
+        atomicAdd(cnt + __ldg(ci + p), 1);   // integer counts: order-independent
+}
+__global__ void hybrid_code_kernel(int64_t nnz, const int32_t* __restrict__ ci, const int32_t* __restrict__ slot,
+                                   int32_t* __restrict__ code) {
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < nnz; p += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t u = __ldg(ci + p);
+        const int32_t k = __ldg(slot + u);
+        code[p] = k >= 0 ? -(k + 1) : u;
+    }
+}
+}  // namespace
+
+extern "C" fg_status fg_graph_prepare_hybrid(fg_graph* g, int64_t row_bytes, int64_t smem_bytes, fg_stream stream) {
+    if (!g) return fgk::set_error(FG_EINVAL, "fg_graph_prepare_hybrid: NULL handle");
+    if (row_bytes <= 0 || row_bytes % 16 != 0 || smem_bytes < row_bytes || smem_bytes > 200 * 1024)
+        return fgk::set_error(FG_ESHAPE, "fg_graph_prepare_hybrid: row_bytes %lld (multiple of 16) and smem_bytes "
+                              "%lld (row_bytes .. 200 KiB)", (long long)row_bytes, (long long)smem_bytes);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (g->hyb.code) cudaFree(g->hyb.code);
+    if (g->hyb.hot) cudaFree(g->hyb.hot);
+    g->hyb = fg_graph::Hybrid();
+    if (g->nnz == 0 || g->n_src == 0) return FG_OK;
+    const int64_t n = g->n_src, m = g->nnz;
+    const int64_t k = std::min<int64_t>(n, smem_bytes / row_bytes);
+    int32_t *cnt = nullptr, *slot = nullptr;
+    std::vector<int32_t> hc(static_cast<size_t>(n)), hs(static_cast<size_t>(n), -1);
+    std::vector<int32_t> order(static_cast<size_t>(n));
+    std::vector<int32_t> hot;
+    int64_t hot_edges = 0;
+    fg_status st = FG_OK;
+    cudaError_t e = cudaMalloc(&cnt, sizeof(int32_t) * size_t(n));
+    if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, sizeof(int32_t) * size_t(n), s);
+    if (e == cudaSuccess) {
+        out_degree_kernel<<<int(std::min<int64_t>((m + 255) / 256, 148 * 16)), 256, 0, s>>>(m, g->col_idx, cnt);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * size_t(n), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) {
+        // the k sources of highest out-degree (ties: lower id), degree > 0
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return hc[size_t(a)] > hc[size_t(b)]; });
+        for (int64_t i = 0; i < k && hc[size_t(order[size_t(i)])] > 0; ++i) {
+            hs[size_t(order[size_t(i)])] = int32_t(i);
+            hot.push_back(order[size_t(i)]);
+            hot_edges += hc[size_t(order[size_t(i)])];
+        }
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&slot, sizeof(int32_t) * size_t(n));
+    if (e == cudaSuccess) e = cudaMalloc(&g->hyb.code, sizeof(int32_t) * size_t(m));
+    if (e == cudaSuccess) e = cudaMalloc(&g->hyb.hot, sizeof(int32_t) * std::max<size_t>(hot.size(), 1));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(slot, hs.data(), sizeof(int32_t) * size_t(n), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && !hot.empty())
+        e = cudaMemcpyAsync(g->hyb.hot, hot.data(), sizeof(int32_t) * hot.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+        hybrid_code_kernel<<<int(std::min<int64_t>((m + 255) / 256, 148 * 16)), 256, 0, s>>>(m, g->col_idx, slot,
+                                                                                           g->hyb.code);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(cnt);
+    cudaFree(slot);
+    if (e != cudaSuccess) {
+        st = fgk::set_error(e == cudaErrorMemoryAllocation ? FG_ENOMEM : FG_ECUDA, "fg_graph_prepare_hybrid: %s",
+                            cudaGetErrorString(e));
+        if (g->hyb.code) cudaFree(g->hyb.code);
+        if (g->hyb.hot) cudaFree(g->hyb.hot);
+        g->hyb = fg_graph::Hybrid();
+        return st;
+    }
+    g->hyb.row_bytes = row_bytes;
+    g->hyb.k = int64_t(hot.size());
+    g->hyb.hot_edge_share = double(hot_edges) / double(m);
+    g->device_bytes += 4 * m + 4 * g->hyb.k;
+    return FG_OK;
+}
+
+extern "C" fg_status fg_graph_hybrid_info(const fg_graph* g, int64_t* k, double* hot_edge_share) {
+    if (!g || !k || !hot_edge_share) return fgk::set_error(FG_EINVAL, "fg_graph_hybrid_info: NULL argument");
+    *k = g->hyb.k;
+    *hot_edge_share = g->hyb.hot_edge_share;
+    return FG_OK;
 }

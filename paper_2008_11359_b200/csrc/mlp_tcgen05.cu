@@ -22,7 +22,7 @@
 //     destination row in a 32-row window of row_ptr (register binary search),
 //     loads x_u and x_v (L2-resident: n x d1 x 4 B), forms s_e, splits it into
 //     tensor-core operands and stores them into the B operand (K-major,
-//     no-swizzle canonical layout) of an 8-stage shared-memory ring;
+//     no-swizzle canonical layout) of a 6-stage shared-memory ring;
 //   * one thread issues the MMAs, M = 128 features (W^T, staged once), N = 64
 //     edges, accumulating in TMEM (2 x 64 columns, double-buffered):
 //       3xTF32 (default): tcgen05.mma.kind::tf32, K = 8, hi*hi + hi*lo + lo*hi
@@ -48,12 +48,21 @@ namespace {
 
 constexpr int NT = 64;                    // edges per tile (MMA N; 32 with 4 buffers: 4.7 vs 4.04 ms)
 constexpr int NBUF = 2;                   // TMEM accumulator buffers (double buffer)
-constexpr int CTAS_PER_SM = 4;            // 4 independent pipelines per SM hide the MMA/commit latency
+#ifndef FG_MLP_CTAS
+#define FG_MLP_CTAS 4
+#endif
+#ifndef FG_MLP_LA
+#define FG_MLP_LA 4
+#endif
+#ifndef FG_MLP_NPROD
+#define FG_MLP_NPROD 2
+#endif
+constexpr int CTAS_PER_SM = FG_MLP_CTAS;  // 4 independent pipelines per SM hide the MMA/commit latency
 constexpr int MT = 128;                   // features per CTA (MMA M)
-constexpr int STAGES = 8;
+constexpr int STAGES = 6;                 // B-operand ring (6 x 4 KB: four CTAs per SM fit with the producer staging)
 constexpr int NEPI = 4;                   // epilogue warps 0..3 (TMEM lane quarters)
 constexpr int MMA_WARP = 4;
-constexpr int NPROD = 1;                  // producer warp 5
+constexpr int NPROD = FG_MLP_NPROD;       // producer warps 5, 6 (on two SM sub-partitions)
 constexpr int THREADS = (NEPI + 1 + NPROD) * 32;
 constexpr int TMEM_COLS = NBUF * NT;      // 128: four CTAs per SM share the 512 columns
 
@@ -146,6 +155,20 @@ __device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[32]) {
         : "memory");
 }
 
+// cp.async of `bytes` (0 or 16) bytes into a 16-byte shared slot, zero-filling the
+// rest: .ca keeps the line in L1 (x_v: consecutive edges share the row), .cg not.
+__device__ __forceinline__ void cp_async16_zfill(uint32_t saddr, const void* g, int bytes, bool l1) {
+    if (l1) asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(bytes) : "memory");
+    else asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t saddr, const void* g, int bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(saddr), "l"(g), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ int64_t lower_bound_rp(const int64_t* rp, int64_t n1, int64_t target) {
     int64_t lo = 0, hi = n1;   // first i in [0, n1) with rp[i] >= target
     while (lo < hi) {
@@ -185,10 +208,15 @@ constexpr int BACKOFF_NS = 128;   // producer / MMA wait back-off (the epilogue 
 // bf16:   a_hi = [w_hi | w_lo] (bf16), b_hi = [s_hi | s_hi], b_lo = [s_lo | s_lo].
 template <int KS>
 struct Smem {
+    static constexpr int LA = KS <= 2 ? FG_MLP_LA : 2;   // tiles of x rows in flight per producer lane
     float a_hi[KS][MT * 8];
     float a_lo[KS][MT * 8];
     float b_hi[STAGES][KS][NT * 8];
     float b_lo[STAGES][KS][NT * 8];
+    float raw_u[LA][NT][KS * 8];                 // producer staging: x_u, x_v rows (fp32, zero-padded)
+    float raw_v[LA][NT][KS * 8];
+    int32_t idx[2 * LA][NT];                     // producer staging: neighbour indices
+    int32_t rowtag[FG_MLP_NPROD][LA];            // the row of a single-row tile (per producer warp), else -1
     uint64_t full[STAGES], empty[STAGES], tfull[NBUF], tempty[NBUF];
     uint32_t tmem_base;
     int64_t r_lo, r_hi;
@@ -317,14 +345,6 @@ struct Epi {
     }
 };
 
-// 4 consecutive input dimensions [k0, k0 + 4) of row r of a [rows][d_in] matrix,
-// zero beyond d_in (vector load when d_in % 4 == 0: rows are then 16-byte aligned)
-__device__ __forceinline__ float4 ld_in4(const float* __restrict__ M, int64_t r, int d_in, int k0, bool vec) {
-    const float* p = M + r * d_in + k0;
-    if (vec) return k0 < d_in ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
-    return make_float4(k0 < d_in ? __ldg(p) : 0.f, k0 + 1 < d_in ? __ldg(p + 1) : 0.f,
-                       k0 + 2 < d_in ? __ldg(p + 2) : 0.f, k0 + 3 < d_in ? __ldg(p + 3) : 0.f);
-}
 __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
@@ -336,12 +356,16 @@ template <bool BF>
 __device__ __forceinline__ void store_split(uint32_t bh, uint32_t bl, int e, const float4& s0, const float4& s1) {
     const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
     if constexpr (!BF) {
+        // hi = s with the low 13 mantissa bits cleared (a tf32 value), lo = s - hi
+        // (exact, <= 13 significant bits), fed as raw fp32: the tensor core reads
+        // its top 19 bits, so |s - hi - tf32(lo)| <= 2^-20 |s| -- two ALU ops per
+        // value instead of two conversions and a subtraction (the producer shares
+        // an SM sub-partition with an epilogue warp)
         uint32_t hi[8], lo[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const float h = tf32_rna(sv[k]);
-            hi[k] = __float_as_uint(h);
-            lo[k] = __float_as_uint(tf32_rna(sv[k] - h));
+            hi[k] = __float_as_uint(sv[k]) & 0xffffe000u;
+            lo[k] = __float_as_uint(sv[k] - __uint_as_float(hi[k]));
         }
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -430,7 +454,20 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
 
     if (warp >= MMA_WARP + 1) {
         // ------------------------------------------------ producer: s_e = x_u + x_v -> B operand
+        // Three-stage software pipeline per lane (cp.async groups, one per tile):
+        //   tile t + 2*LA: this lane's neighbour indices -> S.idx (4-byte cp.async);
+        //   tile t + LA  : destination rows of its edges (window search below), then
+        //                  x_u (and, for tiles that span rows, x_v) -> S.raw_u / S.raw_v
+        //                  (16-byte cp.async, zero-filled beyond d_in);
+        //   tile t       : s = x_u + x_v, split, stored into the B operand.
+        // Every lane reads back only what it copied itself, so a per-thread
+        // cp.async.wait_group is the only synchronisation; no register waits on a
+        // gather round trip (the first register-loaded version ran at 5.6 ms vs 4.0).
+        // Fast path (most tiles of long rows): all of a warp's edges of the tile lie
+        // in one row -- found with two ballots -- whose x_v stays in registers.
         constexpr int EPT = NT / (NPROD * 32);          // edge slots per lane per tile
+        constexpr int LA = Smem<KS>::LA;
+        const int pw = warp - (MMA_WARP + 1);           // producer warp 0 .. NPROD-1
         const int pt = tid - (MMA_WARP + 1) * 32;       // 0 .. NPROD*32-1
         const bool vec = (A.d_in % 4) == 0;
         // destination rows: a window of 32 consecutive rows [wb, wb + 32) whose
@@ -441,75 +478,85 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
             return rr < r_hi ? int(__ldg(A.row_ptr + rr + 1) - E0) : 0x7fffffff;
         };
         int wend = load_window(wb);
-        // neighbour indices are prefetched PF tiles ahead (a register ring, static
-        // slots via the unrolled-by-PF loop): the col_idx round trip would otherwise
-        // bound the pipeline at one tile per load latency
-        constexpr int PF = 4;
-        int u_pf[PF][EPT];
-        auto load_idx = [&](int t, int (&u)[EPT]) {
-            const int64_t tb = E0 + int64_t(t) * NT;
-#pragma unroll
-            for (int i = 0; i < EPT; ++i) {
-                const int64_t p = tb + pt + i * NPROD * 32;
-                u[i] = (t < ntiles && p < E1) ? __ldg(A.col_idx + p) : 0;   // padded columns read row 0 (ignored)
-            }
-        };
-#pragma unroll
-        for (int k = 0; k < PF; ++k) load_idx(k, u_pf[k]);
-        auto tile = [&](int t, int (&u_cur)[EPT]) {
-            const int s = t % STAGES;
-            // the destination row of each edge slot (padded slots: the CTA's last row)
-            int vrow[EPT];
-            bool done[EPT];
-#pragma unroll
-            for (int i = 0; i < EPT; ++i) {
-                vrow[i] = int(r_hi) - 1;
-                done[i] = t * NT + pt + i * NPROD * 32 >= nnz_cta;
-            }
-            for (;;) {
-                const int last = __shfl_sync(0xffffffffu, wend, 31);
-#pragma unroll
-                for (int i = 0; i < EPT; ++i) {
-                    const int pe = t * NT + pt + i * NPROD * 32;
-                    int lo = 0;   // number of window rows ending at or before pe (ends ascend)
-#pragma unroll
-                    for (int step = 16; step >= 1; step >>= 1)
-                        if (__shfl_sync(0xffffffffu, wend, lo + step - 1) <= pe) lo += step;
-                    if (!done[i] && pe < last) {
-                        vrow[i] = wb + lo;
-                        done[i] = true;
-                    }
-                }
-                bool all = true;
-#pragma unroll
-                for (int i = 0; i < EPT; ++i) all = all && done[i];
-                if (__all_sync(0xffffffffu, all)) break;
-                wb += 32;   // some edge lies beyond the window: slide it
-                wend = load_window(wb);
-            }
-            float4 sv[EPT][KS][2];
-#pragma unroll
-            for (int i = 0; i < EPT; ++i)
-#pragma unroll
-                for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        const int k0 = ks * 8 + c * 4;
-                        const float4 a = ld_in4(A.X, u_cur[i], A.d_in, k0, vec);
-                        const float4 b = ld_in4(A.Xd, vrow[i], A.d_in, k0, vec);
-                        sv[i][ks][c] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
-                    }
-            mbar_wait_backoff(&S.empty[s], ((t / STAGES) & 1) ^ 1, BACKOFF_NS);
+        auto issue_idx = [&](int t) {
+            if (t >= ntiles) return;
 #pragma unroll
             for (int i = 0; i < EPT; ++i) {
                 const int e = pt + i * NPROD * 32;
-#pragma unroll
-                for (int ks = 0; ks < KS; ++ks)
-                    store_split<BF>(smem_u32(S.b_hi[s][ks]), smem_u32(S.b_lo[s][ks]), e, sv[i][ks][0], sv[i][ks][1]);
+                const int64_t p = E0 + int64_t(t) * NT + e;
+                cp_async4(smem_u32(&S.idx[t % (2 * LA)][e]), A.col_idx + (p < E1 ? p : E0), p < E1 ? 4 : 0);
             }
-            fence_async_smem();        // generic-proxy stores -> tensor-core (async proxy) reads
-            mbar_arrive(&S.full[s]);
-            load_idx(t + PF, u_cur);   // refill this slot PF tiles ahead
+        };
+        auto copy_row = [&](float* dst, const float* src, bool l1) {
+#pragma unroll
+            for (int k0 = 0; k0 < KS * 8; k0 += 4) {
+                if (vec) {
+                    const int nb = k0 < A.d_in ? 16 : 0;   // zero-fill beyond d_in
+                    cp_async16_zfill(smem_u32(dst + k0), src + (nb ? k0 : 0), nb, l1);
+                } else {
+#pragma unroll
+                    for (int k = k0; k < k0 + 4; ++k) {
+                        const int nb = k < A.d_in ? 4 : 0;
+                        cp_async4(smem_u32(dst + k), src + (nb ? k : 0), nb);
+                    }
+                }
+            }
+        };
+        auto issue_raw = [&](int t) {
+            if (t >= ntiles) return;
+            const int slot = t % LA;
+            // this warp's edges of tile t: pe = t*NT + pw*32 + lane + i*NPROD*32
+            const int pfirst = t * NT + pw * 32;
+            const int plast = min(t * NT + pw * 32 + (EPT - 1) * NPROD * 32 + 31, nnz_cta - 1);
+            int c0 = __popc(__ballot_sync(0xffffffffu, wend <= pfirst));
+            while (c0 == 32) {   // the window ends before this tile: slide it
+                wb += 32;
+                wend = load_window(wb);
+                c0 = __popc(__ballot_sync(0xffffffffu, wend <= pfirst));
+            }
+            const int c1 = __popc(__ballot_sync(0xffffffffu, wend <= plast));
+            int vrow[EPT];
+            int tag = -1;
+            if (c1 == c0) {
+                tag = wb + c0;                     // every edge of this warp's tile lies in row wb + c0
+#pragma unroll
+                for (int i = 0; i < EPT; ++i) vrow[i] = tag;
+            } else {
+                bool done[EPT];
+#pragma unroll
+                for (int i = 0; i < EPT; ++i) {
+                    vrow[i] = int(r_hi) - 1;       // padded slots: the CTA's last row
+                    done[i] = t * NT + pt + i * NPROD * 32 >= nnz_cta;
+                }
+                for (;;) {
+                    const int last = __shfl_sync(0xffffffffu, wend, 31);
+#pragma unroll
+                    for (int i = 0; i < EPT; ++i) {
+                        const int pe = t * NT + pt + i * NPROD * 32;
+                        int lo = 0;   // number of window rows ending at or before pe (ends ascend)
+#pragma unroll
+                        for (int step = 16; step >= 1; step >>= 1)
+                            if (__shfl_sync(0xffffffffu, wend, lo + step - 1) <= pe) lo += step;
+                        if (!done[i] && pe < last) {
+                            vrow[i] = wb + lo;
+                            done[i] = true;
+                        }
+                    }
+                    bool all = true;
+#pragma unroll
+                    for (int i = 0; i < EPT; ++i) all = all && done[i];
+                    if (__all_sync(0xffffffffu, all)) break;
+                    wb += 32;   // some edge lies beyond the window: slide it
+                    wend = load_window(wb);
+                }
+            }
+            if (lane == 0) S.rowtag[pw][slot] = tag;
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                const int e = pt + i * NPROD * 32;
+                copy_row(S.raw_u[slot][e], A.X + int64_t(S.idx[t % (2 * LA)][e]) * A.d_in, false);
+                if (tag < 0) copy_row(S.raw_v[slot][e], A.Xd + int64_t(vrow[i]) * A.d_in, true);
+            }
             // keep the window at the row of this tile's last edge (rows only move forward)
             const int wlast = __shfl_sync(0xffffffffu, vrow[EPT - 1], 31);
             if (wlast >= wb + 32 - 1 && wlast < r_hi) {   // the next tile starts at or beyond the window's end
@@ -517,11 +564,67 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
                 wend = load_window(wb);
             }
         };
-        for (int t0 = 0; t0 < ntiles; t0 += PF) {
+        // x_v of the fast path's row, in registers (reloaded when the row changes)
+        int xrow = -1;
+        float4 xv[KS][2];
+        auto load_xv = [&](int row) {
 #pragma unroll
-            for (int k = 0; k < PF; ++k)
-                if (t0 + k < ntiles) tile(t0 + k, u_pf[k]);
+            for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int k0 = ks * 8 + c * 4;
+                    const float* p = A.Xd + int64_t(row) * A.d_in + k0;
+                    if (vec) {
+                        xv[ks][c] = k0 < A.d_in ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    } else {
+                        xv[ks][c] = make_float4(k0 < A.d_in ? __ldg(p) : 0.f, k0 + 1 < A.d_in ? __ldg(p + 1) : 0.f,
+                                                k0 + 2 < A.d_in ? __ldg(p + 2) : 0.f, k0 + 3 < A.d_in ? __ldg(p + 3) : 0.f);
+                    }
+                }
+            xrow = row;
+        };
+        // prologue: indices of tiles 0 .. LA-1 (waited for), then group j = {x rows of
+        // tile j, indices of tile j + LA} for j < LA
+        for (int j = 0; j < LA; ++j) issue_idx(j);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+        for (int j = 0; j < LA; ++j) {
+            issue_raw(j);
+            issue_idx(j + LA);
+            cp_async_commit();
         }
+        for (int t = 0; t < ntiles; ++t) {
+            const int s = t % STAGES;
+            const int slot = t % LA;
+            cp_async_wait_group<LA - 1>();   // group t: x rows of tile t, indices of tile t + LA
+            __syncwarp();
+            const int tag = S.rowtag[pw][slot];
+            if (tag >= 0 && tag != xrow) load_xv(tag);
+            mbar_wait_backoff(&S.empty[s], ((t / STAGES) & 1) ^ 1, BACKOFF_NS);
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                const int e = pt + i * NPROD * 32;
+                const float4* ru = reinterpret_cast<const float4*>(S.raw_u[slot][e]);
+                const float4* rv = reinterpret_cast<const float4*>(S.raw_v[slot][e]);
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    const float4 a0 = ru[2 * ks], a1 = ru[2 * ks + 1];
+                    const float4 b0 = tag >= 0 ? xv[ks][0] : rv[2 * ks];
+                    const float4 b1 = tag >= 0 ? xv[ks][1] : rv[2 * ks + 1];
+                    store_split<BF>(smem_u32(S.b_hi[s][ks]), smem_u32(S.b_lo[s][ks]), e,
+                                    make_float4(a0.x + b0.x, a0.y + b0.y, a0.z + b0.z, a0.w + b0.w),
+                                    make_float4(a1.x + b1.x, a1.y + b1.y, a1.z + b1.z, a1.w + b1.w));
+                }
+            }
+            fence_async_smem();        // generic-proxy stores -> tensor-core (async proxy) reads
+            mbar_arrive(&S.full[s]);
+            __syncwarp();              // every lane has read S.rowtag[pw][slot] before it is rewritten
+            issue_raw(t + LA);         // into the slot just consumed
+            issue_idx(t + 2 * LA);
+            cp_async_commit();
+        }
+        cp_async_wait_all();
     } else if (warp == MMA_WARP) {
         // ------------------------------------------------ MMA issuer (one thread)
         if (lane == 0) {

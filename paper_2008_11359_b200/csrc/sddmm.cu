@@ -22,19 +22,15 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "device_common.cuh"
 #include "fg_internal.h"
 
 namespace {
+using namespace fgdev;
 
 constexpr int THREADS = 256;
 
 enum { MODE_H1 = 0, MODE_HEADS = 1, MODE_GENERAL = 2 };
-
-template <int G>
-__device__ __forceinline__ unsigned group_mask(int lane) {
-    if constexpr (G == 32) return 0xffffffffu;
-    else return ((1u << G) - 1u) << (lane & ~(G - 1));
-}
 
 struct Args {
     const int32_t* unit_row;
@@ -53,59 +49,12 @@ struct Args {
     const float* E;   // u_dot_v-then-e_mul (fg_sddmm_emul): scores scaled by E[eid][h] at the write-back
 };
 
-// 4 bf16 (one 8-byte chunk, feature 0 in the low half of .x) -> 4 fp32, exact
-__device__ __forceinline__ float4 bf16x4(uint2 w) {
-    return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y << 16),
-                       __uint_as_float(w.y & 0xffff0000u));
-}
-
 // chunk c (4 features) of row r of a feature matrix with F4 chunks per row;
 // XB: bf16 storage (the float4 pointer then addresses 8-byte chunks)
 template <bool XB>
 __device__ __forceinline__ float4 ld_chunk(const float4* __restrict__ M, int64_t r, int F4, int c) {
     if constexpr (XB) return bf16x4(__ldg(reinterpret_cast<const uint2*>(M) + r * F4 + c));
     else return __ldg(M + r * F4 + c);
-}
-
-__device__ __forceinline__ float dot4(const float4& a, const float4& b) {
-    return fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, a.w * b.w)));
-}
-
-// Butterfly sum over W consecutive lanes of the group (W a power of two <= G).
-template <int G>
-__device__ __forceinline__ float group_sum(float x, int W, unsigned mask) {
-#pragma unroll
-    for (int o = G / 2; o >= 1; o >>= 1)
-        if (o < W) x += __shfl_xor_sync(mask, x, o, G);
-    return x;
-}
-
-constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
-
-// Recursive-halving reduce-scatter of K values over W aligned lanes of a group:
-// at offset o the lane keeps the half of its values selected by (gl & o) and adds
-// the partner's copy of that half.  Afterwards lane gl holds, in v[0 .. K/2^L),
-// the W-lane sums of original indices bits*K/2^L + i (bits = the top L bits of
-// gl mod W, L = min(log2 K, log2 W)); remaining levels are a plain butterfly.
-template <int K, int W, int G>
-__device__ __forceinline__ void reduce_scatter(float (&v)[K], int gl, unsigned mask) {
-    if constexpr (W > 1) {
-        constexpr int o = W / 2;
-        if constexpr (K > 1) {
-            const bool up = (gl & o) != 0;
-#pragma unroll
-            for (int i = 0; i < K / 2; ++i) {
-                const float send = up ? v[i] : v[i + K / 2];
-                const float keep = up ? v[i + K / 2] : v[i];
-                v[i] = keep + __shfl_xor_sync(mask, send, o, G);
-            }
-            float (&h)[K / 2] = *reinterpret_cast<float(*)[K / 2]>(&v[0]);
-            reduce_scatter<K / 2, W / 2, G>(h, gl, mask);
-        } else {
-#pragma unroll
-            for (int oo = o; oo >= 1; oo >>= 1) v[0] += __shfl_xor_sync(mask, v[0], oo, G);
-        }
-    }
 }
 
 // MODE_H1      : H == 1 and F <= 4*G*NV: one dot per edge, reduce over all G lanes.
@@ -399,6 +348,41 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_pair_kernel(const Args A, co
     }
 }
 
+// Ablation E6: the per-edge dot product computed by ONE
+// thread, walking the whole feature row (the "thread-per-edge" alternative the
+// paper's tree reduction is measured against: "consume too many registers" at
+// large F).  A warp takes one work unit (<= unit_chunk edges of one destination
+// row), lane l the edges p0 + l, p0 + l + 32, ...; Y[v] is shared by the warp
+// (L1).  Same unit tables, same outputs; the per-edge summation order differs
+// from the lane-partitioned kernels (within tolerance, not bit-identical).
+__global__ void __launch_bounds__(THREADS) sddmm_thread_kernel(const Args A, const float4* __restrict__ X,
+                                                               const float4* __restrict__ Y, float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = int64_t(gridDim.x) * (THREADS / 32);
+    const int F4 = A.F4, D4 = A.D4, H = A.H;
+    for (int64_t unit = (int64_t(blockIdx.x) * THREADS + threadIdx.x) / 32; unit < A.n_units; unit += nwarps) {
+        const int64_t v = A.unit_row[unit];
+        const int64_t s = A.unit_p0[unit];
+        const int64_t e = A.unit_p1 ? A.unit_p1[unit] : min(s + A.unit_chunk, A.row_ptr[v + 1]);
+        for (int64_t p = s + lane; p < e; p += 32) {
+            const int64_t u = __ldg(A.col_idx + p);
+            const int64_t eo = (A.eid ? int64_t(__ldg(A.eid + p)) : p) * H;
+            const float4* xr = X + u * F4;
+            const float4* yr = Y + v * F4;
+            float acc = 0.f;
+            int h = 0;
+            for (int c = 0; c < F4; ++c) {
+                acc += dot4(__ldg(xr + c), __ldg(yr + c));
+                if ((c + 1) % D4 == 0) {   // end of head h
+                    out[eo + h] = A.E ? acc * __ldg(A.E + eo + h) : acc;
+                    acc = 0.f;
+                    ++h;
+                }
+            }
+        }
+    }
+}
+
 template <int G, int NV, bool XB = false>
 fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, cudaStream_t st) {
     using K = void (*)(const Args, const float4*, const float4*, float*);
@@ -559,6 +543,14 @@ static fg_status launch_sddmm_core(const fg_graph* g, int H, int D, const float*
             A.n_units = su->n_units;
             A.persistent = int(g->tune.sddmm_persist);   // CTAs per SM (-1: the occupancy)
         }
+    }
+    if (g->tune.sddmm_dot == 1 && !xb && A.tile4 == 0) {   // ablation E6: thread-per-edge dot products
+        const int64_t per_block = THREADS / 32;
+        int64_t blocks = (A.n_units + per_block - 1) / per_block;
+        if (A.persistent) blocks = std::min<int64_t>(blocks, int64_t(fgk::num_sms()) * 8);
+        if (blocks == 0) return FG_OK;
+        sddmm_thread_kernel<<<unsigned(blocks), THREADS, 0, st>>>(A, X4, Y4, out);
+        return fgk::check_launch("sddmm_thread_kernel");
     }
     int G = 32, NV = 4;
     if (F4 <= 32) {

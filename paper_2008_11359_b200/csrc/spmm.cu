@@ -56,6 +56,10 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     A.out = reinterpret_cast<float4*>(out);
     A.arg_u = reinterpret_cast<int4*>(arg_u);
     A.arg_e = reinterpret_cast<int4*>(arg_e);
+    A.hyb_code = nullptr;
+    A.hyb_hot = nullptr;
+    A.hyb_k = 0;
+    A.n_vblocks = 0;
     const int op = (msg == FG_MSG_COPY_U)    ? OP_COPY
                    : (msg == FG_MSG_U_ADD_E) ? OP_UADDE
                    : (msg == FG_MSG_COPY_E)  ? OP_COPYE
@@ -125,6 +129,15 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
             thr = std::min<int64_t>(4096, std::max<int64_t>(1024, m / std::max<int64_t>(1, groups)));
         }
         A.n_heavy = rows_with_degree_at_least(g, thr);
+    }
+    // hybrid partitioning (FG_TUNE_HYBRID, table from fg_graph_prepare_hybrid for
+    // this row width): copy_u-sum with one float4 per lane and no column tiling
+    if (g->tune.hybrid && g->hyb.code && g->hyb.k > 0 && msg == FG_MSG_COPY_U && red == FG_REDUCE_SUM &&
+        !Xbf16 && NV == 1 && F4 == A.F4 && g->hyb.row_bytes == int64_t(A.F4) * 16) {
+        A.hyb_code = g->hyb.code;
+        A.hyb_hot = g->hyb.hot;
+        A.hyb_k = int(g->hyb.k);
+        return launch_hybrid(A, G, st);
     }
     const int opset = (op == OP_UADDE || op == OP_COPYE) ? 1 : 0;
     if (Xbf16) {   // bf16 storage: copy_u / u_mul_e x {sum, max} (validated by the caller)

@@ -1,9 +1,14 @@
 // spmm_impl.cuh -- the gathered-message gSpMM kernel template (design notes in
 // spmm.cu), instantiated per (reducer, op set) by spmm_inst_*.cu.
 #pragma once
+#include <algorithm>
+
+#include "device_common.cuh"
 #include "fg_internal.h"
 
 namespace fgspmm {
+using fgdev::bf16x4;
+using fgdev::group_mask;
 
 
 // OP_UMULE_GEN: u_mul_e with D % 4 != 0 (the head varies inside a float4);
@@ -12,12 +17,6 @@ namespace fgspmm {
 enum { OP_COPY = 0, OP_UMULE = 1, OP_UMULE_GEN = 2, OP_UADDE = 3, OP_COPYE = 4 };
 enum { R_SUM = 0, R_MAX = 1, R_MIN = 2, R_MEAN = 3 };
 constexpr int THREADS = 256;
-
-template <int G>
-__device__ __forceinline__ unsigned group_mask(int lane) {
-    if constexpr (G == 32) return 0xffffffffu;
-    else return ((1u << G) - 1u) << (lane & ~(G - 1));
-}
 
 struct Args {
     const int32_t* rows;        // rows_by_deg
@@ -33,14 +32,15 @@ struct Args {
     float4* out;
     int4* arg_u;
     int4* arg_e;
+    // hybrid partitioning (HYB kernels only): per-edge source codes (u, or
+    // -(slot+1) for a source staged in shared memory) and the staged sources
+    const int32_t* hyb_code;
+    const int32_t* hyb_hot;
+    int hyb_k;
+    int64_t n_vblocks;          // virtual blocks of the launch (HYB: persistent grid-stride)
 };
 
 __device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); }
-// 4 bf16 (one 8-byte chunk, feature 0 in the low half of .x) -> 4 fp32, exact
-__device__ __forceinline__ float4 bf16x4(uint2 w) {
-    return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y << 16),
-                       __uint_as_float(w.y & 0xffff0000u));
-}
 __device__ __forceinline__ float comp(const float4& v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
 __device__ __forceinline__ void set_comp(float4& v, int k, float a) {
     if (k == 0) v.x = a; else if (k == 1) v.y = a; else if (k == 2) v.z = a; else v.w = a;
@@ -63,10 +63,10 @@ constexpr bool stage_e() {
 }
 
 // Accumulate edges [s, e) of one row into (acc, pos) for this lane's NV chunks.
-template <int G, int NV, int OP, int RED, bool XB, bool PAIR>
+template <int G, int NV, int OP, int RED, bool XB, bool PAIR, bool HYB = false>
 __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e, int gl, unsigned mask,
                                              int c4base, float4 (&acc)[NV], int (&pos)[NV][4],
-                                             float* __restrict__ etile) {
+                                             float* __restrict__ etile, const float4* __restrict__ hot = nullptr) {
     constexpr int B = 32;                                   // edges per index batch
     constexpr int R = B / G;                                // indices per lane per batch
     // edges in flight per lane; PAIR (raw bf16 pairs): 4 -- 8 measured slower
@@ -83,7 +83,8 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int64_t p = p0 + gl + r * G;
-            uix[r] = (OP != OP_COPYE && p < e) ? __ldg(A.col_idx + p) : 0;   // copy_e reads no source row
+            if constexpr (HYB) uix[r] = (p < e) ? __ldg(A.hyb_code + p) : 0;   // u, or -(slot+1): staged
+            else uix[r] = (OP != OP_COPYE && p < e) ? __ldg(A.col_idx + p) : 0;   // copy_e reads no source row
             if constexpr (OP != OP_COPY) eix[r] = (p < e) ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
         }
         // u_mul_e with identity edge ids: the batch's E rows are one contiguous span;
@@ -124,6 +125,8 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                             xw[uu][j / 2] = ok ? __ldg(reinterpret_cast<const uint4*>(xh + c)) : make_uint4(0, 0, 0, 0);
                     } else if constexpr (XB) {
                         x[uu][j] = ok ? bf16x4(__ldg(xh + c)) : f4(0.f);
+                    } else if constexpr (HYB) {   // hot sources from shared memory, the rest from L2 / HBM
+                        x[uu][j] = !ok ? f4(0.f) : (u < 0 ? hot[int64_t(-1 - u) * F4 + c] : __ldg(A.X + int64_t(u) * F4 + c));
                     } else {
                         x[uu][j] = ok ? __ldg(xr + c) : f4(0.f);
                     }
@@ -240,7 +243,11 @@ __device__ __forceinline__ void store_elem(const Args& A, int64_t v, int c, floa
     }
 }
 
-template <int G, int NV, int OP, int RED, bool XB, bool PAIR>
+// HYB: the paper's hybrid partitioning on the GPU: the hyb_k sources
+// of highest out-degree are staged in shared memory once per CTA (persistent
+// grid-stride over the virtual blocks) and read from there; the others from
+// L2 / HBM.  Same values in the same order as the plain kernel: bit-identical.
+template <int G, int NV, int OP, int RED, bool XB, bool PAIR, bool HYB = false>
 __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);
     constexpr int NG = THREADS / G;                 // groups per CTA
@@ -250,23 +257,32 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     __shared__ float s_val[MAX ? NG : 1][MAX ? TW * 4 : 1];
     __shared__ int s_pos[MAX ? NG : 1][MAX ? TW * 4 : 1];
 
+    extern __shared__ float4 s_hot[];   // HYB: hyb_k staged source rows of F4 float4
     const int lane = threadIdx.x & 31;
     const int gl = threadIdx.x & (G - 1);
     const int gi = threadIdx.x / G;
     const unsigned mask = group_mask<G>(lane);
     const int c4base = blockIdx.y * TW;
+    if constexpr (HYB) {
+        for (int i = threadIdx.x; i < A.hyb_k * A.F4; i += THREADS) {
+            const int k = i / A.F4, c = i - k * A.F4;
+            s_hot[i] = __ldg(A.X + int64_t(__ldg(A.hyb_hot + k)) * A.F4 + c);
+        }
+        __syncthreads();
+    }
 
+    for (int64_t vb = blockIdx.x; vb < A.n_vblocks; vb += gridDim.x) {
     float4 acc[NV];
     int pos[NV][4];
     init_acc<NV, RED>(acc, pos);
 
-    if (int64_t(blockIdx.x) < A.n_heavy) {
+    if (vb < A.n_heavy) {
         // ---- CTA-per-row: contiguous edge ranges per group, fixed-order combine
-        const int64_t v = A.rows[blockIdx.x];
+        const int64_t v = A.rows[vb];
         const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
         const int64_t len = (e - s + NG - 1) / NG;
         const int64_t gs = min(e, s + gi * len), ge = min(e, gs + len);
-        gather_range<G, NV, OP, RED, XB, PAIR>(A, gs, ge, gl, mask, c4base, acc, pos, s_etile[gi]);
+        gather_range<G, NV, OP, RED, XB, PAIR, HYB>(A, gs, ge, gl, mask, c4base, acc, pos, s_etile[gi], s_hot);
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
             const int c = colj<G, PAIR>(gl, j);
@@ -301,23 +317,25 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
             }
             store_elem<RED>(A, v, c4base + c, a, ps, e - s);
         }
-        return;
+        __syncthreads();   // the combine buffers are reused by this CTA's next virtual block
+        continue;
     }
 
     // ---- group-per-row
-    const int64_t r = A.n_heavy + (int64_t(blockIdx.x) - A.n_heavy) * NG + gi;
-    if (r >= A.n_rows) return;
+    const int64_t r = A.n_heavy + (vb - A.n_heavy) * NG + gi;
+    if (r >= A.n_rows) continue;
     const int64_t v = A.rows[r];
     const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
-    gather_range<G, NV, OP, RED, XB, PAIR>(A, s, e, gl, mask, c4base, acc, pos, s_etile[gi]);
+    gather_range<G, NV, OP, RED, XB, PAIR, HYB>(A, s, e, gl, mask, c4base, acc, pos, s_etile[gi], s_hot);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const int c = c4base + colj<G, PAIR>(gl, j);
         if (c < A.F4) store_elem<RED>(A, v, c, acc[j], pos[j], e - s);
     }
+    }   // virtual blocks
 }
 
-template <int G, int NV, int OP, int RED, bool XB = false, bool PAIR = false>
+template <int G, int NV, int OP, int RED, bool XB = false, bool PAIR = false, bool HYB = false>
 fg_status launch_t(const Args& A0, cudaStream_t st) {
     Args A = A0;
     constexpr int NG = THREADS / G;
@@ -326,10 +344,26 @@ fg_status launch_t(const Args& A0, cudaStream_t st) {
     const int64_t blocks = A.n_heavy + (light + NG - 1) / NG;
     const int tiles = (A.F4 + TW - 1) / TW;
     if (blocks == 0) return FG_OK;
-    const dim3 grid{unsigned(blocks), unsigned(tiles), 1u};
-    spmm_gather_kernel<G, NV, OP, RED, XB, PAIR><<<grid, THREADS, 0, st>>>(A);
+    A.n_vblocks = blocks;
+    int64_t grid_x = blocks;
+    size_t smem = 0;
+    auto k = spmm_gather_kernel<G, NV, OP, RED, XB, PAIR, HYB>;
+    if constexpr (HYB) {   // persistent: the resident CTAs stage the hot rows once each
+        smem = size_t(A.hyb_k) * A.F4 * 16;   // (plus the kernel's static combine buffers)
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+            return fgk::set_error(FG_ECUDA, "spmm hybrid: %zu bytes of shared memory", smem);
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem) != cudaSuccess || per_sm < 1)
+            per_sm = 1;
+        grid_x = std::min<int64_t>(blocks, int64_t(fgk::num_sms()) * per_sm);
+    }
+    const dim3 grid{unsigned(grid_x), unsigned(tiles), 1u};
+    k<<<grid, THREADS, smem, st>>>(A);
     return fgk::check_launch("spmm_gather_kernel");
 }
+
+// hybrid partitioning (copy_u-sum, one float4 per lane, untiled): spmm_inst_sum_base.cu
+fg_status launch_hybrid(const Args& A, int G, cudaStream_t st);
 
 // One explicit specialisation per (reducer, op set) -- op set 0 = copy_u /
 // u_mul_e, 1 = u_add_e / copy_e -- each compiled in its own translation unit

@@ -2,3 +2,16 @@
 #define FG_RED R_SUM
 #define FG_OPSET 0
 #include "spmm_inst.cuh"
+
+namespace fgspmm {
+fg_status launch_hybrid(const Args& A, int G, cudaStream_t st) {
+    switch (G) {
+        case 1: return launch_t<1, 1, OP_COPY, R_SUM, false, false, true>(A, st);
+        case 2: return launch_t<2, 1, OP_COPY, R_SUM, false, false, true>(A, st);
+        case 4: return launch_t<4, 1, OP_COPY, R_SUM, false, false, true>(A, st);
+        case 8: return launch_t<8, 1, OP_COPY, R_SUM, false, false, true>(A, st);
+        case 16: return launch_t<16, 1, OP_COPY, R_SUM, false, false, true>(A, st);
+        default: return launch_t<32, 1, OP_COPY, R_SUM, false, false, true>(A, st);
+    }
+}
+}  // namespace fgspmm

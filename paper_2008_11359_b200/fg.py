@@ -18,7 +18,8 @@ import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libfg.so")
+# FG_LIBFG: a development variant of libfg.so (tools/variants.py) -- same ABI
+LIB_PATH = os.environ.get("FG_LIBFG") or os.path.join(_PKG, "lib", "libfg.so")
 
 FG_OK, FG_EINVAL, FG_ESHAPE, FG_EUNSUPPORTED, FG_EGRAPH, FG_ECUDA, FG_ENOMEM, FG_ENCCL = range(8)
 MSG = {"copy_u": 0, "u_mul_e": 1, "mlp": 2, "u_add_e": 3, "copy_e": 4}
@@ -26,7 +27,8 @@ REDUCE = {"sum": 0, "max": 1, "min": 2, "mean": 3}
 EDGE = {"u_dot_v": 0, "u_add_v": 1, "u_sub_v": 2, "u_mul_v": 3}
 
 # exported symbols declared in include/fg.h (checked by tests/test_abi.py)
-SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_graph_prepare", "fg_graph_tune",
+SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_graph_prepare", "fg_graph_prepare_hybrid",
+           "fg_graph_hybrid_info", "fg_graph_tune",
            "fg_graph_get_tune", "fg_spmm_workspace_size", "fg_spmm",
            "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
            "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
@@ -66,6 +68,8 @@ def lib() -> ctypes.CDLL:
     L.fg_graph_destroy.argtypes = [vp]
     L.fg_graph_info.argtypes = [vp, ctypes.POINTER(GraphInfo)]
     L.fg_graph_prepare.argtypes = [vp, i64, vp]
+    L.fg_graph_prepare_hybrid.argtypes = [vp, i64, i64, vp]
+    L.fg_graph_hybrid_info.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double)]
     L.fg_graph_tune.argtypes = [vp, i32, i64]
     L.fg_graph_get_tune.argtypes = [vp, i32, ctypes.POINTER(i64)]
     L.fg_spmm_workspace_size.argtypes = [vp, i32, i32, i32, i32, i32, ctypes.POINTER(sz)]
@@ -87,7 +91,8 @@ def lib() -> ctypes.CDLL:
     L.fg_comm_destroy.argtypes = [vp]
     L.fg_comm_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.fg_allgather_rows.argtypes = [vp, vp, i64, vp, vp, vp]
-    for f in ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_graph_prepare", "fg_graph_tune",
+    for f in ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_graph_prepare", "fg_graph_prepare_hybrid",
+              "fg_graph_hybrid_info", "fg_graph_tune",
               "fg_graph_get_tune", "fg_spmm_workspace_size", "fg_spmm",
               "fg_sddmm", "fg_edge_softmax", "fg_gat_attention", "fg_graph_transpose", "fg_spmm_backward", "fg_sddmm_backward",
               "fg_edge_softmax_backward", "fg_comm_unique_id", "fg_comm_init", "fg_comm_destroy",
@@ -187,6 +192,19 @@ class Graph:
         is not segmented).  Call before timing / CUDA-graph capture."""
         _check(lib().fg_graph_prepare(self.handle, int(row_bytes), _stream(stream)), "fg_graph_prepare")
         return self
+
+    def prepare_hybrid(self, row_bytes: int, smem_bytes: int = 48 * 1024, stream=None) -> "Graph":
+        """fg_graph_prepare_hybrid: stage the smem_bytes // row_bytes sources of
+        highest out-degree in shared memory for copy_u-sum; enable
+        with tune("hybrid", 1).  Synchronous."""
+        _check(lib().fg_graph_prepare_hybrid(self.handle, int(row_bytes), int(smem_bytes), _stream(stream)),
+               "fg_graph_prepare_hybrid")
+        return self
+
+    def hybrid_info(self) -> tuple[int, float]:
+        k, share = ctypes.c_int64(0), ctypes.c_double(0)
+        _check(lib().fg_graph_hybrid_info(self.handle, ctypes.byref(k), ctypes.byref(share)), "fg_graph_hybrid_info")
+        return int(k.value), float(share.value)
 
     def tune(self, key: str, value: int) -> "Graph":
         """fg_graph_tune: set one launch knob of this handle (include/fg.h fg_tune_key)."""

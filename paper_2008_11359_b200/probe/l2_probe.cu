@@ -22,6 +22,8 @@
 //   returns 0 on success, else a cudaError_t; synchronises the device.
 #include <cstdint>
 #include <cstdio>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 namespace {
@@ -193,7 +195,144 @@ double tma_gbs(const char* X, int64_t x_bytes, int ctas_per_sm, float* sink, boo
     return gbs;
 }
 
+// The same gathers with the Blackwell TMA row gather (cp.async.bulk.tensor.2d
+// ... tile::gather4): ONE request moves 4 arbitrary rows x BOXC columns of a 2D
+// tensor map over X (rows x F fp32), so the per-request cost is amortised over
+// 4 rows -- the bulk-copy sweep above shows ~1 request per ~32 clk per SM.
+template <int F, int BOXC, int STAGES, int RPS, int NC, bool READ>
+__global__ void __launch_bounds__((NC + 1) * 32) tma_gather4_kernel(const __grid_constant__ CUtensorMap map,
+                                                                    int nrows, int iters, float* sink) {
+    constexpr int ROWB = F * 4;
+    extern __shared__ __align__(128) unsigned char sm[];
+    unsigned char* buf = sm;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * RPS * ROWB);
+    uint64_t* empty = full + STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NC * 32); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    float acc = 0.f;
+    if (warp == 0) {
+        constexpr int NCH = F / BOXC;          // column chunks per row
+        constexpr int NREQ = (RPS / 4) * NCH;  // gather4 requests per stage
+        for (int it = 0; it < iters; ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
+                             "r"(RPS * ROWB) : "memory");
+            __syncwarp();
+            for (int q = lane; q < NREQ; q += 32) {
+                const int g4 = q / NCH, ch = q % NCH;
+                int r[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    r[k] = int(hash32(uint32_t(blockIdx.x * 1000003u + it * RPS + g4 * 4 + k)) % uint32_t(nrows));
+                // smem: the 4 rows' column chunk ch, [4][BOXC] fp32, chunk-major inside the stage
+                unsigned char* dst = buf + s * RPS * ROWB + (g4 * NCH + ch) * 4 * BOXC * 4;
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                    ::"r"(smem_u32(dst)), "l"(&map), "r"(ch * BOXC), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]),
+                    "r"(smem_u32(&full[s])) : "memory");
+            }
+        }
+    } else {
+        const int ct = threadIdx.x - 32;
+        for (int it = 0; it < iters; ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&full[s], (it / STAGES) & 1);
+            if (READ) {
+                const float4* b4 = reinterpret_cast<const float4*>(buf + s * RPS * ROWB);
+                for (int i = ct; i < RPS * ROWB / 16; i += NC * 32) {
+                    const float4 v = b4[i];
+                    acc += v.x + v.y + v.z + v.w;
+                }
+            }
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+        }
+    }
+    if (acc == 1234.5f) sink[0] = acc;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+template <int F, int BOXC, int STAGES, int RPS, int NC, bool READ>
+double gather4_gbs(const char* X, int64_t x_bytes, int ctas_per_sm, float* sink, bool verbose) {
+    constexpr int ROWB = F * 4;
+    const int nrows = int(x_bytes / ROWB);
+    CUtensorMap map;
+    cuuint64_t gdim[2] = {cuuint64_t(F), cuuint64_t(nrows)};
+    cuuint64_t gstride[1] = {cuuint64_t(ROWB)};
+    cuuint32_t box[2] = {cuuint32_t(BOXC), 1u};
+    cuuint32_t estr[2] = {1u, 1u};
+    auto enc = encode_fn();
+    if (!enc) return -1;
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<char*>(X), gdim, gstride, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        if (verbose) printf("gather4 F=%d BOXC=%d: cuTensorMapEncodeTiled error %d\n", F, BOXC, int(r));
+        return -2;
+    }
+    const int smem = STAGES * RPS * ROWB + 2 * STAGES * 8;
+    auto k = tma_gather4_kernel<F, BOXC, STAGES, RPS, NC, READ>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    const int blocks = g_sms * ctas_per_sm;
+    const int64_t total = (1600LL << 20) / ROWB;
+    const int iters = int((total / blocks + RPS - 1) / RPS);
+    const float ms = best_ms([&] { k<<<blocks, (NC + 1) * 32, smem>>>(map, nrows, iters, sink); }, 5);
+    cudaError_t e = cudaGetLastError();
+    const double gbs = double(blocks) * iters * RPS * ROWB / (ms * 1e-3) / 1e9;
+    if (verbose)
+        printf("tma-gather4 F=%4d box=%3d X=%4lld MiB stages=%d rows/stage=%d consumers=%d ctas/SM=%d read=%d: "
+               "%.3f ms %.1f GB/s %s\n", F, BOXC, (long long)(x_bytes >> 20), STAGES, RPS, NC, ctas_per_sm,
+               int(READ), ms, gbs, e == cudaSuccess ? "" : cudaGetErrorString(e));
+    return gbs;
+}
+
 }  // namespace
+
+// TMA gather4 sweep (tooling only): out4 = best GB/s for F = 128 (512 B rows)
+// without / with the shared-memory read, and F = 256 (1 KiB rows) without / with.
+extern "C" int fgprobe_gather4(void* buf, int64_t buf_bytes, double* out4, int verbose) {
+    if (!buf || !out4 || buf_bytes < (96LL << 20)) return int(cudaErrorInvalidValue);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    const char* X = static_cast<const char*>(buf);
+    float* sink = reinterpret_cast<float*>(static_cast<char*>(buf) + buf_bytes - 64);
+    const int64_t xb = 64LL << 20;
+    double a = 0, b = 0, c = 0, d = 0;
+    a = maxd(a, gather4_gbs<128, 128, 8, 16, 4, false>(X, xb, 2, sink, verbose));
+    a = maxd(a, gather4_gbs<128, 128, 4, 32, 4, false>(X, xb, 3, sink, verbose));
+    a = maxd(a, gather4_gbs<128, 128, 8, 8, 4, false>(X, xb, 4, sink, verbose));
+    b = maxd(b, gather4_gbs<128, 128, 8, 16, 4, true>(X, xb, 2, sink, verbose));
+    b = maxd(b, gather4_gbs<128, 128, 4, 32, 8, true>(X, xb, 3, sink, verbose));
+    b = maxd(b, gather4_gbs<128, 128, 8, 8, 4, true>(X, xb, 4, sink, verbose));
+    c = maxd(c, gather4_gbs<256, 256, 8, 8, 4, false>(X, xb, 2, sink, verbose));
+    c = maxd(c, gather4_gbs<256, 256, 4, 16, 4, false>(X, xb, 3, sink, verbose));
+    d = maxd(d, gather4_gbs<256, 256, 8, 8, 4, true>(X, xb, 2, sink, verbose));
+    d = maxd(d, gather4_gbs<256, 256, 4, 16, 8, true>(X, xb, 3, sink, verbose));
+    gather4_gbs<512, 256, 4, 8, 8, true>(X, xb, 3, sink, verbose);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    out4[0] = a; out4[1] = b; out4[2] = c; out4[3] = d;
+    return int(e);
+}
 
 // TMA bulk-copy row gathers vs the LDG gathers (verbose sweep; tooling only).
 // out4: best GB/s for 2 KiB rows without / with the shared-memory read, and for

@@ -21,3 +21,6 @@ o4 = (ctypes.c_double * 4)()
 rc = L.fgprobe_tma(ctypes.c_void_p(buf.data_ptr()), ctypes.c_int64(buf.numel()), o4, 1)
 print("tma best: 2KiB %.1f / read %.1f ; 512B %.1f / read %.1f  rc %d" % (o4[0], o4[1], o4[2], o4[3], rc))
 sys.stdout.flush()
+o4 = (ctypes.c_double * 4)()
+rc = L.fgprobe_gather4(ctypes.c_void_p(buf.data_ptr()), ctypes.c_int64(buf.numel()), o4, 1)
+print("gather4 best: F128 %.1f / read %.1f ; F256 %.1f / read %.1f  rc %d" % (o4[0], o4[1], o4[2], o4[3], rc))
