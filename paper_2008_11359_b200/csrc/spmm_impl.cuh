@@ -243,35 +243,16 @@ __device__ __forceinline__ void store_elem(const Args& A, int64_t v, int c, floa
     }
 }
 
-// HYB: the paper's hybrid partitioning on the GPU (P:534-539): the hyb_k sources
-// of highest out-degree are staged in shared memory once per CTA (persistent
-// grid-stride over the virtual blocks) and read from there; the others from
-// L2 / HBM.  Same values in the same order as the plain kernel: bit-identical.
-template <int G, int NV, int OP, int RED, bool XB, bool PAIR, bool HYB = false>
-__global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
+// One virtual block of the gather launch: CTA-per-row (vb < n_heavy) or a group
+// of rows per CTA.  The shared buffers belong to the calling kernel.
+template <int G, int NV, int OP, int RED, bool XB, bool PAIR, bool HYB, typename SAcc, typename SEt, typename SVal,
+          typename SPos>
+__device__ __forceinline__ void spmm_vblock(const Args& A, int64_t vb, int gl, int gi, unsigned mask, int c4base,
+                                            SAcc& s_acc, SEt& s_etile, SVal& s_val, SPos& s_pos,
+                                            const float4* __restrict__ s_hot) {
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);
     constexpr int NG = THREADS / G;                 // groups per CTA
     constexpr int TW = G * NV;                      // float4 columns per tile
-    __shared__ float4 s_acc[MAX ? 1 : NG][MAX ? 1 : TW];
-    __shared__ float s_etile[stage_e<G, OP, RED>() ? NG : 1][stage_e<G, OP, RED>() ? 32 * 16 : 1];
-    __shared__ float s_val[MAX ? NG : 1][MAX ? TW * 4 : 1];
-    __shared__ int s_pos[MAX ? NG : 1][MAX ? TW * 4 : 1];
-
-    extern __shared__ float4 s_hot[];   // HYB: hyb_k staged source rows of F4 float4
-    const int lane = threadIdx.x & 31;
-    const int gl = threadIdx.x & (G - 1);
-    const int gi = threadIdx.x / G;
-    const unsigned mask = group_mask<G>(lane);
-    const int c4base = blockIdx.y * TW;
-    if constexpr (HYB) {
-        for (int i = threadIdx.x; i < A.hyb_k * A.F4; i += THREADS) {
-            const int k = i / A.F4, c = i - k * A.F4;
-            s_hot[i] = __ldg(A.X + int64_t(__ldg(A.hyb_hot + k)) * A.F4 + c);
-        }
-        __syncthreads();
-    }
-
-    for (int64_t vb = blockIdx.x; vb < A.n_vblocks; vb += gridDim.x) {
     float4 acc[NV];
     int pos[NV][4];
     init_acc<NV, RED>(acc, pos);
@@ -317,13 +298,13 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
             }
             store_elem<RED>(A, v, c4base + c, a, ps, e - s);
         }
-        __syncthreads();   // the combine buffers are reused by this CTA's next virtual block
-        continue;
+        if constexpr (HYB) __syncthreads();   // the combine buffers are reused by this CTA's next virtual block
+        return;
     }
 
     // ---- group-per-row
     const int64_t r = A.n_heavy + (vb - A.n_heavy) * NG + gi;
-    if (r >= A.n_rows) continue;
+    if (r >= A.n_rows) return;
     const int64_t v = A.rows[r];
     const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
     gather_range<G, NV, OP, RED, XB, PAIR, HYB>(A, s, e, gl, mask, c4base, acc, pos, s_etile[gi], s_hot);
@@ -332,7 +313,43 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
         const int c = c4base + colj<G, PAIR>(gl, j);
         if (c < A.F4) store_elem<RED>(A, v, c, acc[j], pos[j], e - s);
     }
-    }   // virtual blocks
+}
+
+// HYB: the paper's hybrid partitioning on the GPU (P:534-539): the hyb_k sources
+// of highest out-degree are staged in shared memory once per CTA (persistent
+// grid-stride over the virtual blocks) and read from there; the others from
+// L2 / HBM.  Same values in the same order as the plain kernel: bit-identical.
+template <int G, int NV, int OP, int RED, bool XB, bool PAIR, bool HYB = false>
+__global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
+    constexpr bool MAX = (RED == R_MAX || RED == R_MIN);
+    constexpr int NG = THREADS / G;                 // groups per CTA
+    constexpr int TW = G * NV;                      // float4 columns per tile
+    __shared__ float4 s_acc[MAX ? 1 : NG][MAX ? 1 : TW];
+    __shared__ float s_etile[stage_e<G, OP, RED>() ? NG : 1][stage_e<G, OP, RED>() ? 32 * 16 : 1];
+    __shared__ float s_val[MAX ? NG : 1][MAX ? TW * 4 : 1];
+    __shared__ int s_pos[MAX ? NG : 1][MAX ? TW * 4 : 1];
+
+    extern __shared__ float4 s_hot[];   // HYB: hyb_k staged source rows of F4 float4
+    const int lane = threadIdx.x & 31;
+    const int gl = threadIdx.x & (G - 1);
+    const int gi = threadIdx.x / G;
+    const unsigned mask = group_mask<G>(lane);
+    const int c4base = blockIdx.y * TW;
+    if constexpr (HYB) {
+        for (int i = threadIdx.x; i < A.hyb_k * A.F4; i += THREADS) {
+            const int k = i / A.F4, c = i - k * A.F4;
+            s_hot[i] = __ldg(A.X + int64_t(__ldg(A.hyb_hot + k)) * A.F4 + c);
+        }
+        __syncthreads();
+    }
+
+    if constexpr (HYB) {
+        for (int64_t vb = blockIdx.x; vb < A.n_vblocks; vb += gridDim.x)
+            spmm_vblock<G, NV, OP, RED, XB, PAIR, HYB>(A, vb, gl, gi, mask, c4base, s_acc, s_etile, s_val, s_pos, s_hot);
+    } else {   // one virtual block per CTA: the plain launch (no loop, no extra registers)
+        spmm_vblock<G, NV, OP, RED, XB, PAIR, HYB>(A, blockIdx.x, gl, gi, mask, c4base, s_acc, s_etile, s_val, s_pos,
+                                                   s_hot);
+    }
 }
 
 template <int G, int NV, int OP, int RED, bool XB = false, bool PAIR = false, bool HYB = false>
