@@ -621,6 +621,7 @@ def main():
         "mlp_tflops": round(mlp_flops(S.m) / (mlp_ms * 1e-3) / 1e12, 2),
         "mlp_roofline": mlp_roofline(S.m, mlp_ms, sm_mhz),
         "roofline": roof,
+        "ops_physical": ops_physical(op_ms, hbm_peak, world, "uniform" if args.uniform_sources else "default"),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": Step.LAUNCHES_PER_STEP * args.steps,
@@ -751,6 +752,29 @@ def sm_max_mhz() -> float:
         return 1965.0
 
 
+def ops_physical(op_ms, hbm_peak, world, variant) -> dict | None:
+    """Per op of the step: the physical DRAM and L2 rates (ncu bytes of one
+    launch of THIS build, profiles/ncu_traffic.json, over this run's event
+    time) -- e.g. the edge softmax, whose traffic must come from HBM, against
+    the measured HBM copy peak."""
+    if world != 1:
+        return None
+    res = {}
+    for op, ms in op_ms.items():
+        rec, fresh, _ = ncu_record(op, variant)
+        if not (rec and fresh):
+            continue
+        t = ms * 1e-3
+        d = {"dram_gbs": round(rec["dram_bytes_per_launch"] / t / 1e9, 1),
+             "dram_frac": round(rec["dram_bytes_per_launch"] / t / 1e9 / hbm_peak, 4)}
+        if rec.get("l2_bytes_per_launch"):
+            d["l2_gbs"] = round(rec["l2_bytes_per_launch"] / t / 1e9, 1)
+        if rec.get("lts_throughput_pct") and rec.get("ncu_time_s"):
+            d["l2_frac_of_ncu_peak"] = round(rec["lts_throughput_pct"] / 100.0 * rec["ncu_time_s"] / t, 4)
+        res[op] = d
+    return res or None
+
+
 def mlp_roofline(m: int, ms: float, sm_mhz: float, d2: int = D2, sms: int = 148) -> dict:
     """The tcgen05 MLP kernel against its bound, reading every fp32 accumulator
     element out of TMEM (m x d2 x 4 bytes) at the guide's LDTM throughput of
@@ -869,22 +893,30 @@ def run_extras(S, args, sync_all, flush, world):
     res["C4_rand100k_copy_u_sum_F128_ms"] = round(timed(
         lambda: fgp.spmm(Gr, "copy_u", "sum", X128, out=o128, stream=st)), 4)
     del Gr, gr, X8, W, o, au, ae, X128, o128
-    # C6: DRAM-bound control: uniform sources, F = 512
+    # C6: the control with uniform sources, F = 512: with the L2
+    # techniques on (column tiles / source segments, the default) and off ("direct":
+    # every gather that misses L2 goes to HBM -- the physical DRAM-bound case)
     gu, Gu = graph_on_gpu("reddit", uniform=True)
     Gu.prepare(F_DOT * 4)
     Xu = S.X["X512"]
     ou = torch.empty(gu.n_dst, F_GCN, device=dev)
     su = torch.empty(gu.nnz, 1, device=dev)
     ob = op_bytes(gu.n_dst, gu.nnz)
+    hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)) if \
+        os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     ctl = {}
-    for name, fn in (("spmm_copy_u_sum_F512", lambda: fgp.spmm(Gu, "copy_u", "sum", Xu, out=ou, stream=st)),
-                     ("sddmm_u_dot_v_H1_F512", lambda: fgp.sddmm(Gu, Xu, Xu, H=1, out=su, stream=st))):
-        t = timed(fn)
-        rec, fresh, _ = ncu_record(name, "uniform")
-        d = {"ms": round(t, 4), "gather_model_gbs": round(ob[name] / (t * 1e-3) / 1e9, 1), "ncu_fresh": bool(fresh)}
-        if rec and fresh and rec.get("dram_bytes_per_launch"):
-            d["dram_gbs"] = round(rec["dram_bytes_per_launch"] / (t * 1e-3) / 1e9, 1)
-        ctl[name] = d
+    for variant, knobs in (("uniform", {}), ("uniform_direct", {"l2_tile_mb": 0, "sddmm_seg_mb": 0})):
+        for k, v in knobs.items():
+            Gu.tune(k, v)
+        for name, fn in (("spmm_copy_u_sum_F512", lambda: fgp.spmm(Gu, "copy_u", "sum", Xu, out=ou, stream=st)),
+                         ("sddmm_u_dot_v_H1_F512", lambda: fgp.sddmm(Gu, Xu, Xu, H=1, out=su, stream=st))):
+            t = timed(fn)
+            rec, fresh, _ = ncu_record(name, variant)
+            d = {"ms": round(t, 4), "gather_model_gbs": round(ob[name] / (t * 1e-3) / 1e9, 1), "ncu_fresh": bool(fresh)}
+            if rec and fresh and rec.get("dram_bytes_per_launch"):
+                d["dram_gbs"] = round(rec["dram_bytes_per_launch"] / (t * 1e-3) / 1e9, 1)
+                d["dram_frac"] = round(d["dram_gbs"] / hbm, 4)
+            ctl[f"{name}_{variant}"] = d
     res["C6_uniform_sources_control"] = ctl
     del Gu, gu, ou, su
     torch.cuda.empty_cache()

@@ -5,6 +5,7 @@
 #   PART=sddmm  ncu --set full of the gSDDMM kernels of one step
 #   PART=2      ncu --set full of softmax, MLP (tcgen05) and the fused GAT
 #   PART=ctl    ncu --set full of the uniform-sources control (copy_u-sum, u_dot_v F=512)
+#   PART=direct the same with the L2 column tiles / source segments off (DRAM-bound)
 mkdir -p gpurun_out
 TAG=${TAG:-r02}
 B="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-extras"
@@ -33,6 +34,11 @@ timeout 600 $NCU -k regex:gat_fused -s 0 -c 1 -o gpurun_out/prof_gat_$TAG python
 ctl)
 timeout 900 $NCU -k regex:spmm_gather -s 9 -c 1 -o gpurun_out/prof_uspmm_$TAG $B --uniform-sources > /dev/null 2>&1; echo uspmm $?
 timeout 900 $NCU -k regex:sddmm_kernel -s 6 -c 1 -o gpurun_out/prof_usddmm_$TAG $B --uniform-sources > /dev/null 2>&1; echo usddmm $?
+;;
+direct)
+export FG_L2_TILE_MB=0 FG_SDDMM_SEG_MB=0
+timeout 900 $NCU -k regex:spmm_gather -s 9 -c 1 -o gpurun_out/prof_dspmm_$TAG $B --uniform-sources > /dev/null 2>&1; echo dspmm $?
+timeout 900 $NCU -k regex:sddmm_kernel -s 6 -c 1 -o gpurun_out/prof_dsddmm_$TAG $B --uniform-sources > /dev/null 2>&1; echo dsddmm $?
 ;;
 esac
 ls -la gpurun_out | tail -12

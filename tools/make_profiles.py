@@ -33,6 +33,8 @@ OPS_BY_FILE = {   # file key -> (variant, ops in capture order)
     "gat": ("default", ["extra_gat_fused_H8_D32"]),
     "uspmm": ("uniform", ["spmm_copy_u_sum_F512"]),
     "usddmm": ("uniform", ["sddmm_u_dot_v_H1_F512"]),
+    "dspmm": ("uniform_direct", ["spmm_copy_u_sum_F512"]),
+    "dsddmm": ("uniform_direct", ["sddmm_u_dot_v_H1_F512"]),
 }
 
 
@@ -52,7 +54,7 @@ lines = [f"# ncu --set full summaries ({tag})", "",
          "kernels of one timed `bench.py` step (reddit-shaped graph, 232,965 v / 114,615,892 e). "
          "Times are ncu replay times (cold-cache, serialised), not bench values.", ""]
 traffic = {"build_hash": os.environ.get("FG_BUILD_HASH") or source_hash(), "capture": tag,
-           "default": {}, "uniform": {}}
+           "default": {}, "uniform": {}, "uniform_direct": {}}
 for key, (variant, ops) in OPS_BY_FILE.items():
     path = os.path.join(ROOT, "gpurun_out", f"prof_{key}_{tag}.ncu-rep")
     if not os.path.exists(path):
@@ -72,7 +74,8 @@ for key, (variant, ops) in OPS_BY_FILE.items():
                                 "dram_write": wr, "l2_bytes_per_launch": lts, "lts_throughput_pct": lpct,
                                 "ncu_time_s": t, "dram_gbs": (rd + wr) / t / 1e9 if t else None,
                                 "l2_hit_pct": d.get("lts__t_sector_hit_rate.pct"), "capture": f"prof_{key}_{tag}"}
-        lines += [f"## {op}" + (" (uniform-sources control)" if variant == "uniform" else ""), "",
+        lines += [f"## {op}" + {"default": "", "uniform": " (uniform-sources control)",
+                                 "uniform_direct": " (uniform sources, L2 tiling / segments off)"}[variant], "",
                   f"`{d['kernel']}`", "", "| metric | value |", "|---|---|"]
         for k, v in d.items():
             if k in ("kernel", "top_stalls"):
