@@ -406,6 +406,41 @@ extern "C" int fgprobe_l2_verbose(void* buf, int64_t buf_bytes, double* out5, in
     return int(e);
 }
 
+
+// X-size sweep (tooling only): random 2 KiB-row LDG gathers and sequential
+// re-reads over an X of 4..160 MiB, ~6.4 GB moved per launch.  Tests whether
+// the gather ceiling depends on how much of the L2 the working set occupies
+// (B200's L2 is two halves, one per die).  out[2*i], out[2*i+1] = gather,
+// stream GB/s for the i-th size in sizes_mb (n sizes).
+extern "C" int fgprobe_xsweep(void* buf, int64_t buf_bytes, const int* sizes_mb, int n, double* out, int verbose) {
+    if (!buf || !out || !sizes_mb) return int(cudaErrorInvalidValue);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    const float4* X = reinterpret_cast<const float4*>(buf);
+    float* sink = reinterpret_cast<float*>(static_cast<char*>(buf) + buf_bytes - 64);
+    for (int i = 0; i < n; ++i) {
+        const int64_t xb = int64_t(sizes_mb[i]) << 20;
+        if (xb + 4096 > buf_bytes) { out[2 * i] = out[2 * i + 1] = 0; continue; }
+        const int F = 512, F4 = 128, G = 32, U = 4;
+        const int nrows = int(xb / (F * 4));
+        const int blocks = g_sms * 4;
+        const int64_t groups = int64_t(blocks) * 256 / G;
+        const int64_t total_rows = (6400LL << 20) / (F * 4);
+        const int64_t rpg = (total_rows / groups + U - 1) / U * U;
+        float ms = best_ms([&] { gather_kernel<32, 4, 4><<<blocks, 256>>>(X, nrows, F4, rpg, sink); }, 3);
+        out[2 * i] = double(groups) * rpg * F * 4 / (ms * 1e-3) / 1e9;
+        const int64_t n4 = xb / 16;
+        const int reps = int((6400LL << 20) / xb);
+        ms = best_ms([&] { stream_kernel<<<g_sms * 8, 256>>>(X, n4, reps, sink); }, 3);
+        out[2 * i + 1] = double(reps) * xb / (ms * 1e-3) / 1e9;
+        if (verbose) printf("xsweep X=%4d MiB: gather 2KiB rows %.1f GB/s, stream %.1f GB/s\n", sizes_mb[i], out[2 * i], out[2 * i + 1]);
+    }
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return int(e);
+}
+
 extern "C" int fgprobe_l2(void* buf, int64_t buf_bytes, double* out5) {
     return fgprobe_l2_verbose(buf, buf_bytes, out5, 0);
 }
