@@ -130,12 +130,19 @@ typedef struct {
 fg_status fg_graph_info(const fg_graph* g, fg_graph_info_t* info);
 
 /*
- * fg_graph_prepare -- the per-topology table of the source-segmented gSDDMM
- * traversal for gathered rows of `row_bytes` bytes (H*D*4 for fp32 features,
- * H*D*2 for bf16 storage): the paper's 1D source partitioning
- * with segments sized to the B200 L2.  It applies only when the
- * source features are wider than the segmentation threshold (48 MB segments
- * for X > 96 MB by default); otherwise it builds nothing and returns FG_OK.
+ * fg_graph_prepare -- the per-topology tables of the source-segmented gSDDMM
+ * traversal and of the source-segmented u_mul_e-sum passes of gSpMM for
+ * gathered rows of `row_bytes` bytes (H*D*4 for fp32 features, H*D*2 for bf16
+ * storage): the paper's 1D source partitioning with segments sized
+ * to the B200 L2.  It applies only when the source features
+ * are wider than the segmentation threshold (48 MB segments for X > 96 MB by
+ * default); otherwise it builds nothing and returns FG_OK.  With
+ * FG_TUNE_SPMM_SEG_MB set (off by default), fg_spmm u_mul_e-sum
+ * (fp32, D % 4 == 0) on a prepared width runs one pass per segment in segment
+ * order, each adding its sources' messages onto out: a group-per-row row keeps
+ * the CSR summation order (bit-identical to the unprepared call); a row split
+ * CTA-per-row (degree >= the heavy threshold) sums in another fixed order
+ * (deterministic, equal to rounding).
  * SYNCHRONOUS on `stream` (allocates device memory, reads counts back), like
  * fg_graph_create; idempotent per width.  fg_sddmm / fg_sddmm_emul /
  * fg_sddmm_x16 / fg_dist_sddmm never allocate or synchronise (so they can be
@@ -175,6 +182,12 @@ fg_status fg_graph_prepare(fg_graph* g, int64_t row_bytes, fg_stream stream);
  *                          copy_u-sum (the paper's hybrid partitioning,
  *                          P:534-539) when fg_graph_prepare_hybrid built the
  *                          table for that width (ablation E7)
+ *   FG_TUNE_SPMM_SEG_MB    source-segment size in MB of the segmented
+ *                          u_mul_e-sum passes of fg_spmm (0 = off, the default:
+ *                          on reddit H=8 D=32 48 MB segments cut DRAM traffic
+ *                          19.7 -> 9.4 GB but ran 8.07 vs 7.47 ms; only for X
+ *                          wider than FG_TUNE_SDDMM_SEG_MIN_MB, and only once
+ *                          fg_graph_prepare built the bounds with it set)
  *   Errors: FG_EINVAL (NULL, unknown key, out-of-range value).
  */
 /*
@@ -207,7 +220,8 @@ typedef enum {
     FG_TUNE_SDDMM_DOT = 7,
     FG_TUNE_GAT_HEAVY_DEG = 8,
     FG_TUNE_MLP_IMPL = 9,
-    FG_TUNE_HYBRID = 10
+    FG_TUNE_HYBRID = 10,
+    FG_TUNE_SPMM_SEG_MB = 11
 } fg_tune_key;
 fg_status fg_graph_tune(fg_graph* g, fg_tune_key key, int64_t value);
 fg_status fg_graph_get_tune(const fg_graph* g, fg_tune_key key, int64_t* value);

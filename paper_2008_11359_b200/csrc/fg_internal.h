@@ -27,6 +27,8 @@ struct fg_tuning {
     int64_t gat_heavy_deg = 4096;   // CTA-per-row threshold of the fused GAT
     int64_t mlp_impl = 0;           // 0: tcgen05 3xTF32, 1: CUDA-core FFMA, 2: tcgen05 bf16 2-split (K = 32)
     int64_t hybrid = 0;             // 1: hot sources staged in shared memory (needs fg_graph_prepare_hybrid)
+    int64_t spmm_seg_mb = 0;        // source-segment size of the segmented u_mul_e-sum passes (0: off;
+                                    // measured slower); only when X > sddmm_seg_min_mb
 };
 
 struct fg_graph {
@@ -58,6 +60,15 @@ struct fg_graph {
         int64_t* p1 = nullptr;
     };
     std::deque<SegUnits> seg_units;      // deque: references stay valid as it grows
+    // source-segmented gSpMM passes (u_mul_e-sum; same 1D source partitioning):
+    // bnd[s * n_dst + v] = first CSR position of row v whose source is >= s * seg_rows,
+    // s = 0..nseg (bnd[0] = row_ptr[v], bnd[nseg] = row_ptr[v + 1]); fg_graph_prepare
+    struct SegBounds {
+        int64_t seg_rows = 0;
+        int nseg = 0;
+        int64_t* bnd = nullptr;   // [(nseg + 1) * n_dst]
+    };
+    std::deque<SegBounds> seg_bounds;
     std::mutex seg_mu;                   // guards seg_units against concurrent fg_graph_prepare calls
 
     // hybrid partitioning table (fg_graph_prepare_hybrid): per-edge
@@ -127,6 +138,10 @@ const fg_graph::SegUnits* find_seg_units(const fg_graph* g, int64_t seg_rows);
 // segment rows of the segmented gSDDMM for gathered rows of row_bytes, or 0 when
 // the rule does not segment (X = n_src x row_bytes within the budget)
 int64_t sddmm_seg_rows(const fg_graph* g, int64_t row_bytes);
+// the same for the segmented u_mul_e-sum passes of gSpMM, and its bound tables
+int64_t spmm_seg_rows(const fg_graph* g, int64_t row_bytes);
+fg_status build_seg_bounds(fg_graph* g, int64_t seg_rows, cudaStream_t st);
+const fg_graph::SegBounds* find_seg_bounds(const fg_graph* g, int64_t seg_rows);
 
 // column-tile budget (bytes of the gathered operand per pass) of the copy_u
 // gather, the paper's feature-dimension tiling retargeted to the L2.

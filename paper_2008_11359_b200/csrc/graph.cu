@@ -35,6 +35,7 @@ void tuning_from_env(fg_tuning* t) {
     rd("FG_GAT_HEAVY_DEG", t->gat_heavy_deg);
     rd("FG_MLP_IMPL", t->mlp_impl);
     rd("FG_HYBRID", t->hybrid);
+    rd("FG_SPMM_SEG_MB", t->spmm_seg_mb);
 }
 }  // namespace fgk
 
@@ -120,7 +121,61 @@ __global__ void seg_write_kernel(int64_t n, int nseg, int64_t seg_rows, int chun
     }
 }
 
+// bounds of the source-segmented gSpMM passes: bnd[s * n + v] for s = 0..nseg
+__global__ void seg_bound_kernel(int64_t n, int nseg, int64_t seg_rows, const int64_t* __restrict__ rp,
+                                 const int32_t* __restrict__ ci, int64_t* __restrict__ bnd) {
+    const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int64_t s0 = rp[v], s1 = rp[v + 1];
+    int64_t lo = s0;
+    bnd[v] = s0;
+    for (int s = 1; s < nseg; ++s) {
+        lo = lb_row(ci, lo, s1, s * seg_rows);
+        bnd[int64_t(s) * n + v] = lo;
+    }
+    bnd[int64_t(nseg) * n + v] = s1;
+}
+
 namespace fgk {
+fg_status build_seg_bounds(fg_graph* g, int64_t seg_rows, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(g->seg_mu);
+    for (auto& sb : g->seg_bounds)
+        if (sb.seg_rows == seg_rows) return FG_OK;
+    const int64_t n = g->n_dst;
+    fg_graph::SegBounds sb;
+    sb.seg_rows = seg_rows;
+    sb.nseg = int((g->n_src + seg_rows - 1) / seg_rows);
+    cudaError_t e = cudaMalloc(&sb.bnd, sizeof(int64_t) * size_t(std::max<int64_t>(1, (sb.nseg + 1) * n)));
+    if (e == cudaSuccess && n > 0) {
+        seg_bound_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(n, sb.nseg, seg_rows, g->row_ptr, g->col_idx,
+                                                                    sb.bnd);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        cudaFree(sb.bnd);
+        return set_error(e == cudaErrorMemoryAllocation ? FG_ENOMEM : FG_ECUDA, "fg_graph_prepare: segment bounds: %s",
+                         cudaGetErrorString(e));
+    }
+    g->device_bytes += 8 * (sb.nseg + 1) * n;
+    g->seg_bounds.push_back(sb);
+    return FG_OK;
+}
+
+const fg_graph::SegBounds* find_seg_bounds(const fg_graph* g, int64_t seg_rows) {
+    std::lock_guard<std::mutex> lock(const_cast<fg_graph*>(g)->seg_mu);
+    for (auto& sb : g->seg_bounds)
+        if (sb.seg_rows == seg_rows) return &sb;
+    return nullptr;
+}
+
+int64_t spmm_seg_rows(const fg_graph* g, int64_t row_bytes) {
+    const int64_t budget = g->tune.spmm_seg_mb << 20;
+    const int64_t min_x = g->tune.sddmm_seg_min_mb << 20;
+    if (budget <= 0 || row_bytes <= 0 || g->n_src * row_bytes <= std::max(budget, min_x)) return 0;
+    return std::max<int64_t>(32, budget / row_bytes);
+}
+
 fg_status build_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t st) {
     std::lock_guard<std::mutex> lock(g->seg_mu);
     for (auto& su : g->seg_units)
@@ -331,6 +386,7 @@ extern "C" fg_status fg_graph_destroy(fg_graph* g) {
         cudaFree(su.p0);
         cudaFree(su.p1);
     }
+    for (auto& sb : g->seg_bounds) cudaFree(sb.bnd);
     if (g->hyb.code) cudaFree(g->hyb.code);
     if (g->hyb.hot) cudaFree(g->hyb.hot);
     if (g->owned_row_ptr) cudaFree(g->owned_row_ptr);
@@ -371,6 +427,7 @@ extern "C" fg_status fg_graph_tune(fg_graph* g, fg_tune_key key, int64_t value) 
             t.mlp_impl = value;
             break;
         case FG_TUNE_HYBRID: t.hybrid = value != 0; break;
+        case FG_TUNE_SPMM_SEG_MB: t.spmm_seg_mb = std::max<int64_t>(0, value); break;
         default: return fgk::set_error(FG_EINVAL, "fg_graph_tune: bad key %d", int(key));
     }
     return FG_OK;
@@ -391,6 +448,7 @@ extern "C" fg_status fg_graph_get_tune(const fg_graph* g, fg_tune_key key, int64
         case FG_TUNE_GAT_HEAVY_DEG: *value = t.gat_heavy_deg; break;
         case FG_TUNE_MLP_IMPL: *value = t.mlp_impl; break;
         case FG_TUNE_HYBRID: *value = t.hybrid; break;
+        case FG_TUNE_SPMM_SEG_MB: *value = t.spmm_seg_mb; break;
         default: return fgk::set_error(FG_EINVAL, "fg_graph_get_tune: bad key %d", int(key));
     }
     return FG_OK;
@@ -399,9 +457,15 @@ extern "C" fg_status fg_graph_get_tune(const fg_graph* g, fg_tune_key key, int64
 extern "C" fg_status fg_graph_prepare(fg_graph* g, int64_t row_bytes, fg_stream stream) {
     if (!g) return fgk::set_error(FG_EINVAL, "fg_graph_prepare: NULL handle");
     if (row_bytes <= 0) return fgk::set_error(FG_ESHAPE, "fg_graph_prepare: row_bytes must be > 0");
-    const int64_t seg_rows = fgk::sddmm_seg_rows(g, row_bytes);
-    if (seg_rows == 0 || g->nnz == 0) return FG_OK;   // this width is not segmented: nothing to build
-    return fgk::build_seg_units(g, seg_rows, g->unit_chunk, reinterpret_cast<cudaStream_t>(stream));
+    if (g->nnz == 0) return FG_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t seg_rows = fgk::sddmm_seg_rows(g, row_bytes);   // 0: this width is not segmented
+    if (seg_rows) {
+        const fg_status s = fgk::build_seg_units(g, seg_rows, g->unit_chunk, st);
+        if (s != FG_OK) return s;
+    }
+    const int64_t spmm_rows = fgk::spmm_seg_rows(g, row_bytes);
+    return spmm_rows ? fgk::build_seg_bounds(g, spmm_rows, st) : FG_OK;
 }
 
 // ---------------------------------------------------------------- hybrid partitioning

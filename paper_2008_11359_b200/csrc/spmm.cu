@@ -60,6 +60,8 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     A.hyb_hot = nullptr;
     A.hyb_k = 0;
     A.n_vblocks = 0;
+    A.seg_lo = A.seg_hi = nullptr;
+    A.seg_acc = 0;
     const int op = (msg == FG_MSG_COPY_U)    ? OP_COPY
                    : (msg == FG_MSG_U_ADD_E) ? OP_UADDE
                    : (msg == FG_MSG_COPY_E)  ? OP_COPYE
@@ -138,6 +140,26 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
         A.hyb_hot = g->hyb.hot;
         A.hyb_k = int(g->hyb.k);
         return launch_hybrid(A, G, st);
+    }
+    // source-segmented u_mul_e-sum (the paper's 1D source partitioning, P:462-465,
+    // with L2-sized segments; bounds from fg_graph_prepare for this row width):
+    // one pass per segment in segment order, each gathering only from its
+    // L2-resident X slice and adding onto out.  Column tiling does not apply to
+    // u_mul_e (every tile would re-read E); segmenting reads E and col_idx once
+    // and re-reads only out (2 x n x F x 4 bytes per extra pass).
+    if (op == OP_UMULE && mx == R_SUM && !Xbf16 && F4 == A.F4) {
+        const int64_t seg_rows = fgk::spmm_seg_rows(g, int64_t(A.F4) * 16);
+        const fg_graph::SegBounds* sb = seg_rows ? fgk::find_seg_bounds(g, seg_rows) : nullptr;
+        if (sb) {
+            for (int s = 0; s < sb->nseg; ++s) {
+                A.seg_lo = sb->bnd + int64_t(s) * g->n_dst;
+                A.seg_hi = sb->bnd + int64_t(s + 1) * g->n_dst;
+                A.seg_acc = s > 0;
+                const fg_status r = launch_seg_pass(A, G, NV, st);
+                if (r != FG_OK) return r;
+            }
+            return FG_OK;
+        }
     }
     const int opset = (op == OP_UADDE || op == OP_COPYE) ? 1 : 0;
     if (Xbf16) {   // bf16 storage: copy_u / u_mul_e x {sum, max} (validated by the caller)

@@ -38,6 +38,13 @@ struct Args {
     const int32_t* hyb_hot;
     int hyb_k;
     int64_t n_vblocks;          // virtual blocks of the launch (HYB: persistent grid-stride)
+    // source-segmented pass (SEG kernels only; u_mul_e / copy_u sum): row v's edges
+    // with sources in this pass's segment are [seg_lo[v], seg_hi[v]); seg_acc != 0:
+    // the pass adds onto out (passes run in segment order, so a group-per-row sum
+    // keeps the CSR order of the unsegmented kernel)
+    const int64_t* seg_lo;
+    const int64_t* seg_hi;
+    int seg_acc;
 };
 
 __device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); }
@@ -245,8 +252,8 @@ __device__ __forceinline__ void store_elem(const Args& A, int64_t v, int c, floa
 
 // One virtual block of the gather launch: CTA-per-row (vb < n_heavy) or a group
 // of rows per CTA.  The shared buffers belong to the calling kernel.
-template <int G, int NV, int OP, int RED, bool XB, bool PAIR, bool HYB, typename SAcc, typename SEt, typename SVal,
-          typename SPos>
+template <int G, int NV, int OP, int RED, bool XB, bool PAIR, bool HYB, bool SEG, typename SAcc, typename SEt,
+          typename SVal, typename SPos>
 __device__ __forceinline__ void spmm_vblock(const Args& A, int64_t vb, int gl, int gi, unsigned mask, int c4base,
                                             SAcc& s_acc, SEt& s_etile, SVal& s_val, SPos& s_pos,
                                             const float4* __restrict__ s_hot) {
@@ -260,7 +267,8 @@ __device__ __forceinline__ void spmm_vblock(const Args& A, int64_t vb, int gl, i
     if (vb < A.n_heavy) {
         // ---- CTA-per-row: contiguous edge ranges per group, fixed-order combine
         const int64_t v = A.rows[vb];
-        const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
+        const int64_t s = SEG ? A.seg_lo[v] : A.row_ptr[v], e = SEG ? A.seg_hi[v] : A.row_ptr[v + 1];
+        if (SEG && A.seg_acc && s == e) return;   // nothing to add (uniform across the CTA)
         const int64_t len = (e - s + NG - 1) / NG;
         const int64_t gs = min(e, s + gi * len), ge = min(e, gs + len);
         gather_range<G, NV, OP, RED, XB, PAIR, HYB>(A, gs, ge, gl, mask, c4base, acc, pos, s_etile[gi], s_hot);
@@ -281,6 +289,11 @@ __device__ __forceinline__ void spmm_vblock(const Args& A, int64_t vb, int gl, i
             int ps[4] = {-1, -1, -1, -1};
             if constexpr (!MAX) {
                 a = s_acc[0][c];
+                if (SEG && A.seg_acc) {   // earlier segments' sum + this pass's partials, fixed order
+                    const float4 b = a;
+                    a = A.out[v * A.F4 + c4base + c];
+                    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+                }
                 for (int g2 = 1; g2 < NG; ++g2) {
                     const float4 b = s_acc[g2][c];
                     a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
@@ -306,7 +319,17 @@ __device__ __forceinline__ void spmm_vblock(const Args& A, int64_t vb, int gl, i
     const int64_t r = A.n_heavy + (vb - A.n_heavy) * NG + gi;
     if (r >= A.n_rows) return;
     const int64_t v = A.rows[r];
-    const int64_t s = A.row_ptr[v], e = A.row_ptr[v + 1];
+    const int64_t s = SEG ? A.seg_lo[v] : A.row_ptr[v], e = SEG ? A.seg_hi[v] : A.row_ptr[v + 1];
+    if constexpr (SEG) {
+        if (A.seg_acc) {
+            if (s == e) return;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {   // continue the running sum of the earlier segments
+                const int c = c4base + colj<G, PAIR>(gl, j);
+                if (c < A.F4) acc[j] = A.out[v * A.F4 + c];
+            }
+        }
+    }
     gather_range<G, NV, OP, RED, XB, PAIR, HYB>(A, s, e, gl, mask, c4base, acc, pos, s_etile[gi], s_hot);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
@@ -319,7 +342,7 @@ __device__ __forceinline__ void spmm_vblock(const Args& A, int64_t vb, int gl, i
 // of highest out-degree are staged in shared memory once per CTA (persistent
 // grid-stride over the virtual blocks) and read from there; the others from
 // L2 / HBM.  Same values in the same order as the plain kernel: bit-identical.
-template <int G, int NV, int OP, int RED, bool XB, bool PAIR, bool HYB = false>
+template <int G, int NV, int OP, int RED, bool XB, bool PAIR, bool HYB = false, bool SEG = false>
 __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);
     constexpr int NG = THREADS / G;                 // groups per CTA
@@ -345,14 +368,15 @@ __global__ void __launch_bounds__(THREADS) spmm_gather_kernel(Args A) {
 
     if constexpr (HYB) {
         for (int64_t vb = blockIdx.x; vb < A.n_vblocks; vb += gridDim.x)
-            spmm_vblock<G, NV, OP, RED, XB, PAIR, HYB>(A, vb, gl, gi, mask, c4base, s_acc, s_etile, s_val, s_pos, s_hot);
+            spmm_vblock<G, NV, OP, RED, XB, PAIR, HYB, SEG>(A, vb, gl, gi, mask, c4base, s_acc, s_etile, s_val, s_pos,
+                                                            s_hot);
     } else {   // one virtual block per CTA: the plain launch (no loop, no extra registers)
-        spmm_vblock<G, NV, OP, RED, XB, PAIR, HYB>(A, blockIdx.x, gl, gi, mask, c4base, s_acc, s_etile, s_val, s_pos,
-                                                   s_hot);
+        spmm_vblock<G, NV, OP, RED, XB, PAIR, HYB, SEG>(A, blockIdx.x, gl, gi, mask, c4base, s_acc, s_etile, s_val,
+                                                        s_pos, s_hot);
     }
 }
 
-template <int G, int NV, int OP, int RED, bool XB = false, bool PAIR = false, bool HYB = false>
+template <int G, int NV, int OP, int RED, bool XB = false, bool PAIR = false, bool HYB = false, bool SEG = false>
 fg_status launch_t(const Args& A0, cudaStream_t st) {
     Args A = A0;
     constexpr int NG = THREADS / G;
@@ -364,7 +388,7 @@ fg_status launch_t(const Args& A0, cudaStream_t st) {
     A.n_vblocks = blocks;
     int64_t grid_x = blocks;
     size_t smem = 0;
-    auto k = spmm_gather_kernel<G, NV, OP, RED, XB, PAIR, HYB>;
+    auto k = spmm_gather_kernel<G, NV, OP, RED, XB, PAIR, HYB, SEG>;
     if constexpr (HYB) {   // persistent: the resident CTAs stage the hot rows once each
         smem = size_t(A.hyb_k) * A.F4 * 16;   // (plus the kernel's static combine buffers)
         if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
@@ -381,6 +405,8 @@ fg_status launch_t(const Args& A0, cudaStream_t st) {
 
 // hybrid partitioning (copy_u-sum, one float4 per lane, untiled): spmm_inst_sum_base.cu
 fg_status launch_hybrid(const Args& A, int G, cudaStream_t st);
+// one source-segmented pass of u_mul_e-sum (A.seg_lo / seg_hi / seg_acc set): spmm_inst_sum_base.cu
+fg_status launch_seg_pass(const Args& A, int G, int NV, cudaStream_t st);
 
 // One explicit specialisation per (reducer, op set) -- op set 0 = copy_u /
 // u_mul_e, 1 = u_add_e / copy_e -- each compiled in its own translation unit

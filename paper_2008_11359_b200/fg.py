@@ -37,7 +37,8 @@ SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_graph_pre
 
 # fg_tune_key (include/fg.h)
 TUNE = {"l2_tile_mb": 0, "spmm_heavy_deg": 1, "balance_nnz": 2, "sddmm_seg_mb": 3, "sddmm_seg_min_mb": 4,
-        "sddmm_persist": 5, "sddmm_l2_tile": 6, "sddmm_dot": 7, "gat_heavy_deg": 8, "mlp_impl": 9, "hybrid": 10}
+        "sddmm_persist": 5, "sddmm_l2_tile": 6, "sddmm_dot": 7, "gat_heavy_deg": 8, "mlp_impl": 9, "hybrid": 10,
+        "spmm_seg_mb": 11}
 
 
 class FGError(RuntimeError):
@@ -187,9 +188,10 @@ class Graph:
         return Graph._from_handle(h, self.n_src, self.n_dst, self.nnz)
 
     def prepare(self, row_bytes: int, stream=None) -> "Graph":
-        """fg_graph_prepare: build the source-segment table of the gSDDMM traversal
-        for gathered rows of `row_bytes` bytes (synchronous; no-op when that width
-        is not segmented).  Call before timing / CUDA-graph capture."""
+        """fg_graph_prepare: build the source-segment tables of the gSDDMM traversal
+        and of the segmented u_mul_e-sum passes for gathered rows of `row_bytes`
+        bytes (synchronous; no-op when that width is not segmented).  Call before
+        timing / CUDA-graph capture."""
         _check(lib().fg_graph_prepare(self.handle, int(row_bytes), _stream(stream)), "fg_graph_prepare")
         return self
 

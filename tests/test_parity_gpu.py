@@ -540,6 +540,43 @@ def _sddmm_source_segmented(g, H, D):
         check_close(outb[pos], rb, rbb, TOL, f"segmented bf16 u_dot_v H={H} D={D}")
 
 
+@pytest.mark.parametrize("H,D", [(8, 32), (1, 512), (2, 4), (4, 64), (8, 16)])
+@pytest.mark.parametrize("use_eid", [False, True])
+@pytest.mark.parametrize("heavy", [0, 64])
+def test_spmm_u_mul_e_source_segmented(skewed, skewed_eid, H, D, use_eid, heavy):
+    """Row f3 / a2: force the source-segmented u_mul_e-sum passes (1 MB segments
+    -> several segments on the small graph; bounds built by fg_graph_prepare),
+    also with most rows split CTA-per-row (heavy = 64), and compare with the
+    oracle.  Rows summed group-per-row keep the CSR order: bit-identical to the
+    unsegmented kernel (include/fg.h fg_graph_prepare)."""
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    F = H * D
+    X = feats((g.n_src, F), 990 + F, gen.REAL)
+    E = gen.features((g.nnz, H), 991, 1, gen.UNIT)
+    ref, ab, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", "sum", X, H=H, E=E, eid=g.eid)
+    with tuned(g.h, spmm_seg_mb=1, sddmm_seg_min_mb=0, spmm_heavy_deg=heavy):
+        g.h.prepare(F * 4)
+        out = torch.full((g.n_dst, F), float("nan"), device="cuda")
+        fgp.spmm(g.h, "u_mul_e", "sum", dev(X), H=H, E=dev(E), out=out)
+        out = out.cpu().numpy()
+        check_close(out, ref, ab, TOL, f"segmented u_mul_e-sum H={H} D={D}")
+        again = fgp.spmm(g.h, "u_mul_e", "sum", dev(X), H=H, E=dev(E)).cpu().numpy()
+        assert np.array_equal(again, out)         # deterministic: fixed segment order, no atomics
+        with tuned(g.h, spmm_seg_mb=0):
+            plain = fgp.spmm(g.h, "u_mul_e", "sum", dev(X), H=H, E=dev(E)).cpu().numpy()
+    deg = np.diff(g.row_ptr)
+    light = deg < (heavy if heavy else 1024)      # the automatic threshold is >= 1024
+    assert np.array_equal(out[light], plain[light])
+    # integer regime: every partial sum exact, so every row (heavy ones too) is bit-exact
+    Xi = feats((g.n_src, F), 992 + F, gen.INT)
+    Ei = gen.features((g.nnz, H), 993, 1, gen.INT, lo=0, hi=4)
+    refi, _, _, _ = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", "sum", Xi, H=H, E=Ei, eid=g.eid)
+    with tuned(g.h, spmm_seg_mb=1, sddmm_seg_min_mb=0, spmm_heavy_deg=heavy):
+        outi = fgp.spmm(g.h, "u_mul_e", "sum", dev(Xi), H=H, E=dev(Ei)).cpu().numpy()
+    assert np.array_equal(outi.astype(np.float64), refi)
+
+
 # ------------------------------------------------------------------ fused GAT (f2)
 @pytest.mark.parametrize("H,D", [(8, 32), (4, 16), (2, 4), (1, 128), (8, 64), (1, 16), (16, 16), (4, 64), (2, 128),
                                  (6, 32), (4, 32), (8, 16), (2, 64), (3, 32), (16, 32), (4, 128)])
