@@ -188,6 +188,17 @@ fg_status fg_graph_prepare(fg_graph* g, int64_t row_bytes, fg_stream stream);
  *                          19.7 -> 9.4 GB but ran 8.07 vs 7.47 ms; only for X
  *                          wider than FG_TUNE_SDDMM_SEG_MIN_MB, and only once
  *                          fg_graph_prepare built the bounds with it set)
+ *   FG_TUNE_SDDMM_PIPE     H == 1 gSDDMM with 33..128 float4 per row: -1 auto
+ *                          (software-pipelined kernel for 65..96), 0 plain,
+ *                          1..3 pipelined variants (U = 1 / 2 edges per stage,
+ *                          2 / 3 CTAs per SM); bit-identical in every setting
+ *   FG_TUNE_SDDMM_ORDER    0 segment-major work units (default), 1 2D tiles
+ *                          (destination block x source segment) in Hilbert-
+ *                          curve order (ablation, measured slower);
+ *                          applies to tables built by fg_graph_prepare with it
+ *                          set; bit-identical either way
+ *   FG_TUNE_SDDMM_RB_MB    Hilbert order: destination-block size in MB of Y
+ *                          rows (0: the segment size)
  *   Errors: FG_EINVAL (NULL, unknown key, out-of-range value).
  */
 /*
@@ -221,7 +232,10 @@ typedef enum {
     FG_TUNE_GAT_HEAVY_DEG = 8,
     FG_TUNE_MLP_IMPL = 9,
     FG_TUNE_HYBRID = 10,
-    FG_TUNE_SPMM_SEG_MB = 11
+    FG_TUNE_SPMM_SEG_MB = 11,
+    FG_TUNE_SDDMM_PIPE = 12,
+    FG_TUNE_SDDMM_ORDER = 13,
+    FG_TUNE_SDDMM_RB_MB = 14
 } fg_tune_key;
 fg_status fg_graph_tune(fg_graph* g, fg_tune_key key, int64_t value);
 fg_status fg_graph_get_tune(const fg_graph* g, fg_tune_key key, int64_t* value);

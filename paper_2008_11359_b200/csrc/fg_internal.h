@@ -27,6 +27,9 @@ struct fg_tuning {
     int64_t gat_heavy_deg = 4096;   // CTA-per-row threshold of the fused GAT
     int64_t mlp_impl = 0;           // 0: tcgen05 3xTF32, 1: CUDA-core FFMA, 2: tcgen05 bf16 2-split (K = 32)
     int64_t hybrid = 0;             // 1: hot sources staged in shared memory (needs fg_graph_prepare_hybrid)
+    int64_t sddmm_pipe = -1;        // H == 1 wide-row gSDDMM: 0 plain, 1..3 software-pipelined variants, -1 auto
+    int64_t sddmm_order = 0;        // segmented gSDDMM unit order: 0 segment-major, 1 Hilbert over (row block, segment)
+    int64_t sddmm_rb_mb = 0;        // Hilbert order: destination-block size in MB of Y rows (0: = sddmm_seg_mb)
     int64_t spmm_seg_mb = 0;        // source-segment size of the segmented u_mul_e-sum passes (0: off;
                                     // measured slower); only when X > sddmm_seg_min_mb
 };
@@ -54,7 +57,7 @@ struct fg_graph {
     // L2): built by fg_graph_prepare (synchronous) per segment width;
     // the launch paths only look them up (no allocation, no synchronisation)
     struct SegUnits {
-        int64_t seg_rows = 0, n_units = 0;
+        int64_t seg_rows = 0, rb_rows = 0, n_units = 0;   // rb_rows > 0: Hilbert-ordered 2D tiles
         int32_t* row = nullptr;
         int64_t* p0 = nullptr;
         int64_t* p1 = nullptr;
@@ -133,8 +136,10 @@ fg_status check_launch(const char* what);
 // source-segmented unit table for segments of seg_rows source vertices:
 // build_seg_units (fg_graph_prepare: allocates, synchronises) and find_seg_units
 // (launch paths: lookup only, NULL when not prepared)
-fg_status build_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t st);
-const fg_graph::SegUnits* find_seg_units(const fg_graph* g, int64_t seg_rows);
+fg_status build_seg_units(fg_graph* g, int64_t seg_rows, int64_t rb_rows, int chunk, cudaStream_t st);
+const fg_graph::SegUnits* find_seg_units(const fg_graph* g, int64_t seg_rows, int64_t rb_rows);
+// destination-block rows of the Hilbert-ordered unit table (0: segment-major order)
+int64_t sddmm_rb_rows(const fg_graph* g, int64_t row_bytes);
 // segment rows of the segmented gSDDMM for gathered rows of row_bytes, or 0 when
 // the rule does not segment (X = n_src x row_bytes within the budget)
 int64_t sddmm_seg_rows(const fg_graph* g, int64_t row_bytes);

@@ -64,22 +64,30 @@ __device__ __forceinline__ void attend_range(const Args& A, const float4* __rest
     // sequential online-softmax updates.
     constexpr int B = 32;
     const int F4 = A.F4, D4 = A.D4, H = A.H;
+    const char* xl = reinterpret_cast<const char*>(X + gl);   // this lane's first column
+    const uint32_t rowb = uint32_t(F4) * 16u;
+    bool cin[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) cin[j] = gl + G * j < F4;
     for (int64_t p0 = s; p0 < e; p0 += B) {
         const int cnt = int(min((int64_t)B, e - p0));
         __syncwarp(mask);
         for (int t = gl; t < cnt; t += G) sidx[t] = __ldg(A.col_idx + p0 + t);
         __syncwarp(mask);
         float4 xn[U][NV];   // software pipeline: next U edges' gathers in flight
+        // past the batch end the last edge's row is re-read (an L1 hit) instead of
+        // predicating each load; those slots are never consumed (t >= cnt breaks below,
+        // and every per-head score reduces one (edge, chunk) slot only).  Rows are
+        // addressed with one 32x32 -> 64-bit multiply-add from the lane's column base.
         auto gather = [&](int tb, float4 (&dst)[U][NV]) {
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
-                const int t = tb + uu;
-                const float4* xr = X + int64_t(t < cnt ? sidx[t] : 0) * F4;
+                const int t = min(tb + uu, cnt - 1);
+                const char* xr = xl + uint64_t(uint32_t(sidx[t])) * rowb;
 #pragma unroll
-                for (int j = 0; j < NV; ++j) {
-                    const int c = gl + G * j;
-                    dst[uu][j] = (t < cnt && c < F4) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
+                for (int j = 0; j < NV; ++j)
+                    dst[uu][j] = cin[j] ? __ldg(reinterpret_cast<const float4*>(xr) + G * j)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         };
         if constexpr (PIPE) gather(0, xn);

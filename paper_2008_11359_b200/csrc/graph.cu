@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <numeric>
+#include <utility>
 
 #include "fg_internal.h"
 
@@ -36,6 +37,9 @@ void tuning_from_env(fg_tuning* t) {
     rd("FG_MLP_IMPL", t->mlp_impl);
     rd("FG_HYBRID", t->hybrid);
     rd("FG_SPMM_SEG_MB", t->spmm_seg_mb);
+    rd("FG_SDDMM_PIPE", t->sddmm_pipe);
+    rd("FG_SDDMM_ORDER", t->sddmm_order);
+    rd("FG_SDDMM_RB_MB", t->sddmm_rb_mb);
 }
 }  // namespace fgk
 
@@ -176,14 +180,32 @@ int64_t spmm_seg_rows(const fg_graph* g, int64_t row_bytes) {
     return std::max<int64_t>(32, budget / row_bytes);
 }
 
-fg_status build_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t st) {
+// Hilbert index of cell (x, y) on an n x n grid (n a power of two)
+static int64_t hilbert_d(int64_t n, int64_t x, int64_t y) {
+    int64_t d = 0;
+    for (int64_t s = n / 2; s > 0; s /= 2) {
+        const int64_t rx = (x & s) > 0, ry = (y & s) > 0;
+        d += s * s * ((3 * rx) ^ ry);
+        if (ry == 0) {
+            if (rx == 1) {
+                x = n - 1 - x;
+                y = n - 1 - y;
+            }
+            std::swap(x, y);
+        }
+    }
+    return d;
+}
+
+fg_status build_seg_units(fg_graph* g, int64_t seg_rows, int64_t rb_rows, int chunk, cudaStream_t st) {
     std::lock_guard<std::mutex> lock(g->seg_mu);
     for (auto& su : g->seg_units)
-        if (su.seg_rows == seg_rows) return FG_OK;
+        if (su.seg_rows == seg_rows && su.rb_rows == rb_rows) return FG_OK;
     const int64_t n = g->n_dst;
     const int nseg = int((g->n_src + seg_rows - 1) / seg_rows);
     fg_graph::SegUnits su;
     su.seg_rows = seg_rows;
+    su.rb_rows = rb_rows;
     int64_t* cnt = nullptr;
     std::vector<int64_t> h(size_t(n) * nseg + 1, 0);
     cudaError_t e = cudaMalloc(&cnt, sizeof(int64_t) * (size_t(n) * nseg + 1));
@@ -193,11 +215,37 @@ fg_status build_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e == cudaSuccess) {
-        int64_t acc = 0;   // exclusive scan, segment-major: all units of segment 0 first
-        for (size_t i = 0; i < size_t(n) * nseg; ++i) {
-            const int64_t c = h[i];
-            h[i] = acc;
-            acc += c;
+        // exclusive scan of the per-(segment, row) unit counts in traversal order:
+        //   rb_rows == 0: segment-major (all units of segment 0 first, rows ascending);
+        //   rb_rows > 0 : 2D tiles (row block of rb_rows destinations x source
+        //                 segment) in Hilbert-curve order, rows
+        //                 ascending inside a tile -- consecutive tiles share their
+        //                 destination block (Y rows stay in L2) or their source
+        //                 segment (X rows stay in L2)
+        int64_t acc = 0;
+        auto take = [&](int s, int64_t v0, int64_t v1) {
+            for (int64_t v = v0; v < v1; ++v) {
+                const size_t i = size_t(s) * size_t(n) + size_t(v);
+                const int64_t c = h[i];
+                h[i] = acc;
+                acc += c;
+            }
+        };
+        if (rb_rows <= 0) {
+            for (int s = 0; s < nseg; ++s) take(s, 0, n);
+        } else {
+            const int64_t nrb = (n + rb_rows - 1) / rb_rows;
+            int64_t side = 1;
+            while (side < std::max<int64_t>(nrb, nseg)) side *= 2;
+            std::vector<std::pair<int64_t, int64_t>> tiles;   // (hilbert index, b * nseg + s)
+            for (int64_t b = 0; b < nrb; ++b)
+                for (int64_t sg = 0; sg < nseg; ++sg) tiles.emplace_back(hilbert_d(side, b, sg), b * nseg + sg);
+            std::sort(tiles.begin(), tiles.end());
+            for (auto& t : tiles) {
+                const int64_t b = t.second / nseg;
+                const int sg = int(t.second % nseg);
+                take(sg, b * rb_rows, std::min(n, (b + 1) * rb_rows));
+            }
         }
         su.n_units = acc;
         e = cudaMemcpyAsync(cnt, h.data(), sizeof(int64_t) * size_t(n) * nseg, cudaMemcpyHostToDevice, st);
@@ -222,11 +270,17 @@ fg_status build_seg_units(fg_graph* g, int64_t seg_rows, int chunk, cudaStream_t
     return FG_OK;
 }
 
-const fg_graph::SegUnits* find_seg_units(const fg_graph* g, int64_t seg_rows) {
+const fg_graph::SegUnits* find_seg_units(const fg_graph* g, int64_t seg_rows, int64_t rb_rows) {
     std::lock_guard<std::mutex> lock(const_cast<fg_graph*>(g)->seg_mu);
     for (auto& su : g->seg_units)
-        if (su.seg_rows == seg_rows) return &su;
+        if (su.seg_rows == seg_rows && su.rb_rows == rb_rows) return &su;
     return nullptr;
+}
+
+int64_t sddmm_rb_rows(const fg_graph* g, int64_t row_bytes) {
+    if (g->tune.sddmm_order != 1 || row_bytes <= 0) return 0;
+    const int64_t mb = g->tune.sddmm_rb_mb > 0 ? g->tune.sddmm_rb_mb : g->tune.sddmm_seg_mb;
+    return std::max<int64_t>(32, (mb << 20) / row_bytes);
 }
 
 int64_t sddmm_seg_rows(const fg_graph* g, int64_t row_bytes) {
@@ -428,6 +482,15 @@ extern "C" fg_status fg_graph_tune(fg_graph* g, fg_tune_key key, int64_t value) 
             break;
         case FG_TUNE_HYBRID: t.hybrid = value != 0; break;
         case FG_TUNE_SPMM_SEG_MB: t.spmm_seg_mb = std::max<int64_t>(0, value); break;
+        case FG_TUNE_SDDMM_PIPE:
+            if (value < -1 || value > 3) return fgk::set_error(FG_EINVAL, "fg_graph_tune: sddmm pipe %lld", (long long)value);
+            t.sddmm_pipe = value;
+            break;
+        case FG_TUNE_SDDMM_ORDER:
+            if (value < 0 || value > 1) return fgk::set_error(FG_EINVAL, "fg_graph_tune: sddmm order %lld", (long long)value);
+            t.sddmm_order = value;
+            break;
+        case FG_TUNE_SDDMM_RB_MB: t.sddmm_rb_mb = std::max<int64_t>(0, value); break;
         default: return fgk::set_error(FG_EINVAL, "fg_graph_tune: bad key %d", int(key));
     }
     return FG_OK;
@@ -449,6 +512,9 @@ extern "C" fg_status fg_graph_get_tune(const fg_graph* g, fg_tune_key key, int64
         case FG_TUNE_MLP_IMPL: *value = t.mlp_impl; break;
         case FG_TUNE_HYBRID: *value = t.hybrid; break;
         case FG_TUNE_SPMM_SEG_MB: *value = t.spmm_seg_mb; break;
+        case FG_TUNE_SDDMM_PIPE: *value = t.sddmm_pipe; break;
+        case FG_TUNE_SDDMM_ORDER: *value = t.sddmm_order; break;
+        case FG_TUNE_SDDMM_RB_MB: *value = t.sddmm_rb_mb; break;
         default: return fgk::set_error(FG_EINVAL, "fg_graph_get_tune: bad key %d", int(key));
     }
     return FG_OK;
@@ -461,7 +527,7 @@ extern "C" fg_status fg_graph_prepare(fg_graph* g, int64_t row_bytes, fg_stream 
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int64_t seg_rows = fgk::sddmm_seg_rows(g, row_bytes);   // 0: this width is not segmented
     if (seg_rows) {
-        const fg_status s = fgk::build_seg_units(g, seg_rows, g->unit_chunk, st);
+        const fg_status s = fgk::build_seg_units(g, seg_rows, fgk::sddmm_rb_rows(g, row_bytes), g->unit_chunk, st);
         if (s != FG_OK) return s;
     }
     const int64_t spmm_rows = fgk::spmm_seg_rows(g, row_bytes);

@@ -47,6 +47,7 @@ struct Args {
     int tile4;        // float4 columns per pass (0: one pass over all F4)
     int persistent;   // != 0: persistent grid (resident CTAs per SM x #SMs; > 0 caps the CTAs per SM)
     const float* E;   // u_dot_v-then-e_mul (fg_sddmm_emul): scores scaled by E[eid][h] at the write-back
+    int pipe;         // H == 1 wide rows: 0 sddmm_kernel, 1..3 sddmm_h1_pipe_kernel variants, -1 auto (FG_TUNE_SDDMM_PIPE)
 };
 
 // chunk c (4 features) of row r of a feature matrix with F4 chunks per row;
@@ -57,12 +58,21 @@ __device__ __forceinline__ float4 ld_chunk(const float4* __restrict__ M, int64_t
     else return __ldg(M + r * F4 + c);
 }
 
+// the chunk at byte address p (fp32: 16 bytes; bf16 storage: 8 bytes decoded)
+template <bool XB>
+__device__ __forceinline__ float4 ld_at(const char* p) {
+    if constexpr (XB) return bf16x4(__ldg(reinterpret_cast<const uint2*>(p)));
+    else return __ldg(reinterpret_cast<const float4*>(p));
+}
+
 // MODE_H1      : H == 1 and F <= 4*G*NV: one dot per edge, reduce over all G lanes.
 // MODE_HEADS   : H > 1, D4 = D/4 <= G (power of two), F <= 4*G*NV: chunk j of a
 //                lane belongs to head c / D4; reduce over D4 lanes per chunk.
 // MODE_GENERAL : H == 1 with F > 4*G*NV (column tiles; Y re-read through L1), or
 //                H > 1 with D4 > G (a head spans several chunks of a lane).
-template <int G, int NV, int MODE, int DW, bool XB, bool EM = false>
+// FULLW: F4 == G*NV exactly (every lane's every chunk is inside the row): no
+// per-chunk column predicate.
+template <int G, int NV, int MODE, int DW, bool XB, bool EM = false, bool FULLW = false>
 __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const float4* __restrict__ X,
                                                            const float4* __restrict__ Y, float* __restrict__ out) {
     constexpr int TW = G * NV;
@@ -87,6 +97,9 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
     const int64_t e = A.unit_p1 ? A.unit_p1[unit] : min(s + A.unit_chunk, A.row_ptr[v + 1]);
     const int F4 = A.F4, H = A.H, D4 = A.D4;
     const bool stage = (H * B <= CAP);
+    constexpr int CB = XB ? 8 : 16;                                        // bytes per 4-feature chunk
+    const char* xl = reinterpret_cast<const char*>(X) + int64_t(A.c4base + gl) * CB;   // this lane's column
+    const uint32_t rowb = uint32_t(F4) * CB;                              // bytes per X row
     int* idx = s_idx[gi];
     float* res = s_res[gi];
 
@@ -118,12 +131,16 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
             int us[U];
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
-                const int t = t0 + uu;
-                us[uu] = (t < cnt) ? idx[t] : 0;
+                // past the batch end: re-read the last edge's row (an L1 hit) instead of
+                // predicating every load -- its result is never stored (staged slots
+                // beyond cnt are not written back; the unstaged path breaks at cnt)
+                const int t = min(t0 + uu, cnt - 1);
+                us[uu] = idx[t];
+                const char* xr = xl + uint64_t(uint32_t(us[uu])) * rowb;   // one IMAD.WIDE.U32
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     const int c = A.c4base + gl + G * j;
-                    x[uu][j] = (t < cnt && c < F4) ? ld_chunk<XB>(X, us[uu], F4, c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    x[uu][j] = (FULLW || c < F4) ? ld_at<XB>(xr + j * G * CB) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
             if constexpr (MODE == MODE_H1 || MODE == MODE_HEADS) {
@@ -383,19 +400,122 @@ __global__ void __launch_bounds__(THREADS) sddmm_thread_kernel(const Args A, con
     }
 }
 
+// Software-pipelined H == 1 gather for wide rows (G = 32 lanes, NV float4 per
+// lane; F = 132..512): a work unit's (<= 64) neighbour indices are staged in
+// shared memory once, then the loop keeps the NEXT U edges' X rows in flight
+// while it reduces the current U (two register buffers, ping-pong by manual
+// unrolling, so no register copy waits on a load).  The non-pipelined kernel
+// drains its loads every U edges: its warps hold 0 bytes in flight while they
+// reduce.  Same per-lane partial dots and the same reduce-scatter tree as
+// sddmm_kernel<32, NV, MODE_H1>: bit-identical results.
+template <int NV, int U, int MINB, bool EM>
+__global__ void __launch_bounds__(THREADS, MINB) sddmm_h1_pipe_kernel(const Args A, const float4* __restrict__ X,
+                                                                      const float4* __restrict__ Y,
+                                                                      float* __restrict__ out) {
+    constexpr int NGRP = THREADS / 32;
+    constexpr int CH = 64;   // max edges per work unit (host-checked: unit_chunk <= 64)
+    __shared__ int s_idx[NGRP][CH];
+    __shared__ float s_res[NGRP][CH];
+    const int gl = threadIdx.x & 31;
+    const int gi = threadIdx.x >> 5;
+    constexpr unsigned mask = 0xffffffffu;
+    int* idx = s_idx[gi];
+    float* res = s_res[gi];
+    const int F4 = A.F4;
+    const char* xl = reinterpret_cast<const char*>(X + gl);   // this lane's first column
+    const uint32_t rowb = uint32_t(F4) * 16u;
+    bool cin[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) cin[j] = gl + 32 * j < F4;
+    const int64_t stride = int64_t(gridDim.x) * NGRP;
+    for (int64_t unit = int64_t(blockIdx.x) * NGRP + gi; unit < A.n_units; unit += stride) {
+        const int64_t v = A.unit_row[unit];
+        const int64_t s = A.unit_p0[unit];
+        const int64_t e = A.unit_p1 ? A.unit_p1[unit] : min(s + A.unit_chunk, A.row_ptr[v + 1]);
+        const int cnt = int(e - s);
+        __syncwarp();
+        for (int t = gl; t < cnt; t += 32) idx[t] = __ldg(A.col_idx + s + t);
+        float4 y0[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const int c = gl + 32 * j;
+            y0[j] = (c < F4) ? __ldg(Y + v * F4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncwarp();
+        auto load = [&](float4 (&x)[U][NV], int t0) {   // past cnt: the last row again, never stored
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+                const char* xr = xl + uint64_t(uint32_t(idx[min(t0 + uu, cnt - 1)])) * rowb;
+#pragma unroll
+                for (int j = 0; j < NV; ++j)
+                    x[uu][j] = cin[j] ? __ldg(reinterpret_cast<const float4*>(xr) + 32 * j)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        };
+        auto reduce = [&](const float4 (&x)[U][NV], int t0) {
+            float pv[U];
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+                float hs = 0.f;
+#pragma unroll
+                for (int j = 0; j < NV; ++j) hs += dot4(x[uu][j], y0[j]);
+                pv[uu] = hs;
+            }
+            reduce_scatter<U, 32, 32>(pv, gl, mask);
+            constexpr int L = ilog2(U) < 5 ? ilog2(U) : 5;
+            constexpr int KEEP = U >> L;
+            const int bits = gl >> (5 - L);
+            if ((gl & ((32 >> L) - 1)) == 0) {
+#pragma unroll
+                for (int i = 0; i < KEEP; ++i) {
+                    const int t = t0 + bits * KEEP + i;
+                    if (t < cnt) res[t] = pv[i];
+                }
+            }
+        };
+        float4 xa[U][NV], xb[U][NV];
+        load(xa, 0);
+        for (int t0 = 0; t0 < cnt; t0 += 2 * U) {
+            if (t0 + U < cnt) load(xb, t0 + U);       // uniform: next U edges in flight ...
+            reduce(xa, t0);                          // ... while this U reduce
+            if (t0 + U >= cnt) break;
+            if (t0 + 2 * U < cnt) load(xa, t0 + 2 * U);
+            reduce(xb, t0 + U);
+        }
+        __syncwarp();
+        if (A.eid == nullptr) {
+            for (int q = gl; q < cnt; q += 32) {
+                if constexpr (EM) out[s + q] = res[q] * __ldg(A.E + s + q);
+                else out[s + q] = res[q];
+            }
+        } else {
+            for (int q = gl; q < cnt; q += 32) {
+                const int64_t oi = __ldg(A.eid + s + q);
+                if constexpr (EM) out[oi] = res[q] * __ldg(A.E + oi);
+                else out[oi] = res[q];
+            }
+        }
+    }
+}
+
 template <int G, int NV, bool XB = false>
 fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, cudaStream_t st) {
     using K = void (*)(const Args, const float4*, const float4*, float*);
     const int TW = G * NV;
     K k;
+    // full-width rows (F4 == G*NV, one pass): the variant without per-chunk column predicates
+    const bool fullw = !XB && A.tile4 == 0 && A.c4base == 0 && A.F4 == TW;
     if (A.H == 1 && (A.tile4 ? A.tile4 : A.F4) <= TW) {
-        k = sddmm_kernel<G, NV, MODE_H1, G, XB>;
+        k = fullw ? sddmm_kernel<G, NV, MODE_H1, G, XB, false, true> : sddmm_kernel<G, NV, MODE_H1, G, XB>;
     } else if (A.H > 1 && A.D4 <= G && A.F4 <= TW) {
         switch (A.D4) {   // heads of D = 4*D4 floats reduce over D4 lanes
             case 1: k = sddmm_kernel<G, NV, MODE_HEADS, 1, XB>; break;
             case 2: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 2 ? 2 : 1), XB>; break;
             case 4: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 4 ? 4 : 1), XB>; break;
-            case 8: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 8 ? 8 : 1), XB>; break;
+            case 8:
+                k = fullw ? sddmm_kernel<G, NV, MODE_HEADS, (G >= 8 ? 8 : 1), XB, false, true>
+                          : sddmm_kernel<G, NV, MODE_HEADS, (G >= 8 ? 8 : 1), XB>;
+                break;
             case 16: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 16 ? 16 : 1), XB>; break;
             default: k = sddmm_kernel<G, NV, MODE_HEADS, (G >= 32 ? 32 : 1), XB>; break;
         }
@@ -418,6 +538,16 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
             } else {
                 k = sddmm_kernel<G, NV, MODE_GENERAL, 1, false, true>;
             }
+        }
+    }
+    if constexpr (G == 32 && NV >= 2 && !XB) {   // software-pipelined wide-row H == 1 kernel (FG_TUNE_SDDMM_PIPE)
+        // auto (-1): the pipelined U=2 kernel for NV = 3 (reddit F=384: 13.18 -> 10.64 ms);
+        // plain for NV = 2 / 4 (F=256: 8.07 vs 8.26-9.12 ms; F=512: 15.50 vs 15.41-30.5 ms)
+        const int pipe = A.pipe < 0 ? (NV == 3 ? 3 : 0) : A.pipe;
+        if (pipe && A.H == 1 && A.tile4 == 0 && A.unit_chunk <= 64) {
+            if (pipe == 1) k = A.E ? sddmm_h1_pipe_kernel<NV, 1, 3, true> : sddmm_h1_pipe_kernel<NV, 1, 3, false>;
+            else if (pipe == 2) k = A.E ? sddmm_h1_pipe_kernel<NV, 2, 2, true> : sddmm_h1_pipe_kernel<NV, 2, 2, false>;
+            else k = A.E ? sddmm_h1_pipe_kernel<NV, 2, 3, true> : sddmm_h1_pipe_kernel<NV, 2, 3, false>;
         }
     }
     const int64_t per_block = THREADS / G;
@@ -480,6 +610,7 @@ static fg_status launch_sddmm_core(const fg_graph* g, int H, int D, const float*
     A.accumulate = 0;
     A.tile4 = 0;
     A.persistent = 0;
+    A.pipe = int(g->tune.sddmm_pipe);
     int F4 = A.F4;
     const float4* X4 = reinterpret_cast<const float4*>(xb ? static_cast<const void*>(Xbf16) : X);
     const float4* Y4 = reinterpret_cast<const float4*>(xb ? static_cast<const void*>(Ybf16) : Y);
@@ -535,7 +666,8 @@ static fg_status launch_sddmm_core(const fg_graph* g, int H, int D, const float*
     // this launch path never allocates or synchronises.
     if (A.tile4 == 0) {
         const int64_t seg_rows = fgk::sddmm_seg_rows(g, int64_t(F4) * (xb ? 8 : 16));
-        const fg_graph::SegUnits* su = seg_rows ? fgk::find_seg_units(g, seg_rows) : nullptr;
+        const int64_t rb_rows = fgk::sddmm_rb_rows(g, int64_t(F4) * (xb ? 8 : 16));
+        const fg_graph::SegUnits* su = seg_rows ? fgk::find_seg_units(g, seg_rows, rb_rows) : nullptr;
         if (su) {
             A.unit_row = su->row;
             A.unit_p0 = su->p0;

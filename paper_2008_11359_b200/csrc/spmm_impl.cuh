@@ -2,6 +2,11 @@
 // spmm.cu), instantiated per (reducer, op set) by spmm_inst_*.cu.
 #pragma once
 #include <algorithm>
+#include <type_traits>
+
+#ifndef FG_SPMM_FULLB
+#define FG_SPMM_FULLB 0   // full-batch fast path: 0 select reducers only (default), 1 all, 2 none
+#endif
 
 #include "device_common.cuh"
 #include "fg_internal.h"
@@ -83,6 +88,15 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
     constexpr int U = PAIR ? 4 : (NV >= 4 ? 2 : (NV >= 2 ? 4 : ((RED == R_MAX || RED == R_MIN) ? 4 : 8)));
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);     // select-type reducers
     const int F4 = A.F4;
+    constexpr int CB = (XB || PAIR) ? 8 : 16;              // bytes of X per 4-feature chunk
+    const char* xl = (OP == OP_COPYE) ? reinterpret_cast<const char*>(A.E)
+                                      : (XB || PAIR) ? reinterpret_cast<const char*>(A.Xh)
+                                                     : reinterpret_cast<const char*>(A.X);
+    xl += int64_t(c4base + colj<G, PAIR>(gl, 0)) * CB;       // this lane's first column
+    const uint32_t rowb = uint32_t(F4) * CB;                 // bytes per source row
+    bool cin[NV];                                            // chunk j inside the row (edge-invariant)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) cin[j] = c4base + colj<G, PAIR>(gl, j) < F4;
     for (int64_t p0 = s; p0 < e; p0 += B) {
         const int cnt = int(min((int64_t)B, e - p0));
         int uix[R];
@@ -107,9 +121,13 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                 __syncwarp(mask);
             }
         }
-#pragma unroll
-        for (int t0 = 0; t0 < B; t0 += U) {
-            if (t0 >= cnt) break;                           // uniform within the group
+        // one step of U edges (t0 a compile-time constant after unrolling); FULL (all
+        // U edges inside the batch) drops the per-edge bounds predicates.
+        // Source rows are addressed from this lane's column base with one
+        // 32x32 -> 64-bit multiply-add per edge (IMAD.WIDE.U32) and immediate
+        // chunk offsets.
+        auto step = [&](int t0, auto full_c) {
+            constexpr bool FULL = decltype(full_c)::value;
             float4 x[PAIR ? 1 : U][PAIR ? 1 : NV];
             uint4 xw[PAIR ? U : 1][PAIR ? NV / 2 : 1];   // PAIR: raw bf16 pairs, converted at use
             constexpr bool PERK = (OP == OP_UMULE_GEN || OP == OP_UADDE);   // head per component
@@ -120,22 +138,27 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                 const int u = __shfl_sync(mask, uix[t / G], t % G, G);
                 int ed = 0;
                 if constexpr (OP != OP_COPY) ed = __shfl_sync(mask, eix[t / G], t % G, G);
-                const float4* xr = (OP == OP_COPYE) ? reinterpret_cast<const float4*>(A.E) + int64_t(ed) * F4
-                                                    : A.X + int64_t(u) * F4;
-                const uint2* xh = A.Xh + int64_t(u) * F4;
+                // u_mul_e keeps the element-indexed form: with the lane-base form the
+                // compiler re-loads kernel parameters per edge (reddit H=8: 7.8 -> 8.3 ms)
+                const int64_t ce = int64_t(u) * F4 + c4base + colj<G, PAIR>(gl, 0);   // element-indexed chunk
+                const char* xr = (OP == OP_UMULE || OP == OP_UMULE_GEN)
+                                     ? ((XB || PAIR) ? reinterpret_cast<const char*>(A.Xh + ce)
+                                                     : reinterpret_cast<const char*>(A.X + ce))
+                                     : xl + uint64_t(uint32_t(OP == OP_COPYE ? ed : u)) * rowb;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     const int c = c4base + colj<G, PAIR>(gl, j);
-                    const bool ok = (t < cnt) && (c < F4);
+                    const bool ok = (FULL || t < cnt) && cin[j];
                     if constexpr (PAIR) {   // F4 even: c even, c + 1 < F4 with c
                         if ((j & 1) == 0)
-                            xw[uu][j / 2] = ok ? __ldg(reinterpret_cast<const uint4*>(xh + c)) : make_uint4(0, 0, 0, 0);
+                            xw[uu][j / 2] = ok ? __ldg(reinterpret_cast<const uint4*>(xr + (2 * G * (j >> 1)) * CB))
+                                               : make_uint4(0, 0, 0, 0);
                     } else if constexpr (XB) {
-                        x[uu][j] = ok ? bf16x4(__ldg(xh + c)) : f4(0.f);
+                        x[uu][j] = ok ? bf16x4(__ldg(reinterpret_cast<const uint2*>(xr + j * G * CB))) : f4(0.f);
                     } else if constexpr (HYB) {   // hot sources from shared memory, the rest from L2 / HBM
                         x[uu][j] = !ok ? f4(0.f) : (u < 0 ? hot[int64_t(-1 - u) * F4 + c] : __ldg(A.X + int64_t(u) * F4 + c));
                     } else {
-                        x[uu][j] = ok ? __ldg(xr + c) : f4(0.f);
+                        x[uu][j] = ok ? __ldg(reinterpret_cast<const float4*>(xr + j * G * CB)) : f4(0.f);
                     }
                     if constexpr (OP == OP_UMULE) {
                         const int h = (4 * c) / A.D;
@@ -152,7 +175,7 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
                 const int t = t0 + uu;
-                if (t >= cnt) break;
+                if (!FULL && t >= cnt) break;
                 const int p = int(p0) + t;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
@@ -198,6 +221,21 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                     }
                 }
             }
+        };
+        // full 32-edge batches of the select reducers take a predicate-free unrolled
+        // copy of the loop (reddit copy_u-max F=128 + args 4.28 -> 3.65 ms); for the
+        // sums the larger code measured equal (copy_u) or slower (u_mul_e 8.2 -> 10.7 ms)
+        if (FG_SPMM_FULLB == 1 || (FG_SPMM_FULLB == 0 && MAX)) {
+          if (cnt == B) {
+#pragma unroll
+            for (int t0 = 0; t0 < B; t0 += U) step(t0, std::true_type{});
+            continue;
+          }
+        }
+#pragma unroll
+        for (int t0 = 0; t0 < B; t0 += U) {
+            if (t0 >= cnt) break;                           // uniform within the group
+            step(t0, std::false_type{});
         }
     }
 }

@@ -441,6 +441,105 @@ extern "C" int fgprobe_xsweep(void* buf, int64_t buf_bytes, const int* sizes_mb,
     return int(e);
 }
 
+
+// ---------------------------------------------------------------- load-flavour sweep
+// The same random whole-row gathers with other LDG flavours: LD = 0 __ldg
+// (LDG.128, L1-allocating), 1 ld.global.nc.L1::no_allocate.v4, 2 the same with
+// the L2::256B prefetch hint, 3 Blackwell 256-bit loads (ld.global.nc.
+// L1::no_allocate.v8.f32 -> LDG.256: half the load instructions per row).
+template <int LD>
+__device__ __forceinline__ void ld_row_piece(const float4* p, float4& a, float4& b) {
+    if constexpr (LD == 0) {
+        a = __ldg(p);
+    } else if constexpr (LD == 1) {
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(p));
+    } else if constexpr (LD == 2) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(p));
+    } else {
+        asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                     : "l"(p));
+    }
+}
+
+// G lanes per row; each lane NV pieces of 16 B (LD < 3) or 32 B (LD == 3)
+template <int G, int NV, int U, int LD>
+__global__ void gather_ld_kernel(const float4* __restrict__ X, int nrows, int F4, int64_t rows_per_group, float* sink) {
+    constexpr int W = LD == 3 ? 2 : 1;   // float4 per piece
+    const int gl = threadIdx.x & (G - 1);
+    const int64_t grp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+    float4 acc = make_float4(0, 0, 0, 0);
+    for (int64_t t = 0; t < rows_per_group; t += U) {
+        float4 x[U][NV], y[U][NV];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t r = hash32(uint32_t(grp * 7919 + t + u)) % uint32_t(nrows);
+#pragma unroll
+            for (int j = 0; j < NV; ++j) ld_row_piece<LD>(X + int64_t(r) * F4 + W * (gl + G * j), x[u][j], y[u][j]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                acc.x += x[u][j].x; acc.y += x[u][j].y; acc.z += x[u][j].z; acc.w += x[u][j].w;
+                if (LD == 3) { acc.x += y[u][j].x; acc.y += y[u][j].y; acc.z += y[u][j].z; acc.w += y[u][j].w; }
+            }
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 1234.5f) sink[0] = acc.x;
+}
+
+template <int G, int NV, int U, int LD>
+double gather_ld_gbs(const float4* X, int64_t x_bytes, int F, int blocks_per_sm, float* sink, bool verbose) {
+    const int F4 = F / 4;
+    const int nrows = int(x_bytes / (int64_t(F) * 4));
+    const int blocks = g_sms * blocks_per_sm;
+    const int64_t groups = int64_t(blocks) * 256 / G;
+    const int64_t total_rows = (6400LL << 20) / (int64_t(F) * 4);
+    const int64_t rpg = (total_rows / groups + U - 1) / U * U;
+    const float ms = best_ms([&] { gather_ld_kernel<G, NV, U, LD><<<blocks, 256>>>(X, nrows, F4, rpg, sink); }, 3);
+    const double gbs = double(groups) * rpg * F * 4 / (ms * 1e-3) / 1e9;
+    if (verbose)
+        printf("gather-ld LD=%d F=%4d X=%4lld MiB G=%2d NV=%d U=%d blocks/SM=%d: %.3f ms %.1f GB/s\n", LD, F,
+               (long long)(x_bytes >> 20), G, NV, U, blocks_per_sm, ms, gbs);
+    return gbs;
+}
+
+extern "C" int fgprobe_ldmodes(void* buf, int64_t buf_bytes, int verbose) {
+    if (!buf || buf_bytes < (64LL << 20)) return int(cudaErrorInvalidValue);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    const float4* X = reinterpret_cast<const float4*>(buf);
+    float* sink = reinterpret_cast<float*>(static_cast<char*>(buf) + buf_bytes - 64);
+    const int64_t xb = 48LL << 20;
+    // F = 512 (2 KiB rows): 16-byte pieces 32 lanes x 4; 32-byte pieces 32 lanes x 2
+    gather_ld_gbs<32, 4, 2, 0>(X, xb, 512, 3, sink, verbose);
+    gather_ld_gbs<32, 4, 4, 0>(X, xb, 512, 4, sink, verbose);
+    gather_ld_gbs<32, 4, 2, 1>(X, xb, 512, 3, sink, verbose);
+    gather_ld_gbs<32, 4, 4, 1>(X, xb, 512, 4, sink, verbose);
+    gather_ld_gbs<32, 4, 2, 2>(X, xb, 512, 3, sink, verbose);
+    gather_ld_gbs<32, 4, 4, 2>(X, xb, 512, 4, sink, verbose);
+    gather_ld_gbs<32, 2, 2, 3>(X, xb, 512, 3, sink, verbose);
+    gather_ld_gbs<32, 2, 4, 3>(X, xb, 512, 4, sink, verbose);
+    gather_ld_gbs<32, 2, 4, 3>(X, xb, 512, 3, sink, verbose);
+    gather_ld_gbs<32, 2, 8, 3>(X, xb, 512, 3, sink, verbose);
+    // F = 256 (1 KiB rows)
+    gather_ld_gbs<32, 2, 4, 0>(X, xb, 256, 4, sink, verbose);
+    gather_ld_gbs<32, 2, 4, 1>(X, xb, 256, 4, sink, verbose);
+    gather_ld_gbs<32, 1, 4, 3>(X, xb, 256, 4, sink, verbose);
+    gather_ld_gbs<32, 1, 8, 3>(X, xb, 256, 4, sink, verbose);
+    // F = 128 (512 B rows)
+    gather_ld_gbs<32, 1, 8, 0>(X, xb, 128, 8, sink, verbose);
+    gather_ld_gbs<32, 1, 8, 1>(X, xb, 128, 8, sink, verbose);
+    gather_ld_gbs<16, 1, 8, 3>(X, xb, 128, 8, sink, verbose);
+    gather_ld_gbs<16, 1, 4, 3>(X, xb, 128, 8, sink, verbose);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return int(e);
+}
+
 extern "C" int fgprobe_l2(void* buf, int64_t buf_bytes, double* out5) {
     return fgprobe_l2_verbose(buf, buf_bytes, out5, 0);
 }

@@ -577,6 +577,39 @@ def test_spmm_u_mul_e_source_segmented(skewed, skewed_eid, H, D, use_eid, heavy)
     assert np.array_equal(outi.astype(np.float64), refi)
 
 
+@pytest.mark.parametrize("F", [260, 384, 512, 200])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_sddmm_pipelined_and_hilbert(skewed, skewed_eid, F, use_eid):
+    """a4 / f3: the software-pipelined wide-row H=1 kernel (every variant) and the
+    Hilbert-ordered 2D unit tables against the oracle, and bit for
+    bit against the plain segment-major kernel (same lane partition and
+    reduction tree; only the schedule differs)."""
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    X = feats((g.n_src, F), 1200 + F, gen.REAL)
+    Y = feats((g.n_dst, F), 1201 + F, gen.REAL)
+    ref, ab = oracle.sddmm(g.row_ptr, g.col_idx, X, Y)
+    pos = np.arange(g.nnz) if g.eid is None else g.eid
+    with tuned(g.h, sddmm_pipe=0):
+        plain = fgp.sddmm(g.h, dev(X), dev(Y)).cpu().numpy()
+    check_close(plain[pos], ref, ab, TOL, f"u_dot_v F={F}")
+    for pipe in (1, 2, 3, -1):
+        with tuned(g.h, sddmm_pipe=pipe):
+            out = fgp.sddmm(g.h, dev(X), dev(Y)).cpu().numpy()
+        assert np.array_equal(out, plain), f"pipe={pipe}"
+        E = gen.features((g.nnz, 1), 1202, 1, gen.UNIT)
+        with tuned(g.h, sddmm_pipe=pipe):
+            em = fgp.sddmm(g.h, dev(X), dev(Y), E=dev(E)).cpu().numpy()
+        assert np.array_equal(em.ravel(), (plain.ravel() * E.ravel()).astype(np.float32)), f"e_mul pipe={pipe}"
+    for order, seg, rb in ((0, 1, 0), (1, 1, 1), (1, 1, 2), (1, 2, 1)):
+        with tuned(g.h, sddmm_order=order, sddmm_seg_mb=seg, sddmm_rb_mb=rb, sddmm_seg_min_mb=0):
+            g.h.prepare(F * 4)
+            for pipe in (0, -1):
+                with tuned(g.h, sddmm_pipe=pipe):
+                    out = fgp.sddmm(g.h, dev(X), dev(Y)).cpu().numpy()
+                assert np.array_equal(out, plain), f"order={order} seg={seg} rb={rb} pipe={pipe}"
+
+
 # ------------------------------------------------------------------ fused GAT (f2)
 @pytest.mark.parametrize("H,D", [(8, 32), (4, 16), (2, 4), (1, 128), (8, 64), (1, 16), (16, 16), (4, 64), (2, 128),
                                  (6, 32), (4, 32), (8, 16), (2, 64), (3, 32), (16, 32), (4, 128)])

@@ -19,3 +19,6 @@ arr = (ctypes.c_int * len(sizes))(*sizes)
 out = (ctypes.c_double * (2 * len(sizes)))()
 rc = L.fgprobe_xsweep(ctypes.c_void_p(buf.data_ptr()), ctypes.c_int64(buf.numel()), arr, len(sizes), out, 1)
 print("rc", rc)
+if "--ld" in os.sys.argv or True:
+    rc = L.fgprobe_ldmodes(ctypes.c_void_p(buf.data_ptr()), ctypes.c_int64(buf.numel()), 1)
+    print("ldmodes rc", rc)
