@@ -199,6 +199,12 @@ fg_status fg_graph_prepare(fg_graph* g, int64_t row_bytes, fg_stream stream);
  *                          set; bit-identical either way
  *   FG_TUNE_SDDMM_RB_MB    Hilbert order: destination-block size in MB of Y
  *                          rows (0: the segment size)
+ *   FG_TUNE_SPMM_LDG256    1: fp32 copy_u gathers read 32-byte chunk pairs
+ *                          (LDG.256) when X is 32-byte aligned and the row /
+ *                          tile width is an even number of 4-feature chunks
+ *                          (ablation: 4-17 % slower on every shaped graph);
+ *                          0 (default): 16-byte loads.  Changes the lanes per
+ *                          row, hence the automatic heavy-row split of sums.
  *   Errors: FG_EINVAL (NULL, unknown key, out-of-range value).
  */
 /*
@@ -235,7 +241,8 @@ typedef enum {
     FG_TUNE_SPMM_SEG_MB = 11,
     FG_TUNE_SDDMM_PIPE = 12,
     FG_TUNE_SDDMM_ORDER = 13,
-    FG_TUNE_SDDMM_RB_MB = 14
+    FG_TUNE_SDDMM_RB_MB = 14,
+    FG_TUNE_SPMM_LDG256 = 15
 } fg_tune_key;
 fg_status fg_graph_tune(fg_graph* g, fg_tune_key key, int64_t value);
 fg_status fg_graph_get_tune(const fg_graph* g, fg_tune_key key, int64_t* value);

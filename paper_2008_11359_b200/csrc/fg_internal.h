@@ -30,6 +30,7 @@ struct fg_tuning {
     int64_t sddmm_pipe = -1;        // H == 1 wide-row gSDDMM: 0 plain, 1..3 software-pipelined variants, -1 auto
     int64_t sddmm_order = 0;        // segmented gSDDMM unit order: 0 segment-major, 1 Hilbert over (row block, segment)
     int64_t sddmm_rb_mb = 0;        // Hilbert order: destination-block size in MB of Y rows (0: = sddmm_seg_mb)
+    int64_t spmm_ldg256 = 0;        // 1: fp32 copy_u gathers as 32-byte chunk-pair loads (measured slower)
     int64_t spmm_seg_mb = 0;        // source-segment size of the segmented u_mul_e-sum passes (0: off;
                                     // measured slower); only when X > sddmm_seg_min_mb
 };

@@ -39,6 +39,7 @@ void tuning_from_env(fg_tuning* t) {
     rd("FG_SPMM_SEG_MB", t->spmm_seg_mb);
     rd("FG_SDDMM_PIPE", t->sddmm_pipe);
     rd("FG_SDDMM_ORDER", t->sddmm_order);
+    rd("FG_SPMM_LDG256", t->spmm_ldg256);
     rd("FG_SDDMM_RB_MB", t->sddmm_rb_mb);
 }
 }  // namespace fgk
@@ -491,6 +492,7 @@ extern "C" fg_status fg_graph_tune(fg_graph* g, fg_tune_key key, int64_t value) 
             t.sddmm_order = value;
             break;
         case FG_TUNE_SDDMM_RB_MB: t.sddmm_rb_mb = std::max<int64_t>(0, value); break;
+        case FG_TUNE_SPMM_LDG256: t.spmm_ldg256 = value != 0; break;
         default: return fgk::set_error(FG_EINVAL, "fg_graph_tune: bad key %d", int(key));
     }
     return FG_OK;
@@ -515,6 +517,7 @@ extern "C" fg_status fg_graph_get_tune(const fg_graph* g, fg_tune_key key, int64
         case FG_TUNE_SDDMM_PIPE: *value = t.sddmm_pipe; break;
         case FG_TUNE_SDDMM_ORDER: *value = t.sddmm_order; break;
         case FG_TUNE_SDDMM_RB_MB: *value = t.sddmm_rb_mb; break;
+        case FG_TUNE_SPMM_LDG256: *value = t.spmm_ldg256; break;
         default: return fgk::set_error(FG_EINVAL, "fg_graph_get_tune: bad key %d", int(key));
     }
     return FG_OK;

@@ -102,7 +102,12 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
     // 16-byte aligned X: lanes read PAIRS of chunks (8 features) with one 16-byte
     // load -- half the load instructions of the 8-byte-per-chunk mapping
     const bool pair = Xbf16 && A.F4 % 2 == 0 && F4 % 2 == 0 && (reinterpret_cast<uintptr_t>(Xbf16) & 15u) == 0;
-    if (pair) {
+    // fp32 copy_u with an even number of 4-feature chunks per (tile) row and a
+    // 32-byte aligned X: lanes read chunk PAIRS with one 32-byte load (LDG.256) --
+    // half the load and address instructions per gathered byte (FG_TUNE_SPMM_LDG256)
+    const bool pair32 = !Xbf16 && g->tune.spmm_ldg256 && op == OP_COPY && A.F4 % 2 == 0 && F4 % 2 == 0 &&
+                        (reinterpret_cast<uintptr_t>(X) & 31u) == 0;
+    if (pair || pair32) {
         const int F8 = F4 / 2;
         NV = 2;
         if (F8 <= 32) {
@@ -162,6 +167,14 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
         }
     }
     const int opset = (op == OP_UADDE || op == OP_COPYE) ? 1 : 0;
+    if (pair32) {
+        switch (mx) {
+            case R_MAX: return dispatch_pair32<R_MAX>(A, G, NV, op, st);
+            case R_MIN: return dispatch_pair32<R_MIN>(A, G, NV, op, st);
+            case R_MEAN: return dispatch_pair32<R_MEAN>(A, G, NV, op, st);
+            default: return dispatch_pair32<R_SUM>(A, G, NV, op, st);
+        }
+    }
     if (Xbf16) {   // bf16 storage: copy_u / u_mul_e x {sum, max} (validated by the caller)
         if (mx == R_MAX) return dispatch_x16<R_MAX>(A, G, NV, op, pair, st);
         return dispatch_x16<R_SUM>(A, G, NV, op, pair, st);

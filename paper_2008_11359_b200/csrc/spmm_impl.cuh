@@ -53,14 +53,21 @@ struct Args {
 };
 
 __device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); }
+// 32 bytes (two adjacent float4) with one 256-bit load (sm_100: LDG.E.256)
+__device__ __forceinline__ void ldg256(const char* p, float4& a, float4& b) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                 : "l"(p));
+}
 __device__ __forceinline__ float comp(const float4& v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
 __device__ __forceinline__ void set_comp(float4& v, int k, float a) {
     if (k == 0) v.x = a; else if (k == 1) v.y = a; else if (k == 2) v.z = a; else v.w = a;
 }
 
-// Column (float4 index within the tile) of a lane's chunk j.  PAIR (bf16
-// storage, NV even): a lane owns pairs of adjacent chunks, read with ONE 16-byte
-// load (8 bf16 features); otherwise chunk j of lane gl is column gl + G*j.
+// Column (float4 index within the tile) of a lane's chunk j.  PAIR (NV even): a
+// lane owns pairs of adjacent chunks, read with ONE load -- 16 bytes for bf16
+// storage (8 features), 32 bytes (LDG.256, ld.global.nc.v8.f32) for fp32;
+// otherwise chunk j of lane gl is column gl + G*j.
 template <int G, bool PAIR>
 __device__ __forceinline__ int colj(int gl, int j) {
     if constexpr (PAIR) return 2 * (gl + G * (j >> 1)) + (j & 1);
@@ -85,12 +92,16 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
     // (reddit bf16 copy_u-sum F=512 9.37 vs 8.49 ms, u_mul_e H=8 10.1 vs 7.5 ms);
     // one chunk per lane: 8 for sum, 4 for the select reducers (reddit copy_u-max
     // F=128 + args 4.84 -> 4.63 ms; sum F=512 unchanged)
-    constexpr int U = PAIR ? 4 : (NV >= 4 ? 2 : (NV >= 2 ? 4 : ((RED == R_MAX || RED == R_MIN) ? 4 : 8)));
+    // fp32 pairs (32-byte loads): the same bytes in flight per lane as the 16-byte
+    // mapping with twice the chunks, i.e. U of the NV / 2 = 1 / 2 pair cases 4 / 2
+    constexpr int U = PAIR ? ((XB || NV < 4) ? 4 : 2)
+                           : (NV >= 4 ? 2 : (NV >= 2 ? 4 : ((RED == R_MAX || RED == R_MIN) ? 4 : 8)));
+    constexpr bool P16 = PAIR && XB;                         // bf16 pairs: raw 16-byte words
     constexpr bool MAX = (RED == R_MAX || RED == R_MIN);     // select-type reducers
     const int F4 = A.F4;
-    constexpr int CB = (XB || PAIR) ? 8 : 16;              // bytes of X per 4-feature chunk
+    constexpr int CB = XB ? 8 : 16;                          // bytes of X per 4-feature chunk
     const char* xl = (OP == OP_COPYE) ? reinterpret_cast<const char*>(A.E)
-                                      : (XB || PAIR) ? reinterpret_cast<const char*>(A.Xh)
+                                      : XB ? reinterpret_cast<const char*>(A.Xh)
                                                      : reinterpret_cast<const char*>(A.X);
     xl += int64_t(c4base + colj<G, PAIR>(gl, 0)) * CB;       // this lane's first column
     const uint32_t rowb = uint32_t(F4) * CB;                 // bytes per source row
@@ -128,8 +139,8 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
         // chunk offsets.
         auto step = [&](int t0, auto full_c) {
             constexpr bool FULL = decltype(full_c)::value;
-            float4 x[PAIR ? 1 : U][PAIR ? 1 : NV];
-            uint4 xw[PAIR ? U : 1][PAIR ? NV / 2 : 1];   // PAIR: raw bf16 pairs, converted at use
+            float4 x[P16 ? 1 : U][P16 ? 1 : NV];
+            uint4 xw[P16 ? U : 1][P16 ? NV / 2 : 1];     // bf16 pairs: raw words, converted at use
             constexpr bool PERK = (OP == OP_UMULE_GEN || OP == OP_UADDE);   // head per component
             float ev[U][NV][PERK ? 4 : 1];
 #pragma unroll
@@ -142,17 +153,26 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
                 // compiler re-loads kernel parameters per edge (reddit H=8: 7.8 -> 8.3 ms)
                 const int64_t ce = int64_t(u) * F4 + c4base + colj<G, PAIR>(gl, 0);   // element-indexed chunk
                 const char* xr = (OP == OP_UMULE || OP == OP_UMULE_GEN)
-                                     ? ((XB || PAIR) ? reinterpret_cast<const char*>(A.Xh + ce)
+                                     ? (XB ? reinterpret_cast<const char*>(A.Xh + ce)
                                                      : reinterpret_cast<const char*>(A.X + ce))
                                      : xl + uint64_t(uint32_t(OP == OP_COPYE ? ed : u)) * rowb;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     const int c = c4base + colj<G, PAIR>(gl, j);
                     const bool ok = (FULL || t < cnt) && cin[j];
-                    if constexpr (PAIR) {   // F4 even: c even, c + 1 < F4 with c
+                    if constexpr (P16) {   // F4 even: c even, c + 1 < F4 with c
                         if ((j & 1) == 0)
                             xw[uu][j / 2] = ok ? __ldg(reinterpret_cast<const uint4*>(xr + (2 * G * (j >> 1)) * CB))
                                                : make_uint4(0, 0, 0, 0);
+                    } else if constexpr (PAIR) {   // fp32 pair: one 32-byte load (32-byte aligned, checked by the host)
+                        if ((j & 1) == 0) {
+                            if (ok) {
+                                ldg256(xr + (2 * G * (j >> 1)) * CB, x[uu][j], x[uu][j + 1]);
+                            } else {
+                                x[uu][j] = f4(0.f);
+                                x[uu][j + 1] = f4(0.f);
+                            }
+                        }
                     } else if constexpr (XB) {
                         x[uu][j] = ok ? bf16x4(__ldg(reinterpret_cast<const uint2*>(xr + j * G * CB))) : f4(0.f);
                     } else if constexpr (HYB) {   // hot sources from shared memory, the rest from L2 / HBM
@@ -180,7 +200,7 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     float4 xv;
-                    if constexpr (PAIR) {
+                    if constexpr (P16) {
                         const uint4 w = xw[uu][j / 2];
                         xv = (j & 1) ? bf16x4(make_uint2(w.z, w.w)) : bf16x4(make_uint2(w.x, w.y));
                     } else {
@@ -467,6 +487,17 @@ template <>
 fg_status dispatch_inst<R_MEAN, 0>(const Args& A, int G, int NV, int op, cudaStream_t st);
 template <>
 fg_status dispatch_inst<R_MEAN, 1>(const Args& A, int G, int NV, int op, cudaStream_t st);
+// fp32 X read as 32-byte chunk pairs (copy_u; every reducer): spmm_inst_*_base.cu
+template <int RED>
+fg_status dispatch_pair32(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_pair32<R_SUM>(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_pair32<R_MAX>(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_pair32<R_MIN>(const Args& A, int G, int NV, int op, cudaStream_t st);
+template <>
+fg_status dispatch_pair32<R_MEAN>(const Args& A, int G, int NV, int op, cudaStream_t st);
 // bf16 storage of X (copy_u, u_mul_e; sum and max): spmm_inst_x16.cu
 // pair: 16-byte loads of adjacent chunk pairs (F4 even; NV even)
 template <int RED>

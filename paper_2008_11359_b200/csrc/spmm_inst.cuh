@@ -36,4 +36,22 @@ fg_status dispatch_inst<FG_RED, FG_OPSET>(const Args& A, int G, int NV, int op, 
     }
 }
 
+#if FG_OPSET == 0
+// fp32 chunk pairs (32-byte loads): the (G, NV) the host chose from F8 = F4 / 2
+template <>
+fg_status dispatch_pair32<FG_RED>(const Args& A, int G, int NV, int op, cudaStream_t st) {
+    (void)op;   // copy_u only
+    switch (G) {
+        case 1: return launch_t<1, 2, OP_COPY, FG_RED, false, true>(A, st);
+        case 2: return launch_t<2, 2, OP_COPY, FG_RED, false, true>(A, st);
+        case 4: return launch_t<4, 2, OP_COPY, FG_RED, false, true>(A, st);
+        case 8: return launch_t<8, 2, OP_COPY, FG_RED, false, true>(A, st);
+        case 16: return launch_t<16, 2, OP_COPY, FG_RED, false, true>(A, st);
+        default:
+            if (NV == 2) return launch_t<32, 2, OP_COPY, FG_RED, false, true>(A, st);
+            return launch_t<32, 4, OP_COPY, FG_RED, false, true>(A, st);   // wider rows: column tiles (grid.y)
+    }
+}
+#endif
+
 }  // namespace fgspmm

@@ -39,7 +39,7 @@ SYMBOLS = ["fg_graph_create", "fg_graph_destroy", "fg_graph_info", "fg_graph_pre
 TUNE = {"l2_tile_mb": 0, "spmm_heavy_deg": 1, "balance_nnz": 2, "sddmm_seg_mb": 3, "sddmm_seg_min_mb": 4,
         "sddmm_persist": 5, "sddmm_l2_tile": 6, "sddmm_dot": 7, "gat_heavy_deg": 8, "mlp_impl": 9, "hybrid": 10,
         "spmm_seg_mb": 11, "sddmm_pipe": 12,
-        "sddmm_order": 13, "sddmm_rb_mb": 14}
+        "sddmm_order": 13, "sddmm_rb_mb": 14, "spmm_ldg256": 15}
 
 
 class FGError(RuntimeError):

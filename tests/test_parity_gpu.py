@@ -610,6 +610,28 @@ def test_sddmm_pipelined_and_hilbert(skewed, skewed_eid, F, use_eid):
                 assert np.array_equal(out, plain), f"order={order} seg={seg} rb={rb} pipe={pipe}"
 
 
+@pytest.mark.parametrize("F", [8, 32, 40, 128, 512])
+@pytest.mark.parametrize("red", ["sum", "max", "min", "mean"])
+def test_copy_u_ldg256_pairs(skewed, F, red):
+    """Ablation FG_TUNE_SPMM_LDG256: fp32 chunk pairs read with 32-byte loads,
+    also under forced column tiling, against the oracle (max / min: values and
+    argmax bit-exact)."""
+    import paper_2008_11359_b200 as fgp
+    g = skewed
+    X = feats((g.n_src, F), 1300 + F, gen.REAL)
+    ref, ab, rau, rae = oracle.spmm(g.row_ptr, g.col_idx, "copy_u", red, X)
+    for tile_mb in (-1, 1):
+        with tuned(g.h, spmm_ldg256=1, l2_tile_mb=tile_mb):
+            if red in ("sum", "mean"):
+                out = fgp.spmm(g.h, "copy_u", red, dev(X)).cpu().numpy()
+                check_close(out, ref, ab, TOL, f"ldg256 copy_u-{red} F={F}")
+            else:
+                out, au, ae = fgp.spmm(g.h, "copy_u", red, dev(X), arg_u=True, arg_e=True)
+                assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
+                assert np.array_equal(au.cpu().numpy(), rau)
+                assert np.array_equal(ae.cpu().numpy(), rae)
+
+
 # ------------------------------------------------------------------ fused GAT (f2)
 @pytest.mark.parametrize("H,D", [(8, 32), (4, 16), (2, 4), (1, 128), (8, 64), (1, 16), (16, 16), (4, 64), (2, 128),
                                  (6, 32), (4, 32), (8, 16), (2, 64), (3, 32), (16, 32), (4, 128)])
