@@ -54,6 +54,9 @@ constexpr int NBUF = 2;                   // TMEM accumulator buffers (double bu
 #ifndef FG_MLP_LA
 #define FG_MLP_LA 4
 #endif
+#ifndef FG_MLP_LDW
+#define FG_MLP_LDW 0    // TMEM read granularity of the epilogue: 0 by reducer (max 16, sum 32), 16, 32
+#endif
 #ifndef FG_MLP_NPROD
 #define FG_MLP_NPROD 2
 #endif
@@ -141,6 +144,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
           "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
           "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+// wait for the outstanding tcgen05.ld of BOTH 16-column buffers (wait::ld covers all of
+// this thread's loads): a is consumed next, b may still be the one in flight
+__device__ __forceinline__ void tmem_wait_ld2(uint32_t (&a)[16], uint32_t (&b)[16]) {
+    asm volatile(
+        "tcgen05.wait::ld.sync.aligned;"
+        : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+          "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]), "+r"(a[12]), "+r"(a[13]), "+r"(a[14]), "+r"(a[15]),
+          "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7]),
+          "+r"(b[8]), "+r"(b[9]), "+r"(b[10]), "+r"(b[11]), "+r"(b[12]), "+r"(b[13]), "+r"(b[14]), "+r"(b[15])
+        :
+        : "memory");
 }
 // wait for this thread's outstanding tcgen05.ld; v is threaded through the asm so no use of
 // the loaded registers can be scheduled before the wait
@@ -278,26 +300,33 @@ struct Epi {
             start_row();
         }
     }
-    // the 32 columns of a chunk that lies inside the current row (the common case)
-    __device__ __forceinline__ void consume_full(const uint32_t (&v)[32], int pc) {
+    // the W columns of a chunk that lies inside the current row (the common case)
+    template <int W>
+    __device__ __forceinline__ void consume_full(const uint32_t (&v)[W], int pc) {
         if (MAX) {
             // the chunk maximum by a 3-input max tree (FMNMX3); the first column
             // attaining it is searched only when it beats the running best (strict:
             // ties keep the earlier winner), skipped when no feature of the warp improves
-            float t[11];
+            constexpr int N3 = (W + 2) / 3;
+            float t[N3];
 #pragma unroll
-            for (int j = 0; j < 10; ++j)
-                t[j] = fmaxf(fmaxf(__uint_as_float(v[3 * j]), __uint_as_float(v[3 * j + 1])),
-                             __uint_as_float(v[3 * j + 2]));
-            t[10] = fmaxf(__uint_as_float(v[30]), __uint_as_float(v[31]));
-            const float m = fmaxf(fmaxf(fmaxf(fmaxf(t[0], t[1]), t[2]), fmaxf(fmaxf(t[3], t[4]), t[5])),
-                                  fmaxf(fmaxf(fmaxf(t[6], t[7]), t[8]), fmaxf(t[9], t[10])));
+            for (int j = 0; j < N3; ++j) {
+                const float a = __uint_as_float(v[3 * j]);
+                const float b = 3 * j + 1 < W ? __uint_as_float(v[(3 * j + 1) % W]) : a;
+                const float c = 3 * j + 2 < W ? __uint_as_float(v[(3 * j + 2) % W]) : a;
+                t[j] = fmaxf(fmaxf(a, b), c);
+            }
+#pragma unroll
+            for (int st = 1; st < N3; st *= 2)
+#pragma unroll
+                for (int j = 0; j + st < N3; j += 2 * st) t[j] = fmaxf(t[j], t[j + st]);
+            const float m = t[0];
             const bool imp = m > best;
             if (__any_sync(0xffffffffu, imp)) {
                 if (imp) {
-                    int k = 31;
+                    int k = W - 1;
 #pragma unroll
-                    for (int c = 30; c >= 0; --c) k = (__uint_as_float(v[c]) == m) ? c : k;
+                    for (int c = W - 2; c >= 0; --c) k = (__uint_as_float(v[c]) == m) ? c : k;
                     best = m;
                     bpos = pc + k;
                 }
@@ -305,7 +334,7 @@ struct Epi {
         } else {
             float sm[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int c = 0; c < 32; c += 4)
+            for (int c = 0; c < W; c += 4)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) sm[k] += fmaxf(__uint_as_float(v[c + k]), 0.f);
             best += (sm[0] + sm[1]) + (sm[2] + sm[3]);
@@ -313,7 +342,8 @@ struct Epi {
     }
     // general case: chunk at relative position pc with nvalid valid columns,
     // possibly spanning row boundaries
-    __device__ __forceinline__ void consume_split(const uint32_t (&v)[32], int pc, int nvalid) {
+    template <int W>
+    __device__ __forceinline__ void consume_split(const uint32_t (&v)[W], int pc, int nvalid) {
         int c0 = 0;
         while (c0 < nvalid) {
             while (pc + c0 >= re) advance();
@@ -322,7 +352,7 @@ struct Epi {
                 float b0 = -INFINITY;   // ties -> lowest column
                 int k0 = 0;
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
+                for (int c = 0; c < W; ++c) {
                     const float x = __uint_as_float(v[c]);
                     if (c >= c0 && c < c1 && x > b0) { b0 = x; k0 = c; }
                 }
@@ -332,16 +362,17 @@ struct Epi {
                 const uint32_t cm = (c1 >= 32 ? 0xffffffffu : ((1u << c1) - 1u)) & ~((1u << c0) - 1u);
                 float sm = 0.f;
 #pragma unroll
-                for (int c = 0; c < 32; ++c)
+                for (int c = 0; c < W; ++c)
                     if ((cm >> c) & 1u) sm += fmaxf(__uint_as_float(v[c]), 0.f);
                 best += sm;
             }
             c0 = c1;
         }
     }
-    __device__ __forceinline__ void consume(const uint32_t (&v)[32], int pc, int nvalid) {
-        if (nvalid == 32 && pc >= rs && pc + 32 <= re) consume_full(v, pc);   // warp-uniform
-        else if (nvalid > 0) consume_split(v, pc, nvalid);
+    template <int W>
+    __device__ __forceinline__ void consume(const uint32_t (&v)[W], int pc, int nvalid) {
+        if (nvalid == W && pc >= rs && pc + W <= re) consume_full<W>(v, pc);   // warp-uniform
+        else if (nvalid > 0) consume_split<W>(v, pc, nvalid);
     }
 };
 
@@ -693,12 +724,33 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) mlp_tcgen05_kernel(const
             const int nv_tile = min(NT, nnz_cta - tb);
             // one 32-column chunk per tcgen05.ld (loading both chunks of the tile at once
             // needs 3 CTAs/SM for the registers and measured slower: 4.29 vs 4.07 ms)
+            // max: 16-column chunks, software-pipelined -- chunk ch + 1 is read out of TMEM
+            // while chunk ch is consumed (same 32 registers as one 32-column chunk):
+            // reddit max + args 4.73 -> 4.35 ms, rand-100K 1.92 -> 1.75 ms; sum: one
+            // 32-column chunk at a time (pipelined 3.20 -> 3.28 ms)
+            constexpr bool LD16 = FG_MLP_LDW == 16 || (FG_MLP_LDW == 0 && MAX);
+            if constexpr (LD16) {
+                uint32_t va[16], vb[16];
+                const uint32_t ta = lane_base + uint32_t(b * NT);
+                tmem_ld16(ta, va);
+                tmem_wait_ld2(va, vb);
+#pragma unroll
+                for (int ch = 0; ch < NT / 16; ch += 2) {
+                    if (ch + 1 < NT / 16) tmem_ld16(ta + uint32_t((ch + 1) * 16), vb);
+                    ep.consume<16>(va, tb + ch * 16, max(0, min(16, nv_tile - ch * 16)));
+                    tmem_wait_ld2(vb, va);
+                    if (ch + 2 < NT / 16) tmem_ld16(ta + uint32_t((ch + 2) * 16), va);
+                    ep.consume<16>(vb, tb + (ch + 1) * 16, max(0, min(16, nv_tile - (ch + 1) * 16)));
+                    tmem_wait_ld2(va, vb);
+                }
+            } else {
 #pragma unroll 1
-            for (int ch = 0; ch < NT / 32; ++ch) {
-                uint32_t v0[32];
-                tmem_ld32(lane_base + uint32_t(b * NT + ch * 32), v0);
-                tmem_wait_ld(v0);
-                ep.consume(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)));
+                for (int ch = 0; ch < NT / 32; ++ch) {
+                    uint32_t v0[32];
+                    tmem_ld32(lane_base + uint32_t(b * NT + ch * 32), v0);
+                    tmem_wait_ld(v0);
+                    ep.consume<32>(v0, tb + ch * 32, max(0, min(32, nv_tile - ch * 32)));
+                }
             }
             tc_fence_before();
             mbar_arrive(&S.tempty[b]);
