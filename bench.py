@@ -52,6 +52,49 @@ def metric_name() -> str:
         return "gSpMM/gSDDMM ms/op & HBM GB/s vs ~8 TB/s, feat 32-512, at 1/2/4/8 B200"
 
 
+def run_backward(S, timed, sync_all) -> dict:
+    """Row f1 at full size (reddit-shaped, N = 1): the gradients of the step's
+    ops through the gradient duality, each timed like the extras
+    (CUDA events, L2 flushed, mean of k).  Bytes: the gather model of the
+    forward op each gradient runs as (dX = a gSpMM over the transposed handle,
+    dE / dY = a gSDDMM / gSpMM over the graph; the max gradient reads the
+    forward's arg_u once per (edge, feature) it tests)."""
+    import torch
+    fgp, st, G, X, n, m = S.fgp, S.stream, S.G, S.X, S.nl, S.m
+    GT = G.transpose(stream=st)
+    sync_all()
+    idx = 8 * (n + 1) + 4 * m
+    r = {}
+
+    def put(name, ms, b):
+        r[name] = {"ms": round(ms, 4), "gbs": round(b / (ms * 1e-3) / 1e9, 1)}
+
+    # copy_u-sum F=512: dX = spmm(gT, dOut)
+    dout = S.out512
+    put("spmm_copy_u_sum_F512_dX", timed(lambda: fgp.spmm_backward(G, GT, "copy_u", "sum", dout, stream=st)),
+        idx + 4 * m * F_GCN + 4 * n * F_GCN)
+    # u_mul_e-sum H=8 D=32: dX over gT (weighted by E) and dE = sddmm(g, X, dOut)
+    d256 = S.o256
+    put("spmm_u_mul_e_sum_H8_D32_dX_dE", timed(lambda: fgp.spmm_backward(
+        G, GT, "u_mul_e", "sum", d256, H=H_GAT, X=X["X256"], E=S.s8, want_dE=True, stream=st)),
+        2 * idx + 2 * 4 * m * H_GAT * D_GAT + 2 * 4 * m * H_GAT + 2 * 4 * n * H_GAT * D_GAT)
+    # copy_u-max F=128: dX masked by the forward's arg_u (gathers dOut and arg_u per edge)
+    put("spmm_copy_u_max_F128_dX", timed(lambda: fgp.spmm_backward(
+        G, GT, "copy_u", "max", S.o128, X=X["X128"], arg_u=S.au128, stream=st)),
+        idx + 2 * 4 * m * F_MAX + 4 * n * F_MAX)
+    # u_dot_v H=8 D=32: dX = spmm_{u_mul_e}(gT, Y, dS), dY = spmm_{u_mul_e}(g, X, dS)
+    put("sddmm_u_dot_v_H8_D32_dX_dY", timed(lambda: fgp.sddmm_backward(
+        G, GT, X["X256"], S.ydst("X256"), S.s8, H=H_GAT, stream=st)),
+        2 * (idx + 4 * m * H_GAT * D_GAT + 4 * m * H_GAT + 4 * n * H_GAT * D_GAT))
+    # edge softmax H=8: ds = alpha * (dalpha - sum_row alpha * dalpha)
+    # (alpha = dalpha = the step's alpha: the timing does not depend on the values)
+    put("edge_softmax_H8_ds", timed(lambda: fgp.edge_softmax_backward(G, S.s8, S.s8, H=H_GAT, stream=st)),
+        8 * (n + 1) + 3 * 4 * m * H_GAT)
+    del GT
+    torch.cuda.empty_cache()
+    return r
+
+
 def op_bytes(n_rows: int, m: int) -> dict:
     """Algorithmic bytes per op (SURVEY §8(d) gather model; row_ptr is int64):
     index arrays + per-edge source-row gathers + per-row reads/writes."""
@@ -857,6 +900,7 @@ def run_extras(S, args, sync_all, flush, world):
     sync_all()
     if world != 1:
         return res
+    res["backward"] = run_backward(S, timed, sync_all)
     import gen
     dev = torch.device("cuda")
 

@@ -26,13 +26,19 @@ constexpr int THREADS = 256;
 
 // dX[u][:] for max/min (MEAN = false: masked by the forward's arg_u) and mean
 // (MEAN = true: every edge, dOut[v] scaled by 1/|N(v)|, rp = g's row_ptr).
-// One warp per row u of gT, lanes over float4 columns.
+// One warp per row u of gT, lanes over float4 columns.  The row's neighbour
+// indices (and edge ids) are loaded 32 at a time by the lanes and broadcast by
+// shuffles, and U edges' arg_u words are in flight per lane; dOut is read only
+// for the (rare) edges whose forward winner is u (max / min) -- a source wins
+// about 1/deg(v) of its (v, feature) pairs.  Per (u, column) the winning edges
+// are added in ascending CSR order of gT: deterministic.
 template <bool UMULE, bool MEAN>
 __global__ void __launch_bounds__(THREADS) sel_backward_dx_kernel(
     const int32_t* __restrict__ rows, int64_t n_rows, const int64_t* __restrict__ rpT,
     const int32_t* __restrict__ ciT, const int32_t* __restrict__ eidT, const float4* __restrict__ dOut,
     const int4* __restrict__ arg_u, const int64_t* __restrict__ rp, const float* __restrict__ E, int H, int D, int F4,
     float4* __restrict__ dX) {
+    constexpr int U = 4;
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t(blockIdx.x) * THREADS + threadIdx.x) >> 5;
     if (r >= n_rows) return;
@@ -40,34 +46,47 @@ __global__ void __launch_bounds__(THREADS) sel_backward_dx_kernel(
     const int64_t s = rpT[u], e = rpT[u + 1];
     for (int c0 = 0; c0 < F4; c0 += 32) {
         const int c = c0 + lane;
-        if (c >= F4) break;
+        const bool cok = c < F4;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int64_t p = s; p < e; ++p) {
-            const int64_t v = __ldg(ciT + p);
-            int4 a = make_int4(int(u), int(u), int(u), int(u));
-            if (!MEAN) {
-                a = __ldg(arg_u + v * F4 + c);
-                if (a.x != u && a.y != u && a.z != u && a.w != u) continue;
+        for (int64_t p0 = s; p0 < e; p0 += 32) {
+            const int cnt = int(min((int64_t)32, e - p0));
+            const int vl = lane < cnt ? __ldg(ciT + p0 + lane) : 0;
+            const int el = (UMULE && lane < cnt) ? (eidT ? __ldg(eidT + p0 + lane) : int(p0 + lane)) : 0;
+            for (int t0 = 0; t0 < cnt; t0 += U) {
+                int64_t vv[U];
+                int4 a[U];
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    vv[k] = __shfl_sync(0xffffffffu, vl, min(t0 + k, cnt - 1));
+                    a[k] = make_int4(int(u), int(u), int(u), int(u));
+                    if (!MEAN && cok) a[k] = __ldg(arg_u + vv[k] * F4 + c);
+                }
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    const int ed = UMULE ? __shfl_sync(0xffffffffu, el, min(t0 + k, cnt - 1)) : 0;
+                    if (t0 + k >= cnt || !cok) continue;
+                    if (a[k].x != u && a[k].y != u && a[k].z != u && a[k].w != u) continue;
+                    const int64_t v = vv[k];
+                    float4 g = __ldg(dOut + v * F4 + c);
+                    if (MEAN) {
+                        const float dg = float(__ldg(rp + v + 1) - __ldg(rp + v));
+                        g = make_float4(g.x / dg, g.y / dg, g.z / dg, g.w / dg);
+                    }
+                    float w0 = 1.f, w1 = 1.f, w2 = 1.f, w3 = 1.f;
+                    if (UMULE) {
+                        w0 = __ldg(E + int64_t(ed) * H + (4 * c + 0) / D);
+                        w1 = __ldg(E + int64_t(ed) * H + (4 * c + 1) / D);
+                        w2 = __ldg(E + int64_t(ed) * H + (4 * c + 2) / D);
+                        w3 = __ldg(E + int64_t(ed) * H + (4 * c + 3) / D);
+                    }
+                    if (a[k].x == u) acc.x = fmaf(g.x, w0, acc.x);
+                    if (a[k].y == u) acc.y = fmaf(g.y, w1, acc.y);
+                    if (a[k].z == u) acc.z = fmaf(g.z, w2, acc.z);
+                    if (a[k].w == u) acc.w = fmaf(g.w, w3, acc.w);
+                }
             }
-            float4 g = __ldg(dOut + v * F4 + c);
-            if (MEAN) {
-                const float dg = float(__ldg(rp + v + 1) - __ldg(rp + v));
-                g = make_float4(g.x / dg, g.y / dg, g.z / dg, g.w / dg);
-            }
-            float w0 = 1.f, w1 = 1.f, w2 = 1.f, w3 = 1.f;
-            if (UMULE) {
-                const int64_t ed = eidT ? int64_t(__ldg(eidT + p)) : p;
-                w0 = __ldg(E + ed * H + (4 * c + 0) / D);
-                w1 = __ldg(E + ed * H + (4 * c + 1) / D);
-                w2 = __ldg(E + ed * H + (4 * c + 2) / D);
-                w3 = __ldg(E + ed * H + (4 * c + 3) / D);
-            }
-            if (a.x == u) acc.x = fmaf(g.x, w0, acc.x);
-            if (a.y == u) acc.y = fmaf(g.y, w1, acc.y);
-            if (a.z == u) acc.z = fmaf(g.z, w2, acc.z);
-            if (a.w == u) acc.w = fmaf(g.w, w3, acc.w);
         }
-        dX[u * F4 + c] = acc;
+        if (cok) dX[u * F4 + c] = acc;
     }
 }
 
@@ -121,6 +140,67 @@ __global__ void __launch_bounds__(THREADS) softmax_backward_warp_kernel(
     for (int64_t q = lane; q < n; q += 32) {
         const int64_t idx = eid ? int64_t(__ldg(eid + s0 + q / H)) * H + h : s0 * H + q;
         ds[idx] = __ldg(alpha + idx) * (__ldg(dalpha + idx) - dot);
+    }
+}
+
+// softmax backward, H % 4 == 0, (H/4) | 32, identity edge ids: the row's
+// alpha / dalpha are the contiguous 16-byte aligned spans [s0*H, s1*H); lane l
+// reads float4 i = l + 32k (heads 4*(l % (H/4)) .. +3 for every k), UN float4
+// of each in flight; lanes of equal l % (H/4) merge their partial dots with a
+// butterfly (as the forward softmax_vec_kernel).
+__global__ void __launch_bounds__(THREADS) softmax_backward_vec_kernel(
+    const int32_t* __restrict__ rows, int64_t n_rows, const int64_t* __restrict__ rp, int H,
+    const float* __restrict__ alpha, const float* __restrict__ dalpha, float* __restrict__ ds) {
+    constexpr int UN = 4;
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t(blockIdx.x) * THREADS + threadIdx.x) >> 5;
+    if (r >= n_rows) return;
+    const int64_t v = rows[r];
+    const int64_t s0 = rp[v], n4 = (rp[v + 1] - s0) * H / 4;
+    const float4* A4 = reinterpret_cast<const float4*>(alpha + s0 * H);
+    const float4* D4 = reinterpret_cast<const float4*>(dalpha + s0 * H);
+    float4* O4 = reinterpret_cast<float4*>(ds + s0 * H);
+    float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i0 = lane; i0 < n4; i0 += 32 * UN) {
+        float4 a[UN], d[UN];
+#pragma unroll
+        for (int k = 0; k < UN; ++k) {
+            const int64_t i = i0 + 32 * k;
+            a[k] = i < n4 ? __ldg(A4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            d[k] = i < n4 ? __ldg(D4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < UN; ++k) {
+            dot.x = fmaf(a[k].x, d[k].x, dot.x);
+            dot.y = fmaf(a[k].y, d[k].y, dot.y);
+            dot.z = fmaf(a[k].z, d[k].z, dot.z);
+            dot.w = fmaf(a[k].w, d[k].w, dot.w);
+        }
+    }
+    const int hq = H / 4;   // lanes l and l ^ o share their heads for o >= hq
+    for (int o = 16; o >= hq; o >>= 1) {
+        dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
+        dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
+        dot.z += __shfl_xor_sync(0xffffffffu, dot.z, o);
+        dot.w += __shfl_xor_sync(0xffffffffu, dot.w, o);
+    }
+    for (int64_t i0 = lane; i0 < n4; i0 += 32 * UN) {
+        float4 a[UN], d[UN];
+#pragma unroll
+        for (int k = 0; k < UN; ++k) {
+            const int64_t i = i0 + 32 * k;
+            if (i < n4) {
+                a[k] = __ldg(A4 + i);
+                d[k] = __ldg(D4 + i);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < UN; ++k) {
+            const int64_t i = i0 + 32 * k;
+            if (i < n4)
+                O4[i] = make_float4(a[k].x * (d[k].x - dot.x), a[k].y * (d[k].y - dot.y), a[k].z * (d[k].z - dot.z),
+                                    a[k].w * (d[k].w - dot.w));
+        }
     }
 }
 
@@ -282,7 +362,13 @@ extern "C" fg_status fg_edge_softmax_backward(const fg_graph* g, int H, const fl
     if (!alpha || !dalpha || !dscores) return set_error(FG_EINVAL, "fg_edge_softmax_backward: NULL tensor");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int64_t n_rows = g->n_nonempty;
-    if (32 % H == 0) {
+    const bool a16 = ((reinterpret_cast<uintptr_t>(alpha) | reinterpret_cast<uintptr_t>(dalpha) |
+                       reinterpret_cast<uintptr_t>(dscores)) & 15u) == 0;
+    if (H % 4 == 0 && 32 % (H / 4) == 0 && g->eid == nullptr && a16) {
+        const int64_t blocks = (n_rows * 32 + THREADS - 1) / THREADS;
+        softmax_backward_vec_kernel<<<unsigned(blocks), THREADS, 0, st>>>(g->rows_by_deg, n_rows, g->row_ptr, H,
+                                                                          alpha, dalpha, dscores);
+    } else if (32 % H == 0) {
         const int64_t blocks = (n_rows * 32 + THREADS - 1) / THREADS;
         softmax_backward_warp_kernel<<<unsigned(blocks), THREADS, 0, st>>>(g->rows_by_deg, n_rows, g->row_ptr, g->eid,
                                                                            H, alpha, dalpha, dscores);

@@ -23,12 +23,6 @@ def G(cuda_ok):
     return g, h, h.transpose()
 
 
-def _abs_bound(row_ptr, col_idx, n_src, *mats):
-    """|terms| bound for a gradient that sums products over edges: use the oracle
-    backward on |inputs| (same structure, all terms non-negative)."""
-    return mats
-
-
 def test_transpose_is_csc(G):
     g, h, hT = G
     assert (hT.n_dst, hT.n_src, hT.nnz) == (g.n_src, g.n_dst, g.nnz)
@@ -84,7 +78,7 @@ def test_sddmm_backward(G):
     check_close(dY.cpu().numpy(), rdY, bdY, 1e-4, "sddmm dY")
 
 
-@pytest.mark.parametrize("H", [1, 8, 3])
+@pytest.mark.parametrize("H", [1, 8, 3, 4, 16, 128])
 def test_edge_softmax_backward(G, H):
     import paper_2008_11359_b200 as fgp
     g, h, hT = G
