@@ -294,8 +294,10 @@ fg_status fg_spmm(const fg_graph* g, fg_msg_op msg, fg_reduce_op red, int H, int
  *     out[eid(p)][h] = sum_{d<D} X[u][h][d] * Y[v][h][d]   for every edge p = (u -> v)
  *   X : [n_src][H][D];  Y : [n_dst][H][D] (may equal X: Eq. (4) uses X_V on
  *       both sides);  out : [nnz][H], fully overwritten.
- *   Heads are independent reductions (Fig. 5b).  Requires (H*D) % 4 == 0 and,
- *   for H > 1, D % 4 == 0 with D/4 a power of two (else FG_ESHAPE).
+ *   Heads are independent reductions (Fig. 5b).  Requires (H*D) % 4 == 0 (else
+ *   FG_ESHAPE).  Any D: D = 4 * 2^k with H*D <= 512 (and every H == 1 width)
+ *   runs the lane-partitioned kernels; other head shapes a thread-per-edge
+ *   kernel (each head's dot one sequential fp32 FMA chain; 2.5-4x slower).
  * Elementwise ops (FG_EDGE_U_ADD_V / _SUB_V / _MUL_V, row f4):
  *     out[eid(p)][j] = X[u][j] OP Y[v][j],  j < H*D;  out : [nnz][H*D] (H is
  *   only a shape factor here); one IEEE fp32 operation per element, so the
@@ -324,7 +326,10 @@ fg_status fg_edge_softmax(const fg_graph* g, int H, const float* scores, float* 
  *   rows -> 0); scores: optional [nnz][H] (edge id) receives the pre-softmax
  *   scores s.  Equal in real arithmetic to fg_sddmm + fg_edge_softmax + fg_spmm
  *   (u_mul_e, sum); here s and alpha never leave the SM and X[u] is read once.
- *   Requires D = 4*2^k <= 128 and H*D <= 512.
+ *   Fused for D = 4*2^k <= 128 with H*D <= 512; any other shape with (H*D) % 4
+ *   == 0 runs that unfused chain through `scores` (then required: alpha is
+ *   formed in place and the pre-softmax scores are written again at the end;
+ *   FG_EUNSUPPORTED when scores is NULL).
  */
 fg_status fg_gat_attention(const fg_graph* g, int H, int D, const float* X, const float* Y, float* out,
                            float* scores, fg_stream stream);
@@ -351,10 +356,11 @@ fg_status fg_sddmm_emul(const fg_graph* g, int H, int D, const float* X, const f
  * the bf16-representable inputs, to the same tolerance (1e-4 * sum|terms|
  * against the fp64 oracle on the decoded inputs).
  *
- * fg_spmm_x16 -- msg in {FG_MSG_COPY_U, FG_MSG_U_MUL_E}, red in {FG_REDUCE_SUM,
- *   FG_REDUCE_MAX} (else FG_EUNSUPPORTED).  X : bf16 bits [n_src][H*D]
- *   (uint16, 8-byte aligned); E : fp32 [nnz][H] for u_mul_e, else NULL;
- *   out fp32 [n_dst][H*D]; arg_u / arg_e as fg_spmm (max only).  Same
+ * fg_spmm_x16 -- msg in {FG_MSG_COPY_U, FG_MSG_U_MUL_E} (else
+ *   FG_EUNSUPPORTED), red any of sum / max / min / mean.  X : bf16 bits
+ *   [n_src][H*D] (uint16, 8-byte aligned); E : fp32 [nnz][H] for u_mul_e,
+ *   else NULL; out fp32 [n_dst][H*D]; arg_u / arg_e as fg_spmm (max / min
+ *   only).  Same
  *   semantics, tie rules, empty-row conventions and errors as fg_spmm.
  * fg_sddmm_x16 -- op FG_EDGE_U_DOT_V only.  X [n_src][H][D], Y [n_dst][H][D]
  *   bf16 bits (8-byte aligned); out fp32 [nnz][H].  Shape rules as fg_sddmm.

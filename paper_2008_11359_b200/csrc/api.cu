@@ -107,10 +107,6 @@ fg_status check_sddmm(const fg_graph* g, fg_edge_op op, int H, int D, const floa
     if (H < 1 || D < 1) return set_error(FG_ESHAPE, "fg_sddmm: H=%d D=%d must be >= 1", H, D);
     const int64_t F = int64_t(H) * D;
     if (F % 4 != 0) return set_error(FG_ESHAPE, "fg_sddmm: H*D must be a multiple of 4");
-    if (op == FG_EDGE_U_DOT_V && H > 1 && (D % 4 != 0 || ((D / 4) & (D / 4 - 1)) != 0))
-        return set_error(FG_ESHAPE, "fg_sddmm: with H > 1, D must be 4 * 2^k (got D=%d)", D);
-    if (op == FG_EDGE_U_DOT_V && H > 1 && F > 512)
-        return set_error(FG_EUNSUPPORTED, "fg_sddmm: multi-head with H*D > 512 not implemented");
     if (F > (int64_t(1) << 20)) return set_error(FG_ESHAPE, "fg_sddmm: H*D too large");
     if (g->nnz == 0) return FG_OK;
     if (!X || !Y || !out) return set_error(FG_EINVAL, "fg_sddmm: NULL tensor");
@@ -151,8 +147,6 @@ extern "C" fg_status fg_sddmm_emul(const fg_graph* g, int H, int D, const float*
     if (H < 1 || D < 1) return set_error(FG_ESHAPE, "fg_sddmm_emul: H=%d D=%d must be >= 1", H, D);
     const int64_t F = int64_t(H) * D;
     if (F % 4 != 0 || F > (int64_t(1) << 20)) return set_error(FG_ESHAPE, "fg_sddmm_emul: H*D must be a multiple of 4");
-    if (H > 1 && (D % 4 != 0 || ((D / 4) & (D / 4 - 1)) != 0))
-        return set_error(FG_ESHAPE, "fg_sddmm_emul: with H > 1, D must be 4 * 2^k (got D=%d)", D);
     if (g->nnz == 0) return FG_OK;
     if (!X || !Y || !E || !out) return set_error(FG_EINVAL, "fg_sddmm_emul: NULL tensor");
     if (!aligned16(X) || !aligned16(Y) || !aligned16(out))
@@ -171,9 +165,10 @@ extern "C" fg_status fg_spmm_x16(const fg_graph* g, fg_msg_op msg, fg_reduce_op 
     if (!g) return set_error(FG_EINVAL, "fg_spmm_x16: NULL graph");
     if (msg != FG_MSG_COPY_U && msg != FG_MSG_U_MUL_E)
         return set_error(FG_EUNSUPPORTED, "fg_spmm_x16: only copy_u and u_mul_e (got msg %d)", int(msg));
-    if (red != FG_REDUCE_SUM && red != FG_REDUCE_MAX)
-        return set_error(FG_EUNSUPPORTED, "fg_spmm_x16: only sum and max (got reduce %d)", int(red));
-    if (red == FG_REDUCE_SUM && (arg_u || arg_e)) return set_error(FG_EINVAL, "fg_spmm_x16: arg_u/arg_e with sum");
+    if (red != FG_REDUCE_SUM && red != FG_REDUCE_MAX && red != FG_REDUCE_MIN && red != FG_REDUCE_MEAN)
+        return set_error(FG_EINVAL, "fg_spmm_x16: bad reducer %d", int(red));
+    if ((red == FG_REDUCE_SUM || red == FG_REDUCE_MEAN) && (arg_u || arg_e))
+        return set_error(FG_EINVAL, "fg_spmm_x16: arg_u/arg_e with sum / mean");
     if (H < 1 || D < 1) return set_error(FG_ESHAPE, "fg_spmm_x16: H=%d D=%d must be >= 1", H, D);
     const int64_t F = int64_t(H) * D;
     if (F % 4 != 0 || F > (int64_t(1) << 20))

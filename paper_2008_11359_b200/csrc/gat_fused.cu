@@ -267,10 +267,25 @@ extern "C" fg_status fg_gat_attention(const fg_graph* g, int H, int D, const flo
                                       float* scores, fg_stream stream) {
     using fgk::set_error;
     if (!g) return set_error(FG_EINVAL, "fg_gat_attention: NULL graph");
-    if (H < 1 || D < 4 || D % 4 != 0 || ((D / 4) & (D / 4 - 1)) != 0 || D / 4 > 32)
-        return set_error(FG_ESHAPE, "fg_gat_attention: D must be 4 * 2^k <= 128 (got %d)", D);
+    if (H < 1 || D < 1 || (int64_t(H) * D) % 4 != 0)
+        return set_error(FG_ESHAPE, "fg_gat_attention: H=%d D=%d (H*D must be a multiple of 4)", H, D);
     const int F4 = H * D / 4;
-    if (F4 > 128) return set_error(FG_EUNSUPPORTED, "fg_gat_attention: H*D > 512 not implemented");
+    if (D % 4 != 0 || ((D / 4) & (D / 4 - 1)) != 0 || D / 4 > 32 || F4 > 128) {
+        // shapes outside the fused kernel (D not 4 * 2^k <= 128, or H*D > 512): the
+        // unfused chain through the caller's scores buffer -- scores, alpha in place,
+        // the alpha-weighted aggregation, then the pre-softmax scores again (the
+        // contract of `scores`); no allocation
+        if (!scores)
+            return set_error(FG_EUNSUPPORTED, "fg_gat_attention: H=%d D=%d runs unfused and needs the scores buffer",
+                             H, D);
+        fg_status r = fg_sddmm(g, FG_EDGE_U_DOT_V, H, D, X, Y, scores, stream);
+        if (r == FG_OK) r = fg_edge_softmax(g, H, scores, scores, stream);
+        if (r == FG_OK)
+            r = fg_spmm(g, FG_MSG_U_MUL_E, FG_REDUCE_SUM, H, D, X, scores, nullptr, 0, nullptr, out, nullptr, nullptr,
+                        nullptr, 0, stream);
+        if (r == FG_OK) r = fg_sddmm(g, FG_EDGE_U_DOT_V, H, D, X, Y, scores, stream);
+        return r;
+    }
     if (g->n_dst == 0) return FG_OK;
     if (!X || !Y || !out) return set_error(FG_EINVAL, "fg_gat_attention: NULL tensor");
     if (!fgk::aligned16(X) || !fgk::aligned16(Y) || !fgk::aligned16(out))

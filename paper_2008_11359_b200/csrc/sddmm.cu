@@ -42,6 +42,7 @@ struct Args {
     const int32_t* col_idx;
     const int32_t* eid;
     int H, D4, F4;
+    int D;            // features per head (the generic multi-head kernel)
     int c4base;       // first float4 column of this pass (feature-dimension tiling, H == 1)
     int accumulate;   // pass > 0: out += partial
     int tile4;        // float4 columns per pass (0: one pass over all F4)
@@ -498,6 +499,48 @@ __global__ void __launch_bounds__(THREADS, MINB) sddmm_h1_pipe_kernel(const Args
     }
 }
 
+// Generic multi-head u_dot_v for shapes the lane-partitioned kernels do not
+// cover (D not a multiple of 4 or D/4 not a power of two, or H*D > 512): a warp
+// per work unit, a thread per edge walking the feature row in float4 chunks and
+// closing head h after its D-th product (heads may start inside a chunk).  Each
+// head's dot is one sequential fp32 FMA chain in feature order.  The support
+// path for unusual head shapes (thread-per-edge gathers are 2.5-4.3x slower
+// than the lane-partitioned kernels at the shapes both run, ablation E6).
+__global__ void __launch_bounds__(THREADS) sddmm_heads_generic_kernel(const Args A, const float4* __restrict__ X,
+                                                                      const float4* __restrict__ Y,
+                                                                      float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = int64_t(gridDim.x) * (THREADS / 32);
+    const int F4 = A.F4, H = A.H, D = A.D;
+    for (int64_t unit = (int64_t(blockIdx.x) * THREADS + threadIdx.x) / 32; unit < A.n_units; unit += nwarps) {
+        const int64_t v = A.unit_row[unit];
+        const int64_t s = A.unit_p0[unit];
+        const int64_t e = A.unit_p1 ? A.unit_p1[unit] : min(s + A.unit_chunk, A.row_ptr[v + 1]);
+        for (int64_t p = s + lane; p < e; p += 32) {
+            const int64_t u = __ldg(A.col_idx + p);
+            const int64_t eo = (A.eid ? int64_t(__ldg(A.eid + p)) : p) * H;
+            const float4* xr = X + u * F4;
+            const float4* yr = Y + v * F4;
+            float acc = 0.f;
+            int h = 0, k = 0;
+            for (int c = 0; c < F4; ++c) {
+                const float4 x = __ldg(xr + c), y = __ldg(yr + c);
+                const float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc = fmaf(xs[q], ys[q], acc);
+                    if (++k == D) {   // head h complete
+                        out[eo + h] = A.E ? acc * __ldg(A.E + eo + h) : acc;
+                        acc = 0.f;
+                        k = 0;
+                        ++h;
+                    }
+                }
+            }
+        }
+    }
+}
+
 template <int G, int NV, bool XB = false>
 fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, cudaStream_t st) {
     using K = void (*)(const Args, const float4*, const float4*, float*);
@@ -606,6 +649,7 @@ static fg_status launch_sddmm_core(const fg_graph* g, int H, int D, const float*
     A.H = H;
     A.F4 = H * D / 4;
     A.D4 = (H > 1) ? D / 4 : A.F4;
+    A.D = D;
     A.c4base = 0;
     A.accumulate = 0;
     A.tile4 = 0;
@@ -675,6 +719,16 @@ static fg_status launch_sddmm_core(const fg_graph* g, int H, int D, const float*
             A.n_units = su->n_units;
             A.persistent = int(g->tune.sddmm_persist);   // CTAs per SM (-1: the occupancy)
         }
+    }
+    // multi-head shapes outside the lane-partitioned kernels (D not 4 * 2^k, or
+    // H*D > 512): the generic thread-per-edge kernel, any D (fp32 storage)
+    if (!xb && H > 1 && (D % 4 != 0 || ((D / 4) & (D / 4 - 1)) != 0 || F4 > 128)) {
+        const int64_t per_block = THREADS / 32;
+        int64_t blocks = (A.n_units + per_block - 1) / per_block;
+        if (A.persistent) blocks = std::min<int64_t>(blocks, int64_t(fgk::num_sms()) * 8);
+        if (blocks == 0) return FG_OK;
+        sddmm_heads_generic_kernel<<<unsigned(blocks), THREADS, 0, st>>>(A, X4, Y4, out);
+        return fgk::check_launch("sddmm_heads_generic_kernel");
     }
     if (g->tune.sddmm_dot == 1 && !xb && A.tile4 == 0) {   // ablation E6: thread-per-edge dot products
         const int64_t per_block = THREADS / 32;

@@ -175,8 +175,10 @@ fg_status launch_spmm_gather(const fg_graph* g, fg_msg_op msg, fg_reduce_op red,
             default: return dispatch_pair32<R_SUM>(A, G, NV, op, st);
         }
     }
-    if (Xbf16) {   // bf16 storage: copy_u / u_mul_e x {sum, max} (validated by the caller)
+    if (Xbf16) {   // bf16 storage: copy_u / u_mul_e x {sum, max, min, mean} (validated by the caller)
         if (mx == R_MAX) return dispatch_x16<R_MAX>(A, G, NV, op, pair, st);
+        if (mx == R_MIN) return dispatch_x16<R_MIN>(A, G, NV, op, pair, st);
+        if (mx == R_MEAN) return dispatch_x16<R_MEAN>(A, G, NV, op, pair, st);
         return dispatch_x16<R_SUM>(A, G, NV, op, pair, st);
     }
     switch (mx) {

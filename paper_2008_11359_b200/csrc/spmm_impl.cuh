@@ -506,5 +506,9 @@ template <>
 fg_status dispatch_x16<R_SUM>(const Args& A, int G, int NV, int op, bool pair, cudaStream_t st);
 template <>
 fg_status dispatch_x16<R_MAX>(const Args& A, int G, int NV, int op, bool pair, cudaStream_t st);
+template <>
+fg_status dispatch_x16<R_MIN>(const Args& A, int G, int NV, int op, bool pair, cudaStream_t st);
+template <>
+fg_status dispatch_x16<R_MEAN>(const Args& A, int G, int NV, int op, bool pair, cudaStream_t st);
 
 }  // namespace fgspmm

@@ -241,7 +241,7 @@ def spmm(g: Graph, msg: str, reduce: str, X: torch.Tensor, *, H: int = 1, E: tor
          arg_u: torch.Tensor | bool | None = None, arg_e: torch.Tensor | bool | None = None, stream=None):
     """featgraph.spmm (Eq. (1)).  Returns out, or (out, arg_u, arg_e) when args requested.
     copy_e takes X=None and E [nnz][F].  A torch.bfloat16 X selects bf16 feature
-    storage (fg_spmm_x16: copy_u / u_mul_e, sum / max; fp32 arithmetic and out)."""
+    storage (fg_spmm_x16: copy_u / u_mul_e, any reducer; fp32 arithmetic and out)."""
     if X is not None and X.dtype == torch.bfloat16:
         return _spmm_x16(g, msg, reduce, X, H=H, E=E, out=out, arg_u=arg_u, arg_e=arg_e, stream=stream)
     X = _dev(X, torch.float32, "X")
@@ -292,7 +292,7 @@ def _spmm_x16(g, msg, reduce, X, *, H, E, out, arg_u, arg_e, stream):
     out = _out(out, (g.n_dst, F), torch.float32, "out")
     if out is None:
         out = torch.empty((g.n_dst, F), dtype=torch.float32, device=X.device)
-    want = reduce == "max" and (arg_u is not None or arg_e is not None)
+    want = reduce in ("max", "min") and (arg_u is not None or arg_e is not None)
     if arg_u is True:
         arg_u = torch.empty((g.n_dst, F), dtype=torch.int32, device=X.device)
     if arg_e is True:

@@ -654,30 +654,72 @@ def test_gat_fused(skewed, skewed_eid, H, D, use_eid):
     check_close(o2, ref, ab, TOL, "unfused chain")
 
 
+@pytest.mark.parametrize("H,D", [(3, 12), (4, 3), (2, 6), (16, 64), (6, 20), (3, 44)])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_sddmm_generic_heads(skewed, skewed_eid, H, D, use_eid):
+    """Head shapes outside the lane-partitioned kernels (D not 4 * 2^k, or
+    H*D > 512): the generic thread-per-edge kernel, plain, segmented and with
+    the e_mul scale, against the oracle."""
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    X = feats((g.n_src, H * D), 1400 + D, gen.REAL)
+    Y = feats((g.n_dst, H * D), 1401 + D, gen.REAL)
+    ref, ab = oracle.sddmm(g.row_ptr, g.col_idx, X, Y, H=H)
+    pos = np.arange(g.nnz) if g.eid is None else g.eid
+    out = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+    check_close(out[pos], ref, ab, TOL, f"generic u_dot_v H={H} D={D}")
+    with tuned(g.h, sddmm_seg_mb=1, sddmm_seg_min_mb=0):
+        g.h.prepare(H * D * 4)
+        seg = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+    assert np.array_equal(seg, out)               # same per-edge arithmetic, other unit order
+    E = gen.features((g.nnz, H), 1402, 1, gen.UNIT)
+    em = fgp.sddmm(g.h, dev(X), dev(Y), H=H, E=dev(E)).cpu().numpy()
+    assert np.array_equal(em, (out * E).astype(np.float32))
+
+
+@pytest.mark.parametrize("H,D", [(3, 12), (4, 3), (16, 64), (1, 256), (2, 6)])
+def test_gat_unfused_fallback(skewed, H, D):
+    """fg_gat_attention outside the fused kernel's shapes: the unfused chain
+    through the scores buffer (include/fg.h), against the GAT definition; the
+    scores buffer ends with the pre-softmax scores; without it FG_EUNSUPPORTED."""
+    import paper_2008_11359_b200 as fgp
+    g = skewed
+    X = feats((g.n_src, H * D), 1410 + D, gen.REAL) * 0.5
+    Y = feats((g.n_dst, H * D), 1411 + D, gen.REAL) * 0.5
+    out, sc = fgp.gat_attention(g.h, dev(X), dev(Y), H=H, scores=True)
+    ref, ab = oracle.gat(g.row_ptr, g.col_idx, X, Y, H=H)
+    check_close(out.cpu().numpy(), ref, ab, TOL, f"gat fallback H={H} D={D}")
+    rs, rab = oracle.sddmm(g.row_ptr, g.col_idx, X, Y, H=H)
+    check_close(sc.cpu().numpy(), rs, rab, TOL, "gat fallback scores")
+    with pytest.raises(fgp.FGError) as e:
+        fgp.gat_attention(g.h, dev(X), dev(Y), H=H)
+    assert e.value.status == 3   # FG_EUNSUPPORTED
+
+
 # ------------------------------------------------------------------ bf16 feature storage (row f4)
 def bf16_dev(bits):
     return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).cuda().view(torch.bfloat16)
 
 
 @pytest.mark.parametrize("F", [4, 32, 128, 200, 512, 640])
-@pytest.mark.parametrize("red", ["sum", "max"])
+@pytest.mark.parametrize("red", ["sum", "max", "min", "mean"])
 def test_copy_u_bf16(skewed, F, red):
     """fg_spmm_x16: the oracle runs on the exact fp32 decoding of the same bf16
     inputs; sum to tolerance, max values and argmax exact."""
     import paper_2008_11359_b200 as fgp
     bits, dec = gen.to_bf16(feats((skewed.n_src, F), 700 + F, gen.REAL))
     ref, ab, rau, rae = oracle.spmm(skewed.row_ptr, skewed.col_idx, "copy_u", red, dec)
-    if red == "sum":
-        out = fgp.spmm(skewed.h, "copy_u", "sum", bf16_dev(bits)).cpu().numpy()
-        check_close(out, ref, ab, TOL, f"bf16 copy_u-sum F={F}")
+    if red in ("sum", "mean"):
+        out = fgp.spmm(skewed.h, "copy_u", red, bf16_dev(bits)).cpu().numpy()
+        check_close(out, ref, ab, TOL, f"bf16 copy_u-{red} F={F}")
     else:
-        out, au, ae = fgp.spmm(skewed.h, "copy_u", "max", bf16_dev(bits), arg_u=True, arg_e=True)
+        out, au, ae = fgp.spmm(skewed.h, "copy_u", red, bf16_dev(bits), arg_u=True, arg_e=True)
         assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
         assert np.array_equal(au.cpu().numpy(), rau) and np.array_equal(ae.cpu().numpy(), rae)
 
 
 @pytest.mark.parametrize("H,D", [(8, 32), (4, 2), (1, 512)])
-@pytest.mark.parametrize("red", ["sum", "max"])
+@pytest.mark.parametrize("red", ["sum", "max", "min", "mean"])
 @pytest.mark.parametrize("use_eid", [False, True])
 def test_u_mul_e_bf16(skewed, skewed_eid, H, D, red, use_eid):
     import paper_2008_11359_b200 as fgp
@@ -685,11 +727,11 @@ def test_u_mul_e_bf16(skewed, skewed_eid, H, D, red, use_eid):
     bits, dec = gen.to_bf16(feats((g.n_src, H * D), 710 + D, gen.REAL))
     E = gen.features((g.nnz, H), 711, 0, gen.UNIT)
     ref, ab, rau, rae = oracle.spmm(g.row_ptr, g.col_idx, "u_mul_e", red, dec, H=H, E=E, eid=g.eid)
-    if red == "sum":
-        out = fgp.spmm(g.h, "u_mul_e", "sum", bf16_dev(bits), H=H, E=dev(E)).cpu().numpy()
-        check_close(out, ref, ab, TOL, f"bf16 u_mul_e-sum H={H} D={D}")
+    if red in ("sum", "mean"):
+        out = fgp.spmm(g.h, "u_mul_e", red, bf16_dev(bits), H=H, E=dev(E)).cpu().numpy()
+        check_close(out, ref, ab, TOL, f"bf16 u_mul_e-{red} H={H} D={D}")
     else:
-        out, au, ae = fgp.spmm(g.h, "u_mul_e", "max", bf16_dev(bits), H=H, E=dev(E), arg_u=True, arg_e=True)
+        out, au, ae = fgp.spmm(g.h, "u_mul_e", red, bf16_dev(bits), H=H, E=dev(E), arg_u=True, arg_e=True)
         assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
         assert np.array_equal(au.cpu().numpy(), rau) and np.array_equal(ae.cpu().numpy(), rae)
 
@@ -710,8 +752,9 @@ def test_sddmm_bf16(skewed, skewed_eid, H, D, use_eid):
 def test_bf16_rejects_unsupported(skewed):
     import paper_2008_11359_b200 as fgp
     bits, _ = gen.to_bf16(feats((skewed.n_src, 32), 730, gen.REAL))
+    E = torch.zeros(skewed.nnz, 1, device="cuda")
     with pytest.raises(fgp.FGError) as e:
-        fgp.spmm(skewed.h, "copy_u", "mean", bf16_dev(bits))
+        fgp.spmm(skewed.h, "u_add_e", "sum", bf16_dev(bits), E=E)
     assert e.value.status == 3   # FG_EUNSUPPORTED
 
 
