@@ -100,7 +100,7 @@ double gather_gbs(const float4* X, int64_t x_bytes, int F, int blocks_per_sm, fl
     const int threads = 256;
     const int blocks = g_sms * blocks_per_sm;
     const int64_t groups = int64_t(blocks) * threads / G;
-    const int64_t total_rows = (1600LL << 20) / (int64_t(F) * 4);   // ~1.6 GB of row reads per launch
+    const int64_t total_rows = (6400LL << 20) / (int64_t(F) * 4);   // ~6.4 GB of row reads per launch (long enough that ramp-up does not cap the rate)
     const int64_t rpg = (total_rows / groups + U - 1) / U * U;
     const float ms = best_ms([&] { gather_kernel<G, NV, U><<<blocks, threads>>>(X, nrows, F4, rpg, sink); }, 5);
     const double gbs = double(groups) * rpg * F * 4 / (ms * 1e-3) / 1e9;

@@ -41,4 +41,7 @@ timeout 900 $NCU -k regex:spmm_gather -s 9 -c 1 -o gpurun_out/prof_dspmm_$TAG $B
 timeout 900 $NCU -k regex:sddmm_kernel -s 6 -c 1 -o gpurun_out/prof_dsddmm_$TAG $B --uniform-sources > /dev/null 2>&1; echo dsddmm $?
 ;;
 esac
+# captures travel back compressed (gpurun_out/ is capped at 64 MiB per call);
+# locally: gunzip gpurun_out/*.ncu-rep.gz before tools/make_profiles.py
+for f in gpurun_out/*.ncu-rep; do [ -f "$f" ] && gzip -f -6 "$f"; done
 ls -la gpurun_out | tail -12
