@@ -14,9 +14,12 @@ gpurun_out/launches_<tag>.csv; writes
   profiles/launches_<tag>.md       per-launch device times of one bench step
 """
 import csv
+import gzip
 import json
 import os
+import shutil
 import sys
+import tempfile
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_summary import summarise  # noqa: E402
@@ -55,10 +58,18 @@ lines = [f"# ncu --set full summaries ({tag})", "",
          "Times are ncu replay times (cold-cache, serialised), not bench values.", ""]
 traffic = {"build_hash": os.environ.get("FG_BUILD_HASH") or source_hash(), "capture": tag,
            "default": {}, "uniform": {}, "uniform_direct": {}}
+found = 0
 for key, (variant, ops) in OPS_BY_FILE.items():
     path = os.path.join(ROOT, "gpurun_out", f"prof_{key}_{tag}.ncu-rep")
+    if not os.path.exists(path) and os.path.exists(path + ".gz"):
+        # captures travel back gzip'd (gpurun_out/ is capped at 64 MiB per call)
+        tmp = os.path.join(tempfile.gettempdir(), os.path.basename(path))
+        with gzip.open(path + ".gz", "rb") as fi, open(tmp, "wb") as fo:
+            shutil.copyfileobj(fi, fo)
+        path = tmp
     if not os.path.exists(path):
         continue
+    found += 1
     for op, d in zip(ops, summarise(path)):
         t = num(d.get("gpu__time_duration.sum", ""))
         rd = num(d.get("dram__bytes_read.sum", "")) or 0.0
@@ -87,6 +98,8 @@ for key, (variant, ops) in OPS_BY_FILE.items():
                 lines.append(f"| L2 GB/s (lts__t_sectors x 32 B / time) | {lts / t / 1e9:.1f} |")
         lines.append(f"| top stall samples | {', '.join(f'{k}={v}' for k, v in d['top_stalls'].items())} |")
         lines.append("")
+if not found:
+    sys.exit(f"make_profiles: no prof_*_{tag}.ncu-rep[.gz] under gpurun_out/ -- refusing to overwrite the summaries")
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
 open(os.path.join(ROOT, "profiles", f"ncu_summary_{tag}.md"), "w").write("\n".join(lines) + "\n")
 json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
