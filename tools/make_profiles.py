@@ -121,7 +121,11 @@ if os.path.exists(lp):
             # (the flush's read-back reduction and the L2 probe are not step kernels)
             cur.append((k, v))
     segs.append(cur)
-    step = [sg for sg in segs if len(sg) >= 7][-1]   # last full step (extras follow it)
+    # the last timed (flushed) step: the modal segment length is the step's launch count
+    # (the warm-L2 steps that follow run without a flush, so they land in one segment)
+    full = [sg for sg in segs if len(sg) >= 7]
+    modal = max(set(len(sg) for sg in full), key=lambda n: sum(len(sg) == n for sg in full))
+    step = [sg for sg in full if len(sg) == modal][-1]
     tot = sum(v for _, v in step)
     out = [f"# Launch list of one bench step ({tag})", "",
            "`ncu --metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 2 --warmup 3`; "
