@@ -63,4 +63,19 @@ __device__ __forceinline__ void reduce_scatter(float (&v)[K], int gl, unsigned m
     }
 }
 
+// cp.async (LDGSTS) into shared memory without registers in flight: 16 bytes
+// bypassing L1 (.cg), or 4 bytes (.ca; .cg takes 16 only); one commit group per
+// call of cp_async_commit, cp_async_wait<N> = at most N groups still pending.
+__device__ __forceinline__ void cp_async16_cg(void* smem, const void* g) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async4_ca(void* smem, const void* g) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 }  // namespace fgdev

@@ -48,7 +48,7 @@ struct Args {
     int tile4;        // float4 columns per pass (0: one pass over all F4)
     int persistent;   // != 0: persistent grid (resident CTAs per SM x #SMs; > 0 caps the CTAs per SM)
     const float* E;   // u_dot_v-then-e_mul (fg_sddmm_emul): scores scaled by E[eid][h] at the write-back
-    int pipe;         // H == 1 wide rows: 0 sddmm_kernel, 1..3 sddmm_h1_pipe_kernel variants, -1 auto (FG_TUNE_SDDMM_PIPE)
+    int pipe;         // H == 1 wide rows: 0 sddmm_kernel, 1..3 sddmm_h1_pipe_kernel, 4..6 sddmm_h1_pf_kernel variants, -1 auto (FG_TUNE_SDDMM_PIPE)
 };
 
 // chunk c (4 features) of row r of a feature matrix with F4 chunks per row;
@@ -499,6 +499,140 @@ __global__ void __launch_bounds__(THREADS, MINB) sddmm_h1_pipe_kernel(const Args
     }
 }
 
+// shared-memory float4 read that the compiler may not hoist out of a loop (keeps
+// the Y chunks of sddmm_h1_pf_kernel<YS = true> out of registers)
+__device__ __forceinline__ float4 lds_f4(const float4* p) {
+    float4 r;
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(a));
+    return r;
+}
+
+// Unit-prefetching H == 1 gather for wide rows (G = 32 lanes, NV float4 per
+// lane).  A work unit (<= 64 edges of one row inside one source segment; 35 on
+// average on the reddit-shaped graph) starts with two dependent global round
+// trips before its first X gather: the unit table, then the row's neighbour
+// indices and Y[v].  Here each warp stages the NEXT unit's indices and Y row
+// into a second shared-memory buffer with cp.async (LDGSTS: no registers held)
+// and loads the unit table entry of the one after, while it gathers the current
+// unit; so a unit's X gathers start as soon as the previous unit ends.
+//   YS == false: Y[v] copied into registers at the unit start (as sddmm_kernel);
+//   YS == true : Y read from shared memory chunk by chunk inside the edge loop
+//                (12 fewer registers; one LDS.128 per chunk per U edges).
+// Same per-lane partial dots (chunk order j), U = 2 edges per reduce-scatter,
+// same tree as sddmm_kernel<32, NV, MODE_H1>: bit-identical results.
+template <int NV, bool YS, int MINB, bool EM>
+__global__ void __launch_bounds__(THREADS, MINB) sddmm_h1_pf_kernel(const Args A, const float4* __restrict__ X,
+                                                                    const float4* __restrict__ Y,
+                                                                    float* __restrict__ out) {
+    constexpr int NGRP = THREADS / 32;
+    constexpr int CH = 64;   // max edges per work unit (host-checked: unit_chunk <= 64)
+    constexpr int U = 2;
+    __shared__ int s_idx[NGRP][2][CH];
+    __shared__ float4 s_y[NGRP][2][32 * NV];
+    __shared__ float s_res[NGRP][CH];
+    const int gl = threadIdx.x & 31;
+    const int gi = threadIdx.x >> 5;
+    constexpr unsigned mask = 0xffffffffu;
+    float* res = s_res[gi];
+    const int F4 = A.F4;
+    const char* xl = reinterpret_cast<const char*>(X + gl);   // this lane's first column
+    const uint32_t rowb = uint32_t(F4) * 16u;
+    bool cin[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) cin[j] = gl + 32 * j < F4;
+    const int64_t stride = int64_t(gridDim.x) * NGRP;
+    const int64_t n_units = A.n_units;
+    auto meta = [&](int64_t u, int64_t& v, int64_t& s, int& cnt) {
+        v = A.unit_row[u];
+        s = A.unit_p0[u];
+        const int64_t e = A.unit_p1 ? A.unit_p1[u] : min(s + A.unit_chunk, A.row_ptr[v + 1]);
+        cnt = int(e - s);
+    };
+    auto stage = [&](int buf, int64_t v, int64_t s, int cnt) {   // one commit group per unit
+        int* idx = s_idx[gi][buf];
+        for (int t = gl; t < cnt; t += 32) cp_async4_ca(idx + t, A.col_idx + s + t);
+        float4* yb = s_y[gi][buf];
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            if (cin[j]) cp_async16_cg(yb + gl + 32 * j, Y + v * F4 + gl + 32 * j);
+        cp_async_commit();
+    };
+    int64_t unit = int64_t(blockIdx.x) * NGRP + gi;
+    if (unit >= n_units) return;
+    int64_t v0, s0, v1 = 0, s1 = 0;
+    int c0, c1 = 0;
+    meta(unit, v0, s0, c0);
+    stage(0, v0, s0, c0);
+    if (unit + stride < n_units) meta(unit + stride, v1, s1, c1);
+    int buf = 0;
+    for (; unit < n_units; unit += stride) {
+        // the next unit's indices and Y row into the other buffer (an empty group at
+        // the end keeps the wait count uniform), then the unit table entry after it
+        if (unit + stride < n_units) stage(buf ^ 1, v1, s1, c1);
+        else cp_async_commit();
+        int64_t v2 = 0, s2 = 0;
+        int c2 = 0;
+        if (unit + 2 * stride < n_units) meta(unit + 2 * stride, v2, s2, c2);
+        cp_async_wait<1>();   // this unit's group has landed (this lane's copies) ...
+        __syncwarp();         // ... and every lane's
+        const int* idx = s_idx[gi][buf];
+        const float4* yb = s_y[gi][buf];
+        const int cnt = c0;
+        float4 y0[YS ? 1 : NV];
+        if constexpr (!YS) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) y0[j] = cin[j] ? yb[gl + 32 * j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll 1
+        for (int t0 = 0; t0 < cnt; t0 += U) {
+            float4 x[U][NV];
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {   // past cnt: the last row again, never stored
+                const char* xr = xl + uint64_t(uint32_t(idx[min(t0 + uu, cnt - 1)])) * rowb;
+#pragma unroll
+                for (int j = 0; j < NV; ++j)
+                    x[uu][j] = cin[j] ? __ldg(reinterpret_cast<const float4*>(xr) + 32 * j)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            float pv[U];
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) pv[uu] = 0.f;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                float4 yj;
+                if constexpr (YS) yj = cin[j] ? lds_f4(yb + gl + 32 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+                else yj = y0[j];
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) pv[uu] += dot4(x[uu][j], yj);
+            }
+            reduce_scatter<U, 32, 32>(pv, gl, mask);
+            // U = 2: lanes 0 and 16 hold the sums of edges t0 and t0 + 1
+            if ((gl & 15) == 0) {
+                const int t = t0 + (gl >> 4);
+                if (t < cnt) res[t] = pv[0];
+            }
+        }
+        __syncwarp();
+        if (A.eid == nullptr) {
+            for (int q = gl; q < cnt; q += 32) {
+                if constexpr (EM) out[s0 + q] = res[q] * __ldg(A.E + s0 + q);
+                else out[s0 + q] = res[q];
+            }
+        } else {
+            for (int q = gl; q < cnt; q += 32) {
+                const int64_t oi = __ldg(A.eid + s0 + q);
+                if constexpr (EM) out[oi] = res[q] * __ldg(A.E + oi);
+                else out[oi] = res[q];
+            }
+        }
+        __syncwarp();   // res / idx / y of this buffer are free before they are refilled
+        v0 = v1; s0 = s1; c0 = c1;
+        v1 = v2; s1 = s2; c1 = c2;
+        buf ^= 1;
+    }
+}
+
 // Generic multi-head u_dot_v for shapes the lane-partitioned kernels do not
 // cover (D not a multiple of 4 or D/4 not a power of two, or H*D > 512): a warp
 // per work unit, a thread per edge walking the feature row in float4 chunks and
@@ -585,12 +719,18 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
     }
     if constexpr (G == 32 && NV >= 2 && !XB) {   // software-pipelined wide-row H == 1 kernel (FG_TUNE_SDDMM_PIPE)
         // auto (-1): the pipelined U=2 kernel for NV = 3 (reddit F=384: 13.18 -> 10.64 ms);
-        // plain for NV = 2 / 4 (F=256: 8.07 vs 8.26-9.12 ms; F=512: 15.50 vs 15.41-30.5 ms)
-        const int pipe = A.pipe < 0 ? (NV == 3 ? 3 : 0) : A.pipe;
+        // the unit-prefetching kernel for NV = 4 (F=512: 15.20 -> 15.03 ms median, 14.77 ->
+        // 14.57 best; the software-pipelined variants 15.41-30.5); plain for NV = 2 (F=256:
+        // 7.14 ms vs 8.26-9.12 pipelined, 7.80-8.39 prefetching)
+        const int pipe = A.pipe < 0 ? (NV == 3 ? 3 : (NV == 4 ? 4 : 0)) : A.pipe;
         if (pipe && A.H == 1 && A.tile4 == 0 && A.unit_chunk <= 64) {
             if (pipe == 1) k = A.E ? sddmm_h1_pipe_kernel<NV, 1, 3, true> : sddmm_h1_pipe_kernel<NV, 1, 3, false>;
             else if (pipe == 2) k = A.E ? sddmm_h1_pipe_kernel<NV, 2, 2, true> : sddmm_h1_pipe_kernel<NV, 2, 2, false>;
-            else k = A.E ? sddmm_h1_pipe_kernel<NV, 2, 3, true> : sddmm_h1_pipe_kernel<NV, 2, 3, false>;
+            else if (pipe == 3) k = A.E ? sddmm_h1_pipe_kernel<NV, 2, 3, true> : sddmm_h1_pipe_kernel<NV, 2, 3, false>;
+            // 4..6: unit-prefetching kernel (next unit's indices + Y row staged by cp.async)
+            else if (pipe == 4) k = A.E ? sddmm_h1_pf_kernel<NV, false, 3, true> : sddmm_h1_pf_kernel<NV, false, 3, false>;
+            else if (pipe == 5) k = A.E ? sddmm_h1_pf_kernel<NV, true, 4, true> : sddmm_h1_pf_kernel<NV, true, 4, false>;
+            else k = A.E ? sddmm_h1_pf_kernel<NV, true, 3, true> : sddmm_h1_pf_kernel<NV, true, 3, false>;
         }
     }
     const int64_t per_block = THREADS / G;

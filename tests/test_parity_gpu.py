@@ -593,7 +593,7 @@ def test_sddmm_pipelined_and_hilbert(skewed, skewed_eid, F, use_eid):
     with tuned(g.h, sddmm_pipe=0):
         plain = fgp.sddmm(g.h, dev(X), dev(Y)).cpu().numpy()
     check_close(plain[pos], ref, ab, TOL, f"u_dot_v F={F}")
-    for pipe in (1, 2, 3, -1):
+    for pipe in (1, 2, 3, 4, 5, 6, -1):
         with tuned(g.h, sddmm_pipe=pipe):
             out = fgp.sddmm(g.h, dev(X), dev(Y)).cpu().numpy()
         assert np.array_equal(out, plain), f"pipe={pipe}"
