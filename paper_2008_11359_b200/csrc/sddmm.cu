@@ -48,7 +48,7 @@ struct Args {
     int tile4;        // float4 columns per pass (0: one pass over all F4)
     int persistent;   // != 0: persistent grid (resident CTAs per SM x #SMs; > 0 caps the CTAs per SM)
     const float* E;   // u_dot_v-then-e_mul (fg_sddmm_emul): scores scaled by E[eid][h] at the write-back
-    int pipe;         // H == 1 wide rows: 0 sddmm_kernel, 1..3 sddmm_h1_pipe_kernel, 4..6 sddmm_h1_pf_kernel variants, -1 auto (FG_TUNE_SDDMM_PIPE)
+    int pipe;         // H == 1 wide rows: 0 sddmm_kernel, 1..3 sddmm_h1_pipe_kernel, 4..6 sddmm_pf_kernel variants, -1 auto (FG_TUNE_SDDMM_PIPE)
 };
 
 // chunk c (4 features) of row r of a feature matrix with F4 chunks per row;
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(THREADS, MINB) sddmm_h1_pipe_kernel(const Args
 }
 
 // shared-memory float4 read that the compiler may not hoist out of a loop (keeps
-// the Y chunks of sddmm_h1_pf_kernel<YS = true> out of registers)
+// the Y chunks of sddmm_pf_kernel<YS = true> out of registers)
 __device__ __forceinline__ float4 lds_f4(const float4* p) {
     float4 r;
     const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -508,34 +508,36 @@ __device__ __forceinline__ float4 lds_f4(const float4* p) {
     return r;
 }
 
-// Unit-prefetching H == 1 gather for wide rows (G = 32 lanes, NV float4 per
-// lane).  A work unit (<= 64 edges of one row inside one source segment; 35 on
-// average on the reddit-shaped graph) starts with two dependent global round
-// trips before its first X gather: the unit table, then the row's neighbour
-// indices and Y[v].  Here each warp stages the NEXT unit's indices and Y row
-// into a second shared-memory buffer with cp.async (LDGSTS: no registers held)
-// and loads the unit table entry of the one after, while it gathers the current
-// unit; so a unit's X gathers start as soon as the previous unit ends.
+// Unit-prefetching gather (G = 32 lanes, NV float4 per lane; H == 1 with DW =
+// 32, or H heads of D = 4*DW features).  A work unit (<= 64 edges of one row
+// inside one source segment; 35 on average on the reddit-shaped graph) starts
+// with two dependent global round trips before its first X gather: the unit
+// table, then the row's neighbour indices and Y[v].  Here each warp stages the
+// NEXT unit's indices and Y row into a second shared-memory buffer with cp.async
+// (LDGSTS: no registers held) and loads the unit table entry of the one after,
+// while it gathers the current unit; so a unit's X gathers start as soon as the
+// previous unit ends.
 //   YS == false: Y[v] copied into registers at the unit start (as sddmm_kernel);
-//   YS == true : Y read from shared memory chunk by chunk inside the edge loop
-//                (12 fewer registers; one LDS.128 per chunk per U edges).
-// Same per-lane partial dots (chunk order j), U = 2 edges per reduce-scatter,
-// same tree as sddmm_kernel<32, NV, MODE_H1>: bit-identical results.
-template <int NV, bool YS, int MINB, bool EM>
-__global__ void __launch_bounds__(THREADS, MINB) sddmm_h1_pf_kernel(const Args A, const float4* __restrict__ X,
-                                                                    const float4* __restrict__ Y,
-                                                                    float* __restrict__ out) {
+//   YS == true : Y read from shared memory chunk by chunk inside the edge loop.
+// Same per-lane partial dots, same U edges per reduce-scatter and the same tree
+// as sddmm_kernel<32, NV, MODE_H1 / MODE_HEADS, DW>: bit-identical results.
+template <int NV, int DW, bool YS, int MINB, bool EM>
+__global__ void __launch_bounds__(THREADS, MINB) sddmm_pf_kernel(const Args A, const float4* __restrict__ X,
+                                                                 const float4* __restrict__ Y,
+                                                                 float* __restrict__ out) {
     constexpr int NGRP = THREADS / 32;
-    constexpr int CH = 64;   // max edges per work unit (host-checked: unit_chunk <= 64)
-    constexpr int U = 2;
+    constexpr int CH = 64;                                   // max edges per work unit (host-checked)
+    constexpr bool H1 = (DW == 32);
+    constexpr int U = NV >= 3 ? 2 : (NV == 2 ? 4 : 8);       // as sddmm_kernel
+    constexpr int HMAX = H1 ? 1 : 32 * NV / DW;              // heads per row
     __shared__ int s_idx[NGRP][2][CH];
     __shared__ float4 s_y[NGRP][2][32 * NV];
-    __shared__ float s_res[NGRP][CH];
+    __shared__ float s_res[NGRP][CH * HMAX];
     const int gl = threadIdx.x & 31;
     const int gi = threadIdx.x >> 5;
     constexpr unsigned mask = 0xffffffffu;
     float* res = s_res[gi];
-    const int F4 = A.F4;
+    const int F4 = A.F4, H = H1 ? 1 : A.H;
     const char* xl = reinterpret_cast<const char*>(X + gl);   // this lane's first column
     const uint32_t rowb = uint32_t(F4) * 16u;
     bool cin[NV];
@@ -595,33 +597,52 @@ __global__ void __launch_bounds__(THREADS, MINB) sddmm_h1_pf_kernel(const Args A
                     x[uu][j] = cin[j] ? __ldg(reinterpret_cast<const float4*>(xr) + 32 * j)
                                       : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            float pv[U];
+            constexpr int K = H1 ? U : U * NV;
+            float pv[K];
 #pragma unroll
-            for (int uu = 0; uu < U; ++uu) pv[uu] = 0.f;
+            for (int k = 0; k < K; ++k) pv[k] = 0.f;
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
                 float4 yj;
                 if constexpr (YS) yj = cin[j] ? lds_f4(yb + gl + 32 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
                 else yj = y0[j];
 #pragma unroll
-                for (int uu = 0; uu < U; ++uu) pv[uu] += dot4(x[uu][j], yj);
+                for (int uu = 0; uu < U; ++uu) {
+                    if constexpr (H1) pv[uu] += dot4(x[uu][j], yj);
+                    else pv[uu * NV + j] = dot4(x[uu][j], yj);
+                }
             }
-            reduce_scatter<U, 32, 32>(pv, gl, mask);
-            // U = 2: lanes 0 and 16 hold the sums of edges t0 and t0 + 1
-            if ((gl & 15) == 0) {
-                const int t = t0 + (gl >> 4);
-                if (t < cnt) res[t] = pv[0];
+            reduce_scatter<K, DW, 32>(pv, gl, mask);
+            constexpr int L = ilog2(K) < ilog2(DW) ? ilog2(K) : ilog2(DW);
+            constexpr int KEEP = K >> L;                       // values held per lane
+            const int sub = gl & (DW - 1);
+            const int bits = sub >> (ilog2(DW) - L);
+            if ((sub & ((DW >> L) - 1)) == 0) {
+#pragma unroll
+                for (int i = 0; i < KEEP; ++i) {
+                    const int id = bits * KEEP + i;
+                    if constexpr (H1) {
+                        if (t0 + id < cnt) res[t0 + id] = pv[i];
+                    } else {
+                        const int uu = id / NV, j = id % NV;
+                        const int head = gl / DW + j * (32 / DW);
+                        if (head < H && t0 + uu < cnt) res[(t0 + uu) * H + head] = pv[i];
+                    }
+                }
             }
         }
         __syncwarp();
+        const int tot = cnt * H;
         if (A.eid == nullptr) {
-            for (int q = gl; q < cnt; q += 32) {
-                if constexpr (EM) out[s0 + q] = res[q] * __ldg(A.E + s0 + q);
-                else out[s0 + q] = res[q];
+            float* o = out + s0 * H;
+            for (int q = gl; q < tot; q += 32) {
+                if constexpr (EM) o[q] = res[q] * __ldg(A.E + s0 * H + q);
+                else o[q] = res[q];
             }
         } else {
-            for (int q = gl; q < cnt; q += 32) {
-                const int64_t oi = __ldg(A.eid + s0 + q);
+            for (int q = gl; q < tot; q += 32) {
+                const int t = H1 ? q : q / H, h = q - t * H;
+                const int64_t oi = int64_t(__ldg(A.eid + s0 + t)) * H + h;
                 if constexpr (EM) out[oi] = res[q] * __ldg(A.E + oi);
                 else out[oi] = res[q];
             }
@@ -728,9 +749,17 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
             else if (pipe == 2) k = A.E ? sddmm_h1_pipe_kernel<NV, 2, 2, true> : sddmm_h1_pipe_kernel<NV, 2, 2, false>;
             else if (pipe == 3) k = A.E ? sddmm_h1_pipe_kernel<NV, 2, 3, true> : sddmm_h1_pipe_kernel<NV, 2, 3, false>;
             // 4..6: unit-prefetching kernel (next unit's indices + Y row staged by cp.async)
-            else if (pipe == 4) k = A.E ? sddmm_h1_pf_kernel<NV, false, 3, true> : sddmm_h1_pf_kernel<NV, false, 3, false>;
-            else if (pipe == 5) k = A.E ? sddmm_h1_pf_kernel<NV, true, 4, true> : sddmm_h1_pf_kernel<NV, true, 4, false>;
-            else k = A.E ? sddmm_h1_pf_kernel<NV, true, 3, true> : sddmm_h1_pf_kernel<NV, true, 3, false>;
+            else if (pipe == 4) k = A.E ? sddmm_pf_kernel<NV, 32, false, 3, true> : sddmm_pf_kernel<NV, 32, false, 3, false>;
+            else if (pipe == 5) k = A.E ? sddmm_pf_kernel<NV, 32, true, 4, true> : sddmm_pf_kernel<NV, 32, true, 4, false>;
+            else k = A.E ? sddmm_pf_kernel<NV, 32, true, 3, true> : sddmm_pf_kernel<NV, 32, true, 3, false>;
+        }
+    }
+    if constexpr (G == 32 && NV >= 2 && !XB) {   // unit-prefetching multi-head kernel (FG_TUNE_SDDMM_PIPE = 4)
+        // heads of D = 32 / 64 (D4 = 8 / 16 lanes per head); other head widths run sddmm_kernel
+        const int pipe = A.pipe < 0 ? -1 : A.pipe;
+        if (pipe == 4 && A.H > 1 && A.F4 <= TW && A.unit_chunk <= 64 && (A.D4 == 8 || A.D4 == 16)) {
+            if (A.D4 == 8) k = A.E ? sddmm_pf_kernel<NV, 8, false, 3, true> : sddmm_pf_kernel<NV, 8, false, 3, false>;
+            else k = A.E ? sddmm_pf_kernel<NV, 16, false, 3, true> : sddmm_pf_kernel<NV, 16, false, 3, false>;
         }
     }
     const int64_t per_block = THREADS / G;

@@ -610,6 +610,36 @@ def test_sddmm_pipelined_and_hilbert(skewed, skewed_eid, F, use_eid):
                 assert np.array_equal(out, plain), f"order={order} seg={seg} rb={rb} pipe={pipe}"
 
 
+@pytest.mark.parametrize("H,D", [(8, 32), (4, 64), (16, 32), (6, 32), (3, 64), (2, 64)])
+@pytest.mark.parametrize("use_eid", [False, True])
+def test_sddmm_heads_unit_prefetch(skewed, skewed_eid, H, D, use_eid):
+    """a4: the unit-prefetching multi-head kernel (FG_TUNE_SDDMM_PIPE = 4, heads of
+    D = 32 / 64) against the oracle, and bit for bit against the plain kernel
+    (same lane partition and reduction tree), also with the e_mul write-back."""
+    import paper_2008_11359_b200 as fgp
+    g = skewed_eid if use_eid else skewed
+    F = H * D
+    X = feats((g.n_src, F), 1400 + F, gen.REAL)
+    Y = feats((g.n_dst, F), 1401 + F, gen.REAL)
+    ref, ab = oracle.sddmm(g.row_ptr, g.col_idx, X, Y, H=H)
+    pos = np.arange(g.nnz) if g.eid is None else g.eid
+    with tuned(g.h, sddmm_pipe=0):
+        plain = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+    with tuned(g.h, sddmm_pipe=4):
+        out = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+    check_close(out[pos], ref, ab, TOL, f"u_dot_v H={H} D={D} pf")
+    assert np.array_equal(out, plain)
+    E = gen.features((g.nnz, H), 1402, 1, gen.UNIT)
+    with tuned(g.h, sddmm_pipe=4):
+        em = fgp.sddmm(g.h, dev(X), dev(Y), H=H, E=dev(E)).cpu().numpy()
+    assert np.array_equal(em, (plain * E).astype(np.float32))
+    with tuned(g.h, sddmm_seg_mb=1, sddmm_seg_min_mb=0):   # source-segmented unit tables
+        g.h.prepare(F * 4)
+        with tuned(g.h, sddmm_pipe=4):
+            seg = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+    assert np.array_equal(seg, plain)
+
+
 @pytest.mark.parametrize("F", [8, 32, 40, 128, 512])
 @pytest.mark.parametrize("red", ["sum", "max", "min", "mean"])
 def test_copy_u_ldg256_pairs(skewed, F, red):
