@@ -51,6 +51,10 @@ struct Args {
     int pipe;         // H == 1 wide rows: 0 sddmm_kernel, 1..3 sddmm_h1_pipe_kernel, 4..6 sddmm_pf_kernel variants, -1 auto (FG_TUNE_SDDMM_PIPE)
 };
 
+// smallest power of two >= x: reduce_scatter halves its value count per level,
+// so U*NV partial dots with NV = 3 are zero-padded to the next power of two
+constexpr int pow2ceil(int x) { return x <= 1 ? 1 : 2 * pow2ceil((x + 1) / 2); }
+
 // chunk c (4 features) of row r of a feature matrix with F4 chunks per row;
 // XB: bf16 storage (the float4 pointer then addresses 8-byte chunks)
 template <bool XB>
@@ -149,8 +153,11 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                     // reduce-scatter of the U edges' (x NV chunk) partial dots over the DW
                     // lanes that share a head: ~log2(DW) + (K-1)/... shuffles per U edges
                     // instead of log2(DW) per edge and chunk
-                    constexpr int K = (MODE == MODE_H1) ? U : U * NV;
+                    constexpr int KR = (MODE == MODE_H1) ? U : U * NV;   // real partial dots
+                    constexpr int K = pow2ceil(KR);
                     float pv[K];
+#pragma unroll
+                    for (int k = KR; k < K; ++k) pv[k] = 0.f;
 #pragma unroll
                     for (int uu = 0; uu < U; ++uu) {
                         if constexpr (MODE == MODE_H1) {
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(THREADS, 3) sddmm_kernel(const Args A, const f
                             } else {
                                 const int uu = id / NV, j = id % NV;
                                 const int head = gl / DW + j * (G / DW);
-                                if (head < H) res[(t0 + uu) * H + head] = pv[i];
+                                if (id < KR && head < H) res[(t0 + uu) * H + head] = pv[i];
                             }
                         }
                     }
@@ -530,9 +537,12 @@ __global__ void __launch_bounds__(THREADS, MINB) sddmm_pf_kernel(const Args A, c
     constexpr bool H1 = (DW == 32);
     constexpr int U = NV >= 3 ? 2 : (NV == 2 ? 4 : 8);       // as sddmm_kernel
     constexpr int HMAX = H1 ? 1 : 32 * NV / DW;              // heads per row
-    __shared__ int s_idx[NGRP][2][CH];
-    __shared__ float4 s_y[NGRP][2][32 * NV];
-    __shared__ float s_res[NGRP][CH * HMAX];
+    // dynamic shared memory (pf_smem_bytes): per warp two Y buffers, two index
+    // buffers and the unit's staged results
+    extern __shared__ __align__(16) unsigned char pf_smem[];
+    auto s_y = reinterpret_cast<float4 (*)[2][32 * NV]>(pf_smem);
+    auto s_idx = reinterpret_cast<int (*)[2][CH]>(pf_smem + NGRP * 2 * 32 * NV * 16);
+    auto s_res = reinterpret_cast<float (*)[CH * HMAX]>(pf_smem + NGRP * (2 * 32 * NV * 16 + 2 * CH * 4));
     const int gl = threadIdx.x & 31;
     const int gi = threadIdx.x >> 5;
     constexpr unsigned mask = 0xffffffffu;
@@ -597,7 +607,8 @@ __global__ void __launch_bounds__(THREADS, MINB) sddmm_pf_kernel(const Args A, c
                     x[uu][j] = cin[j] ? __ldg(reinterpret_cast<const float4*>(xr) + 32 * j)
                                       : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            constexpr int K = H1 ? U : U * NV;
+            constexpr int KR = H1 ? U : U * NV;   // real partial dots (zero-padded to a power of two)
+            constexpr int K = pow2ceil(KR);
             float pv[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) pv[k] = 0.f;
@@ -626,7 +637,7 @@ __global__ void __launch_bounds__(THREADS, MINB) sddmm_pf_kernel(const Args A, c
                     } else {
                         const int uu = id / NV, j = id % NV;
                         const int head = gl / DW + j * (32 / DW);
-                        if (head < H && t0 + uu < cnt) res[(t0 + uu) * H + head] = pv[i];
+                        if (id < KR && head < H && t0 + uu < cnt) res[(t0 + uu) * H + head] = pv[i];
                     }
                 }
             }
@@ -696,11 +707,17 @@ __global__ void __launch_bounds__(THREADS) sddmm_heads_generic_kernel(const Args
     }
 }
 
+// shared-memory bytes of sddmm_pf_kernel<NV, DW>
+constexpr int pf_smem_bytes(int NV, int DW) {
+    return (THREADS / 32) * (2 * 32 * NV * 16 + 2 * 64 * 4 + 64 * (DW == 32 ? 1 : 32 * NV / DW) * 4);
+}
+
 template <int G, int NV, bool XB = false>
 fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, cudaStream_t st) {
     using K = void (*)(const Args, const float4*, const float4*, float*);
     const int TW = G * NV;
     K k;
+    int dsmem = 0;   // dynamic shared memory of the chosen kernel (sddmm_pf_kernel only)
     // full-width rows (F4 == G*NV, one pass): the variant without per-chunk column predicates
     const bool fullw = !XB && A.tile4 == 0 && A.c4base == 0 && A.F4 == TW;
     if (A.H == 1 && (A.tile4 ? A.tile4 : A.F4) <= TW) {
@@ -739,12 +756,12 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
         }
     }
     if constexpr (G == 32 && NV >= 2 && !XB) {   // software-pipelined wide-row H == 1 kernel (FG_TUNE_SDDMM_PIPE)
-        // auto (-1): the pipelined U=2 kernel for NV = 3 (reddit F=384: 13.18 -> 10.64 ms);
-        // the unit-prefetching kernel for NV = 4 (F=512: 15.20 -> 15.03 ms median, 14.77 ->
-        // 14.57 best; the software-pipelined variants 15.41-30.5); plain for NV = 2 (F=256:
-        // 7.14 ms vs 8.26-9.12 pipelined, 7.80-8.39 prefetching)
-        const int pipe = A.pipe < 0 ? (NV == 3 ? 3 : (NV == 4 ? 4 : 0)) : A.pipe;
-        if (pipe && A.H == 1 && A.tile4 == 0 && A.unit_chunk <= 64) {
+        // auto (-1), measured on reddit (tools/sddmm_ab.py): the software-pipelined U=2
+        // kernel for NV = 3 (F=384: 12.21 plain -> 10.27 ms; unit-prefetching 11.5-11.7);
+        // the unit-prefetching kernel for NV = 2 and 4 (F=256: 7.07 -> 6.72 ms, F=512:
+        // 14.98 -> 14.54; the software-pipelined variants 8.26-9.12 / 15.41-30.5)
+        const int pipe = A.pipe < 0 ? (NV == 3 ? 3 : 4) : A.pipe;
+        if (pipe && A.H == 1 && A.tile4 == 0 && A.F4 <= TW && A.unit_chunk <= 64) {
             if (pipe == 1) k = A.E ? sddmm_h1_pipe_kernel<NV, 1, 3, true> : sddmm_h1_pipe_kernel<NV, 1, 3, false>;
             else if (pipe == 2) k = A.E ? sddmm_h1_pipe_kernel<NV, 2, 2, true> : sddmm_h1_pipe_kernel<NV, 2, 2, false>;
             else if (pipe == 3) k = A.E ? sddmm_h1_pipe_kernel<NV, 2, 3, true> : sddmm_h1_pipe_kernel<NV, 2, 3, false>;
@@ -752,27 +769,38 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
             else if (pipe == 4) k = A.E ? sddmm_pf_kernel<NV, 32, false, 3, true> : sddmm_pf_kernel<NV, 32, false, 3, false>;
             else if (pipe == 5) k = A.E ? sddmm_pf_kernel<NV, 32, true, 4, true> : sddmm_pf_kernel<NV, 32, true, 4, false>;
             else k = A.E ? sddmm_pf_kernel<NV, 32, true, 3, true> : sddmm_pf_kernel<NV, 32, true, 3, false>;
+            if (pipe >= 4) dsmem = pf_smem_bytes(NV, 32);
         }
     }
     if constexpr (G == 32 && NV >= 2 && !XB) {   // unit-prefetching multi-head kernel (FG_TUNE_SDDMM_PIPE = 4)
-        // heads of D = 32 / 64 (D4 = 8 / 16 lanes per head); other head widths run sddmm_kernel
-        const int pipe = A.pipe < 0 ? -1 : A.pipe;
+        // heads of D = 32 / 64 (D4 = 8 / 16 lanes per head); other head widths run sddmm_kernel.
+        // auto (-1): on for H*D <= 384 (reddit H=8 D=32 7.63 -> 7.30 ms, H=4 D=64 8.20 -> 7.36,
+        // H=6 D=32 7.82 -> 6.43, H=12 D=32 13.96 -> 13.14, H=6 D=64 14.98 -> 13.25) and for
+        // H*D = 512 with D = 64 (H=8: 18.16 -> 16.03); off for H*D = 512 with D = 32 (H=16:
+        // 16.30 plain vs 20.12 -- 70 KB of staged results per CTA)
+        const bool dflt = NV <= 3 || (NV == 4 && A.D4 == 16);
+        const int pipe = A.pipe < 0 ? (dflt ? 4 : 0) : A.pipe;
         if (pipe == 4 && A.H > 1 && A.F4 <= TW && A.unit_chunk <= 64 && (A.D4 == 8 || A.D4 == 16)) {
             if (A.D4 == 8) k = A.E ? sddmm_pf_kernel<NV, 8, false, 3, true> : sddmm_pf_kernel<NV, 8, false, 3, false>;
             else k = A.E ? sddmm_pf_kernel<NV, 16, false, 3, true> : sddmm_pf_kernel<NV, 16, false, 3, false>;
+            dsmem = pf_smem_bytes(NV, A.D4 == 8 ? 8 : 16);
         }
+    }
+    if (dsmem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem);
+        if (e != cudaSuccess) return fgk::set_error(FG_ECUDA, "sddmm: smem attribute: %s", cudaGetErrorString(e));
     }
     const int64_t per_block = THREADS / G;
     int64_t blocks = (A.n_units + per_block - 1) / per_block;
     if (blocks == 0) return FG_OK;
     if (A.persistent) {   // exactly the resident CTAs: the groups then walk the unit list together
         int per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, 0) != cudaSuccess || per_sm < 1)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, dsmem) != cudaSuccess || per_sm < 1)
             per_sm = 1;
         if (A.persistent > 0 && A.persistent < per_sm) per_sm = A.persistent;
         blocks = std::min<int64_t>(blocks, int64_t(fgk::num_sms()) * per_sm);
     }
-    k<<<unsigned(blocks), THREADS, 0, st>>>(A, X, Y, out);
+    k<<<unsigned(blocks), THREADS, dsmem, st>>>(A, X, Y, out);
     return fgk::check_launch("sddmm_kernel");
 }
 

@@ -270,7 +270,8 @@ def test_mlp_separate_x_dst():
 
 # ------------------------------------------------------------------ sddmm
 @pytest.mark.parametrize("H,D", [(1, 4), (1, 16), (1, 48), (1, 128), (1, 512), (1, 1024), (2, 4), (8, 4),
-                                 (8, 32), (4, 64), (2, 256), (8, 8)])
+                                 (8, 32), (4, 64), (2, 256), (8, 8), (12, 32), (6, 64), (3, 128), (24, 16),
+                                 (5, 64)])
 @pytest.mark.parametrize("use_eid", [False, True])
 def test_sddmm(skewed, skewed_eid, H, D, use_eid):
     import paper_2008_11359_b200 as fgp
@@ -610,7 +611,8 @@ def test_sddmm_pipelined_and_hilbert(skewed, skewed_eid, F, use_eid):
                 assert np.array_equal(out, plain), f"order={order} seg={seg} rb={rb} pipe={pipe}"
 
 
-@pytest.mark.parametrize("H,D", [(8, 32), (4, 64), (16, 32), (6, 32), (3, 64), (2, 64)])
+@pytest.mark.parametrize("H,D", [(8, 32), (4, 64), (16, 32), (6, 32), (3, 64), (2, 64), (12, 32), (6, 64),
+                                 (8, 64), (10, 32)])
 @pytest.mark.parametrize("use_eid", [False, True])
 def test_sddmm_heads_unit_prefetch(skewed, skewed_eid, H, D, use_eid):
     """a4: the unit-prefetching multi-head kernel (FG_TUNE_SDDMM_PIPE = 4, heads of

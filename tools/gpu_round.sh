@@ -24,7 +24,7 @@ spmm)
 timeout 900 $NCU -k regex:spmm_gather -s 9 -c 3 -o gpurun_out/prof_spmm_$TAG $B > /dev/null 2>&1; echo spmm $?
 ;;
 sddmm)
-timeout 900 $NCU -k regex:sddmm_kernel -s 6 -c 2 -o gpurun_out/prof_sddmm_$TAG $B > /dev/null 2>&1; echo sddmm $?
+timeout 900 $NCU -k regex:"sddmm_(pf_)?kernel" -s 6 -c 2 -o gpurun_out/prof_sddmm_$TAG $B > /dev/null 2>&1; echo sddmm $?
 ;;
 2)
 timeout 600 $NCU -k regex:softmax -s 3 -c 1 -o gpurun_out/prof_softmax_$TAG $B > /dev/null 2>&1; echo softmax $?
@@ -33,12 +33,12 @@ timeout 600 $NCU -k regex:gat_fused -s 0 -c 1 -o gpurun_out/prof_gat_$TAG python
 ;;
 ctl)
 timeout 900 $NCU -k regex:spmm_gather -s 9 -c 1 -o gpurun_out/prof_uspmm_$TAG $B --uniform-sources > /dev/null 2>&1; echo uspmm $?
-timeout 900 $NCU -k regex:sddmm_kernel -s 6 -c 1 -o gpurun_out/prof_usddmm_$TAG $B --uniform-sources > /dev/null 2>&1; echo usddmm $?
+timeout 900 $NCU -k regex:"sddmm_(pf_)?kernel" -s 6 -c 1 -o gpurun_out/prof_usddmm_$TAG $B --uniform-sources > /dev/null 2>&1; echo usddmm $?
 ;;
 direct)
 export FG_L2_TILE_MB=0 FG_SDDMM_SEG_MB=0
 timeout 900 $NCU -k regex:spmm_gather -s 9 -c 1 -o gpurun_out/prof_dspmm_$TAG $B --uniform-sources > /dev/null 2>&1; echo dspmm $?
-timeout 900 $NCU -k regex:sddmm_kernel -s 6 -c 1 -o gpurun_out/prof_dsddmm_$TAG $B --uniform-sources > /dev/null 2>&1; echo dsddmm $?
+timeout 900 $NCU -k regex:"sddmm_(pf_)?kernel" -s 6 -c 1 -o gpurun_out/prof_dsddmm_$TAG $B --uniform-sources > /dev/null 2>&1; echo dsddmm $?
 ;;
 esac
 # captures travel back compressed (gpurun_out/ is capped at 64 MiB per call);
