@@ -263,18 +263,30 @@ class Step:
         # e2e leg: the last op (GAT aggregation) runs on two row halves of this
         # rank's graph (two fg_graph handles over contiguous row ranges, global
         # source ids) so the first half's result ships while the second computes
-        self.halves = []
-        # split row: nnz-balanced, moved to the nearest row whose first edge is a
-        # multiple of 4 (the per-edge H=1 scores s1[e0:e1] must stay 16-byte aligned)
-        mid = int(np.searchsorted(rp, rp[-1] // 2))
-        cand = [r for r in range(max(1, mid - 64), min(len(rp) - 1, mid + 64)) if rp[r] % 4 == 0]
-        split = min(cand, key=lambda r: abs(r - mid)) if cand else 0
-        offs = np.array([0, split, len(rp) - 1], np.int64)
-        for r in range(2):
-            h = make_shard_fn(rp, ci, r, 2, offsets=offs)
+        # (the X512 ops on halves, the final GAT aggregation on quarters: its last
+        # piece's D2H is the e2e tail)
+        self.halves = self.row_pieces(fgp, torch, dev, g, rp, ci, make_shard_fn, 2)
+        self.quarters = self.row_pieces(fgp, torch, dev, g, rp, ci, make_shard_fn, 4)
+
+    def row_pieces(self, fgp, torch, dev, g, rp, ci, make_shard_fn, k):
+        """k nnz-balanced contiguous row ranges of this rank's graph as fg_graph
+        handles (global source ids): [(handle, row_lo, row_hi, edge_lo, edge_hi)].
+        Each split row is moved to the nearest row whose first edge is a multiple
+        of 4 (the per-edge H=1 scores s1[e0:e1] must stay 16-byte aligned)."""
+        offs = [0]
+        for q in range(1, k):
+            mid = int(np.searchsorted(rp, rp[-1] * q // k))
+            cand = [r for r in range(max(1, mid - 64), min(len(rp) - 1, mid + 64)) if rp[r] % 4 == 0]
+            offs.append(max(offs[-1], min(cand, key=lambda r: abs(r - mid)) if cand else 0))
+        offs.append(len(rp) - 1)
+        offs = np.array(offs, np.int64)
+        pieces = []
+        for r in range(k):
+            h = make_shard_fn(rp, ci, r, k, offsets=offs)
             Gh = fgp.Graph(torch.from_numpy(h.row_ptr).to(dev), torch.from_numpy(h.col_idx).to(dev), n_src=g.n_src)
             self.prepare(Gh, g.nnz)
-            self.halves.append((Gh, h.lo, h.hi, h.edge_lo, h.edge_lo + h.nnz))
+            pieces.append((Gh, h.lo, h.hi, h.edge_lo, h.edge_lo + h.nnz))
+        return pieces
 
     @staticmethod
     def prepare(G, nnz_total):
@@ -400,7 +412,7 @@ class Step:
         for Gh, rlo, rhi, elo, ehi in self.halves:
             fgp.sddmm(Gh, X["X512"], self.ydst("X512")[rlo:rhi], H=1, out=self.s1[elo:ehi], stream=st)
             ship([self.s1], rows=(elo, ehi))
-        for Gh, rlo, rhi, elo, ehi in self.halves:   # halves: the first half's D2H overlaps the second
+        for Gh, rlo, rhi, elo, ehi in self.quarters:   # each quarter's D2H overlaps the next
             fgp.spmm(Gh, "u_mul_e", "sum", X["X256"], H=H_GAT, E=self.s8[elo:ehi], out=self.o256[rlo:rhi], stream=st)
             ship([self.o256], rows=(rlo, rhi))
 

@@ -7,6 +7,13 @@
 #ifndef FG_SPMM_FULLB
 #define FG_SPMM_FULLB 0   // full-batch fast path: 0 select reducers only (default), 1 all, 2 none
 #endif
+#ifndef FG_SPMM_IDXPF
+// next-batch index prefetch in the gather loop (development variant, -DFG_SPMM_IDXPF=1):
+// measured slower on reddit -- copy_u-sum F=512 12.1 -> 12.9 ms (the two extra index
+// registers per lane spill at the 64-register cap), u_mul_e H=8 7.6 -> 7.8, copy_u-max
+// F=128 unchanged (48 -> 64 registers); the product loads a batch's indices at its start
+#define FG_SPMM_IDXPF 0
+#endif
 
 #include "device_common.cuh"
 #include "fg_internal.h"
@@ -108,16 +115,35 @@ __device__ __forceinline__ void gather_range(const Args& A, int64_t s, int64_t e
     bool cin[NV];                                            // chunk j inside the row (edge-invariant)
 #pragma unroll
     for (int j = 0; j < NV; ++j) cin[j] = c4base + colj<G, PAIR>(gl, j) < F4;
+    // the batch's neighbour indices (and edge ids), one per lane and R per lane
+    auto load_idx = [&](int64_t q0, int (&ui)[R], int (&ei)[R]) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t p = q0 + gl + r * G;
+            if constexpr (HYB) ui[r] = (p < e) ? __ldg(A.hyb_code + p) : 0;   // u, or -(slot+1): staged
+            else ui[r] = (OP != OP_COPYE && p < e) ? __ldg(A.col_idx + p) : 0;   // copy_e reads no source row
+            if constexpr (OP != OP_COPY) ei[r] = (p < e) ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
+        }
+    };
+    // FG_SPMM_IDXPF: the next batch's indices are loaded while this batch gathers, so
+    // a batch's first X gathers do not wait an index round trip
+    int uixn[R], eixn[R];
+    if constexpr (FG_SPMM_IDXPF) {
+        if (s < e) load_idx(s, uixn, eixn);
+    }
     for (int64_t p0 = s; p0 < e; p0 += B) {
         const int cnt = int(min((int64_t)B, e - p0));
         int uix[R];
         int eix[R];
+        if constexpr (FG_SPMM_IDXPF) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int64_t p = p0 + gl + r * G;
-            if constexpr (HYB) uix[r] = (p < e) ? __ldg(A.hyb_code + p) : 0;   // u, or -(slot+1): staged
-            else uix[r] = (OP != OP_COPYE && p < e) ? __ldg(A.col_idx + p) : 0;   // copy_e reads no source row
-            if constexpr (OP != OP_COPY) eix[r] = (p < e) ? (A.eid ? __ldg(A.eid + p) : int(p)) : 0;
+            for (int r = 0; r < R; ++r) {
+                uix[r] = uixn[r];
+                eix[r] = eixn[r];
+            }
+            if (p0 + B < e) load_idx(p0 + B, uixn, eixn);
+        } else {
+            load_idx(p0, uix, eix);
         }
         // u_mul_e with identity edge ids: the batch's E rows are one contiguous span;
         // stage it in shared memory with coalesced loads instead of one dependent
