@@ -190,14 +190,16 @@ fg_status fg_graph_prepare(fg_graph* g, int64_t row_bytes, fg_stream stream);
  *                          fg_graph_prepare built the bounds with it set)
  *   FG_TUNE_SDDMM_PIPE     fp32 gSDDMM with 33..128 float4 per row: -1 auto
  *                          (H == 1: software-pipelined kernel for 65..96,
- *                          unit-prefetching kernel for 33..64 and 97..128;
- *                          heads of D = 32 / 64: unit-prefetching up to 96
- *                          float4, and at 128 for D = 64), 0 plain,
- *                          1..3 pipelined variants (H == 1; U = 1 / 2 edges per
- *                          stage, 2 / 3 CTAs per SM), 4 unit-prefetching (the
- *                          next unit's indices and Y row staged by cp.async;
- *                          Y in registers), 5 / 6 the same with Y read from
- *                          shared memory (H == 1; 4 / 3 CTAs per SM);
+ *                          unit-prefetching kernel for 33..64 (4) and 97..128
+ *                          (7); heads of D = 32 / 64: unit-prefetching up to 64
+ *                          float4 (4), 65..96 (7), and at 128 for D = 64 (7)),
+ *                          0 plain, 1..3 pipelined variants (H == 1; U = 1 / 2
+ *                          edges per stage, 2 / 3 CTAs per SM), 4 unit-
+ *                          prefetching (the next unit's indices and Y row
+ *                          staged by cp.async; Y in registers, 3 CTAs per SM),
+ *                          5 / 6 the same with Y read from shared memory
+ *                          (H == 1; 4 / 3 CTAs per SM), 7 unit-prefetching
+ *                          with twice the edges in flight at 2 CTAs per SM;
  *                          bit-identical in every setting
  *   FG_TUNE_SDDMM_ORDER    0 segment-major work units (default), 1 2D tiles
  *                          (destination block x source segment) in Hilbert-

@@ -484,7 +484,7 @@ extern "C" fg_status fg_graph_tune(fg_graph* g, fg_tune_key key, int64_t value) 
         case FG_TUNE_HYBRID: t.hybrid = value != 0; break;
         case FG_TUNE_SPMM_SEG_MB: t.spmm_seg_mb = std::max<int64_t>(0, value); break;
         case FG_TUNE_SDDMM_PIPE:
-            if (value < -1 || value > 6) return fgk::set_error(FG_EINVAL, "fg_graph_tune: sddmm pipe %lld", (long long)value);
+            if (value < -1 || value > 7) return fgk::set_error(FG_EINVAL, "fg_graph_tune: sddmm pipe %lld", (long long)value);
             t.sddmm_pipe = value;
             break;
         case FG_TUNE_SDDMM_ORDER:

@@ -528,14 +528,16 @@ __device__ __forceinline__ float4 lds_f4(const float4* p) {
 //   YS == true : Y read from shared memory chunk by chunk inside the edge loop.
 // Same per-lane partial dots, same U edges per reduce-scatter and the same tree
 // as sddmm_kernel<32, NV, MODE_H1 / MODE_HEADS, DW>: bit-identical results.
-template <int NV, int DW, bool YS, int MINB, bool EM>
+template <int NV, int DW, bool YS, int MINB, bool EM, int UO = 0>
 __global__ void __launch_bounds__(THREADS, MINB) sddmm_pf_kernel(const Args A, const float4* __restrict__ X,
                                                                  const float4* __restrict__ Y,
                                                                  float* __restrict__ out) {
     constexpr int NGRP = THREADS / 32;
     constexpr int CH = 64;                                   // max edges per work unit (host-checked)
     constexpr bool H1 = (DW == 32);
-    constexpr int U = NV >= 3 ? 2 : (NV == 2 ? 4 : 8);       // as sddmm_kernel
+    // edges per reduce-scatter: as sddmm_kernel (UO != 0: an override, same tree only
+    // for the same U)
+    constexpr int U = UO ? UO : (NV >= 3 ? 2 : (NV == 2 ? 4 : 8));
     constexpr int HMAX = H1 ? 1 : 32 * NV / DW;              // heads per row
     // dynamic shared memory (pf_smem_bytes): per warp two Y buffers, two index
     // buffers and the unit's staged results
@@ -707,6 +709,11 @@ __global__ void __launch_bounds__(THREADS) sddmm_heads_generic_kernel(const Args
     }
 }
 
+// FG_TUNE_SDDMM_PIPE = 7: the unit-prefetching kernel with twice the plain kernel's
+// edges per lane in flight at 2 CTAs per SM (NV = 2: 8, NV = 3 / 4: 4)
+template <int NV>
+constexpr int PF2U = NV >= 3 ? 4 : (NV == 2 ? 8 : 16);
+
 // shared-memory bytes of sddmm_pf_kernel<NV, DW>
 constexpr int pf_smem_bytes(int NV, int DW) {
     return (THREADS / 32) * (2 * 32 * NV * 16 + 2 * 64 * 4 + 64 * (DW == 32 ? 1 : 32 * NV / DW) * 4);
@@ -757,10 +764,12 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
     }
     if constexpr (G == 32 && NV >= 2 && !XB) {   // software-pipelined wide-row H == 1 kernel (FG_TUNE_SDDMM_PIPE)
         // auto (-1), measured on reddit (tools/sddmm_ab.py): the software-pipelined U=2
-        // kernel for NV = 3 (F=384: 12.21 plain -> 10.27 ms; unit-prefetching 11.5-11.7);
-        // the unit-prefetching kernel for NV = 2 and 4 (F=256: 7.07 -> 6.72 ms, F=512:
-        // 14.98 -> 14.54; the software-pipelined variants 8.26-9.12 / 15.41-30.5)
-        const int pipe = A.pipe < 0 ? (NV == 3 ? 3 : 4) : A.pipe;
+        // kernel for NV = 3 (F=384: 12.21 plain -> 10.27 ms; unit-prefetching 11.2-11.7);
+        // the unit-prefetching kernel for NV = 2 (F=256: 7.07 -> 6.72 ms) and, with 4
+        // edges in flight per lane at 2 CTAs per SM, for NV = 4 (F=512: 14.79 plain,
+        // 14.38 at U = 2 / 3 CTAs, 14.20 at U = 4 / 2 CTAs; on another box 14.55 /
+        // 14.15 / 13.84); the software-pipelined variants 8.26-9.12 / 15.41-30.5
+        const int pipe = A.pipe < 0 ? (NV == 3 ? 3 : (NV == 4 ? 7 : 4)) : A.pipe;
         if (pipe && A.H == 1 && A.tile4 == 0 && A.F4 <= TW && A.unit_chunk <= 64) {
             if (pipe == 1) k = A.E ? sddmm_h1_pipe_kernel<NV, 1, 3, true> : sddmm_h1_pipe_kernel<NV, 1, 3, false>;
             else if (pipe == 2) k = A.E ? sddmm_h1_pipe_kernel<NV, 2, 2, true> : sddmm_h1_pipe_kernel<NV, 2, 2, false>;
@@ -768,7 +777,8 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
             // 4..6: unit-prefetching kernel (next unit's indices + Y row staged by cp.async)
             else if (pipe == 4) k = A.E ? sddmm_pf_kernel<NV, 32, false, 3, true> : sddmm_pf_kernel<NV, 32, false, 3, false>;
             else if (pipe == 5) k = A.E ? sddmm_pf_kernel<NV, 32, true, 4, true> : sddmm_pf_kernel<NV, 32, true, 4, false>;
-            else k = A.E ? sddmm_pf_kernel<NV, 32, true, 3, true> : sddmm_pf_kernel<NV, 32, true, 3, false>;
+            else if (pipe == 6) k = A.E ? sddmm_pf_kernel<NV, 32, true, 3, true> : sddmm_pf_kernel<NV, 32, true, 3, false>;
+            else k = A.E ? sddmm_pf_kernel<NV, 32, false, 2, true, PF2U<NV>> : sddmm_pf_kernel<NV, 32, false, 2, false, PF2U<NV>>;
             if (pipe >= 4) dsmem = pf_smem_bytes(NV, 32);
         }
     }
@@ -778,11 +788,17 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
         // H=6 D=32 7.82 -> 6.43, H=12 D=32 13.96 -> 13.14, H=6 D=64 14.98 -> 13.25) and for
         // H*D = 512 with D = 64 (H=8: 18.16 -> 16.03); off for H*D = 512 with D = 32 (H=16:
         // 16.30 plain vs 20.12 -- 70 KB of staged results per CTA)
+        // with 2 CTAs per SM and twice the edges in flight (pipe 7): H=12 D=32 12.96 -> 12.74,
+        // H=8 D=64 16.04 -> 15.28, but H=8 D=32 7.32 -> 7.67: 7 for NV = 3 / 4, 4 for NV = 2
         const bool dflt = NV <= 3 || (NV == 4 && A.D4 == 16);
-        const int pipe = A.pipe < 0 ? (dflt ? 4 : 0) : A.pipe;
+        const int pipe = A.pipe < 0 ? (dflt ? (NV == 2 ? 4 : 7) : 0) : A.pipe;
         if (pipe == 4 && A.H > 1 && A.F4 <= TW && A.unit_chunk <= 64 && (A.D4 == 8 || A.D4 == 16)) {
             if (A.D4 == 8) k = A.E ? sddmm_pf_kernel<NV, 8, false, 3, true> : sddmm_pf_kernel<NV, 8, false, 3, false>;
             else k = A.E ? sddmm_pf_kernel<NV, 16, false, 3, true> : sddmm_pf_kernel<NV, 16, false, 3, false>;
+            dsmem = pf_smem_bytes(NV, A.D4 == 8 ? 8 : 16);
+        } else if (pipe == 7 && A.H > 1 && A.F4 <= TW && A.unit_chunk <= 64 && (A.D4 == 8 || A.D4 == 16)) {
+            if (A.D4 == 8) k = A.E ? sddmm_pf_kernel<NV, 8, false, 2, true, PF2U<NV>> : sddmm_pf_kernel<NV, 8, false, 2, false, PF2U<NV>>;
+            else k = A.E ? sddmm_pf_kernel<NV, 16, false, 2, true, PF2U<NV>> : sddmm_pf_kernel<NV, 16, false, 2, false, PF2U<NV>>;
             dsmem = pf_smem_bytes(NV, A.D4 == 8 ? 8 : 16);
         }
     }

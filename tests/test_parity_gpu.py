@@ -594,7 +594,7 @@ def test_sddmm_pipelined_and_hilbert(skewed, skewed_eid, F, use_eid):
     with tuned(g.h, sddmm_pipe=0):
         plain = fgp.sddmm(g.h, dev(X), dev(Y)).cpu().numpy()
     check_close(plain[pos], ref, ab, TOL, f"u_dot_v F={F}")
-    for pipe in (1, 2, 3, 4, 5, 6, -1):
+    for pipe in (1, 2, 3, 4, 5, 6, 7, -1):
         with tuned(g.h, sddmm_pipe=pipe):
             out = fgp.sddmm(g.h, dev(X), dev(Y)).cpu().numpy()
         assert np.array_equal(out, plain), f"pipe={pipe}"
@@ -627,19 +627,20 @@ def test_sddmm_heads_unit_prefetch(skewed, skewed_eid, H, D, use_eid):
     pos = np.arange(g.nnz) if g.eid is None else g.eid
     with tuned(g.h, sddmm_pipe=0):
         plain = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
-    with tuned(g.h, sddmm_pipe=4):
-        out = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
-    check_close(out[pos], ref, ab, TOL, f"u_dot_v H={H} D={D} pf")
-    assert np.array_equal(out, plain)
     E = gen.features((g.nnz, H), 1402, 1, gen.UNIT)
-    with tuned(g.h, sddmm_pipe=4):
-        em = fgp.sddmm(g.h, dev(X), dev(Y), H=H, E=dev(E)).cpu().numpy()
-    assert np.array_equal(em, (plain * E).astype(np.float32))
-    with tuned(g.h, sddmm_seg_mb=1, sddmm_seg_min_mb=0):   # source-segmented unit tables
-        g.h.prepare(F * 4)
-        with tuned(g.h, sddmm_pipe=4):
-            seg = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
-    assert np.array_equal(seg, plain)
+    for pipe in (4, 7, -1):
+        with tuned(g.h, sddmm_pipe=pipe):
+            out = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+        check_close(out[pos], ref, ab, TOL, f"u_dot_v H={H} D={D} pf pipe={pipe}")
+        assert np.array_equal(out, plain), f"pipe={pipe}"
+        with tuned(g.h, sddmm_pipe=pipe):
+            em = fgp.sddmm(g.h, dev(X), dev(Y), H=H, E=dev(E)).cpu().numpy()
+        assert np.array_equal(em, (plain * E).astype(np.float32)), f"e_mul pipe={pipe}"
+        with tuned(g.h, sddmm_seg_mb=1, sddmm_seg_min_mb=0):   # source-segmented unit tables
+            g.h.prepare(F * 4)
+            with tuned(g.h, sddmm_pipe=pipe):
+                seg = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+        assert np.array_equal(seg, plain), f"segmented pipe={pipe}"
 
 
 @pytest.mark.parametrize("F", [8, 32, 40, 128, 512])
