@@ -643,6 +643,28 @@ def test_sddmm_heads_unit_prefetch(skewed, skewed_eid, H, D, use_eid):
         assert np.array_equal(seg, plain), f"segmented pipe={pipe}"
 
 
+@pytest.mark.parametrize("chunk", ["40", "128"])
+def test_sddmm_unit_chunk_override(skewed, chunk, monkeypatch):
+    """a4: work units of a non-default size (FG_SDDMM_CHUNK, read by
+    fg_graph_create): 40 edges (not a multiple of a warp; the unit-prefetching
+    kernels stage partial index batches) and 128 (above the prefetching kernels'
+    64-edge buffers: those fall back to the plain kernel) -- H = 1 at F = 256 /
+    512 and H = 8 D = 32, segmented and not, against the oracle."""
+    import paper_2008_11359_b200 as fgp
+    monkeypatch.setenv("FG_SDDMM_CHUNK", chunk)
+    g = G(skewed.row_ptr, skewed.col_idx, skewed.n_src)
+    for H, F in ((1, 256), (1, 512), (8, 256)):
+        X = feats((g.n_src, F), 1500 + F + H, gen.REAL)
+        Y = feats((g.n_dst, F), 1501 + F + H, gen.REAL)
+        ref, ab = oracle.sddmm(g.row_ptr, g.col_idx, X, Y, H=H)
+        out = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+        check_close(out, ref, ab, TOL, f"u_dot_v H={H} F={F} chunk={chunk}")
+        with tuned(g.h, sddmm_seg_mb=1, sddmm_seg_min_mb=0):
+            g.h.prepare(F * 4)
+            seg = fgp.sddmm(g.h, dev(X), dev(Y), H=H).cpu().numpy()
+        check_close(seg, ref, ab, TOL, f"segmented u_dot_v H={H} F={F} chunk={chunk}")
+
+
 @pytest.mark.parametrize("F", [8, 32, 40, 128, 512])
 @pytest.mark.parametrize("red", ["sum", "max", "min", "mean"])
 def test_copy_u_ldg256_pairs(skewed, F, red):
