@@ -782,6 +782,15 @@ fg_status launch_t(const Args& A, const float4* X, const float4* Y, float* out, 
             if (pipe >= 4) dsmem = pf_smem_bytes(NV, 32);
         }
     }
+    if constexpr (G == 32 && NV == 1 && !XB) {   // H == 1, 17..32 float4 per row: unit prefetch
+        // auto (-1) = 4: reddit F=128 4.36 -> 4.03 ms, proteins 3.10 -> 2.91 (7: 4.17 / 3.14)
+        const int pipe = A.pipe < 0 ? 4 : A.pipe;
+        if (A.H == 1 && A.tile4 == 0 && A.F4 <= TW && A.unit_chunk <= 64 && (pipe == 4 || pipe == 7)) {
+            if (pipe == 4) k = A.E ? sddmm_pf_kernel<1, 32, false, 3, true> : sddmm_pf_kernel<1, 32, false, 3, false>;
+            else k = A.E ? sddmm_pf_kernel<1, 32, false, 2, true, PF2U<1>> : sddmm_pf_kernel<1, 32, false, 2, false, PF2U<1>>;
+            dsmem = pf_smem_bytes(1, 32);
+        }
+    }
     if constexpr (G == 32 && NV >= 2 && !XB) {   // unit-prefetching multi-head kernel (FG_TUNE_SDDMM_PIPE = 4)
         // heads of D = 32 / 64 (D4 = 8 / 16 lanes per head); other head widths run sddmm_kernel.
         // auto (-1): on for H*D <= 384 (reddit H=8 D=32 7.63 -> 7.30 ms, H=4 D=64 8.20 -> 7.36,

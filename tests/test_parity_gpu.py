@@ -578,7 +578,7 @@ def test_spmm_u_mul_e_source_segmented(skewed, skewed_eid, H, D, use_eid, heavy)
     assert np.array_equal(outi.astype(np.float64), refi)
 
 
-@pytest.mark.parametrize("F", [260, 384, 512, 200])
+@pytest.mark.parametrize("F", [260, 384, 512, 200, 128, 100])
 @pytest.mark.parametrize("use_eid", [False, True])
 def test_sddmm_pipelined_and_hilbert(skewed, skewed_eid, F, use_eid):
     """a4 / f3: the software-pipelined wide-row H=1 kernel (every variant) and the
